@@ -1,0 +1,147 @@
+"""CPU oracle — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+import this package.  It shares no code with the CUDA library (paper_2112_11880_b200/) and
+the product path never imports it.
+
+Thin ctypes wrapper over ``zk_oracle.c`` (plain C, fp64, -ffp-contract=off).  Each function
+cites the passage it follows; see the C file header for the pins and for what is
+"parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_DIR = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_DIR, "zk_oracle.c")
+_SO = os.path.join(_DIR, "liboracle.so")
+
+ORD_SEQ, ORD_REV, ORD_BLOCK256, ORD_NEUMAIER = 0, 1, 2, 3
+
+STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN_RHO", 3: "BREAKDOWN_SIGMA",
+          4: "BREAKDOWN_OMEGA", 5: "NOT_HPD", 6: "NONFINITE", 7: "ZERO_RHS"}
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
+                               "-fPIC", "-shared", "-o", _SO, _SRC, "-lm"])
+    return _SO
+
+
+_h = None
+
+
+def _lib():
+    global _h
+    if _h is None:
+        lib = ctypes.CDLL(build())
+        P, I64, D, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+        lib.oracle_zdotc.argtypes = [I64, P, P, I, P]
+        lib.oracle_zdotc.restype = None
+        lib.oracle_sumsq.argtypes = [I64, P, I]
+        lib.oracle_sumsq.restype = D
+        lib.oracle_dznrm2.argtypes = [I64, P, I]
+        lib.oracle_dznrm2.restype = D
+        lib.oracle_zaxpy.argtypes = [I64, D, D, P, P]
+        lib.oracle_zaxpy.restype = None
+        lib.oracle_zscal.argtypes = [I64, D, D, P]
+        lib.oracle_zscal.restype = None
+        lib.oracle_zcsrmv.argtypes = [I64, P, P, P, D, D, P, D, D, P, I]
+        lib.oracle_zcsrmv.restype = None
+        for f in (lib.oracle_bicgstab, lib.oracle_cg):
+            f.argtypes = [I64, P, P, P, P, P, D, ctypes.c_int32, I, P, P, P, P]
+            f.restype = I
+        _h = lib
+    return _h
+
+
+def _c128(a) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    return a
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def zcsrmv(A: dict, x, alpha=1.0, beta=0.0, y=None, order=ORD_SEQ) -> np.ndarray:
+    """O1: y ← αAx + βy (T8).  Returns a new array."""
+    rp = np.ascontiguousarray(A["row_ptr"], dtype=np.int64)
+    col = np.ascontiguousarray(A["col_idx"], dtype=np.int32)
+    val = _c128(A["values"])
+    x = _c128(x)
+    n = len(rp) - 1
+    out = np.zeros(n, np.complex128) if y is None else _c128(y).copy()
+    alpha, beta = complex(alpha), complex(beta)
+    _lib().oracle_zcsrmv(n, _ptr(rp), _ptr(col), _ptr(val), alpha.real, alpha.imag, _ptr(x),
+                         beta.real, beta.imag, _ptr(out), order)
+    return out
+
+
+def zdotc(x, y, order=ORD_NEUMAIER) -> complex:
+    """O2: Σ conj(x_i) y_i (L1).  Default: compensated (parity reference, L2)."""
+    x, y = _c128(x), _c128(y)
+    assert x.shape == y.shape
+    out = np.zeros(2)
+    _lib().oracle_zdotc(len(x), _ptr(x), _ptr(y), order, _ptr(out))
+    return complex(out[0], out[1])
+
+
+def dznrm2(x, order=ORD_NEUMAIER) -> float:
+    """O3: sqrt(Σ re² + im²) (L3)."""
+    x = _c128(x)
+    return float(_lib().oracle_dznrm2(len(x), _ptr(x), order))
+
+
+def sumsq(x, order=ORD_NEUMAIER) -> float:
+    x = _c128(x)
+    return float(_lib().oracle_sumsq(len(x), _ptr(x), order))
+
+
+def zaxpy(alpha, x, y) -> np.ndarray:
+    """O4: returns α·x + y."""
+    x, out = _c128(x), _c128(y).copy()
+    a = complex(alpha)
+    _lib().oracle_zaxpy(len(x), a.real, a.imag, _ptr(x), _ptr(out))
+    return out
+
+
+def zscal(alpha, x) -> np.ndarray:
+    """O5: returns α·x."""
+    out = _c128(x).copy()
+    a = complex(alpha)
+    _lib().oracle_zscal(len(out), a.real, a.imag, _ptr(out))
+    return out
+
+
+def _solve(fn, A, b, x0, tol, maxit, order):
+    rp = np.ascontiguousarray(A["row_ptr"], dtype=np.int64)
+    col = np.ascontiguousarray(A["col_idx"], dtype=np.int32)
+    val = _c128(A["values"])
+    b = _c128(b)
+    n = len(rp) - 1
+    x0 = None if x0 is None else _c128(x0)
+    x = np.zeros(n, np.complex128)
+    iters = ctypes.c_int32(0)
+    hist = np.full(maxit + 1, np.nan)
+    tr = ctypes.c_double(0.0)
+    st = fn(n, _ptr(rp), _ptr(col), _ptr(val), _ptr(b), _ptr(x0), float(tol), int(maxit), order,
+            _ptr(x), ctypes.addressof(iters), _ptr(hist), ctypes.addressof(tr))
+    it = iters.value
+    return dict(x=x, iters=it, hist=hist[: it + 1].copy(), status=STATUS[st],
+                true_relres=tr.value)
+
+
+def bicgstab(A, b, x0=None, tol=1e-8, maxit=1000, order=ORD_SEQ) -> dict:
+    """O6 BiCGStab (§4)."""
+    return _solve(_lib().oracle_bicgstab, A, b, x0, tol, maxit, order)
+
+
+def cg(A, b, x0=None, tol=1e-8, maxit=1000, order=ORD_SEQ) -> dict:
+    """O7 CG (north-star addition)."""
+    return _solve(_lib().oracle_cg, A, b, x0, tol, maxit, order)

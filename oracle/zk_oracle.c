@@ -1,0 +1,374 @@
+/*
+ * zk_oracle.c — TEST INFRASTRUCTURE ONLY.  The plain, slow, obviously correct CPU
+ * oracle for the hot path of arXiv 2112.11880 ("Alinea" complex-double Krylov).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this.  It shares no code, header, table or
+ * helper with the CUDA library (paper_2112_11880_b200/csrc); neither includes
+ * or links the other.
+ *
+ * Every routine is the plain definition (SpMV, dot, norm, axpy, scal) or the
+ * textbook algorithm step by step (BiCGStab, CG), in IEEE binary64, complex
+ * numbers as interleaved (re, im) pairs, complex products written out as
+ * (a+bi)(c+di) = (ac − bd) + (ad + bc)i.  Compile with -ffp-contract=off
+ * (no FMA contraction) and without -ffast-math.
+ *
+ * Citations: P:L = /root/reference/PAPER.md line L; S:L = SPEC.md line L;
+ * SURVEY.md §8(c) O1–O7 and ledger L1–L21 give the readings; DESIGN.md lists them.
+ *
+ * Pins: tests/test_oracle_*.py (dense brute force, closed-form eigenvectors,
+ * integer exactness, closed-form sums, A = cI, DST-I direct solves, gauge and
+ * phase invariance, true-vs-recurrence residual).  Parity unpinned: nothing
+ * here reproduces PAPER.md T9/T10 iteration counts (other matrices and an
+ * unnamed preconditioner).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* summation orders */
+enum { ORD_SEQ = 0, ORD_REV = 1, ORD_BLOCK256 = 2, ORD_NEUMAIER = 3 };
+
+/* solver outcomes */
+enum {
+    ST_CONVERGED = 0, ST_MAXIT = 1, ST_BREAKDOWN_RHO = 2, ST_BREAKDOWN_SIGMA = 3,
+    ST_BREAKDOWN_OMEGA = 4, ST_NOT_HPD = 5, ST_NONFINITE = 6, ST_ZERO_RHS = 7
+};
+
+#define RE(v, i) ((v)[2 * (i)])
+#define IM(v, i) ((v)[2 * (i) + 1])
+
+/* ------------------------------------------------------------------------ */
+/* summation helper: adds term[i] for i in [0,n) in the requested order     */
+/* ------------------------------------------------------------------------ */
+typedef double (*term_fn)(const void* ctx, int64_t i);
+
+static double ordered_sum(int64_t n, term_fn f, const void* ctx, int order) {
+    double s = 0.0;
+    if (order == ORD_REV) {
+        for (int64_t i = n - 1; i >= 0; i--) s += f(ctx, i);
+    } else if (order == ORD_BLOCK256) {
+        /* partial per block of 256 in ascending order, then partials in ascending order
+           (the "two distinct tasks" reduction of P:199-200) */
+        for (int64_t b0 = 0; b0 < n; b0 += 256) {
+            double part = 0.0;
+            int64_t e = b0 + 256 < n ? b0 + 256 : n;
+            for (int64_t i = b0; i < e; i++) part += f(ctx, i);
+            s += part;
+        }
+    } else if (order == ORD_NEUMAIER) {
+        double c = 0.0;
+        for (int64_t i = 0; i < n; i++) {
+            double t = f(ctx, i);
+            double u = s + t;
+            if (fabs(s) >= fabs(t)) c += (s - u) + t;
+            else c += (t - u) + s;
+            s = u;
+        }
+        s += c;
+    } else {
+        for (int64_t i = 0; i < n; i++) s += f(ctx, i);
+    }
+    return s;
+}
+
+typedef struct { const double* x; const double* y; } pair_ctx;
+
+/* Re(conj(x_i) y_i) = xr·yr + xi·yi ;  Im(conj(x_i) y_i) = xr·yi − xi·yr   (O2) */
+static double dot_re_term(const void* c, int64_t i) {
+    const pair_ctx* p = (const pair_ctx*)c;
+    return RE(p->x, i) * RE(p->y, i) + IM(p->x, i) * IM(p->y, i);
+}
+static double dot_im_term(const void* c, int64_t i) {
+    const pair_ctx* p = (const pair_ctx*)c;
+    return RE(p->x, i) * IM(p->y, i) - IM(p->x, i) * RE(p->y, i);
+}
+static double sq_term(const void* c, int64_t i) {
+    const pair_ctx* p = (const pair_ctx*)c;
+    return RE(p->x, i) * RE(p->x, i) + IM(p->x, i) * IM(p->x, i);
+}
+
+/* O2 zdotc: Σ conj(x_i)·y_i, conjugating the FIRST argument (L1; BLAS zdotc).
+   PAPER.md P:199-200 (ZDOT, "two distinct tasks"). */
+void oracle_zdotc(int64_t n, const double* x, const double* y, int order, double* out) {
+    pair_ctx c = {x, y};
+    out[0] = ordered_sum(n, dot_re_term, &c, order);
+    out[1] = ordered_sum(n, dot_im_term, &c, order);
+}
+
+/* Σ re² + im² (no scaling, L3) */
+double oracle_sumsq(int64_t n, const double* x, int order) {
+    pair_ctx c = {x, x};
+    return ordered_sum(n, sq_term, &c, order);
+}
+
+/* O3 dznrm2: sqrt(Σ re² + im²).  PAPER.md P:257 (ZNORM, T7). */
+double oracle_dznrm2(int64_t n, const double* x, int order) {
+    return sqrt(oracle_sumsq(n, x, order));
+}
+
+/* O4 zaxpy: y_i ← α·x_i + y_i.  PAPER.md P:143-150 (listing "d_y[idx] = alpha * d_x[idx] + d_y[idx]"). */
+void oracle_zaxpy(int64_t n, double ar, double ai, const double* x, double* y) {
+    for (int64_t i = 0; i < n; i++) {
+        double pr = ar * RE(x, i) - ai * IM(x, i);
+        double pi = ar * IM(x, i) + ai * RE(x, i);
+        RE(y, i) = pr + RE(y, i);
+        IM(y, i) = pi + IM(y, i);
+    }
+}
+
+/* O5 zscal: x_i ← α·x_i.  PAPER.md P:116-122 (listing "d_x[idx] = alpha * d_x[idx]"). */
+void oracle_zscal(int64_t n, double ar, double ai, double* x) {
+    for (int64_t i = 0; i < n; i++) {
+        double xr = RE(x, i), xi = IM(x, i);
+        RE(x, i) = ar * xr - ai * xi;
+        IM(x, i) = ar * xi + ai * xr;
+    }
+}
+
+/* O1 zcsrmv: y_i ← α·Σ_{p ∈ row i} values[p]·x[col[p]] + β·y_i, row entries in stored order
+   (order = ORD_REV accumulates each row back to front; used only for the BiCGStab envelope, L11).
+   β = 0 ⇒ y is not read.  PAPER.md P:279-281 (SpMV CSR, T8). */
+void oracle_zcsrmv(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, const double* val,
+                   double ar, double ai, const double* x, double br, double bi, double* y,
+                   int order) {
+    for (int64_t i = 0; i < n_rows; i++) {
+        double sr = 0.0, si = 0.0;
+        if (order == ORD_REV) {
+            for (int64_t p = row_ptr[i + 1] - 1; p >= row_ptr[i]; p--) {
+                double a = RE(val, p), b = IM(val, p);
+                double c = RE(x, col[p]), d = IM(x, col[p]);
+                sr += a * c - b * d;
+                si += a * d + b * c;
+            }
+        } else {
+            for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; p++) {
+                double a = RE(val, p), b = IM(val, p);
+                double c = RE(x, col[p]), d = IM(x, col[p]);
+                sr += a * c - b * d;
+                si += a * d + b * c;
+            }
+        }
+        double yr = ar * sr - ai * si;
+        double yi = ar * si + ai * sr;
+        if (br != 0.0 || bi != 0.0) {
+            double qr = br * RE(y, i) - bi * IM(y, i);
+            double qi = br * IM(y, i) + bi * RE(y, i);
+            yr += qr;
+            yi += qi;
+        }
+        RE(y, i) = yr;
+        IM(y, i) = yi;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* complex scalar helpers (written out; no Annex-G handling)                 */
+/* ------------------------------------------------------------------------ */
+typedef struct { double re, im; } cplx;
+static cplx cmul(cplx a, cplx b) { cplx r = {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; return r; }
+static cplx cdiv(cplx a, cplx b) {
+    double den = b.re * b.re + b.im * b.im;
+    cplx r = {(a.re * b.re + a.im * b.im) / den, (a.im * b.re - a.re * b.im) / den};
+    return r;
+}
+static double cabs_(cplx a) { return sqrt(a.re * a.re + a.im * a.im); }
+static int cfinite(cplx a) { return isfinite(a.re) && isfinite(a.im); }
+
+typedef struct {
+    int64_t n;
+    const int64_t* row_ptr;
+    const int32_t* col;
+    const double* val;
+    int order;
+} csr_t;
+
+static void spmv(const csr_t* A, const double* x, double* y) {
+    oracle_zcsrmv(A->n, A->row_ptr, A->col, A->val, 1.0, 0.0, x, 0.0, 0.0, y,
+                  A->order == ORD_REV ? ORD_REV : ORD_SEQ);
+}
+static cplx dotc(const csr_t* A, const double* x, const double* y) {
+    double o[2];
+    oracle_zdotc(A->n, x, y, A->order, o);
+    cplx r = {o[0], o[1]};
+    return r;
+}
+static double nrm(const csr_t* A, const double* x) { return oracle_dznrm2(A->n, x, A->order); }
+
+/* true_relres = ‖b − A x‖/nb */
+static double true_relres(const csr_t* A, const double* b, const double* x, double nb, double* tmp) {
+    spmv(A, x, tmp);
+    for (int64_t i = 0; i < 2 * A->n; i++) tmp[i] = b[i] - tmp[i];
+    return nrm(A, tmp) / nb;
+}
+
+/*
+ * O6 BiCGStab (van der Vorst 1992, Barrett et al. "Templates" form, Hermitian inner product).
+ * PAPER.md §4 P:308-310 (P-Bi-CGSTAB; residual tolerance, zero initial guess, maxit);
+ * unpreconditioned per L8; half-step exit per L6; breakdown floors per L20.
+ * x0 may be NULL (zero initial guess).  hist has room for maxit+1 entries.
+ * Returns the status; *iters = completed loop passes (half-step exit counts as one, L7).
+ */
+int oracle_bicgstab(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                    const double* b, const double* x0, double tol, int32_t maxit, int order,
+                    double* x, int32_t* iters, double* hist, double* out_true_relres) {
+    csr_t A = {n, row_ptr, col, val, order};
+    size_t bytes = (size_t)(2 * n) * sizeof(double);
+    double *r = malloc(bytes), *rh = malloc(bytes), *p = malloc(bytes), *v = malloc(bytes),
+           *s = malloc(bytes), *t = malloc(bytes);
+    int status = ST_MAXIT;
+    *iters = 0;
+    *out_true_relres = NAN;
+
+    /* r = b − A x0 (r = b if x0 = 0) */
+    if (x0) {
+        memcpy(x, x0, bytes);
+        spmv(&A, x, r);
+        for (int64_t i = 0; i < 2 * n; i++) r[i] = b[i] - r[i];
+    } else {
+        memset(x, 0, bytes);
+        memcpy(r, b, bytes);
+    }
+    double nb = nrm(&A, b);
+    if (nb == 0.0) { status = ST_ZERO_RHS; goto done; }
+    double rnorm = nrm(&A, r);
+    hist[0] = rnorm / nb;
+    if (!isfinite(hist[0])) { status = ST_NONFINITE; goto done; }
+    if (hist[0] <= tol) { status = ST_CONVERGED; goto done_true; }
+
+    memcpy(rh, r, bytes);                      /* r̂ = r0 (L6) */
+    double nrh = rnorm;
+    cplx rho_prev = {1, 0}, alpha = {1, 0}, omega = {1, 0};
+    memset(p, 0, bytes);
+    memset(v, 0, bytes);
+
+    for (int32_t j = 1; j <= maxit; j++) {
+        cplx rho = dotc(&A, rh, r);                            /* ρ = ⟨r̂, r⟩ */
+        if (!cfinite(rho)) { status = ST_NONFINITE; break; }
+        if (cabs_(rho) <= 1e-30 * nrh * rnorm) { status = ST_BREAKDOWN_RHO; break; }
+        if (j == 1) {
+            memcpy(p, r, bytes);                               /* p = r */
+        } else {
+            cplx beta = cmul(cdiv(rho, rho_prev), cdiv(alpha, omega));  /* β = (ρ/ρ_prev)(α/ω) */
+            for (int64_t i = 0; i < n; i++) {                  /* p = r + β(p − ω v) */
+                cplx pv = {RE(p, i), IM(p, i)}, vv = {RE(v, i), IM(v, i)};
+                cplx wv = cmul(omega, vv);
+                cplx d = {pv.re - wv.re, pv.im - wv.im};
+                cplx bd = cmul(beta, d);
+                RE(p, i) = RE(r, i) + bd.re;
+                IM(p, i) = IM(r, i) + bd.im;
+            }
+        }
+        spmv(&A, p, v);                                        /* v = A p */
+        cplx sigma = dotc(&A, rh, v);                          /* σ = ⟨r̂, v⟩ */
+        double vnorm = nrm(&A, v);
+        if (!cfinite(sigma)) { status = ST_NONFINITE; break; }
+        if (cabs_(sigma) <= 1e-30 * nrh * vnorm) { status = ST_BREAKDOWN_SIGMA; break; }
+        alpha = cdiv(rho, sigma);                              /* α = ρ/σ */
+        for (int64_t i = 0; i < n; i++) {                      /* s = r − α v */
+            cplx vv = {RE(v, i), IM(v, i)};
+            cplx av = cmul(alpha, vv);
+            RE(s, i) = RE(r, i) - av.re;
+            IM(s, i) = IM(r, i) - av.im;
+        }
+        double snorm = nrm(&A, s);
+        if (!isfinite(snorm)) { status = ST_NONFINITE; break; }
+        if (snorm / nb <= tol) {                               /* half-step exit (L6) */
+            for (int64_t i = 0; i < n; i++) {
+                cplx pv = {RE(p, i), IM(p, i)};
+                cplx ap = cmul(alpha, pv);
+                RE(x, i) += ap.re;
+                IM(x, i) += ap.im;
+            }
+            hist[j] = snorm / nb;
+            *iters = j;
+            status = ST_CONVERGED;
+            goto done_true;
+        }
+        spmv(&A, s, t);                                        /* t = A s */
+        double tau = oracle_sumsq(n, t, order);                /* τ = ⟨t, t⟩ */
+        if (!isfinite(tau)) { status = ST_NONFINITE; break; }
+        if (tau == 0.0) { status = ST_BREAKDOWN_OMEGA; break; }
+        cplx ts = dotc(&A, t, s);                              /* ω = ⟨t, s⟩/τ */
+        omega.re = ts.re / tau;
+        omega.im = ts.im / tau;
+        for (int64_t i = 0; i < n; i++) {                      /* x += αp + ωs ; r = s − ωt */
+            cplx pv = {RE(p, i), IM(p, i)}, sv = {RE(s, i), IM(s, i)}, tv = {RE(t, i), IM(t, i)};
+            cplx ap = cmul(alpha, pv), ws = cmul(omega, sv), wt = cmul(omega, tv);
+            RE(x, i) += ap.re + ws.re;
+            IM(x, i) += ap.im + ws.im;
+            RE(r, i) = sv.re - wt.re;
+            IM(r, i) = sv.im - wt.im;
+        }
+        rnorm = nrm(&A, r);
+        hist[j] = rnorm / nb;
+        *iters = j;
+        if (!isfinite(hist[j]) || !cfinite(omega)) { status = ST_NONFINITE; break; }
+        if (hist[j] <= tol) { status = ST_CONVERGED; break; }
+        if (cabs_(omega) <= 1e-30) { status = ST_BREAKDOWN_OMEGA; break; }
+        rho_prev = rho;
+    }
+done_true:
+    *out_true_relres = true_relres(&A, b, x, nb, t);
+done:
+    free(r); free(rh); free(p); free(v); free(s); free(t);
+    return status;
+}
+
+/*
+ * O7 CG (Hestenes–Stiefel, Hermitian inner product; A Hermitian positive definite).
+ * Not in the paper (north-star addition, SPEC S:410 lists it as a non-goal of the CPU program);
+ * run on the gauge-twisted η = 0 variant (L9).  NOT_HPD if Re⟨p, Ap⟩ ≤ 0.
+ */
+int oracle_cg(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+              const double* b, const double* x0, double tol, int32_t maxit, int order, double* x,
+              int32_t* iters, double* hist, double* out_true_relres) {
+    csr_t A = {n, row_ptr, col, val, order};
+    size_t bytes = (size_t)(2 * n) * sizeof(double);
+    double *r = malloc(bytes), *p = malloc(bytes), *q = malloc(bytes);
+    int status = ST_MAXIT;
+    *iters = 0;
+    *out_true_relres = NAN;
+
+    if (x0) {                                                  /* r = b − A x0 */
+        memcpy(x, x0, bytes);
+        spmv(&A, x, r);
+        for (int64_t i = 0; i < 2 * n; i++) r[i] = b[i] - r[i];
+    } else {
+        memset(x, 0, bytes);
+        memcpy(r, b, bytes);
+    }
+    double nb = nrm(&A, b);
+    if (nb == 0.0) { status = ST_ZERO_RHS; goto done; }
+    memcpy(p, r, bytes);                                       /* p = r */
+    double gamma = oracle_sumsq(n, r, order);                  /* γ = ⟨r, r⟩ */
+    hist[0] = sqrt(gamma) / nb;
+    if (!isfinite(hist[0])) { status = ST_NONFINITE; goto done; }
+    if (hist[0] <= tol) { status = ST_CONVERGED; goto done_true; }
+
+    for (int32_t j = 1; j <= maxit; j++) {
+        spmv(&A, p, q);                                        /* q = A p */
+        cplx delta = dotc(&A, p, q);                           /* δ = ⟨p, q⟩ */
+        if (!cfinite(delta)) { status = ST_NONFINITE; break; }
+        if (delta.re <= 0.0) { status = ST_NOT_HPD; break; }
+        double alpha = gamma / delta.re;                       /* α = γ / Re δ */
+        for (int64_t i = 0; i < 2 * n; i++) {                  /* x += α p ; r −= α q */
+            x[i] += alpha * p[i];
+            r[i] -= alpha * q[i];
+        }
+        double gamma_new = oracle_sumsq(n, r, order);          /* γ' = ⟨r, r⟩ */
+        hist[j] = sqrt(gamma_new) / nb;
+        *iters = j;
+        if (!isfinite(hist[j])) { status = ST_NONFINITE; break; }
+        if (hist[j] <= tol) { status = ST_CONVERGED; break; }
+        double beta = gamma_new / gamma;                       /* p = r + (γ'/γ) p */
+        for (int64_t i = 0; i < 2 * n; i++) p[i] = r[i] + beta * p[i];
+        gamma = gamma_new;
+    }
+done_true:
+    *out_true_relres = true_relres(&A, b, x, nb, q);
+done:
+    free(r); free(p); free(q);
+    return status;
+}

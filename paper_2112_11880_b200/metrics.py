@@ -1,0 +1,41 @@
+"""Work and byte models used for reporting (no arithmetic of the method itself).
+
+Flop conventions (per element / per nonzero) are the paper's own, recovered from every row of
+PAPER.md Tables 2-8 as Gflops × time / h:
+assign 1, scal 6, axpy 8, ewp 6, dot 8, norm 5, SpMV 8 per nnz.  Pinned by
+tests/test_metrics.py against tests/golden/paper_flop_tables.json.
+
+Algorithmic bytes: complex128 = 16 B, col_idx int32 = 4 B, row_ptr int64 = 8 B.
+"""
+FLOPS_PER_ELEM = {"zassign": 1, "zscal": 6, "zaxpy": 8, "zaxmy": 6, "zdotc": 8, "dznrm2": 5}
+FLOPS_PER_NNZ_SPMV = 8
+
+Z = 16  # bytes per complex128
+
+
+def csr_bytes(n: int, nnz: int) -> int:
+    """Mat = 20·nnz + 8·(n+1): values + int32 col_idx + int64 row_ptr."""
+    return 20 * nnz + 8 * (n + 1)
+
+
+def spmv_bytes(n: int, nnz: int, beta_nonzero: bool = False) -> int:
+    """ZSpMV y ← αAx + βy: Mat + x once + y written (+ y read if β ≠ 0)."""
+    return csr_bytes(n, nnz) + Z * n + Z * n + (Z * n if beta_nonzero else 0)
+
+
+def blas1_bytes(op: str, n: int) -> int:
+    return {"zdotc": 2 * Z * n, "dznrm2": Z * n, "zaxpy": 3 * Z * n, "zscal": 2 * Z * n}[op]
+
+
+def bicgstab_iter_bytes(n: int, nnz: int) -> int:
+    """Schedule F: 2·Mat + 304n (19 complex vector passes)."""
+    return 2 * csr_bytes(n, nnz) + 19 * Z * n
+
+
+def cg_iter_bytes(n: int, nnz: int) -> int:
+    """Mat + 176n (11 vector passes)."""
+    return csr_bytes(n, nnz) + 11 * Z * n
+
+
+def spmv_flops(nnz: int) -> int:
+    return FLOPS_PER_NNZ_SPMV * nnz

@@ -1,0 +1,190 @@
+"""Pins for the oracle's BiCGStab (O6) and CG (O7) — SURVEY.md §8(c) 'Pins' rows BiCGStab/CG.
+
+Fixed from outside the oracle by: one-step exactness (A = cI), dense LU (numpy.linalg.solve),
+DST-I closed-form solves of the box Helmholtz system with κ in closed form, gauge and global
+phase invariance (a missing conjugate breaks both), the CG κ bound, true vs recurrence
+residual, and constructed breakdowns.  PAPER.md T9/T10 iteration counts: parity unpinned
+(other matrices, unnamed preconditioner)."""
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import gen
+import oracle
+from tests import closed_form as cf
+
+
+def csr_from_dense(D):
+    S = sp.csr_matrix(D)
+    S.sort_indices()
+    return dict(row_ptr=S.indptr.astype(np.int64), col_idx=S.indices.astype(np.int32),
+                values=S.data.astype(np.complex128), n=D.shape[0])
+
+
+def diag_csr(d):
+    n = len(d)
+    return dict(row_ptr=np.arange(n + 1, dtype=np.int64), col_idx=np.arange(n, dtype=np.int32),
+                values=np.asarray(d, np.complex128), n=n)
+
+
+def twisted(spec, eta):
+    """(A_g, D) with A_g = D·A·Dᴴ (L9)."""
+    m = gen.make_matrix(spec, eta=eta, twist_seed=gen.SEED_TWIST)
+    D = np.exp(1j * m["phase"])
+    return m, D
+
+
+# ------------------------------------------------------------------ BiCGStab
+@pytest.mark.parametrize("c", [2.0, -1.0, 1j, 0.3 - 2j])
+def test_bicgstab_scalar_identity(c):
+    """A = cI converges at the half step of iteration 1 (L6)."""
+    b = gen.rand_vector(50, 1)
+    r = oracle.bicgstab(diag_csr(np.full(50, c)), b, tol=1e-12)
+    assert r["status"] == "CONVERGED" and r["iters"] == 1
+    assert np.max(np.abs(r["x"] - b / c)) <= 4e-16 * np.max(np.abs(b / c))
+    assert r["hist"][0] == 1.0
+
+
+@pytest.mark.parametrize("cfg", ["C1", "T0"])
+def test_bicgstab_dense_lu(cfg):
+    """‖x − x_LU‖/‖x_LU‖ ≤ 1e-7 at tol 1e-10."""
+    m = gen.make_matrix(cfg)
+    b = gen.make_rhs(m)
+    D = sp.csr_matrix((m["values"], m["col_idx"], m["row_ptr"]), shape=(m["n"], m["n"])).toarray()
+    x_lu = np.linalg.solve(D, b)
+    r = oracle.bicgstab(m, b, tol=1e-10)
+    assert r["status"] == "CONVERGED"
+    assert np.linalg.norm(r["x"] - x_lu) / np.linalg.norm(x_lu) <= 1e-7
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "A3"])
+def test_bicgstab_dst_exact(cfg):
+    """Forward error vs the DST-I exact solution ≤ 2κ·tol, κ in closed form (L12)."""
+    spec = gen.CONFIGS[cfg]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    tol = 1e-8
+    r = oracle.bicgstab(m, b, tol=tol)
+    xe = cf.box_solve(spec, b, gen.ETA)
+    kappa = cf.box_kappa(spec, gen.ETA)
+    assert r["status"] == "CONVERGED"
+    assert np.linalg.norm(r["x"] - xe) / np.linalg.norm(xe) <= 2 * kappa * tol
+    # true vs recurrence residual (S:388 allows 10·tol; we require tol)
+    assert abs(r["true_relres"] - r["hist"][-1]) <= tol
+    assert r["true_relres"] <= 2 * tol
+    # solution-agreement reading L12 is binding literally on C1/C2
+    if cfg in ("C1", "C2"):
+        assert np.linalg.norm(r["x"] - xe) / np.linalg.norm(xe) <= 1e-6
+
+
+def test_bicgstab_gauge_invariance():
+    """(D·A·Dᴴ, D·b) gives the same count, hist equal to 1e-11 and x_g = D·x (App. B4)."""
+    spec = gen.CONFIGS["C2"]
+    m = gen.make_matrix(spec)
+    mg, D = twisted(spec, gen.ETA)
+    b = gen.make_rhs(m)
+    r = oracle.bicgstab(m, b, tol=1e-8)
+    rg = oracle.bicgstab(mg, D * b, tol=1e-8)
+    assert r["iters"] == rg["iters"]
+    n = min(12, r["iters"])
+    assert np.max(np.abs(r["hist"][:n] - rg["hist"][:n]) / r["hist"][:n]) <= 1e-11
+    assert np.linalg.norm(rg["x"] - D * r["x"]) / np.linalg.norm(r["x"]) <= 1e-6
+
+
+def test_bicgstab_global_phase():
+    spec = gen.CONFIGS["C1"]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    th = 0.7
+    mp = dict(m, values=m["values"] * np.exp(1j * th))
+    r, rp = oracle.bicgstab(m, b), oracle.bicgstab(mp, b)
+    assert r["iters"] == rp["iters"]
+    assert np.max(np.abs(r["hist"] - rp["hist"]) / r["hist"]) <= 1e-10
+    assert np.linalg.norm(rp["x"] - r["x"] * np.exp(-1j * th)) / np.linalg.norm(r["x"]) <= 1e-7
+
+
+def test_bicgstab_x0_restart():
+    """Restart from the returned x converges immediately (x0 path of O6)."""
+    m = gen.make_matrix("C1")
+    b = gen.make_rhs(m)
+    r = oracle.bicgstab(m, b, tol=1e-8)
+    r2 = oracle.bicgstab(m, b, x0=r["x"], tol=1e-7)
+    assert r2["status"] == "CONVERGED" and r2["iters"] == 0
+
+
+def test_bicgstab_statuses():
+    # ZERO_RHS
+    assert oracle.bicgstab(diag_csr([1, 2]), np.zeros(2))["status"] == "ZERO_RHS"
+    # σ = ⟨r̂, A r̂⟩ = 0 for a real skew matrix → BREAKDOWN_SIGMA
+    A = csr_from_dense(np.array([[0, 1], [-1, 0]], complex))
+    assert oracle.bicgstab(A, np.array([1, 0], complex))["status"] == "BREAKDOWN_SIGMA"
+    # MAXIT
+    m = gen.make_matrix("C2")
+    r = oracle.bicgstab(m, gen.make_rhs(m), tol=1e-14, maxit=3)
+    assert r["status"] == "MAXIT" and r["iters"] == 3 and len(r["hist"]) == 4
+    # NONFINITE
+    bad = dict(m, values=m["values"].copy())
+    bad["values"][5] = np.inf
+    assert oracle.bicgstab(bad, gen.make_rhs(m))["status"] == "NONFINITE"
+
+
+def test_bicgstab_order_envelope_small():
+    """Summation order perturbs the count only mildly on C2 (L11 context)."""
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    its = [oracle.bicgstab(m, b, order=o)["iters"] for o in (0, 1, 2, 3)]
+    assert max(its) - min(its) <= 0.15 * min(its)
+
+
+# ------------------------------------------------------------------ CG
+def test_cg_scalar_identity():
+    b = gen.rand_vector(40, 2)
+    r = oracle.cg(diag_csr(np.full(40, 3.0)), b)
+    assert r["status"] == "CONVERGED" and r["iters"] == 1
+    assert np.max(np.abs(r["x"] - b / 3)) <= 4e-16
+
+
+def test_cg_two_eigenvalues():
+    """A = I + uuᴴ has two distinct eigenvalues → CG exact in ≤ 2 iterations."""
+    u = gen.rand_vector(60, 3)
+    A = np.eye(60) + np.outer(u, u.conj())
+    b = gen.rand_vector(60, 4)
+    r = oracle.cg(csr_from_dense(A), b, tol=1e-12)
+    assert r["status"] == "CONVERGED" and r["iters"] <= 2
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "A3"])
+def test_cg_twisted_closed_form(cfg):
+    """CG on the gauge-twisted HPD box (η = 0): x_g = D·x_exact within 2κ·tol and the
+    iteration count within the κ bound ⌈ln(2√κ/tol)/ln((√κ+1)/(√κ−1))⌉."""
+    spec = gen.CONFIGS[cfg]
+    mg, D = twisted(spec, 0.0)
+    b = gen.make_rhs(mg)
+    tol = 1e-8
+    r = oracle.cg(mg, D * b, tol=tol)
+    xe = D * cf.box_solve(spec, b, 0.0)
+    kappa = cf.box_kappa(spec, 0.0)
+    assert r["status"] == "CONVERGED"
+    assert np.linalg.norm(r["x"] - xe) / np.linalg.norm(xe) <= 2 * kappa * tol
+    sk = math.sqrt(kappa)
+    bound = math.ceil(math.log(2 * sk / tol) / math.log((sk + 1) / (sk - 1)))
+    assert r["iters"] <= bound
+    assert abs(r["true_relres"] - r["hist"][-1]) <= tol
+
+
+def test_cg_gauge_invariance():
+    spec = gen.CONFIGS["C2"]
+    m0 = gen.make_matrix(spec, eta=0.0)
+    mg, D = twisted(spec, 0.0)
+    b = gen.make_rhs(m0)
+    r, rg = oracle.cg(m0, b), oracle.cg(mg, D * b)
+    assert r["iters"] == rg["iters"]
+    assert np.max(np.abs(r["hist"] - rg["hist"]) / r["hist"]) <= 1e-12
+
+
+def test_cg_not_hpd():
+    r = oracle.cg(diag_csr(np.full(10, -1.0)), gen.rand_vector(10, 1))
+    assert r["status"] == "NOT_HPD" and r["iters"] == 0
+    assert oracle.cg(diag_csr([1.0]), np.zeros(1))["status"] == "ZERO_RHS"
