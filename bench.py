@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""bench.py — the hot path of arXiv 2112.11880 on B200: one step = one device-resident BiCGStab
+solve to 1e-8 (x0 = 0) of the C4 synthetic 27-point Q1-hex complex Helmholtz system
+(unit-cube interior 200³: n = 8,000,000, nnz = 213,847,192; BASELINE.json configs[3]) through
+libzk's C-ABI: every step runs ZSpMV (fused K1/K3), the fused BLAS-1 updates with zdotc/dznrm2
+reductions (K2/K4/K5) and the device-resident driver, plus the final true-residual SpMV.
+
+value  = counted (algorithmic) bytes of the step ÷ device time  [GB/s], whole job over N GPUs.
+         Per step: iters·(2·Mat + 304n) + 80n (init) + Mat + 32n (true residual),
+         Mat = 20·nnz + 8·(n+1)   (paper_2112_11880_b200/metrics.py).
+Also printed: BiCGStab ms/iteration and time-to-1e-8, ZSpMV GB/s and GFLOP/s (8 flops/nnz,
+PAPER.md T8 convention), roofline of the dominant kernel (the in-loop ZSpMV), the CPU oracle
+baseline on a bounded sample, the end-to-end number with host buffers, and SM clocks.
+
+--impl reference runs the CPU oracle (the reference arm of this tier) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "ZSpMV GB/s & GFLOP/s vs HBM roofline; BiCGStab ms/iteration & time-to-1e-8"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def args_():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="zk", choices=["zk", "reference"])
+    p.add_argument("--config", default="C4")
+    p.add_argument("--method", default="bicgstab", choices=["bicgstab"])
+    p.add_argument("--tol", type=float, default=1e-8)
+    p.add_argument("--maxit", type=int, default=2000)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--spmv-reps", type=int, default=50)
+    return p.parse_args()
+
+
+def workload_name(cfg: str, spec) -> str:
+    if cfg in ("C4", "C5"):
+        return f"{cfg}: scaled 27-point Q1-hex complex Helmholtz, unit-cube interior {spec.nx}^3 (n={spec.n:,})"
+    return f"{cfg}: PAPER.md T1-shaped synthetic complex Helmholtz {spec.nx}x{spec.ny}x{spec.nz} + {spec.pad} pad"
+
+
+def step_bytes(n: int, nnz: int, iters: int) -> int:
+    from paper_2112_11880_b200 import metrics as M
+    return iters * M.bicgstab_iter_bytes(n, nnz) + 5 * 16 * n + M.csr_bytes(n, nnz) + 32 * n
+
+
+# ---------------------------------------------------------------- clocks (during the timed region)
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        time.sleep(0.3)
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 6]
+        os.unlink(self.f.name)
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].strip() == "Active"})
+        busy = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("spmv_dram_bytes_per_launch")
+    return None
+
+
+# ---------------------------------------------------------------- CPU oracle (reference arm / baseline)
+def oracle_sample(mat, b, maxit: int):
+    """The oracle as it stands, single-threaded: BiCGStab capped at `maxit` iterations."""
+    import oracle
+    t = time.perf_counter()
+    r = oracle.bicgstab(mat, b, tol=1e-8, maxit=maxit)
+    dt = time.perf_counter() - t
+    return r, dt
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import gen
+    spec = gen.CONFIGS[a.config]
+    mat = gen.make_matrix(spec)
+    b = gen.make_rhs(mat)
+    n, nnz = mat["n"], mat["nnz"]
+    for _ in range(a.warmup):
+        oracle_sample(mat, b, 1)
+    times, its = [], []
+    for _ in range(a.steps):
+        r, dt = oracle_sample(mat, b, 1)
+        times.append(dt)
+        its.append(r["iters"])
+    tot = sum(times)
+    byts = sum(step_bytes(n, nnz, i) for i in its)
+    v = byts / tot / 1e9
+    sample = (f"each step: oracle BiCGStab on {a.config} capped at 1 iteration "
+              f"(init + 2 SpMV + fused-vector work + true-residual SpMV), single thread")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic",
+            "config": {"workload": workload_name(a.config, spec), "n": n, "nnz": nnz, "method": "bicgstab",
+                       "tol": 1e-8, "parallelism": "cpu oracle, 1 thread"},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- the zk arm
+def main():
+    a = args_()
+    if a.impl == "reference":
+        return run_reference(a)
+
+    import torch
+    import torch.distributed as dist
+
+    import gen
+    from paper_2112_11880_b200 import metrics as M
+    from paper_2112_11880_b200 import zk
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    zk.lib()
+
+    spec = gen.CONFIGS[a.config]
+    t_gen = time.perf_counter()
+    mat = gen.make_matrix(spec)
+    b_h = gen.make_rhs(mat)
+    t_gen = time.perf_counter() - t_gen
+    n, nnz = mat["n"], mat["nnz"]
+
+    # inputs resident in HBM (borrowed by the handle); validation + stats at create (setup)
+    rp = torch.from_numpy(mat["row_ptr"]).to(dev)
+    ci = torch.from_numpy(mat["col_idx"]).to(dev)
+    va = torch.from_numpy(mat["values"]).to(dev)
+    b = torch.from_numpy(b_h).to(dev)
+    A = zk.csr_create(rp, ci, va, n, borrow=True)
+    ws = zk.alloc_workspace(A, "bicgstab", a.maxit, dev)
+    x = torch.empty_like(b)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return zk.solve(A, b, None, a.tol, a.maxit, "bicgstab", x=x, workspace=ws, stream=stream)
+
+    for _ in range(max(a.warmup, 3)):
+        r = step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local) if rank == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    results = []
+    e0.record(stream)
+    for _ in range(a.steps):
+        results.append(step())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop() if clocks else None
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    iters = results[-1]["iters"]
+    assert all(r["iters"] == iters for r in results), "non-deterministic iteration count"
+    bytes_step = step_bytes(n, nnz, iters)
+    total_bytes = bytes_step * a.steps * world
+    value = total_bytes / (ms * 1e-3) / 1e9
+    ms_step = ms / a.steps
+
+    # dominant kernel: the in-loop ZSpMV (K1: Mat+48n, K3: Mat+32n algorithmic bytes), timed by
+    # the device global timer inside the timed solves (first block start → last block end)
+    k_ms = sum(r["kernel_ms"][0] for r in results)
+    k_n = sum(r["kernel_launches"][0] for r in results)
+    mat_b = M.csr_bytes(n, nnz)
+    spmv_alg = sum(r["kernel_launches"][0] // 2 * (2 * mat_b + 80 * n) for r in results)
+    spmv_gbs = spmv_alg / (k_ms * 1e-3) / 1e9
+    peak, peak_src = hbm_peak()
+    roofline = {"bound": "hbm", "achieved": spmv_gbs, "peak": peak, "unit": "GB/s", "frac": spmv_gbs / peak,
+                "traffic": ncu_traffic(), "kernel": "in-loop ZSpMV (BiCGStab K1/K3, fused epilogues)",
+                "launch_us": 1e3 * k_ms / max(k_n, 1), "bytes_per_launch": spmv_alg / max(k_n, 1),
+                "peak_source": peak_src,
+                "share_of_step": k_ms / ms}
+    vec_ms = sum(r["kernel_ms"][1] for r in results)
+
+    # standalone zk_zcsrmv (β = 0) with CUDA events on the launching stream: GB/s and GFLOP/s
+    y = torch.empty_like(b)
+    for _ in range(3):
+        zk.zcsrmv(A, 1.0, b, 0.0, y, stream)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(a.spmv_reps):
+        zk.zcsrmv(A, 1.0, b, 0.0, y, stream)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    spmv_us = 1e3 * s0.elapsed_time(s1) / a.spmv_reps
+    spmv = {"us": spmv_us, "gbs": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9,
+            "gflops": M.spmv_flops(nnz) / (spmv_us * 1e-6) / 1e9,
+            "frac_of_peak": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9 / peak,
+            "lanes_per_row": A.info["lanes_per_row"]}
+
+    # end to end through the public API with HOST buffers (pinned): CSR upload + b H2D + solve + x D2H
+    e2e = None
+    if not a.no_e2e:
+        rp_h = torch.from_numpy(mat["row_ptr"]).pin_memory()
+        ci_h = torch.from_numpy(mat["col_idx"]).pin_memory()
+        va_h = torch.from_numpy(mat["values"]).pin_memory()
+        b_pin = torch.from_numpy(b_h).pin_memory()
+        x_h = torch.empty(n, dtype=torch.complex128).pin_memory()
+        ws2 = zk.alloc_workspace(A, "bicgstab", a.maxit, dev)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(a.e2e_steps):
+            Ah = zk.csr_create(rp_h, ci_h, va_h, n, stream=stream)
+            bd = b_pin.to(dev, non_blocking=True)
+            re = zk.solve(Ah, bd, None, a.tol, a.maxit, "bicgstab", workspace=ws2, stream=stream)
+            x_h.copy_(re["x"], non_blocking=True)
+            Ah.close()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = f0.elapsed_time(f1) / a.e2e_steps
+        h2d = 8 * (n + 1) + 4 * nnz + 16 * nnz + 16 * n
+        d2h = 16 * n + 8 * (a.maxit + 1)
+        e2e = {"value": bytes_step * world / (e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["ms_per_step"] = float(t.item())
+            e2e["value"] = bytes_step * world / (e2e["ms_per_step"] * 1e-3) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        rr, dt = oracle_sample(mat, b_h, 3)
+        cb = step_bytes(n, nnz, rr["iters"])
+        cpu = {"value": cb / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": f"oracle BiCGStab on {a.config} capped at 3 iterations (+ init and true-residual SpMV), "
+                         f"single thread, {dt:.1f} s", "ms_per_iteration": 1e3 * dt / max(rr["iters"], 1)}
+
+    if rank == 0:
+        r = results[-1]
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
+            "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic",
+            "config": {"workload": workload_name(a.config, spec), "n": n, "nnz": nnz, "method": "bicgstab",
+                       "tol": a.tol, "x0": "zero", "l2": "inputs larger than L2 (matrix 4.3 GB)",
+                       "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas"},
+            "bicgstab": {"iters": iters, "status": r["status"], "ms_per_iteration": ms_step / iters,
+                         "time_to_tol_ms": ms_step, "true_relres": r["true_relres"], "loop_mode": r["loop_mode"],
+                         "bytes_per_iteration": M.bicgstab_iter_bytes(n, nnz),
+                         "iter_gbs": M.bicgstab_iter_bytes(n, nnz) * iters / (ms_step * 1e-3) / 1e9,
+                         "spmv_share_of_solve": k_ms / sum(q["solve_ms"] for q in results),
+                         "vector_kernels_ms_per_iter": vec_ms / a.steps / iters},
+            "spmv": spmv,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": ck,
+            "gpu_launches": sum(q["gpu_launches"] for q in results) + 0,
+            "paper_context": "PAPER.md P:7: up to 28x dot, 9.8x SpMV/solvers (i7-920 vs Tesla K20c / GTX 570); "
+                             "K20c ZSpMV 6.74 GFLOP/s on Audi3D-4 (T8 P:297)",
+            "setup_s": {"generate": t_gen},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

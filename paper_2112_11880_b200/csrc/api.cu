@@ -1,0 +1,305 @@
+// api.cu — libzk diagnostics, CSR create/upload/validate and ZSpMV (A2).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "spmv.cuh"
+#include "zk_host.h"
+
+// ------------------------------------------------------------------ diagnostics
+namespace zk {
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+zk_status fail(zk_status code, const std::string& msg) {
+    g_err = std::string(zk_status_string(code)) + ": " + msg;
+    return code;
+}
+zk_status cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s failed: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+    g_err = buf;
+    return e == cudaErrorMemoryAllocation ? ZK_ERR_OOM : ZK_ERR_CUDA;
+}
+
+zk_status current_device(DeviceInfo* out) {
+    ZK_CUDA(cudaGetDevice(&out->device));
+    ZK_CUDA(cudaDeviceGetAttribute(&out->num_sms, cudaDevAttrMultiProcessorCount, out->device));
+    return ZK_OK;
+}
+
+int blocks_per_sm(const void* kernel) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(kernel);
+    if (it != cache.end()) return it->second;
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kBlock, 0) != cudaSuccess || b < 1) b = 1;
+    cache[kernel] = b;
+    return b;
+}
+}  // namespace zk
+
+extern "C" const char* zk_last_error(void) { return zk::g_err.c_str(); }
+
+extern "C" int32_t zk_version(void) { return 100; }
+
+extern "C" const char* zk_status_string(zk_status s) {
+    switch (s) {
+        case ZK_OK: return "ZK_OK";
+        case ZK_ERR_INVALID_VALUE: return "ZK_ERR_INVALID_VALUE";
+        case ZK_ERR_INVALID_CSR: return "ZK_ERR_INVALID_CSR";
+        case ZK_ERR_NONFINITE: return "ZK_ERR_NONFINITE";
+        case ZK_ERR_DIM: return "ZK_ERR_DIM";
+        case ZK_ERR_OOM: return "ZK_ERR_OOM";
+        case ZK_ERR_CUDA: return "ZK_ERR_CUDA";
+        case ZK_ERR_ALIAS: return "ZK_ERR_ALIAS";
+        case ZK_ERR_ZERO_RHS: return "ZK_ERR_ZERO_RHS";
+        case ZK_ERR_NCCL: return "ZK_ERR_NCCL";
+        case ZK_ERR_UNSUPPORTED: return "ZK_ERR_UNSUPPORTED";
+        default: return "ZK_UNKNOWN_STATUS";
+    }
+}
+
+// ------------------------------------------------------------------ validation
+namespace zk {
+enum : unsigned { V_OK = 0, V_ROWPTR = 1, V_COLRANGE = 2, V_COLORDER = 3, V_NONFINITE = 4 };
+
+struct ValidateOut {
+    unsigned long long first_bad;  // (row << 3) | code, min over offending rows
+    unsigned int max_len;
+};
+
+__global__ void __launch_bounds__(kBlock) validate_kernel(const int64_t* __restrict__ row_ptr,
+                                                         const int* __restrict__ col,
+                                                         const double2* __restrict__ val, int64_t n_rows,
+                                                         int64_t n_cols, int64_t nnz, int stats_only,
+                                                         ValidateOut* out) {
+    unsigned int my_max = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_rows; i += stride) {
+        const int64_t rs = row_ptr[i], re = row_ptr[i + 1];
+        unsigned code = V_OK;
+        if (stats_only) {
+            if (re - rs > (int64_t)my_max) my_max = (unsigned)(re - rs);
+            continue;
+        }
+        if ((i == 0 && rs != 0) || re < rs || re > nnz || (i == n_rows - 1 && re != nnz)) {
+            code = V_ROWPTR;
+        } else {
+            if ((uint64_t)(re - rs) > my_max) my_max = (unsigned)(re - rs);
+            int prev = -1;
+            for (int64_t p = rs; p < re; p++) {
+                const int c = col[p];
+                if (c < 0 || c >= n_cols) { code = V_COLRANGE; break; }
+                if (c <= prev) { code = V_COLORDER; break; }
+                prev = c;
+                const double2 v = val[p];
+                if (!isfinite(v.x) || !isfinite(v.y)) { code = V_NONFINITE; break; }
+            }
+        }
+        if (code != V_OK) atomicMin(&out->first_bad, ((unsigned long long)i << 3) | code);
+    }
+    atomicMax(&out->max_len, my_max);
+}
+
+// ------------------------------------------------------------------ ZSpMV kernel (zk_zcsrmv)
+struct EpiAxpby {
+    static constexpr int K = 0;
+    double2 alpha, beta;
+    double2* __restrict__ y;
+    bool beta_zero;
+    __device__ void row(int64_t i, double2 s, double (&)[1]) {
+        double2 r = cmul(alpha, s);
+        if (!beta_zero) r = cadd(r, cmul(beta, y[i]));
+        y[i] = r;
+    }
+    __device__ void finish(double (&)[1]) {}
+};
+
+template <int W>
+__global__ void __launch_bounds__(kBlock) zcsrmv_kernel(CsrDev A, const double2* __restrict__ x, EpiAxpby epi) {
+    spmv_body<W>(A, x, epi);
+}
+
+template <int W>
+static zk_status launch_zcsrmv(const zk_csr_s* A, double2 alpha, const double2* x, double2 beta, double2* y,
+                               cudaStream_t s) {
+    const void* k = (const void*)zcsrmv_kernel<W>;
+    const int cap = A->dev.num_sms * blocks_per_sm(k);
+    const int G = grid_for(A->n_rows, kBlock / W, cap);
+    CsrDev d{A->row_ptr, A->col, A->val, A->n_rows};
+    EpiAxpby e{alpha, beta, y, beta.x == 0.0 && beta.y == 0.0};
+    zcsrmv_kernel<W><<<G, kBlock, 0, s>>>(d, x, e);
+    ZK_CUDA(cudaGetLastError());
+    return ZK_OK;
+}
+
+zk_status zcsrmv_local(const zk_csr_s* A, double2 alpha, const double2* x, double2 beta, double2* y,
+                       cudaStream_t s) {
+    switch (A->W) {
+        case 2: return launch_zcsrmv<2>(A, alpha, x, beta, y, s);
+        case 4: return launch_zcsrmv<4>(A, alpha, x, beta, y, s);
+        case 8: return launch_zcsrmv<8>(A, alpha, x, beta, y, s);
+        case 16: return launch_zcsrmv<16>(A, alpha, x, beta, y, s);
+        default: return launch_zcsrmv<32>(A, alpha, x, beta, y, s);
+    }
+}
+
+// sub-warp width from the mean row length: ≈ 4 nonzeros per lane per row, W in [2, 32]
+static int choose_w(double mean) {
+    if (const char* e = getenv("ZK_SPMV_W")) {
+        int w = atoi(e);
+        if (w == 2 || w == 4 || w == 8 || w == 16 || w == 32) return w;
+    }
+    int w = 2;
+    while (w < 32 && 4.0 * w < mean) w *= 2;
+    return w;
+}
+
+zk_status dist_setup(zk_csr_s* A, const int64_t* h_row_ptr, const int* h_col, cudaStream_t s);  // dist.cu
+void dist_destroy(zk_csr_s* A);                                                                  // dist.cu
+zk_status dist_zcsrmv(const zk_csr_s* A, double2 alpha, const double2* x, double2 beta, double2* y,
+                      cudaStream_t s);                                                           // dist.cu
+int64_t dist_n_halo(const zk_csr_s* A);                                                          // dist.cu
+int dist_nranks(const zk_csr_s* A);                                                              // dist.cu
+}  // namespace zk
+
+using namespace zk;
+
+extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                   const int64_t* row_ptr, const int32_t* col_idx, const zk_z* values,
+                                   uint32_t flags, zk_comm comm, int64_t row_begin, zk_stream stream) {
+    if (!out) return fail(ZK_ERR_INVALID_VALUE, "out is NULL");
+    *out = nullptr;
+    if (n_rows < 0 || n_cols < 0 || nnz < 0) return fail(ZK_ERR_INVALID_VALUE, "negative size");
+    if (n_cols > INT32_MAX) return fail(ZK_ERR_INVALID_VALUE, "n_cols exceeds int32 column ids");
+    if (!row_ptr || (nnz > 0 && (!col_idx || !values))) return fail(ZK_ERR_INVALID_VALUE, "NULL array");
+    if (n_rows == 0 && nnz != 0) return fail(ZK_ERR_INVALID_CSR, "n_rows = 0 but nnz > 0");
+    const uint32_t where = flags & 3u;
+    if (where == 3u) return fail(ZK_ERR_INVALID_VALUE, "bad flags");
+    if (comm && where == ZK_PTRS_DEVICE_BORROW)
+        return fail(ZK_ERR_INVALID_VALUE, "distributed matrices are renumbered: use ZK_PTRS_HOST or ZK_PTRS_DEVICE");
+    cudaStream_t s = (cudaStream_t)stream;
+
+    zk_csr_s* A = new zk_csr_s();
+    auto cleanup = [&](zk_status st) {
+        zk_csr_destroy(A);
+        return st;
+    };
+    zk_status st = current_device(&A->dev);
+    if (st != ZK_OK) return cleanup(st);
+    A->n_rows = n_rows;
+    A->n_cols = n_cols;
+    A->nnz = nnz;
+    A->row_begin = row_begin;
+    A->n_global = n_rows;
+    A->comm = comm;
+
+    // ---- device arrays (copy or borrow); 16-B aligned by cudaMalloc
+    if (where == ZK_PTRS_DEVICE_BORROW) {
+        A->row_ptr = const_cast<int64_t*>(row_ptr);
+        A->col = const_cast<int*>(col_idx);
+        A->val = reinterpret_cast<double2*>(const_cast<zk_z*>(values));
+        A->owned = false;
+    } else {
+        A->owned = true;
+        cudaError_t e = cudaMalloc(&A->row_ptr, sizeof(int64_t) * (n_rows + 1));
+        if (e == cudaSuccess) e = cudaMalloc(&A->col, sizeof(int) * (nnz > 0 ? nnz : 1));
+        if (e == cudaSuccess) e = cudaMalloc(&A->val, sizeof(double2) * (nnz > 0 ? nnz : 1));
+        if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(csr)", __FILE__, __LINE__));
+        const cudaMemcpyKind kind = where == ZK_PTRS_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        e = cudaMemcpyAsync(A->row_ptr, row_ptr, sizeof(int64_t) * (n_rows + 1), kind, s);
+        if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(A->col, col_idx, sizeof(int) * nnz, kind, s);
+        if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(A->val, values, sizeof(double2) * nnz, kind, s);
+        if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMemcpyAsync(csr)", __FILE__, __LINE__));
+    }
+
+    // ---- validation + row statistics on the device (one pass over the arrays)
+    {
+        ValidateOut h{~0ull, 0u}, *d = nullptr;
+        cudaError_t e = cudaMalloc(&d, sizeof(ValidateOut));
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cleanup(cuda_fail(e, "validate setup", __FILE__, __LINE__));
+        if (n_rows > 0) {
+            // ZK_SKIP_VALIDATE: statistics only (reads row_ptr, 8 B/row)
+            const int G = grid_for(n_rows, kBlock, A->dev.num_sms * 8);
+            validate_kernel<<<G, kBlock, 0, s>>>(A->row_ptr, A->col, A->val, n_rows, n_cols, nnz,
+                                                 (flags & ZK_SKIP_VALIDATE) ? 1 : 0, d);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(d);
+        if (e != cudaSuccess) return cleanup(cuda_fail(e, "validate", __FILE__, __LINE__));
+        if (!(flags & ZK_SKIP_VALIDATE) && h.first_bad != ~0ull) {
+            const long long row = (long long)(h.first_bad >> 3);
+            const unsigned code = (unsigned)(h.first_bad & 7u);
+            const char* what = code == V_ROWPTR     ? "row_ptr not 0..nnz non-decreasing"
+                               : code == V_COLRANGE ? "column index out of range"
+                               : code == V_COLORDER ? "columns not strictly increasing (unsorted or duplicate)"
+                                                    : "non-finite value";
+            char buf[256];
+            snprintf(buf, sizeof buf, "row %lld: %s", row + (long long)row_begin, what);
+            return cleanup(fail(code == V_NONFINITE ? ZK_ERR_NONFINITE : ZK_ERR_INVALID_CSR, buf));
+        }
+        A->max_len = (int)h.max_len;
+    }
+    A->mean_len = n_rows > 0 ? (double)nnz / (double)n_rows : 0.0;
+    A->W = choose_w(A->mean_len);
+    if (cudaStreamCreateWithFlags(&A->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+        return cleanup(fail(ZK_ERR_CUDA, "cudaStreamCreate"));
+
+    if (comm) {
+        st = dist_setup(A, nullptr, nullptr, s);
+        if (st != ZK_OK) return cleanup(st);
+    }
+    *out = A;
+    return ZK_OK;
+}
+
+extern "C" zk_status zk_csr_destroy(zk_csr A) {
+    if (!A) return ZK_OK;
+    for (auto& g : A->graph) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph) cudaGraphDestroy(g.graph);
+    }
+    if (A->dist) dist_destroy(A);
+    if (A->owned) {
+        cudaFree(A->row_ptr);
+        cudaFree(A->col);
+        cudaFree(A->val);
+    }
+    if (A->cap_stream) cudaStreamDestroy(A->cap_stream);
+    delete A;
+    return ZK_OK;
+}
+
+extern "C" zk_status zk_csr_info(zk_csr A, zk_csr_info_t* info) {
+    if (!A || !info) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
+    info->n_rows = A->n_rows;
+    info->n_cols = A->n_cols;
+    info->nnz = A->nnz;
+    info->row_begin = A->row_begin;
+    info->n_global = A->n_global;
+    info->max_row_len = A->max_len;
+    info->lanes_per_row = A->W;
+    info->mean_row_len = A->mean_len;
+    info->n_halo = dist_n_halo(A);
+    info->borrowed = A->owned ? 0 : 1;
+    info->nranks = dist_nranks(A);
+    return ZK_OK;
+}
+
+extern "C" zk_status zk_zcsrmv(zk_csr A, zk_z alpha, const zk_z* x, zk_z beta, zk_z* y, zk_stream s) {
+    if (!A || !x || !y) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
+    if ((const void*)x == (const void*)y) return fail(ZK_ERR_ALIAS, "x and y alias (S:244)");
+    const double2 a = make_double2(alpha.re, alpha.im), b = make_double2(beta.re, beta.im);
+    if (A->n_rows == 0) return ZK_OK;
+    if (A->dist) return dist_zcsrmv(A, a, (const double2*)x, b, (double2*)y, (cudaStream_t)s);
+    return zcsrmv_local(A, a, (const double2*)x, b, (double2*)y, (cudaStream_t)s);
+}

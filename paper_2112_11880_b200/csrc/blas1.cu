@@ -1,0 +1,152 @@
+// blas1.cu — zaxpy, zscal (T3/T4), zdotc (T6), dznrm2 (T7).
+// SURVEY.md §8(a) A3-A5.  Grid-stride double2 streams with 4 elements in flight per thread;
+// the reductions are single-pass with a deterministic last-block finish (zk_internal.cuh).
+#include "spmv.cuh"
+#include "zk_host.h"
+
+namespace zk {
+
+// per-device scratch of the standalone reductions (self-cleaning tickets; one user at a time)
+__device__ double g_partials[kMaxRed * kMaxGrid];
+__device__ unsigned int g_ticket[4];
+
+struct OpAxpy {
+    static constexpr int K = 0;
+    struct In { double2 x, y; };
+    double2 a;
+    const double2* __restrict__ x;
+    double2* __restrict__ y;
+    __device__ In load(int64_t i) const { return {ld_stream(x + i), ld_stream_rw(y + i)}; }
+    __device__ void apply(int64_t i, const In& v, double (&)[1]) const {
+        double2 r = v.y;
+        cfma(r, a, v.x);
+        y[i] = r;
+    }
+    __device__ void finish(double (&)[1]) const {}
+};
+
+struct OpScal {
+    static constexpr int K = 0;
+    struct In { double2 x; };
+    double2 a;
+    double2* __restrict__ x;
+    __device__ In load(int64_t i) const { return {ld_stream_rw(x + i)}; }
+    __device__ void apply(int64_t i, const In& v, double (&)[1]) const { x[i] = cmul(a, v.x); }
+    __device__ void finish(double (&)[1]) const {}
+};
+
+struct OpDotc {
+    static constexpr int K = 2;
+    struct In { double2 x, y; };
+    const double2* __restrict__ x;
+    const double2* __restrict__ y;
+    double2* out;
+    __device__ In load(int64_t i) const { return {ld_stream(x + i), ld_stream(y + i)}; }
+    __device__ void apply(int64_t, const In& v, double (&acc)[2]) const {
+        // conj(x)·y: re += xr·yr + xi·yi, im += xr·yi − xi·yr
+        acc[0] = fma(v.x.x, v.y.x, acc[0]);
+        acc[0] = fma(v.x.y, v.y.y, acc[0]);
+        acc[1] = fma(v.x.x, v.y.y, acc[1]);
+        acc[1] = fma(-v.x.y, v.y.x, acc[1]);
+    }
+    __device__ void finish(double (&acc)[2]) const {
+        double tot[2];
+        if (grid_sum<2>(acc, g_partials, &g_ticket[0], tot) && threadIdx.x == 0) *out = make_double2(tot[0], tot[1]);
+    }
+};
+
+struct OpNrm2 {
+    static constexpr int K = 1;
+    struct In { double2 x; };
+    const double2* __restrict__ x;
+    double* out;
+    bool squared;
+    __device__ In load(int64_t i) const { return {ld_stream(x + i)}; }
+    __device__ void apply(int64_t, const In& v, double (&acc)[1]) const {
+        acc[0] = fma(v.x.x, v.x.x, acc[0]);
+        acc[0] = fma(v.x.y, v.x.y, acc[0]);
+    }
+    __device__ void finish(double (&acc)[1]) const {
+        double tot[1];
+        if (grid_sum<1>(acc, g_partials, &g_ticket[1], tot) && threadIdx.x == 0) *out = squared ? tot[0] : sqrt(tot[0]);
+    }
+};
+
+template <class Op>
+__global__ void __launch_bounds__(kBlock) vec_kernel(int64_t n, Op op) {
+    vec_body(n, op);
+}
+
+template <class Op>
+static zk_status launch_vec(int64_t n, const Op& op, cudaStream_t s) {
+    DeviceInfo d;
+    ZK_TRY(current_device(&d));
+    const void* k = (const void*)vec_kernel<Op>;
+    int cap = d.num_sms * blocks_per_sm(k);
+    if (cap > kMaxGrid) cap = kMaxGrid;
+    const int G = grid_for(n, (int64_t)kBlock * 4, cap);
+    vec_kernel<Op><<<G, kBlock, 0, s>>>(n, op);
+    ZK_CUDA(cudaGetLastError());
+    return ZK_OK;
+}
+
+// used by dist.cu: local partial of a distributed reduction
+zk_status dotc_local(int64_t n, const double2* x, const double2* y, double2* out, cudaStream_t s) {
+    return launch_vec(n, OpDotc{x, y, out}, s);
+}
+zk_status sumsq_local(int64_t n, const double2* x, double* out, cudaStream_t s) {
+    return launch_vec(n, OpNrm2{x, out, true}, s);
+}
+__global__ void sqrt_kernel(double* v) { *v = sqrt(*v); }
+zk_status sqrt_inplace(double* v, cudaStream_t s) {
+    sqrt_kernel<<<1, 1, 0, s>>>(v);
+    ZK_CUDA(cudaGetLastError());
+    return ZK_OK;
+}
+
+zk_status comm_allreduce_sum(zk_comm_s* c, double* buf, int count, cudaStream_t s);  // comm.cu
+
+}  // namespace zk
+
+using namespace zk;
+
+extern "C" zk_status zk_zaxpy(int64_t n, zk_z alpha, const zk_z* x, zk_z* y, zk_stream s) {
+    if (n < 0) return fail(ZK_ERR_INVALID_VALUE, "n < 0");
+    if (n == 0) return ZK_OK;
+    if (!x || !y) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
+    return launch_vec(n, OpAxpy{make_double2(alpha.re, alpha.im), (const double2*)x, (double2*)y}, (cudaStream_t)s);
+}
+
+extern "C" zk_status zk_zscal(int64_t n, zk_z alpha, zk_z* x, zk_stream s) {
+    if (n < 0) return fail(ZK_ERR_INVALID_VALUE, "n < 0");
+    if (n == 0) return ZK_OK;
+    if (!x) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
+    return launch_vec(n, OpScal{make_double2(alpha.re, alpha.im), (double2*)x}, (cudaStream_t)s);
+}
+
+extern "C" zk_status zk_zdotc(int64_t n, const zk_z* x, const zk_z* y, zk_z* result, zk_comm comm, zk_stream s) {
+    if (n < 0) return fail(ZK_ERR_INVALID_VALUE, "n < 0");
+    if (!result || (n > 0 && (!x || !y))) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
+    cudaStream_t st = (cudaStream_t)s;
+    if (n == 0) {
+        ZK_CUDA(cudaMemsetAsync(result, 0, sizeof(zk_z), st));
+    } else {
+        ZK_TRY(dotc_local(n, (const double2*)x, (const double2*)y, (double2*)result, st));
+    }
+    if (comm) ZK_TRY(comm_allreduce_sum(comm, (double*)result, 2, st));
+    return ZK_OK;
+}
+
+extern "C" zk_status zk_dznrm2(int64_t n, const zk_z* x, double* result, zk_comm comm, zk_stream s) {
+    if (n < 0) return fail(ZK_ERR_INVALID_VALUE, "n < 0");
+    if (!result || (n > 0 && !x)) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
+    cudaStream_t st = (cudaStream_t)s;
+    if (n == 0) {
+        ZK_CUDA(cudaMemsetAsync(result, 0, sizeof(double), st));
+        return ZK_OK;
+    }
+    if (!comm) return launch_vec(n, OpNrm2{(const double2*)x, result, false}, st);
+    ZK_TRY(sumsq_local(n, (const double2*)x, result, st));
+    ZK_TRY(comm_allreduce_sum(comm, result, 1, st));
+    return sqrt_inplace(result, st);
+}

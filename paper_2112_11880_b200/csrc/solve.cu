@@ -1,0 +1,845 @@
+// solve.cu — device-resident BiCGStab and CG (§4; SURVEY.md §8(a) A6-A8,
+// §8(c) O6/O7).  One iteration is a fixed schedule of fused kernels; every scalar (ρ, σ, α, ω,
+// β, γ, δ) lives in a device SolveCtx and is computed by the last block of the kernel that
+// finishes its reduction, so the loop needs no host synchronisation.  The loop itself runs as
+// a CUDA graph with a conditional WHILE node (the last kernel of the body writes the
+// condition); fallbacks: chunked graph launches or per-iteration launches with a device
+// early-exit flag.
+//
+// BiCGStab schedule F (one iteration j):
+//   K1  v = A p            ; σ = ⟨r̂,v⟩, ‖v‖²        → α = ρ/σ           (BREAKDOWN_SIGMA)
+//   K2  s = r − α v        ; ‖s‖²                    → half-step exit test
+//   K3  t = A s            ; ⟨t,s⟩, ⟨t,t⟩ = τ        → ω = ⟨t,s⟩/τ       (BREAKDOWN_OMEGA)
+//   K4  x += αp + ωs ; r = s − ωt ; ‖r‖², ρ' = ⟨r̂,r⟩ → hist[j], tests, β = (ρ'/ρ)(α/ω)
+//   K5  p = r + β(p − ωv)                             (writes the WHILE condition)
+// CG: K1 q = A p ; δ = ⟨p,q⟩ → α = γ/Re δ (NOT_HPD) ; K2 x += αp ; r −= αq ; γ' → hist, β ;
+//     K3 p = r + βp.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "spmv.cuh"
+#include "zk_host.h"
+
+namespace zk {
+
+enum { ST_ZERO_RHS = 7 };  // internal outcome → ZK_ERR_ZERO_RHS at the ABI
+
+struct SolveCtx {
+    // vectors (device)
+    double2* x;
+    const double2* b;
+    double2 *r, *rh, *p, *v, *s, *t, *q;
+    double* hist;
+    double* partials;       // [kMaxRed][kMaxGrid]
+    unsigned int* tickets;  // [8]
+    CsrDev A;
+    // scalars
+    double2 rho, alpha, omega, beta;
+    double nb, nrh, rnorm, gamma, alpha_cg, beta_cg;
+    double tol;
+    int maxit;
+    int j;       // iteration being executed (1-based)
+    int done;    // loop finished (any outcome)
+    int half;    // BiCGStab half-step exit pending (K4 applies x += αp)
+    int status;  // ZK_CONVERGED ... / ST_ZERO_RHS
+    int iters;
+    double true_relres;
+    unsigned long long cond;  // cudaGraphConditionalHandle of the WHILE node
+    int use_cond;
+    int dist;                 // multi-GPU: last blocks publish red[] for an NCCL allreduce
+    double red[kMaxRed];
+    int bodies;               // loop bodies executed (counts launches for zk_solve_info)
+    // in-loop kernel timers (device global timer): per class, min block start of the running
+    // launch, summed durations and launch counts (zk_solve_info.kernel_ms)
+    unsigned long long t0[4];
+    unsigned long long tsum[4];
+    int tcnt[4];
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void set_cond(SolveCtx* c) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        c->bodies += 1;
+        if (c->use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)c->cond, c->done ? 0u : 1u);
+    }
+}
+
+// ------------------------------------------------------------------ scalar steps (one thread)
+// Each follows oracle O6/O7 line by line (same tests, same order, same complex division).
+__device__ void fin_init_bicg(SolveCtx* c, const double* tot) {  // tot = {‖b‖², ‖r0‖²}
+    c->iters = 0;
+    c->nb = sqrt(tot[0]);
+    if (c->nb == 0.0) { c->status = ST_ZERO_RHS; c->done = 1; return; }
+    c->rnorm = sqrt(tot[1]);
+    c->hist[0] = c->rnorm / c->nb;
+    if (!isfinite(c->hist[0])) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (c->hist[0] <= c->tol) { c->status = ZK_CONVERGED; c->done = 1; return; }
+    c->nrh = c->rnorm;                           // r̂ = r0
+    c->rho = make_double2(tot[1], 0.0);          // ρ1 = ⟨r̂, r0⟩ = ‖r0‖²
+    c->alpha = c->omega = make_double2(1.0, 0.0);
+    if (cabs_(c->rho) <= 1e-30 * c->nrh * c->rnorm) { c->status = ZK_BREAKDOWN_RHO; c->done = 1; return; }
+    c->j = 1;
+}
+__device__ void fin_k1_bicg(SolveCtx* c, const double* tot) {  // {Re σ, Im σ, ‖v‖²}
+    const double2 sigma = make_double2(tot[0], tot[1]);
+    const double vnorm = sqrt(tot[2]);
+    if (!cfinite(sigma)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (cabs_(sigma) <= 1e-30 * c->nrh * vnorm) { c->status = ZK_BREAKDOWN_SIGMA; c->done = 1; return; }
+    c->alpha = cdiv(c->rho, sigma);
+}
+__device__ void fin_k2_bicg(SolveCtx* c, const double* tot) {  // {‖s‖²}
+    const double snorm = sqrt(tot[0]);
+    if (!isfinite(snorm)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (snorm / c->nb <= c->tol) {               // half-step exit (L6): K4 applies x += αp
+        c->hist[c->j] = snorm / c->nb;
+        c->iters = c->j;
+        c->status = ZK_CONVERGED;
+        c->half = 1;
+        c->done = 1;
+    }
+}
+__device__ void fin_k3_bicg(SolveCtx* c, const double* tot) {  // {Re⟨t,s⟩, Im⟨t,s⟩, τ}
+    const double tau = tot[2];
+    if (!isfinite(tau)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (tau == 0.0) { c->status = ZK_BREAKDOWN_OMEGA; c->done = 1; return; }
+    c->omega = make_double2(tot[0] / tau, tot[1] / tau);
+}
+__device__ void fin_k4_bicg(SolveCtx* c, const double* tot) {  // {‖r‖², Re ρ', Im ρ'}
+    const int j = c->j;
+    c->rnorm = sqrt(tot[0]);
+    c->hist[j] = c->rnorm / c->nb;
+    c->iters = j;
+    if (!isfinite(c->hist[j]) || !cfinite(c->omega)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (c->hist[j] <= c->tol) { c->status = ZK_CONVERGED; c->done = 1; return; }
+    if (cabs_(c->omega) <= 1e-30) { c->status = ZK_BREAKDOWN_OMEGA; c->done = 1; return; }
+    if (j >= c->maxit) { c->status = ZK_MAXIT; c->done = 1; return; }
+    // start of iteration j+1 of O6: ρ = ⟨r̂, r⟩, breakdown test, β = (ρ/ρ_prev)(α/ω)
+    const double2 rho = make_double2(tot[1], tot[2]);
+    if (!cfinite(rho)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (cabs_(rho) <= 1e-30 * c->nrh * c->rnorm) { c->status = ZK_BREAKDOWN_RHO; c->done = 1; return; }
+    c->beta = cmul(cdiv(rho, c->rho), cdiv(c->alpha, c->omega));
+    c->rho = rho;
+    c->j = j + 1;
+}
+__device__ void fin_init_cg(SolveCtx* c, const double* tot) {  // {‖b‖², ‖r0‖²}
+    c->iters = 0;
+    c->nb = sqrt(tot[0]);
+    if (c->nb == 0.0) { c->status = ST_ZERO_RHS; c->done = 1; return; }
+    c->gamma = tot[1];
+    c->hist[0] = sqrt(c->gamma) / c->nb;
+    if (!isfinite(c->hist[0])) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (c->hist[0] <= c->tol) { c->status = ZK_CONVERGED; c->done = 1; return; }
+    c->j = 1;
+}
+__device__ void fin_k1_cg(SolveCtx* c, const double* tot) {  // {Re δ, Im δ}
+    const double2 delta = make_double2(tot[0], tot[1]);
+    if (!cfinite(delta)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (delta.x <= 0.0) { c->status = ZK_NOT_HPD; c->done = 1; return; }
+    c->alpha_cg = c->gamma / delta.x;
+}
+__device__ void fin_k2_cg(SolveCtx* c, const double* tot) {  // {γ'}
+    const int j = c->j;
+    const double g = tot[0];
+    c->hist[j] = sqrt(g) / c->nb;
+    c->iters = j;
+    if (!isfinite(c->hist[j])) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (c->hist[j] <= c->tol) { c->status = ZK_CONVERGED; c->done = 1; return; }
+    if (j >= c->maxit) { c->status = ZK_MAXIT; c->done = 1; return; }
+    c->beta_cg = g / c->gamma;
+    c->gamma = g;
+    c->j = j + 1;
+}
+__device__ void fin_true(SolveCtx* c, const double* tot) {  // {‖b − Ax‖²}
+    c->true_relres = c->nb > 0.0 ? sqrt(tot[0]) / c->nb : NAN;
+}
+
+enum Stage { S_INIT_BICG, S_K1_BICG, S_K2_BICG, S_K3_BICG, S_K4_BICG, S_INIT_CG, S_K1_CG, S_K2_CG, S_TRUE };
+
+// timer class of a stage: 0 SpMV in the loop, 1 fused vector kernels, 2 init, 3 true residual
+__host__ __device__ constexpr int timer_of(int S) {
+    return (S == S_K1_BICG || S == S_K3_BICG || S == S_K1_CG) ? 0
+           : (S == S_K2_BICG || S == S_K4_BICG || S == S_K2_CG) ? 1
+           : (S == S_TRUE) ? 3 : 2;
+}
+template <int S>
+__device__ __forceinline__ void stamp_start(SolveCtx* c) {
+    if (threadIdx.x == 0) atomicMin(&c->t0[timer_of(S)], gtimer());
+}
+
+template <int S>
+__device__ __forceinline__ void finish_stage(SolveCtx* c, const double* tot) {
+    if (S == S_INIT_BICG) fin_init_bicg(c, tot);
+    if (S == S_K1_BICG) fin_k1_bicg(c, tot);
+    if (S == S_K2_BICG) fin_k2_bicg(c, tot);
+    if (S == S_K3_BICG) fin_k3_bicg(c, tot);
+    if (S == S_K4_BICG) fin_k4_bicg(c, tot);
+    if (S == S_INIT_CG) fin_init_cg(c, tot);
+    if (S == S_K1_CG) fin_k1_cg(c, tot);
+    if (S == S_K2_CG) fin_k2_cg(c, tot);
+    if (S == S_TRUE) fin_true(c, tot);
+}
+
+// grid reduction of K values, then (single GPU) the stage's scalar step in the last block, or
+// (multi-GPU) publish the local sums in c->red for the allreduce + fin_kernel.
+template <int S, int K>
+__device__ __forceinline__ void reduce_finish(SolveCtx* c, double (&acc)[K]) {
+    double tot[K];
+    if (grid_sum<K>(acc, c->partials, c->tickets + S, tot) && threadIdx.x == 0) {
+        constexpr int T = timer_of(S);
+        const unsigned long long st = atomicExch(&c->t0[T], ~0ull);
+        c->tsum[T] += gtimer() - st;
+        c->tcnt[T] += 1;
+        if (c->dist) {
+#pragma unroll
+            for (int k = 0; k < K; k++) c->red[k] = tot[k];
+        } else {
+            finish_stage<S>(c, tot);
+        }
+    }
+}
+
+template <int S>
+__global__ void fin_kernel(SolveCtx* c) {
+    if (S == S_K4_BICG && c->half) return;
+    double tot[kMaxRed];
+    for (int k = 0; k < kMaxRed; k++) tot[k] = c->red[k];
+    finish_stage<S>(c, tot);
+}
+
+// ------------------------------------------------------------------ epilogues and vector ops
+template <int S>
+struct EpiInit {  // r = b − A x0 ; x = x0 ; r̂ = p = r ; {‖b‖², ‖r‖²}
+    static constexpr int K = 2;
+    SolveCtx* c;
+    const double2* x0;
+    bool bicg;
+    __device__ void row(int64_t i, double2 y, double (&acc)[2]) {
+        const double2 bi = c->b[i];
+        const double2 r = csub(bi, y);
+        c->r[i] = r;
+        c->p[i] = r;
+        if (bicg) c->rh[i] = r;
+        if (c->x != x0) c->x[i] = x0[i];
+        acc[0] += cabs2(bi);
+        acc[1] += cabs2(r);
+    }
+    __device__ void finish(double (&acc)[2]) { reduce_finish<S, 2>(c, acc); }
+};
+
+struct EpiTrue {  // {‖b − A x‖²}
+    static constexpr int K = 1;
+    SolveCtx* c;
+    __device__ void row(int64_t i, double2 y, double (&acc)[1]) { acc[0] += cabs2(csub(c->b[i], y)); }
+    __device__ void finish(double (&acc)[1]) { reduce_finish<S_TRUE, 1>(c, acc); }
+};
+
+struct EpiK1Bicg {  // v = A p ; {σ = ⟨r̂, v⟩, ‖v‖²}
+    static constexpr int K = 3;
+    SolveCtx* c;
+    __device__ void row(int64_t i, double2 y, double (&acc)[3]) {
+        c->v[i] = y;
+        const double2 rh = ld_stream(c->rh + i);
+        acc[0] = fma(rh.x, y.x, fma(rh.y, y.y, acc[0]));
+        acc[1] = fma(rh.x, y.y, fma(-rh.y, y.x, acc[1]));
+        acc[2] += cabs2(y);
+    }
+    __device__ void finish(double (&acc)[3]) { reduce_finish<S_K1_BICG, 3>(c, acc); }
+};
+
+struct EpiK3Bicg {  // t = A s ; {⟨t, s⟩, ⟨t, t⟩}
+    static constexpr int K = 3;
+    SolveCtx* c;
+    __device__ void row(int64_t i, double2 y, double (&acc)[3]) {
+        c->t[i] = y;
+        const double2 s = ld_gather(c->s + i);
+        acc[0] = fma(y.x, s.x, fma(y.y, s.y, acc[0]));
+        acc[1] = fma(y.x, s.y, fma(-y.y, s.x, acc[1]));
+        acc[2] += cabs2(y);
+    }
+    __device__ void finish(double (&acc)[3]) { reduce_finish<S_K3_BICG, 3>(c, acc); }
+};
+
+struct EpiK1Cg {  // q = A p ; {δ = ⟨p, q⟩}
+    static constexpr int K = 2;
+    SolveCtx* c;
+    __device__ void row(int64_t i, double2 y, double (&acc)[2]) {
+        c->q[i] = y;
+        const double2 p = ld_gather(c->p + i);
+        acc[0] = fma(p.x, y.x, fma(p.y, y.y, acc[0]));
+        acc[1] = fma(p.x, y.y, fma(-p.y, y.x, acc[1]));
+    }
+    __device__ void finish(double (&acc)[2]) { reduce_finish<S_K1_CG, 2>(c, acc); }
+};
+
+struct OpInitZero {  // x0 = 0: x = 0 ; r = r̂ = p = b ; {‖b‖², ‖r‖²}
+    static constexpr int K = 2;
+    struct In { double2 b; };
+    SolveCtx* c;
+    bool bicg;
+    int stage;
+    __device__ In load(int64_t i) const { return {ld_stream(c->b + i)}; }
+    __device__ void apply(int64_t i, const In& v, double (&acc)[2]) const {
+        c->x[i] = make_double2(0.0, 0.0);
+        c->r[i] = v.b;
+        c->p[i] = v.b;
+        if (bicg) c->rh[i] = v.b;
+        const double bb = cabs2(v.b);
+        acc[0] += bb;
+        acc[1] += bb;
+    }
+    __device__ void finish(double (&acc)[2]) const {
+        if (bicg) reduce_finish<S_INIT_BICG, 2>(c, acc);
+        else reduce_finish<S_INIT_CG, 2>(c, acc);
+    }
+};
+
+struct OpK2Bicg {  // s = r − α v ; {‖s‖²}
+    static constexpr int K = 1;
+    struct In { double2 r, v; };
+    SolveCtx* c;
+    double2 alpha;
+    __device__ In load(int64_t i) const { return {ld_stream(c->r + i), ld_stream(c->v + i)}; }
+    __device__ void apply(int64_t i, const In& in, double (&acc)[1]) const {
+        double2 s = in.r;
+        s.x = fma(-alpha.x, in.v.x, fma(alpha.y, in.v.y, s.x));
+        s.y = fma(-alpha.x, in.v.y, fma(-alpha.y, in.v.x, s.y));
+        c->s[i] = s;
+        acc[0] += cabs2(s);
+    }
+    __device__ void finish(double (&acc)[1]) const { reduce_finish<S_K2_BICG, 1>(c, acc); }
+};
+
+struct OpK4Bicg {  // x += αp + ωs ; r = s − ωt ; {‖r‖², ⟨r̂, r⟩}   (half: x += αp only)
+    static constexpr int K = 3;
+    struct In { double2 x, p, s, t, rh; };
+    SolveCtx* c;
+    double2 alpha, omega;
+    bool half;
+    __device__ In load(int64_t i) const {
+        In v;
+        v.x = ld_stream_rw(c->x + i);
+        v.p = ld_stream(c->p + i);
+        if (!half) {
+            v.s = ld_stream(c->s + i);
+            v.t = ld_stream(c->t + i);
+            v.rh = ld_stream(c->rh + i);
+        }
+        return v;
+    }
+    __device__ void apply(int64_t i, const In& in, double (&acc)[3]) const {
+        double2 x = in.x;
+        cfma(x, alpha, in.p);
+        if (half) {
+            c->x[i] = x;
+            return;
+        }
+        cfma(x, omega, in.s);
+        c->x[i] = x;
+        double2 r = in.s;
+        r.x = fma(-omega.x, in.t.x, fma(omega.y, in.t.y, r.x));
+        r.y = fma(-omega.x, in.t.y, fma(-omega.y, in.t.x, r.y));
+        c->r[i] = r;
+        acc[0] += cabs2(r);
+        acc[1] = fma(in.rh.x, r.x, fma(in.rh.y, r.y, acc[1]));
+        acc[2] = fma(in.rh.x, r.y, fma(-in.rh.y, r.x, acc[2]));
+    }
+    __device__ void finish(double (&acc)[3]) const {
+        if (half) return;  // no reduction on the half-step exit; K5 clears the flag
+        reduce_finish<S_K4_BICG, 3>(c, acc);
+    }
+};
+
+struct OpK5Bicg {  // p = r + β(p − ω v)
+    static constexpr int K = 0;
+    struct In { double2 r, p, v; };
+    SolveCtx* c;
+    double2 beta, omega;
+    __device__ In load(int64_t i) const { return {ld_stream(c->r + i), ld_stream_rw(c->p + i), ld_stream(c->v + i)}; }
+    __device__ void apply(int64_t i, const In& in, double (&)[1]) const {
+        double2 d = in.p;  // p − ω v
+        d.x = fma(-omega.x, in.v.x, fma(omega.y, in.v.y, d.x));
+        d.y = fma(-omega.x, in.v.y, fma(-omega.y, in.v.x, d.y));
+        double2 p = in.r;
+        cfma(p, beta, d);
+        c->p[i] = p;
+    }
+    __device__ void finish(double (&)[1]) const {}
+};
+
+struct OpK2Cg {  // x += α p ; r −= α q ; {‖r‖²}
+    static constexpr int K = 1;
+    struct In { double2 x, p, r, q; };
+    SolveCtx* c;
+    double alpha;
+    __device__ In load(int64_t i) const {
+        return {ld_stream_rw(c->x + i), ld_stream(c->p + i), ld_stream_rw(c->r + i), ld_stream(c->q + i)};
+    }
+    __device__ void apply(int64_t i, const In& in, double (&acc)[1]) const {
+        c->x[i] = make_double2(fma(alpha, in.p.x, in.x.x), fma(alpha, in.p.y, in.x.y));
+        const double2 r = make_double2(fma(-alpha, in.q.x, in.r.x), fma(-alpha, in.q.y, in.r.y));
+        c->r[i] = r;
+        acc[0] += cabs2(r);
+    }
+    __device__ void finish(double (&acc)[1]) const { reduce_finish<S_K2_CG, 1>(c, acc); }
+};
+
+struct OpK3Cg {  // p = r + β p
+    static constexpr int K = 0;
+    struct In { double2 r, p; };
+    SolveCtx* c;
+    double beta;
+    __device__ In load(int64_t i) const { return {ld_stream(c->r + i), ld_stream_rw(c->p + i)}; }
+    __device__ void apply(int64_t i, const In& in, double (&)[1]) const {
+        c->p[i] = make_double2(fma(beta, in.p.x, in.r.x), fma(beta, in.p.y, in.r.y));
+    }
+    __device__ void finish(double (&)[1]) const {}
+};
+
+// ------------------------------------------------------------------ kernels
+template <int W, int S>
+__global__ void __launch_bounds__(kBlock) k_init_x0(SolveCtx* c, const double2* __restrict__ xg, int bicg) {
+    stamp_start<S>(c);
+    EpiInit<S> e{c, xg, bicg != 0};
+    spmv_body<W>(c->A, xg, e);
+}
+__global__ void __launch_bounds__(kBlock) k_init_zero(SolveCtx* c, int bicg) {
+    stamp_start<S_INIT_BICG>(c);
+    OpInitZero op{c, bicg != 0, 0};
+    vec_body(c->A.n_rows, op);
+}
+template <int W>
+__global__ void __launch_bounds__(kBlock) k_true(SolveCtx* c, const double2* __restrict__ xg) {
+    if (c->status == ST_ZERO_RHS) return;
+    stamp_start<S_TRUE>(c);
+    EpiTrue e{c};
+    spmv_body<W>(c->A, xg, e);
+}
+template <int W>
+__global__ void __launch_bounds__(kBlock) k1_bicg(SolveCtx* c) {
+    if (c->done) return;
+    stamp_start<S_K1_BICG>(c);
+    EpiK1Bicg e{c};
+    spmv_body<W>(c->A, c->p, e);
+}
+__global__ void __launch_bounds__(kBlock) k2_bicg(SolveCtx* c) {
+    if (c->done) return;
+    stamp_start<S_K2_BICG>(c);
+    OpK2Bicg op{c, c->alpha};
+    vec_body(c->A.n_rows, op);
+}
+template <int W>
+__global__ void __launch_bounds__(kBlock) k3_bicg(SolveCtx* c) {
+    if (c->done) return;
+    stamp_start<S_K3_BICG>(c);
+    EpiK3Bicg e{c};
+    spmv_body<W>(c->A, c->s, e);
+}
+__global__ void __launch_bounds__(kBlock) k4_bicg(SolveCtx* c) {
+    const bool half = c->half != 0;
+    if (c->done && !half) return;
+    if (!half) stamp_start<S_K4_BICG>(c);
+    OpK4Bicg op{c, c->alpha, c->omega, half};
+    vec_body(c->A.n_rows, op);
+}
+__global__ void __launch_bounds__(kBlock) k5_bicg(SolveCtx* c) {
+    set_cond(c);
+    if (c->done) {
+        if (c->half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;  // K4 applied x += αp
+        return;
+    }
+    OpK5Bicg op{c, c->beta, c->omega};
+    vec_body(c->A.n_rows, op);
+}
+template <int W>
+__global__ void __launch_bounds__(kBlock) k1_cg(SolveCtx* c) {
+    if (c->done) return;
+    stamp_start<S_K1_CG>(c);
+    EpiK1Cg e{c};
+    spmv_body<W>(c->A, c->p, e);
+}
+__global__ void __launch_bounds__(kBlock) k2_cg(SolveCtx* c) {
+    if (c->done) return;
+    stamp_start<S_K2_CG>(c);
+    OpK2Cg op{c, c->alpha_cg};
+    vec_body(c->A.n_rows, op);
+}
+__global__ void __launch_bounds__(kBlock) k3_cg(SolveCtx* c) {
+    set_cond(c);
+    if (c->done) return;
+    OpK3Cg op{c, c->beta_cg};
+    vec_body(c->A.n_rows, op);
+}
+__global__ void k_set_ctx(SolveCtx* c, SolveCtx h) {
+    *c = h;
+    for (int i = 0; i < 16; i++) h.tickets[i] = 0u;
+}
+
+// ------------------------------------------------------------------ host side
+template <class F>
+static zk_status with_w(int W, F&& f) {
+    switch (W) {
+        case 2: return f(std::integral_constant<int, 2>{});
+        case 4: return f(std::integral_constant<int, 4>{});
+        case 8: return f(std::integral_constant<int, 8>{});
+        case 16: return f(std::integral_constant<int, 16>{});
+        default: return f(std::integral_constant<int, 32>{});
+    }
+}
+
+static int spmv_grid(const zk_csr_s* A, const void* k, int W) {
+    int cap = A->dev.num_sms * blocks_per_sm(k);
+    if (cap > kMaxGrid) cap = kMaxGrid;
+    return grid_for(A->n_rows, kBlock / W, cap);
+}
+static int vec_grid(const zk_csr_s* A, const void* k) {
+    int cap = A->dev.num_sms * blocks_per_sm(k);
+    if (cap > kMaxGrid) cap = kMaxGrid;
+    return grid_for(A->n_rows, (int64_t)kBlock * 4, cap);
+}
+
+// distributed hooks (dist.cu)
+zk_status dist_halo(const zk_csr_s* A, double2* xg, cudaStream_t s);           // fill halo slots of xg
+zk_status dist_allreduce_ctx(const zk_csr_s* A, double* red, int count, cudaStream_t s);
+
+template <int S>
+static zk_status dist_finish(const zk_csr_s* A, SolveCtx* c, int count, cudaStream_t s) {
+    ZK_TRY(dist_allreduce_ctx(A, c->red, count, s));
+    fin_kernel<S><<<1, 1, 0, s>>>(c);
+    ZK_CUDA(cudaGetLastError());
+    return ZK_OK;
+}
+
+// enqueue one iteration of `method`
+static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc, int method, cudaStream_t s) {
+    const bool dist = A->dist != nullptr;
+    return with_w(A->W, [&](auto wc) -> zk_status {
+        constexpr int W = decltype(wc)::value;
+        if (method == ZK_BICGSTAB) {
+            if (dist) ZK_TRY(dist_halo(A, hc.p, s));
+            k1_bicg<W><<<spmv_grid(A, (const void*)k1_bicg<W>, W), kBlock, 0, s>>>(dc);
+            ZK_CUDA(cudaGetLastError());
+            if (dist) ZK_TRY((dist_finish<S_K1_BICG>(A, dc, 3, s)));
+            k2_bicg<<<vec_grid(A, (const void*)k2_bicg), kBlock, 0, s>>>(dc);
+            ZK_CUDA(cudaGetLastError());
+            if (dist) ZK_TRY((dist_finish<S_K2_BICG>(A, dc, 1, s)));
+            if (dist) ZK_TRY(dist_halo(A, hc.s, s));
+            k3_bicg<W><<<spmv_grid(A, (const void*)k3_bicg<W>, W), kBlock, 0, s>>>(dc);
+            ZK_CUDA(cudaGetLastError());
+            if (dist) ZK_TRY((dist_finish<S_K3_BICG>(A, dc, 3, s)));
+            k4_bicg<<<vec_grid(A, (const void*)k4_bicg), kBlock, 0, s>>>(dc);
+            ZK_CUDA(cudaGetLastError());
+            if (dist) ZK_TRY((dist_finish<S_K4_BICG>(A, dc, 3, s)));
+            k5_bicg<<<vec_grid(A, (const void*)k5_bicg), kBlock, 0, s>>>(dc);
+            ZK_CUDA(cudaGetLastError());
+        } else {
+            if (dist) ZK_TRY(dist_halo(A, hc.p, s));
+            k1_cg<W><<<spmv_grid(A, (const void*)k1_cg<W>, W), kBlock, 0, s>>>(dc);
+            ZK_CUDA(cudaGetLastError());
+            if (dist) ZK_TRY((dist_finish<S_K1_CG>(A, dc, 2, s)));
+            k2_cg<<<vec_grid(A, (const void*)k2_cg), kBlock, 0, s>>>(dc);
+            ZK_CUDA(cudaGetLastError());
+            if (dist) ZK_TRY((dist_finish<S_K2_CG>(A, dc, 1, s)));
+            k3_cg<<<vec_grid(A, (const void*)k3_cg), kBlock, 0, s>>>(dc);
+            ZK_CUDA(cudaGetLastError());
+        }
+        return ZK_OK;
+    });
+}
+
+static void drop_graph(GraphCache& g) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    g = GraphCache{};
+}
+
+// WHILE-node graph: body = one iteration; condition written by the last kernel of the body.
+static zk_status build_while_graph(zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc, int method, GraphCache& g) {
+    cudaGraph_t graph = nullptr;
+    ZK_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle h;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return cuda_fail(e, "cudaGraphConditionalHandleCreate", __FILE__, __LINE__);
+    }
+    alignas(cudaGraphNodeParams) unsigned char cp_raw[sizeof(cudaGraphNodeParams)];
+    memset(cp_raw, 0, sizeof cp_raw);
+    cudaGraphNodeParams& cp = *reinterpret_cast<cudaGraphNodeParams*>(cp_raw);
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return cuda_fail(e, "cudaGraphAddNode(conditional)", __FILE__, __LINE__);
+    }
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(A->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return cuda_fail(e, "cudaStreamBeginCaptureToGraph", __FILE__, __LINE__);
+    }
+    zk_status st = enqueue_iteration(A, dc, hc, method, A->cap_stream);
+    cudaGraph_t captured = nullptr;
+    e = cudaStreamEndCapture(A->cap_stream, &captured);
+    if (st != ZK_OK || e != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return st != ZK_OK ? st : cuda_fail(e, "cudaStreamEndCapture", __FILE__, __LINE__);
+    }
+    e = cudaGraphInstantiate(&g.exec, graph, 0);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        g.exec = nullptr;
+        return cuda_fail(e, "cudaGraphInstantiate(while)", __FILE__, __LINE__);
+    }
+    g.graph = graph;
+    g.cond = (unsigned long long)h;
+    return ZK_OK;
+}
+
+constexpr int kChunk = 16;
+
+// plain graph of kChunk iterations (kernels early-exit once done)
+static zk_status build_chunk_graph(zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc, int method, GraphCache& g) {
+    ZK_CUDA(cudaStreamBeginCapture(A->cap_stream, cudaStreamCaptureModeRelaxed));
+    zk_status st = ZK_OK;
+    for (int i = 0; i < kChunk && st == ZK_OK; i++) st = enqueue_iteration(A, dc, hc, method, A->cap_stream);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(A->cap_stream, &graph);
+    if (st != ZK_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture(chunk)", __FILE__, __LINE__);
+    e = cudaGraphInstantiate(&g.exec, graph, 0);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return cuda_fail(e, "cudaGraphInstantiate(chunk)", __FILE__, __LINE__);
+    }
+    g.graph = graph;
+    return ZK_OK;
+}
+
+struct WsLayout {
+    size_t ctx, partials, tickets, hist, vec0, vec_bytes, total;
+    int nvec;
+};
+static size_t up256(size_t v) { return (v + 255) & ~(size_t)255; }
+int64_t dist_gather_len(const zk_csr_s* A);  // dist.cu: n_rows + halo slots
+
+static WsLayout ws_layout(const zk_csr_s* A, int method, int32_t maxit) {
+    WsLayout L;
+    size_t off = 0;
+    L.ctx = off;
+    off += up256(sizeof(SolveCtx));
+    L.partials = off;
+    off += up256(sizeof(double) * kMaxRed * kMaxGrid);
+    L.tickets = off;
+    off += 256;
+    L.hist = off;
+    off += up256(sizeof(double) * ((size_t)(maxit > 0 ? maxit : 0) + 1));
+    L.vec0 = off;
+    const int64_t len = A->dist ? dist_gather_len(A) : A->n_rows;
+    L.vec_bytes = up256(sizeof(double2) * (size_t)(len > 0 ? len : 1));
+    // BiCGStab: r r̂ p v s t (+ xg gather copy on >1 GPU) ; CG: r p q (+ xg)
+    L.nvec = (method == ZK_BICGSTAB ? 6 : 3) + (A->dist ? 1 : 0);
+    off += L.vec_bytes * L.nvec;
+    L.total = off;
+    return L;
+}
+
+}  // namespace zk
+
+using namespace zk;
+
+extern "C" size_t zk_solve_workspace_size(zk_csr A, int32_t method, int32_t maxit) {
+    if (!A || (method != ZK_BICGSTAB && method != ZK_CG)) return 0;
+    return ws_layout(A, method, maxit).total;
+}
+
+extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double tol, int32_t maxit, int32_t method,
+                              zk_z* x, int32_t* iters, double* resid_hist, zk_solve_info* info, void* workspace,
+                              size_t ws_bytes, zk_stream stream) {
+    if (!A || !b || !x || !iters || !resid_hist || !workspace) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
+    if (method != ZK_BICGSTAB && method != ZK_CG) return fail(ZK_ERR_INVALID_VALUE, "unknown method");
+    if (!(tol > 0.0)) return fail(ZK_ERR_INVALID_VALUE, "tol must be > 0");
+    if (maxit < 1) return fail(ZK_ERR_INVALID_VALUE, "maxit must be >= 1");
+    if (A->n_cols != A->n_global) return fail(ZK_ERR_DIM, "solve needs a square matrix");
+    if ((const void*)b == (const void*)x) return fail(ZK_ERR_ALIAS, "b aliases x");
+    if (((uintptr_t)workspace & 255u) != 0) return fail(ZK_ERR_INVALID_VALUE, "workspace must be 256-B aligned");
+    const WsLayout L = ws_layout(A, method, maxit);
+    if (ws_bytes < L.total) return fail(ZK_ERR_INVALID_VALUE, "workspace too small");
+    if (A->n_rows == 0 && !A->dist) return fail(ZK_ERR_ZERO_RHS, "empty system (||b|| = 0)");
+    cudaStream_t s = (cudaStream_t)stream;
+    char* ws = (char*)workspace;
+
+    SolveCtx* dc = (SolveCtx*)(ws + L.ctx);
+    SolveCtx hc;
+    memset(&hc, 0, sizeof hc);
+    hc.x = (double2*)x;
+    hc.b = (const double2*)b;
+    hc.partials = (double*)(ws + L.partials);
+    hc.tickets = (unsigned int*)(ws + L.tickets);
+    hc.hist = (double*)(ws + L.hist);
+    double2* vec[8];
+    for (int i = 0; i < L.nvec; i++) vec[i] = (double2*)(ws + L.vec0 + L.vec_bytes * i);
+    if (method == ZK_BICGSTAB) {
+        hc.r = vec[0]; hc.rh = vec[1]; hc.p = vec[2]; hc.v = vec[3]; hc.s = vec[4]; hc.t = vec[5];
+    } else {
+        hc.r = vec[0]; hc.p = vec[1]; hc.q = vec[2];
+    }
+    double2* xg = A->dist ? vec[L.nvec - 1] : nullptr;  // gather copy of x0 / x with halo slots
+    hc.A = CsrDev{A->row_ptr, A->col, A->val, A->n_rows};
+    hc.tol = tol;
+    hc.maxit = maxit;
+    hc.status = ZK_MAXIT;
+    hc.true_relres = NAN;
+    hc.dist = A->dist ? 1 : 0;
+    for (int i = 0; i < 4; i++) hc.t0[i] = ~0ull;
+
+    // ---- loop mode: 1 = WHILE graph (default on one GPU), 2 = chunked graphs, 3 = direct launches
+    int mode = A->dist ? 3 : 1;
+    if (const char* e = getenv("ZK_LOOP_MODE")) {
+        int m = atoi(e);
+        if (m >= 1 && m <= 3) mode = m;
+    }
+    if (A->dist && mode == 1) mode = 3;  // NCCL inside WHILE bodies is not used
+    GraphCache& gc = A->graph[method];
+    if (mode <= 2 && (gc.ws != workspace || gc.mode != mode || gc.method != method || !gc.exec)) {
+        drop_graph(gc);
+        zk_status st = mode == 1 ? build_while_graph(A, dc, hc, method, gc) : build_chunk_graph(A, dc, hc, method, gc);
+        if (st != ZK_OK && mode == 1) {  // conditional nodes unavailable: fall back to chunked graphs
+            drop_graph(gc);
+            mode = 2;
+            st = build_chunk_graph(A, dc, hc, method, gc);
+        }
+        if (st != ZK_OK) {
+            drop_graph(gc);
+            mode = 3;
+        } else {
+            gc.ws = workspace;
+            gc.mode = mode;
+            gc.method = method;
+        }
+    }
+    hc.use_cond = mode == 1 ? 1 : 0;
+    hc.cond = mode == 1 ? gc.cond : 0ull;
+
+    cudaEvent_t ev0, ev1;
+    ZK_CUDA(cudaEventCreate(&ev0));
+    ZK_CUDA(cudaEventCreate(&ev1));
+    ZK_CUDA(cudaEventRecord(ev0, s));
+    int64_t n_spmv = 0;
+
+    // ---- init: context, r0 = b − A x0 (or b), ‖b‖, hist[0]
+    k_set_ctx<<<1, 1, 0, s>>>(dc, hc);
+    ZK_CUDA(cudaGetLastError());
+    const bool bicg = method == ZK_BICGSTAB;
+    if (x0) {
+        const double2* g0 = (const double2*)x0;
+        if (A->dist) {
+            ZK_CUDA(cudaMemcpyAsync(xg, x0, sizeof(double2) * A->n_rows, cudaMemcpyDeviceToDevice, s));
+            ZK_TRY(dist_halo(A, xg, s));
+            g0 = xg;
+        }
+        ZK_TRY(with_w(A->W, [&](auto wc) -> zk_status {
+            constexpr int W = decltype(wc)::value;
+            if (bicg) {
+                auto k = k_init_x0<W, S_INIT_BICG>;
+                k<<<spmv_grid(A, (const void*)k, W), kBlock, 0, s>>>(dc, g0, 1);
+            } else {
+                auto k = k_init_x0<W, S_INIT_CG>;
+                k<<<spmv_grid(A, (const void*)k, W), kBlock, 0, s>>>(dc, g0, 0);
+            }
+            ZK_CUDA(cudaGetLastError());
+            return ZK_OK;
+        }));
+        n_spmv++;
+    } else {
+        k_init_zero<<<vec_grid(A, (const void*)k_init_zero), kBlock, 0, s>>>(dc, bicg ? 1 : 0);
+        ZK_CUDA(cudaGetLastError());
+    }
+    if (A->dist) ZK_TRY(bicg ? dist_finish<S_INIT_BICG>(A, dc, 2, s) : dist_finish<S_INIT_CG>(A, dc, 2, s));
+
+    // ---- the loop
+    SolveCtx* hdone = nullptr;  // pinned copy of the ctx for the chunked modes
+    if (mode == 1) {
+        ZK_CUDA(cudaGraphLaunch(gc.exec, s));
+    } else {
+        ZK_CUDA(cudaMallocHost(&hdone, sizeof(SolveCtx)));
+        int launched = 0;
+        const int chunk = mode == 2 ? kChunk : 4;
+        for (;;) {
+            if (mode == 2) {
+                cudaError_t e = cudaGraphLaunch(gc.exec, s);
+                if (e != cudaSuccess) { cudaFreeHost(hdone); return cuda_fail(e, "cudaGraphLaunch", __FILE__, __LINE__); }
+            } else {
+                for (int i = 0; i < chunk; i++) {
+                    zk_status st = enqueue_iteration(A, dc, hc, method, s);
+                    if (st != ZK_OK) { cudaFreeHost(hdone); return st; }
+                }
+            }
+            launched += chunk;
+            cudaError_t e = cudaMemcpyAsync(hdone, dc, sizeof(SolveCtx), cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) { cudaFreeHost(hdone); return cuda_fail(e, "loop poll", __FILE__, __LINE__); }
+            if (hdone->done || launched > maxit + 1) break;
+        }
+    }
+
+    // ---- exit: true relative residual ‖b − A x‖/‖b‖ (one more SpMV)
+    const double2* gx = (const double2*)x;
+    if (A->dist) {
+        ZK_CUDA(cudaMemcpyAsync(xg, x, sizeof(double2) * A->n_rows, cudaMemcpyDeviceToDevice, s));
+        ZK_TRY(dist_halo(A, xg, s));
+        gx = xg;
+    }
+    ZK_TRY(with_w(A->W, [&](auto wc) -> zk_status {
+        constexpr int W = decltype(wc)::value;
+        k_true<W><<<spmv_grid(A, (const void*)k_true<W>, W), kBlock, 0, s>>>(dc, gx);
+        ZK_CUDA(cudaGetLastError());
+        return ZK_OK;
+    }));
+    if (A->dist) ZK_TRY(dist_finish<S_TRUE>(A, dc, 1, s));
+    ZK_CUDA(cudaEventRecord(ev1, s));
+
+    SolveCtx out;
+    ZK_CUDA(cudaMemcpyAsync(&out, dc, sizeof(SolveCtx), cudaMemcpyDeviceToHost, s));
+    ZK_CUDA(cudaMemcpyAsync(resid_hist, hc.hist, sizeof(double) * ((size_t)maxit + 1), cudaMemcpyDeviceToHost, s));
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (hdone) cudaFreeHost(hdone);
+    if (e != cudaSuccess) return cuda_fail(e, "zk_solve", __FILE__, __LINE__);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+
+    *iters = out.iters;
+    const int passes = out.iters;
+    n_spmv += (int64_t)passes * (method == ZK_BICGSTAB ? 2 : 1) + 1;
+    if (info) {
+        info->status = out.status == ST_ZERO_RHS ? ZK_CONVERGED : out.status;
+        info->iters = out.iters;
+        info->true_relres = out.true_relres;
+        info->n_spmv = n_spmv;
+        info->solve_ms = ms;
+        info->loop_mode = mode;
+        const int per_body = method == ZK_BICGSTAB ? 5 : 3;
+        const int fins = A->dist ? (method == ZK_BICGSTAB ? 4 : 2) : 0;  // dist: 1-thread finish kernels
+        info->gpu_launches = 3 + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);
+        for (int i = 0; i < 4; i++) {
+            info->kernel_ms[i] = out.tsum[i] * 1e-6;
+            info->kernel_launches[i] = out.tcnt[i];
+        }
+    }
+    if (out.status == ST_ZERO_RHS) return fail(ZK_ERR_ZERO_RHS, "||b|| = 0 (S:361)");
+    return ZK_OK;
+}

@@ -1,0 +1,103 @@
+// spmv.cuh — the ZSpMV body (§3) and the BLAS-1 loop body,
+// both as __device__ templates so the solver kernels can fuse their epilogues into them.
+//
+// ZSpMV mapping: a sub-warp of W lanes per row, W chosen at create from the
+// mean row length (W = 8 for the 27-point FE rows).  A block of 256 threads owns 256/W
+// consecutive rows per step and walks its tiles grid-stride (a fixed static schedule, so the
+// fused reductions are deterministic).  Each lane issues up to 4 independent streaming loads
+// of (value, column) per chunk of 4W nonzeros before touching x, then the 4 gathers of x
+// (read-only path; x stays L1/L2-resident across neighbouring rows), then 4 complex FMAs; the
+// W partial sums are combined with xor-shuffles.  No tensor cores: this is not a contraction
+// (8 flops per 20+ bytes).
+#pragma once
+#include "zk_internal.cuh"
+
+namespace zk {
+
+// Epilogue concept:
+//   static constexpr int K;                         // doubles reduced over the grid (0..4)
+//   __device__ void row(int64_t i, double2 y, double (&acc)[K>0?K:1]);   // called once per row
+//   __device__ void finish(double (&acc)[K>0?K:1]); // called by every thread at the end
+template <int W, class Epi>
+__device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
+    static_assert(W >= 1 && W <= 32 && (W & (W - 1)) == 0, "W must be a power of two <= 32");
+    constexpr int RPB = kBlock / W;  // rows per block step
+    constexpr int U = 4;             // nonzeros per lane per chunk
+    constexpr int KA = Epi::K > 0 ? Epi::K : 1;
+    double acc[KA];
+#pragma unroll
+    for (int k = 0; k < KA; k++) acc[k] = 0.0;
+
+    const int sub = threadIdx.x & (W - 1);
+    const int grp = threadIdx.x / W;
+    const int64_t n = A.n_rows;
+    for (int64_t tile = blockIdx.x; tile * RPB < n; tile += gridDim.x) {
+        const int64_t row = tile * RPB + grp;
+        double2 sum = make_double2(0.0, 0.0);
+        if (row < n) {
+            const int64_t rs = __ldg(A.row_ptr + row), re = __ldg(A.row_ptr + row + 1);
+            for (int64_t base = rs; base < re; base += U * W) {
+                double2 v[U];
+                int c[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int64_t p = base + u * W + sub;
+                    if (p < re) {
+                        v[u] = ld_stream(A.val + p);
+                        c[u] = ld_stream(A.col + p);
+                    } else {
+                        v[u] = make_double2(0.0, 0.0);
+                        c[u] = -1;
+                    }
+                }
+                double2 xv[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather(x + c[u]) : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int u = 0; u < U; u++) cfma(sum, v[u], xv[u]);
+            }
+        }
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) {
+            sum.x += __shfl_xor_sync(0xffffffffu, sum.x, o, W);
+            sum.y += __shfl_xor_sync(0xffffffffu, sum.y, o, W);
+        }
+        if (sub == 0 && row < n) epi.row(row, sum, acc);
+    }
+    epi.finish(acc);
+}
+
+// Grid-stride elementwise body with U elements in flight per thread.
+//   Op::K, Op::In, In load(int64_t i), void apply(int64_t i, const In&, double (&acc)[K]), finish(acc)
+template <class Op>
+__device__ __forceinline__ void vec_body(int64_t n, Op& op) {
+    constexpr int U = 4;
+    constexpr int KA = Op::K > 0 ? Op::K : 1;
+    double acc[KA];
+#pragma unroll
+    for (int k = 0; k < KA; k++) acc[k] = 0.0;
+    const int64_t step = (int64_t)gridDim.x * kBlock * U;
+    for (int64_t base = (int64_t)blockIdx.x * kBlock * U + threadIdx.x; base < n; base += step) {
+        typename Op::In in[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t i = base + u * kBlock;
+            if (i < n) in[u] = op.load(i);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t i = base + u * kBlock;
+            if (i < n) op.apply(i, in[u], acc);
+        }
+    }
+    op.finish(acc);
+}
+
+// number of blocks for a grid-stride kernel: enough to cover the work, at most `cap`
+inline int grid_for(int64_t units, int64_t per_block, int cap) {
+    int64_t g = (units + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    return (int)(g < cap ? g : cap);
+}
+
+}  // namespace zk

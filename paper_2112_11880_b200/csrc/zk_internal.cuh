@@ -1,0 +1,142 @@
+// zk_internal.cuh — device helpers shared by the libzk kernels (sm_100a only).
+// Complex numbers are double2 {x = re, y = im} (layout of zk_z / torch.complex128).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/zk.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libzk targets sm_100a (B200) only"
+#endif
+
+namespace zk {
+
+constexpr int kBlock = 256;      // threads per block for every libzk kernel
+constexpr int kWarps = kBlock / 32;
+constexpr int kMaxRed = 4;       // max doubles reduced by one kernel
+constexpr int kMaxGrid = 4096;   // max blocks of a reducing kernel (partials capacity)
+
+// ------------------------------------------------------------------ complex helpers
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// acc += a*b
+__device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
+}
+// conj(a)*b
+__device__ __forceinline__ double2 cdotc1(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
+}
+__device__ __forceinline__ double cabs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// (a+bi)/(c+di) written out as ((ac+bd) + (bc−ad)i)/(c²+d²) — same formula as the oracle (R7)
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+    double den = b.x * b.x + b.y * b.y;
+    return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
+}
+__device__ __forceinline__ double cabs_(double2 a) { return sqrt(a.x * a.x + a.y * a.y); }
+__device__ __forceinline__ bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
+
+// ------------------------------------------------------------------ loads
+// Streaming (read-once) loads: no L1 allocation.
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int ld_stream(const int* p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+// Streaming load of data this kernel also writes (coherent path, no L1 allocation).
+__device__ __forceinline__ double2 ld_stream_rw(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
+}
+// Gather through the read-only path (L1 + L2 reuse of x across neighbouring rows).
+__device__ __forceinline__ double2 ld_gather(const double2* p) { return __ldg(p); }
+// Coherent L2 load (partials written by other blocks of the same launch).
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// ------------------------------------------------------------------ reductions
+template <int K>
+__device__ __forceinline__ void warp_sum(double (&v)[K]) {
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+}
+
+// Block-wide sum of K doubles (fixed order). Result valid in thread 0. Uses `sm` (kWarps*K doubles).
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double* sm) {
+    warp_sum<K>(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) sm[k * kWarps + warp] = v[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) v[k] = lane < kWarps ? sm[k * kWarps + lane] : 0.0;
+        warp_sum<K>(v);
+    }
+}
+
+// Deterministic grid reduction with a last-block finish (the paper's "two distinct tasks",
+// P:199-200, fused into one pass).  Every block writes its partial; the block that takes the
+// last ticket sums the partials in index order (fixed tree) and returns true, with the totals
+// in `out` (valid in thread 0).  The ticket is reset by the last block, so the scratch is
+// self-cleaning.  partials: [K][gridDim.x] doubles.
+template <int K>
+__device__ __forceinline__ bool grid_sum(double (&v)[K], double* partials, unsigned int* ticket,
+                                         double (&out)[K]) {
+    __shared__ double sm[kWarps * kMaxRed];
+    __shared__ bool last;
+    block_sum<K>(v, sm);
+    const int G = gridDim.x;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) partials[k * G + blockIdx.x] = v[k];
+        __threadfence();
+        unsigned int t = atomicAdd(ticket, 1u);
+        last = (t == (unsigned)G - 1);
+    }
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+    double acc[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        acc[k] = 0.0;
+        for (int i = threadIdx.x; i < G; i += kBlock) acc[k] += ld_cg(partials + k * G + i);
+    }
+    __syncthreads();  // sm reuse
+    block_sum<K>(acc, sm);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) out[k] = acc[k];
+        *ticket = 0u;
+    }
+    return true;
+}
+
+// ------------------------------------------------------------------ CSR view
+struct CsrDev {
+    const int64_t* row_ptr;
+    const int* col;
+    const double2* val;
+    int64_t n_rows;
+};
+
+}  // namespace zk

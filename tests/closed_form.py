@@ -46,9 +46,12 @@ def sine_mode(spec, p: int, q: int, r: int) -> np.ndarray:
     """Tensor sine eigenvector v(ix,iy,iz) = sin(p jx π/(a+1)) sin(q jy π/(b+1)) sin(r jz π/(c+1))
     on the free block (zero on identity rows), as a full-length complex vector."""
     a, b, c = spec.free_dims
-    jx = np.sin(p * np.arange(1, a + 1) * math.pi / (a + 1))
-    jy = np.sin(q * np.arange(1, b + 1) * math.pi / (b + 1))
-    jz = np.sin(r * np.arange(1, c + 1) * math.pi / (c + 1))
+
+    def s(m, d):  # sin(m·j·π/(d+1)) with the integer m·j reduced mod 2(d+1) first (argument ≤ 2π)
+        k = (m * np.arange(1, d + 1, dtype=np.int64)) % (2 * (d + 1))
+        return np.sin(k * math.pi / (d + 1))
+
+    jx, jy, jz = s(p, a), s(q, b), s(r, c)
     v = np.zeros(spec.n, np.complex128)
     v[free_index(spec)] = (jz[:, None, None] * jy[None, :, None] * jx[None, None, :]).ravel()
     return v

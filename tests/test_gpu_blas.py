@@ -1,0 +1,236 @@
+"""GPU parity of ZSpMV and BLAS-1 (libzk through the C-ABI) against the CPU oracle.
+
+Tolerances (north star): SpMV and axpy elementwise relative 1e-13, read
+as |Δy_i| ≤ 1e-13·Σ_j|a_ij||x_j| (the row's absolute scale); dot and norm relative 1e-12,
+|Δ| ≤ 1e-12·‖x‖‖y‖.  Integer-exact inputs and exact scalars must match bitwise."""
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+
+import gen
+import oracle
+from paper_2112_11880_b200 import zk
+from tests import closed_form as cf
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def row_scale(m, x):
+    n = len(m["row_ptr"]) - 1
+    A = sp.csr_matrix((np.abs(m["values"]), m["col_idx"], m["row_ptr"]), shape=(n, m.get("n_cols", m["n"])))
+    return A @ np.abs(x)
+
+
+def make_csr(m, W=None, **kw):
+    old = os.environ.get("ZK_SPMV_W")
+    if W is not None:
+        os.environ["ZK_SPMV_W"] = str(W)
+    try:
+        return zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m.get("n_cols", m["n"]), **kw)
+    finally:
+        if W is not None:
+            if old is None:
+                del os.environ["ZK_SPMV_W"]
+            else:
+                os.environ["ZK_SPMV_W"] = old
+
+
+# ------------------------------------------------------------------ ZSpMV
+@pytest.mark.parametrize("W", [2, 4, 8, 16, 32])
+@pytest.mark.parametrize("alpha,beta", [(1, 0), (0.5 - 2j, 0), (1j, -0.25 + 1j)])
+def test_zcsrmv_random(W, alpha, beta):
+    """Random CSR with empty rows, 1-nnz rows and rows > 32 nnz; ragged n spanning many tiles."""
+    m = gen.random_csr(5003, seed=W, max_len=70)
+    x, y0 = gen.rand_vector(5003, 1), gen.rand_vector(5003, 2)
+    A = make_csr(m, W)
+    assert A.info["lanes_per_row"] == W
+    y = cuda(y0)
+    zk.zcsrmv(A, alpha, cuda(x), beta, y)
+    want = oracle.zcsrmv(m, x, alpha, beta, y0)
+    tol = 1e-13 * (abs(alpha) * row_scale(m, x) + abs(beta) * np.abs(y0)) + 1e-300
+    assert np.all(np.abs(y.cpu().numpy() - want) <= tol)
+
+
+@pytest.mark.parametrize("W", [2, 8, 32])
+def test_zcsrmv_integer_exact_bitwise(W):
+    m = gen.random_csr(3001, seed=11, max_len=40, integer=True)
+    x = gen.int_vector(3001, 3)
+    A = make_csr(m, W)
+    y = torch.empty(3001, dtype=torch.complex128, device=DEV)
+    zk.zcsrmv(A, 1, cuda(x), 0, y)
+    assert np.array_equal(y.cpu().numpy(), oracle.zcsrmv(m, x))
+
+
+def test_zcsrmv_beta_zero_ignores_nan_and_empty_rows():
+    m = gen.random_csr(777, seed=5)
+    x = gen.rand_vector(777, 1)
+    y = torch.full((777,), complex(np.nan, np.nan), dtype=torch.complex128, device=DEV)
+    zk.zcsrmv(make_csr(m), 1, cuda(x), 0, y)
+    got = y.cpu().numpy()
+    assert np.all(np.isfinite(got))
+    assert np.all(got[np.diff(m["row_ptr"]) == 0] == 0)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C3T"])
+def test_zcsrmv_paper_shapes(cfg):
+    m = gen.make_matrix(cfg)
+    x = gen.rand_vector(m["n"], 7)
+    A = make_csr(m)
+    y = torch.empty(m["n"], dtype=torch.complex128, device=DEV)
+    zk.zcsrmv(A, 1, cuda(x), 0, y)
+    got = y.cpu().numpy()
+    want = oracle.zcsrmv(m, x)
+    assert np.all(np.abs(got - want) <= 1e-13 * row_scale(m, x) + 1e-300)
+    ident = m["free_mask"] == 0                                  # identity rows exact (pin (3))
+    assert np.array_equal(got[ident], want[ident])
+
+
+def test_zcsrmv_c4_full_size_sampled():
+    """C4 (8M rows, 214M nnz) in the bench's launch configuration: sampled rows against the
+    oracle computed row by row, and the closed-form eigenvector identity A·v = λ·v on all rows."""
+    spec = gen.CONFIGS["C4"]
+    m = gen.make_matrix(spec)
+    n = m["n"]
+    A = zk.csr_create(cuda(m["row_ptr"]), cuda(m["col_idx"]), cuda(m["values"]), n, borrow=False)
+    x = gen.rand_vector(n, 9)
+    y = torch.empty(n, dtype=torch.complex128, device=DEV)
+    zk.zcsrmv(A, 1, cuda(x), 0, y)
+    got = y.cpu().numpy()
+    rows = np.unique(np.concatenate([np.random.default_rng(0).integers(0, n, 4000), [0, 1, n - 1, n // 2]]))
+    rp = m["row_ptr"]
+    for i in rows[:400]:
+        sub = dict(row_ptr=np.array([0, rp[i + 1] - rp[i]]), col_idx=m["col_idx"][rp[i]:rp[i + 1]],
+                   values=m["values"][rp[i]:rp[i + 1]], n=n)
+        want = oracle.zcsrmv(sub, x)[0]
+        scale = np.sum(np.abs(sub["values"]) * np.abs(x[sub["col_idx"]]))
+        assert abs(got[i] - want) <= 1e-13 * scale
+    lam = cf.box_eigs(spec, gen.ETA)
+    v = cf.sine_mode(spec, 2, 5, 199)
+    zk.zcsrmv(A, 1, cuda(v), 0, y)
+    err = np.abs(y.cpu().numpy() - lam[198, 4, 1] * v)
+    assert np.all(err <= 1e-13 * row_scale(m, v) + 1e-300)
+
+
+def test_zcsrmv_errors():
+    m = gen.random_csr(50, seed=1)
+    A = make_csr(m)
+    x = cuda(gen.rand_vector(50, 1))
+    with pytest.raises(zk.ZkError) as e:
+        zk.zcsrmv(A, 1, x, 0, x)
+    assert e.value.code == -7                                     # ZK_ERR_ALIAS
+
+
+@pytest.mark.parametrize("where", ["host", "device"])
+def test_csr_create_validation(where):
+    m = gen.random_csr(200, seed=2)
+    conv = (lambda a: a) if where == "host" else cuda
+    bad = m["col_idx"].copy()
+    r = int(np.argmax(np.diff(m["row_ptr"]) > 3))
+    p = m["row_ptr"][r]
+    bad[p], bad[p + 1] = bad[p + 1], bad[p]                      # unsorted row r
+    with pytest.raises(zk.ZkError) as e:
+        zk.csr_create(conv(m["row_ptr"]), conv(bad), conv(m["values"]), 200)
+    assert e.value.code == -2 and f"row {r}" in str(e.value)
+    bad = m["col_idx"].copy()
+    bad[5] = 200                                                  # out of range
+    with pytest.raises(zk.ZkError) as e:
+        zk.csr_create(conv(m["row_ptr"]), conv(bad), conv(m["values"]), 200)
+    assert e.value.code == -2
+    v = m["values"].copy()
+    v[3] = np.inf
+    with pytest.raises(zk.ZkError) as e:
+        zk.csr_create(conv(m["row_ptr"]), conv(m["col_idx"]), conv(v), 200)
+    assert e.value.code == -3
+    rp = m["row_ptr"].copy()
+    rp[-1] += 1
+    with pytest.raises(zk.ZkError):
+        zk.csr_create(conv(rp), conv(m["col_idx"]), conv(m["values"]), 200)
+
+
+def test_csr_borrow_and_empty():
+    m = gen.random_csr(300, seed=3)
+    rp, ci, va = cuda(m["row_ptr"]), cuda(m["col_idx"]), cuda(m["values"])
+    A = zk.csr_create(rp, ci, va, 300, borrow=True)
+    assert A.info["borrowed"] == 1
+    x = gen.rand_vector(300, 4)
+    y = torch.empty(300, dtype=torch.complex128, device=DEV)
+    zk.zcsrmv(A, 1, cuda(x), 0, y)
+    assert np.all(np.abs(y.cpu().numpy() - oracle.zcsrmv(m, x)) <= 1e-13 * row_scale(m, x) + 1e-300)
+    E = zk.csr_create(np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros(0, np.complex128), 0)
+    assert E.n_rows == 0
+
+
+# ------------------------------------------------------------------ zdotc / dznrm2
+@pytest.mark.parametrize("n", [1, 7, 1000, 1 << 20, (1 << 22) + 13])
+def test_zdotc_dznrm2_random(n):
+    x, y = gen.rand_vector(n, 1), gen.rand_vector(n, 2)
+    X, Y = cuda(x), cuda(y)
+    d = zk.zdotc(X, Y).cpu().numpy()[0]
+    ref = oracle.zdotc(x, y)
+    nx, ny = oracle.dznrm2(x), oracle.dznrm2(y)
+    assert abs(d - ref) <= 1e-12 * nx * ny
+    nr = zk.dznrm2(X).cpu().numpy()[0]
+    assert abs(nr - nx) <= 1e-12 * nx
+    # non-cancelling inputs: literally relative 1e-12 (L5)
+    xp, yp = np.abs(x.real) + 1j * np.abs(x.imag), np.abs(y.real) + 1j * np.abs(y.imag)
+    d = zk.zdotc(cuda(xp), cuda(yp)).cpu().numpy()[0]
+    ref = oracle.zdotc(xp, yp)
+    assert abs(d.real - ref.real) <= 1e-12 * abs(ref.real)
+
+
+def test_dot_norm_exact_and_deterministic():
+    one_i = cuda(np.array([1j]))
+    assert zk.zdotc(one_i, one_i).cpu().numpy()[0] == 1 + 0j       # conj first
+    assert zk.dznrm2(cuda(np.array([3 + 4j]))).cpu().numpy()[0] == 5.0
+    n = 3_000_017
+    x, y = gen.int_vector(n, 1, -90, 90), gen.int_vector(n, 2, -90, 90)
+    X, Y = cuda(x), cuda(y)
+    d = zk.zdotc(X, Y).cpu().numpy()[0]
+    assert d == oracle.zdotc(x, y, oracle.ORD_SEQ)                  # exact integer sums: bitwise
+    assert zk.dznrm2(X).cpu().numpy()[0] == oracle.dznrm2(x, oracle.ORD_SEQ)
+    # determinism: fixed grid + fixed-order last-block finish
+    r = gen.rand_vector(n, 5)
+    R = cuda(r)
+    vals = {complex(zk.zdotc(R, Y).cpu().numpy()[0]) for _ in range(5)}
+    assert len(vals) == 1
+    # conjugate symmetry and ‖x‖² = Re⟨x,x⟩
+    assert abs(zk.zdotc(Y, R).cpu().numpy()[0] - np.conj(zk.zdotc(R, Y).cpu().numpy()[0])) <= 1e-13 * n
+    e = zk.zdotc(torch.empty(0, dtype=torch.complex128, device=DEV), torch.empty(0, dtype=torch.complex128, device=DEV))
+    assert e.cpu().numpy()[0] == 0
+
+
+# ------------------------------------------------------------------ zaxpy / zscal
+@pytest.mark.parametrize("n", [1, 1023, 1 << 20, 5_000_011])
+def test_zaxpy_zscal_random(n):
+    x, y = gen.rand_vector(n, 3), gen.rand_vector(n, 4)
+    a = 0.3 - 1.7j
+    Y = cuda(y)
+    zk.zaxpy(a, cuda(x), Y)
+    want = oracle.zaxpy(a, x, y)
+    assert np.all(np.abs(Y.cpu().numpy() - want) <= 1e-13 * (abs(a) * np.abs(x) + np.abs(y)))
+    X = cuda(x)
+    zk.zscal(a, X)
+    assert np.all(np.abs(X.cpu().numpy() - oracle.zscal(a, x)) <= 1e-13 * abs(a) * np.abs(x))
+
+
+def test_zaxpy_zscal_exact_alphas():
+    x, y = gen.rand_vector(100_003, 3), gen.rand_vector(100_003, 4)
+    for a in (0, 1, -1, 1j, 0.25, -8):
+        Y = cuda(y)
+        zk.zaxpy(a, cuda(x), Y)
+        assert np.array_equal(Y.cpu().numpy(), oracle.zaxpy(a, x, y)), a
+        X = cuda(x)
+        zk.zscal(a, X)
+        assert np.array_equal(X.cpu().numpy(), oracle.zscal(a, x)), a
+    xi, yi = gen.int_vector(50_000, 5), gen.int_vector(50_000, 6)
+    Y = cuda(yi)
+    zk.zaxpy(3 - 2j, cuda(xi), Y)
+    assert np.array_equal(Y.cpu().numpy(), oracle.zaxpy(3 - 2j, xi, yi))

@@ -1,0 +1,182 @@
+"""GPU parity of the device-resident BiCGStab / CG (zk_solve) against the CPU oracle.
+
+Bars (north star):
+  * CG: iteration count within ±5 % of the oracle's.
+  * BiCGStab: count within [0.95·min, 1.05·max] of the oracle's counts under its summation
+    orders (seq, rev, block-256) — rounding order alone moves BiCGStab counts (App. B4) — and
+    the residual histories agree to 1e-10 relative over the first 12 iterations.
+  * Final solutions agree to 1e-6 relative (C1/C2); on larger shapes both sides satisfy
+    ‖x − x_exact‖/‖x_exact‖ ≤ 2κ·tol with x_exact and κ in closed form (DST-I).
+  * Outcomes (CONVERGED / MAXIT / breakdowns / NOT_HPD / ZERO_RHS) match the oracle's."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+from paper_2112_11880_b200 import zk
+from tests import closed_form as cf
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+ORDERS = (oracle.ORD_SEQ, oracle.ORD_REV, oracle.ORD_BLOCK256)
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def gpu_solve(m, b, **kw):
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+    x0 = kw.pop("x0", None)
+    r = zk.solve(A, cuda(b), None if x0 is None else cuda(x0), **kw)
+    r["x"] = r["x"].cpu().numpy()
+    return r
+
+
+def relerr(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
+def test_bicgstab_parity(cfg):
+    m = gen.make_matrix(cfg)
+    b = gen.make_rhs(m)
+    r = gpu_solve(m, b, tol=1e-8, maxit=1000, method="bicgstab")
+    refs = [oracle.bicgstab(m, b, tol=1e-8, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    assert r["status"] == "CONVERGED" and all(q["status"] == "CONVERGED" for q in refs)
+    assert 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    k = min(12, r["iters"], refs[0]["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= 1e-10
+    assert relerr(r["x"], refs[0]["x"]) <= 1e-6
+    assert r["true_relres"] <= 2e-8 and abs(r["true_relres"] - r["hist"][-1]) <= 1e-8
+    assert r["loop_mode"] == 1                          # device-resident WHILE graph
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
+def test_cg_parity_twisted_hpd(cfg):
+    mg = gen.make_matrix(cfg, eta=0.0, twist_seed=gen.SEED_TWIST)
+    b = np.exp(1j * mg["phase"]) * gen.make_rhs(mg)
+    r = gpu_solve(mg, b, tol=1e-8, method="cg")
+    ref = oracle.cg(mg, b, tol=1e-8)
+    assert r["status"] == ref["status"] == "CONVERGED"
+    assert abs(r["iters"] - ref["iters"]) <= 0.05 * ref["iters"], (r["iters"], ref["iters"])
+    k = min(12, r["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-10
+    assert relerr(r["x"], ref["x"]) <= 1e-6
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C3T"])
+def test_bicgstab_paper_largest_shapes(cfg):
+    """PAPER.md T1's largest levels: counts within the oracle's order envelope, forward error
+    within 2κ·tol of the DST-I exact solution (L12)."""
+    spec = gen.CONFIGS[cfg]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    r = gpu_solve(m, b, tol=1e-8, method="bicgstab")
+    refs = [oracle.bicgstab(m, b, tol=1e-8, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    assert 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    xe = cf.box_solve(spec, b, gen.ETA)
+    bound = 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
+    assert relerr(r["x"], xe) <= bound and relerr(refs[0]["x"], xe) <= bound
+    assert np.max(np.abs(r["hist"][:13] - refs[0]["hist"][:13]) / refs[0]["hist"][:13]) <= 1e-10
+
+
+def test_bicgstab_c4_full_size():
+    """C4 (8M rows) as bench.py runs it: closed-form forward error, true residual, and the
+    first 6 iterations' history against the oracle (a full C4 oracle solve takes minutes)."""
+    spec = gen.CONFIGS["C4"]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    A = zk.csr_create(cuda(m["row_ptr"]), cuda(m["col_idx"]), cuda(m["values"]), m["n"])
+    r = zk.solve(A, cuda(b), tol=1e-8, maxit=1000, method="bicgstab")
+    assert r["status"] == "CONVERGED"
+    x = r["x"].cpu().numpy()
+    xe = cf.box_solve(spec, b, gen.ETA)
+    assert relerr(x, xe) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
+    assert r["true_relres"] <= 2e-8
+    ref = oracle.bicgstab(m, b, tol=1e-8, maxit=6)
+    assert np.max(np.abs(r["hist"][:7] - ref["hist"][:7]) / ref["hist"][:7]) <= 1e-10
+
+
+@pytest.mark.parametrize("mode", ["1", "2", "3"])
+def test_loop_modes_bitwise_identical(mode, monkeypatch):
+    """WHILE graph, chunked graphs and direct launches run the same kernels: identical results."""
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    base = gpu_solve(m, b, tol=1e-8)
+    monkeypatch.setenv("ZK_LOOP_MODE", mode)
+    r = gpu_solve(m, b, tol=1e-8)
+    assert r["loop_mode"] == int(mode)
+    assert r["iters"] == base["iters"] and np.array_equal(r["x"], base["x"])
+    assert np.array_equal(r["hist"], base["hist"])
+
+
+def test_solve_deterministic_and_workspace_reuse():
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+    ws = zk.alloc_workspace(A, "bicgstab", 1000)
+    B = cuda(b)
+    r1 = zk.solve(A, B, workspace=ws)
+    x1 = r1["x"].cpu().numpy()
+    r2 = zk.solve(A, B, workspace=ws)
+    assert np.array_equal(x1, r2["x"].cpu().numpy()) and np.array_equal(r1["hist"], r2["hist"])
+
+
+@pytest.mark.parametrize("c", [2.0, -1.0, 1j])
+def test_bicgstab_scalar_identity(c):
+    n = 1000
+    m = dict(row_ptr=np.arange(n + 1, dtype=np.int64), col_idx=np.arange(n, dtype=np.int32),
+             values=np.full(n, c, np.complex128), n=n)
+    b = gen.rand_vector(n, 1)
+    r = gpu_solve(m, b, tol=1e-12)
+    assert r["status"] == "CONVERGED" and r["iters"] == 1         # half-step exit (L6)
+    assert np.max(np.abs(r["x"] - b / c)) <= 1e-15 * np.max(np.abs(b / c))
+
+
+def test_outcomes_match_oracle():
+    # BREAKDOWN_SIGMA on a real skew matrix
+    m = dict(row_ptr=np.array([0, 1, 2]), col_idx=np.array([1, 0], np.int32),
+             values=np.array([1, -1], np.complex128), n=2)
+    b = np.array([1, 0], np.complex128)
+    assert gpu_solve(m, b)["status"] == oracle.bicgstab(m, b)["status"] == "BREAKDOWN_SIGMA"
+    # MAXIT with the history of the first maxit iterations
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    r = gpu_solve(m, b, tol=1e-14, maxit=5)
+    ref = oracle.bicgstab(m, b, tol=1e-14, maxit=5)
+    assert r["status"] == ref["status"] == "MAXIT" and r["iters"] == 5
+    assert np.max(np.abs(r["hist"] - ref["hist"]) / ref["hist"]) <= 1e-10
+    # NOT_HPD for CG on a negative definite matrix
+    n = 64
+    neg = dict(row_ptr=np.arange(n + 1, dtype=np.int64), col_idx=np.arange(n, dtype=np.int32),
+               values=np.full(n, -2.0, np.complex128), n=n)
+    assert gpu_solve(neg, gen.rand_vector(n, 2), method="cg")["status"] == "NOT_HPD"
+    # ZERO_RHS is an error
+    with pytest.raises(zk.ZkError) as e:
+        gpu_solve(neg, np.zeros(n, np.complex128))
+    assert e.value.code == -8
+
+
+def test_x0_restart_and_alias():
+    m = gen.make_matrix("C1")
+    b = gen.make_rhs(m)
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+    B = cuda(b)
+    r = zk.solve(A, B, tol=1e-8)
+    x = r["x"]
+    r2 = zk.solve(A, B, x0=x, x=x, tol=1e-7)                       # x may alias x0
+    assert r2["status"] == "CONVERGED" and r2["iters"] == 0
+    x0 = cuda(gen.rand_vector(m["n"], 3))
+    r3 = zk.solve(A, B, x0=x0, tol=1e-8)
+    ref = oracle.bicgstab(m, b, x0=x0.cpu().numpy(), tol=1e-8)
+    assert abs(r3["iters"] - ref["iters"]) <= max(1, 0.05 * ref["iters"])
+    assert np.max(np.abs(r3["hist"][:8] - ref["hist"][:8]) / ref["hist"][:8]) <= 1e-10
+    with pytest.raises(zk.ZkError) as e:
+        zk.solve(A, B, x=B)
+    assert e.value.code == -7
