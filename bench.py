@@ -173,19 +173,37 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     zk.lib()
 
-    spec = gen.CONFIGS[a.config]
+    comm = None
+    if world > 1:
+        # row-partitioned weak scaling: a 200 x 200 x (200*N) box at the C4 spacing, rank r owns
+        # the z-slab of rows [r*8M, (r+1)*8M) (exactly C4 at N = 1); NCCL halo + allreduce
+        base = gen.CONFIGS[a.config]
+        spec = gen.BoxSpec(base.nx, base.ny, base.nz * world, base.h, base.lam, base.shell, 0)
+        uid = [zk.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = zk.Comm(uid[0], world, rank, local)
+        plane = spec.nx * spec.ny
+        row_range = (rank * base.nz * plane, (rank + 1) * base.nz * plane)
+    else:
+        spec = gen.CONFIGS[a.config]
+        row_range = None
     t_gen = time.perf_counter()
-    mat = gen.make_matrix(spec)
+    mat = gen.make_matrix(spec, row_range=row_range)
     b_h = gen.make_rhs(mat)
     t_gen = time.perf_counter() - t_gen
-    n, nnz = mat["n"], mat["nnz"]
+    n_glob = mat["n"]
+    n, nnz = len(mat["row_ptr"]) - 1, mat["nnz"]   # this rank's rows / nonzeros
 
-    # inputs resident in HBM (borrowed by the handle); validation + stats at create (setup)
-    rp = torch.from_numpy(mat["row_ptr"]).to(dev)
-    ci = torch.from_numpy(mat["col_idx"]).to(dev)
-    va = torch.from_numpy(mat["values"]).to(dev)
+    # inputs resident in HBM; validation + stats (+ halo plan on N > 1) at create (setup)
     b = torch.from_numpy(b_h).to(dev)
-    A = zk.csr_create(rp, ci, va, n, borrow=True)
+    if comm is None:
+        rp = torch.from_numpy(mat["row_ptr"]).to(dev)
+        ci = torch.from_numpy(mat["col_idx"]).to(dev)
+        va = torch.from_numpy(mat["values"]).to(dev)
+        A = zk.csr_create(rp, ci, va, n, borrow=True)
+    else:
+        A = zk.csr_create(mat["row_ptr"], mat["col_idx"], mat["values"], n_glob, comm=comm,
+                          row_begin=mat["row_begin"])
     ws = zk.alloc_workspace(A, "bicgstab", a.maxit, dev)
     x = torch.empty_like(b)
     stream = torch.cuda.current_stream()
@@ -217,8 +235,14 @@ def main():
 
     iters = results[-1]["iters"]
     assert all(r["iters"] == iters for r in results), "non-deterministic iteration count"
-    bytes_step = step_bytes(n, nnz, iters)
-    total_bytes = bytes_step * a.steps * world
+    bytes_step = step_bytes(n, nnz, iters)           # this rank's HBM bytes per step
+    if world > 1:
+        t = torch.tensor([float(bytes_step)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t)                            # units all ranks processed
+        bytes_step_all = float(t.item())
+    else:
+        bytes_step_all = float(bytes_step)
+    total_bytes = bytes_step_all * a.steps
     value = total_bytes / (ms * 1e-3) / 1e9
     ms_step = ms / a.steps
 
@@ -238,6 +262,7 @@ def main():
     vec_ms = sum(r["kernel_ms"][1] for r in results)
 
     # standalone zk_zcsrmv (β = 0) with CUDA events on the launching stream: GB/s and GFLOP/s
+    # (on N > 1 it includes the halo copy + exchange of zk_zcsrmv's distributed path)
     y = torch.empty_like(b)
     for _ in range(3):
         zk.zcsrmv(A, 1.0, b, 0.0, y, stream)
@@ -266,7 +291,10 @@ def main():
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(a.e2e_steps):
-            Ah = zk.csr_create(rp_h, ci_h, va_h, n, stream=stream)
+            if comm is None:
+                Ah = zk.csr_create(rp_h, ci_h, va_h, n, stream=stream)
+            else:
+                Ah = zk.csr_create(rp_h, ci_h, va_h, n_glob, comm=comm, row_begin=mat["row_begin"], stream=stream)
             bd = b_pin.to(dev, non_blocking=True)
             re = zk.solve(Ah, bd, None, a.tol, a.maxit, "bicgstab", workspace=ws2, stream=stream)
             x_h.copy_(re["x"], non_blocking=True)
@@ -276,13 +304,13 @@ def main():
         e_ms = f0.elapsed_time(f1) / a.e2e_steps
         h2d = 8 * (n + 1) + 4 * nnz + 16 * nnz + 16 * n
         d2h = 16 * n + 8 * (a.maxit + 1)
-        e2e = {"value": bytes_step * world / (e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+        e2e = {"value": bytes_step_all / (e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world}
         if world > 1:
             t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e["ms_per_step"] = float(t.item())
-            e2e["value"] = bytes_step * world / (e2e["ms_per_step"] * 1e-3) / 1e9
+            e2e["value"] = bytes_step_all / (e2e["ms_per_step"] * 1e-3) / 1e9
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -298,9 +326,13 @@ def main():
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
             "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic",
-            "config": {"workload": workload_name(a.config, spec), "n": n, "nnz": nnz, "method": "bicgstab",
-                       "tol": a.tol, "x0": "zero", "l2": "inputs larger than L2 (matrix 4.3 GB)",
-                       "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas"},
+            "config": {"workload": workload_name(a.config, spec) if world == 1 else
+                       f"{a.config} per rank: 27-point Q1-hex complex Helmholtz box {spec.nx}x{spec.ny}x{spec.nz} "
+                       f"(n={n_glob:,}), z-slab row blocks of {n:,} rows per GPU",
+                       "n": n_glob, "nnz_rank0": nnz, "method": "bicgstab",
+                       "tol": a.tol, "x0": "zero", "l2": "inputs larger than L2 (matrix 4.3 GB per GPU)",
+                       "parallelism": "1 GPU" if world == 1 else
+                       f"row-partitioned x{world}: NCCL halo exchange per SpMV + allreduce per reduction point"},
             "bicgstab": {"iters": iters, "status": r["status"], "ms_per_iteration": ms_step / iters,
                          "time_to_tol_ms": ms_step, "true_relres": r["true_relres"], "loop_mode": r["loop_mode"],
                          "bytes_per_iteration": M.bicgstab_iter_bytes(n, nnz),

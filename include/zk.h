@@ -80,6 +80,9 @@ typedef struct {
     int64_t n_halo;        /* off-rank x entries received per SpMV (0 on one GPU) */
     int32_t borrowed;      /* 1 if the arrays are borrowed (ZK_PTRS_DEVICE_BORROW) */
     int32_t nranks;
+    int32_t spmv_mode;     /* 0 = sub-warp rows, 1 = TMA bulk-copy staged row tiles */
+    int32_t rows_per_tile; /* TMA mode: rows per staged tile */
+    int32_t tma_stages;    /* TMA mode: pipeline depth */
 } zk_csr_info_t;
 
 typedef struct {

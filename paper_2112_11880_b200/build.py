@@ -39,16 +39,19 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile csrc/*.cu into libzk.so (or `out` with extra -D defines, for A/B variants)."""
+    so = out or SO
+    if not force and out is None and not stale():
         return SO
     inc, lib = nccl_dirs()
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build", "obj_" + os.path.basename(so).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     flags = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-I", inc,
                     "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    flags += [f"-D{d}" for d in defines]
     objs = []
     procs = []
     for src in sources():
@@ -58,11 +61,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     rc = [p.wait() for p in procs]
     if any(rc):
         raise RuntimeError(f"nvcc failed: {rc}")
-    link = ["nvcc", "-shared", "-o", SO] + objs + ARCH + [
+    link = ["nvcc", "-shared", "-o", so] + objs + ARCH + [
         "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}"]
     subprocess.check_call(link)
-    return SO
+    return so
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--out")
+    ap.add_argument("-D", action="append", default=[])
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, out=a.out, defines=a.D))

@@ -31,15 +31,16 @@ zk_status current_device(DeviceInfo* out) {
     return ZK_OK;
 }
 
-int blocks_per_sm(const void* kernel) {
+int blocks_per_sm(const void* kernel, int smem) {
     static std::mutex mu;
-    static std::unordered_map<const void*, int> cache;
+    static std::unordered_map<const void*, std::pair<int, int>> cache;  // kernel → (smem, blocks)
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(kernel);
-    if (it != cache.end()) return it->second;
+    if (it != cache.end() && it->second.first == smem) return it->second.second;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kBlock, 0) != cudaSuccess || b < 1) b = 1;
-    cache[kernel] = b;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kBlock, smem) != cudaSuccess || b < 1) b = 1;
+    cache[kernel] = {smem, b};
     return b;
 }
 }  // namespace zk
@@ -110,55 +111,87 @@ __global__ void __launch_bounds__(kBlock) validate_kernel(const int64_t* __restr
 // ------------------------------------------------------------------ ZSpMV kernel (zk_zcsrmv)
 struct EpiAxpby {
     static constexpr int K = 0;
+    using Pre = double2;
     double2 alpha, beta;
     double2* __restrict__ y;
     bool beta_zero;
-    __device__ void row(int64_t i, double2 s, double (&)[1]) {
+    __device__ Pre pre(int64_t i) const { return beta_zero ? make_double2(0, 0) : y[i]; }
+    __device__ void row(int64_t i, double2 s, const Pre& yo, double (&)[1]) {
         double2 r = cmul(alpha, s);
-        if (!beta_zero) r = cadd(r, cmul(beta, y[i]));
+        if (!beta_zero) r = cadd(r, cmul(beta, yo));
         y[i] = r;
     }
     __device__ void finish(double (&)[1]) {}
 };
 
-template <int W>
-__global__ void __launch_bounds__(kBlock) zcsrmv_kernel(CsrDev A, const double2* __restrict__ x, EpiAxpby epi) {
-    spmv_body<W>(A, x, epi);
+template <int W, int MODE>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) zcsrmv_kernel(CsrDev A, TmaPlan T, const double2* __restrict__ x,
+                                                       EpiAxpby epi) {
+    spmv_any<W, MODE>(A, T, x, epi);
 }
-
-template <int W>
-static zk_status launch_zcsrmv(const zk_csr_s* A, double2 alpha, const double2* x, double2 beta, double2* y,
-                               cudaStream_t s) {
-    const void* k = (const void*)zcsrmv_kernel<W>;
-    const int cap = A->dev.num_sms * blocks_per_sm(k);
-    const int G = grid_for(A->n_rows, kBlock / W, cap);
-    CsrDev d{A->row_ptr, A->col, A->val, A->n_rows};
-    EpiAxpby e{alpha, beta, y, beta.x == 0.0 && beta.y == 0.0};
-    zcsrmv_kernel<W><<<G, kBlock, 0, s>>>(d, x, e);
+// load-policy sweep variants of the sub-warp kernel (tools/microbench.py; env ZK_SPMV_LP)
+template <int W, int LP, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) zcsrmv_lp_kernel(CsrDev A, const double2* __restrict__ x,
+                                                                EpiAxpby epi) {
+    spmv_body<W, EpiAxpby, LP>(A, x, epi);
+}
+template <int LP, int MINB>
+static zk_status launch_lp(const zk_csr_s* A, const double2* x, EpiAxpby e, cudaStream_t s) {
+    const void* k = (const void*)zcsrmv_lp_kernel<8, LP, MINB>;
+    const int G = grid_for(A->n_rows, kBlock / 8, A->dev.num_sms * blocks_per_sm(k, 0));
+    zcsrmv_lp_kernel<8, LP, MINB><<<G, kBlock, 0, s>>>(CsrDev{A->row_ptr, A->col, A->val, A->n_rows}, x, e);
     ZK_CUDA(cudaGetLastError());
     return ZK_OK;
 }
 
 zk_status zcsrmv_local(const zk_csr_s* A, double2 alpha, const double2* x, double2 beta, double2* y,
                        cudaStream_t s) {
-    switch (A->W) {
-        case 2: return launch_zcsrmv<2>(A, alpha, x, beta, y, s);
-        case 4: return launch_zcsrmv<4>(A, alpha, x, beta, y, s);
-        case 8: return launch_zcsrmv<8>(A, alpha, x, beta, y, s);
-        case 16: return launch_zcsrmv<16>(A, alpha, x, beta, y, s);
-        default: return launch_zcsrmv<32>(A, alpha, x, beta, y, s);
+    const int lp = getenv("ZK_SPMV_LP") ? atoi(getenv("ZK_SPMV_LP")) : -1;
+    if (lp >= 0 && A->spmv_mode == 0) {
+        EpiAxpby e{alpha, beta, y, beta.x == 0.0 && beta.y == 0.0};
+        switch (lp) {  // 10·minBlocksPerSM + policy
+            case 0: return launch_lp<0, 1>(A, x, e, s);
+            case 1: return launch_lp<1, 1>(A, x, e, s);
+            case 2: return launch_lp<2, 1>(A, x, e, s);
+            case 3: return launch_lp<3, 1>(A, x, e, s);
+            case 41: return launch_lp<1, 4>(A, x, e, s);
+            case 51: return launch_lp<1, 5>(A, x, e, s);
+            case 61: return launch_lp<1, 6>(A, x, e, s);
+            default: return launch_lp<1, 8>(A, x, e, s);
+        }
     }
+    return with_spmv(A, [&](auto wc, auto mc) -> zk_status {
+        constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
+        const void* k = (const void*)zcsrmv_kernel<W, MODE>;
+        const LaunchCfg L = spmv_cfg(A, k, W, MODE);
+        CsrDev d{A->row_ptr, A->col, A->val, A->n_rows};
+        EpiAxpby e{alpha, beta, y, beta.x == 0.0 && beta.y == 0.0};
+        zcsrmv_kernel<W, MODE><<<L.grid, kBlock, L.smem, s>>>(d, A->tma, x, e);
+        ZK_CUDA(cudaGetLastError());
+        return ZK_OK;
+    });
 }
 
-// sub-warp width from the mean row length: ≈ 4 nonzeros per lane per row, W in [2, 32]
-static int choose_w(double mean) {
-    if (const char* e = getenv("ZK_SPMV_W")) {
-        int w = atoi(e);
-        if (w == 2 || w == 4 || w == 8 || w == 16 || w == 32) return w;
+// SpMV mapping from the row statistics (env ZK_SPMV_MODE / ZK_SPMV_W override, for sweeps):
+//  TMA-staged tiles whenever rows are short enough to tile (max_len ≤ 128) and not nearly empty;
+//  lanes per row ≈ mean/4 (sub-warp) or 8 for the 27-point rows (TMA: W ∈ {4, 8, 16}).
+static void choose_mapping(zk_csr_s* A) {
+    int mode = -1, w = -1;
+    if (const char* e = getenv("ZK_SPMV_MODE")) mode = atoi(e);
+    if (const char* e = getenv("ZK_SPMV_W")) w = atoi(e);
+    int stages = 4, stage_nnz = 756;
+    if (const char* e = getenv("ZK_TMA_STAGES")) stages = atoi(e) < 2 ? 2 : (atoi(e) > 8 ? 8 : atoi(e));
+    if (const char* e = getenv("ZK_TMA_NNZ")) stage_nnz = atoi(e) < 256 ? 256 : atoi(e);
+    const bool tma_ok = make_tma_plan(A->n_rows, A->nnz, A->max_len, &A->tma, stages, stage_nnz);
+    if (mode != 0 && mode != 1) mode = 0;  // measured: sub-warp + L2 evict_normal beats TMA staging on C4
+    if (mode == 1 && !tma_ok) mode = 0;
+    A->spmv_mode = mode;
+    if (w != 2 && w != 4 && w != 8 && w != 16 && w != 32) {
+        w = 2;
+        while (w < 32 && 4.0 * w < A->mean_len) w *= 2;
     }
-    int w = 2;
-    while (w < 32 && 4.0 * w < mean) w *= 2;
-    return w;
+    if (mode == 1) w = w <= 4 ? 4 : (w >= 16 ? 16 : 8);
+    A->W = w;
 }
 
 zk_status dist_setup(zk_csr_s* A, const int64_t* h_row_ptr, const int* h_col, cudaStream_t s);  // dist.cu
@@ -250,7 +283,7 @@ extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, 
         A->max_len = (int)h.max_len;
     }
     A->mean_len = n_rows > 0 ? (double)nnz / (double)n_rows : 0.0;
-    A->W = choose_w(A->mean_len);
+    choose_mapping(A);
     if (cudaStreamCreateWithFlags(&A->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
         return cleanup(fail(ZK_ERR_CUDA, "cudaStreamCreate"));
 
@@ -292,6 +325,9 @@ extern "C" zk_status zk_csr_info(zk_csr A, zk_csr_info_t* info) {
     info->n_halo = dist_n_halo(A);
     info->borrowed = A->owned ? 0 : 1;
     info->nranks = dist_nranks(A);
+    info->spmv_mode = A->spmv_mode;
+    info->rows_per_tile = A->spmv_mode == 1 ? A->tma.R : 0;
+    info->tma_stages = A->spmv_mode == 1 ? A->tma.S : 0;
     return ZK_OK;
 }
 

@@ -34,6 +34,7 @@ struct SolveCtx {
     double* partials;       // [kMaxRed][kMaxGrid]
     unsigned int* tickets;  // [8]
     CsrDev A;
+    TmaPlan T;
     // scalars
     double2 rho, alpha, omega, beta;
     double nb, nrh, rnorm, gamma, alpha_cg, beta_cg;
@@ -206,47 +207,64 @@ __device__ __forceinline__ void reduce_finish(SolveCtx* c, double (&acc)[K]) {
 
 template <int S>
 __global__ void fin_kernel(SolveCtx* c) {
-    if (S == S_K4_BICG && c->half) return;
+    // the reducing kernel skipped its work (loop already finished): nothing to finish — the
+    // chunked loop launches whole iterations past convergence (regression: tools/debug/dist1.py)
+    if (S != S_TRUE && S != S_INIT_BICG && S != S_INIT_CG && c->done) return;
     double tot[kMaxRed];
     for (int k = 0; k < kMaxRed; k++) tot[k] = c->red[k];
     finish_stage<S>(c, tot);
 }
 
 // ------------------------------------------------------------------ epilogues and vector ops
+// Epilogues: pre(i) loads the row's own operands (issued one tile ahead by spmv_body, so the
+// load is off the critical path); row(i, y, pre, acc) consumes them.  Pointers are cached from
+// the SolveCtx at kernel start.
 template <int S>
 struct EpiInit {  // r = b − A x0 ; x = x0 ; r̂ = p = r ; {‖b‖², ‖r‖²}
     static constexpr int K = 2;
+    struct Pre { double2 b, x0; };
     SolveCtx* c;
-    const double2* x0;
-    bool bicg;
-    __device__ void row(int64_t i, double2 y, double (&acc)[2]) {
-        const double2 bi = c->b[i];
-        const double2 r = csub(bi, y);
-        c->r[i] = r;
-        c->p[i] = r;
-        if (bicg) c->rh[i] = r;
-        if (c->x != x0) c->x[i] = x0[i];
-        acc[0] += cabs2(bi);
-        acc[1] += cabs2(r);
+    const double2* __restrict__ x0;
+    const double2* __restrict__ b;
+    double2 *r, *p, *rh, *x;
+    __device__ EpiInit(SolveCtx* c_, const double2* x0_, bool bicg)
+        : c(c_), x0(x0_), b(c_->b), r(c_->r), p(c_->p), rh(bicg ? c_->rh : nullptr), x(c_->x) {}
+    __device__ Pre pre(int64_t i) const { return {ld_stream(b + i), x != x0 ? ld_gather(x0 + i) : make_double2(0, 0)}; }
+    __device__ void row(int64_t i, double2 y, const Pre& q, double (&acc)[2]) {
+        const double2 rr = csub(q.b, y);
+        r[i] = rr;
+        p[i] = rr;
+        if (rh) rh[i] = rr;
+        if (x != x0) x[i] = q.x0;
+        acc[0] += cabs2(q.b);
+        acc[1] += cabs2(rr);
     }
     __device__ void finish(double (&acc)[2]) { reduce_finish<S, 2>(c, acc); }
 };
 
 struct EpiTrue {  // {‖b − A x‖²}
     static constexpr int K = 1;
+    using Pre = double2;
     SolveCtx* c;
-    __device__ void row(int64_t i, double2 y, double (&acc)[1]) { acc[0] += cabs2(csub(c->b[i], y)); }
+    const double2* __restrict__ b;
+    __device__ explicit EpiTrue(SolveCtx* c_) : c(c_), b(c_->b) {}
+    __device__ Pre pre(int64_t i) const { return ld_stream(b + i); }
+    __device__ void row(int64_t, double2 y, const Pre& bi, double (&acc)[1]) { acc[0] += cabs2(csub(bi, y)); }
     __device__ void finish(double (&acc)[1]) { reduce_finish<S_TRUE, 1>(c, acc); }
 };
 
 struct EpiK1Bicg {  // v = A p ; {σ = ⟨r̂, v⟩, ‖v‖²}
     static constexpr int K = 3;
+    using Pre = double2;
     SolveCtx* c;
-    __device__ void row(int64_t i, double2 y, double (&acc)[3]) {
-        c->v[i] = y;
-        const double2 rh = ld_stream(c->rh + i);
-        acc[0] = fma(rh.x, y.x, fma(rh.y, y.y, acc[0]));
-        acc[1] = fma(rh.x, y.y, fma(-rh.y, y.x, acc[1]));
+    double2* __restrict__ v;
+    const double2* __restrict__ rh;
+    __device__ explicit EpiK1Bicg(SolveCtx* c_) : c(c_), v(c_->v), rh(c_->rh) {}
+    __device__ Pre pre(int64_t i) const { return ld_stream(rh + i); }
+    __device__ void row(int64_t i, double2 y, const Pre& r, double (&acc)[3]) {
+        v[i] = y;
+        acc[0] = fma(r.x, y.x, fma(r.y, y.y, acc[0]));
+        acc[1] = fma(r.x, y.y, fma(-r.y, y.x, acc[1]));
         acc[2] += cabs2(y);
     }
     __device__ void finish(double (&acc)[3]) { reduce_finish<S_K1_BICG, 3>(c, acc); }
@@ -254,12 +272,16 @@ struct EpiK1Bicg {  // v = A p ; {σ = ⟨r̂, v⟩, ‖v‖²}
 
 struct EpiK3Bicg {  // t = A s ; {⟨t, s⟩, ⟨t, t⟩}
     static constexpr int K = 3;
+    using Pre = double2;
     SolveCtx* c;
-    __device__ void row(int64_t i, double2 y, double (&acc)[3]) {
-        c->t[i] = y;
-        const double2 s = ld_gather(c->s + i);
-        acc[0] = fma(y.x, s.x, fma(y.y, s.y, acc[0]));
-        acc[1] = fma(y.x, s.y, fma(-y.y, s.x, acc[1]));
+    double2* __restrict__ t;
+    const double2* __restrict__ s;
+    __device__ explicit EpiK3Bicg(SolveCtx* c_) : c(c_), t(c_->t), s(c_->s) {}
+    __device__ Pre pre(int64_t i) const { return ld_gather(s + i); }
+    __device__ void row(int64_t i, double2 y, const Pre& si, double (&acc)[3]) {
+        t[i] = y;
+        acc[0] = fma(y.x, si.x, fma(y.y, si.y, acc[0]));
+        acc[1] = fma(y.x, si.y, fma(-y.y, si.x, acc[1]));
         acc[2] += cabs2(y);
     }
     __device__ void finish(double (&acc)[3]) { reduce_finish<S_K3_BICG, 3>(c, acc); }
@@ -267,12 +289,16 @@ struct EpiK3Bicg {  // t = A s ; {⟨t, s⟩, ⟨t, t⟩}
 
 struct EpiK1Cg {  // q = A p ; {δ = ⟨p, q⟩}
     static constexpr int K = 2;
+    using Pre = double2;
     SolveCtx* c;
-    __device__ void row(int64_t i, double2 y, double (&acc)[2]) {
-        c->q[i] = y;
-        const double2 p = ld_gather(c->p + i);
-        acc[0] = fma(p.x, y.x, fma(p.y, y.y, acc[0]));
-        acc[1] = fma(p.x, y.y, fma(-p.y, y.x, acc[1]));
+    double2* __restrict__ q;
+    const double2* __restrict__ p;
+    __device__ explicit EpiK1Cg(SolveCtx* c_) : c(c_), q(c_->q), p(c_->p) {}
+    __device__ Pre pre(int64_t i) const { return ld_gather(p + i); }
+    __device__ void row(int64_t i, double2 y, const Pre& pi, double (&acc)[2]) {
+        q[i] = y;
+        acc[0] = fma(pi.x, y.x, fma(pi.y, y.y, acc[0]));
+        acc[1] = fma(pi.x, y.y, fma(-pi.y, y.x, acc[1]));
     }
     __device__ void finish(double (&acc)[2]) { reduce_finish<S_K1_CG, 2>(c, acc); }
 };
@@ -402,30 +428,30 @@ struct OpK3Cg {  // p = r + β p
 };
 
 // ------------------------------------------------------------------ kernels
-template <int W, int S>
-__global__ void __launch_bounds__(kBlock) k_init_x0(SolveCtx* c, const double2* __restrict__ xg, int bicg) {
+template <int W, int MODE, int S>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_init_x0(SolveCtx* c, const double2* __restrict__ xg, int bicg) {
     stamp_start<S>(c);
-    EpiInit<S> e{c, xg, bicg != 0};
-    spmv_body<W>(c->A, xg, e);
+    EpiInit<S> e(c, xg, bicg != 0);
+    spmv_any<W, MODE>(c->A, c->T, xg, e);
 }
 __global__ void __launch_bounds__(kBlock) k_init_zero(SolveCtx* c, int bicg) {
     stamp_start<S_INIT_BICG>(c);
     OpInitZero op{c, bicg != 0, 0};
     vec_body(c->A.n_rows, op);
 }
-template <int W>
-__global__ void __launch_bounds__(kBlock) k_true(SolveCtx* c, const double2* __restrict__ xg) {
+template <int W, int MODE>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_true(SolveCtx* c, const double2* __restrict__ xg) {
     if (c->status == ST_ZERO_RHS) return;
     stamp_start<S_TRUE>(c);
-    EpiTrue e{c};
-    spmv_body<W>(c->A, xg, e);
+    EpiTrue e(c);
+    spmv_any<W, MODE>(c->A, c->T, xg, e);
 }
-template <int W>
-__global__ void __launch_bounds__(kBlock) k1_bicg(SolveCtx* c) {
+template <int W, int MODE>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_bicg(SolveCtx* c) {
     if (c->done) return;
     stamp_start<S_K1_BICG>(c);
-    EpiK1Bicg e{c};
-    spmv_body<W>(c->A, c->p, e);
+    EpiK1Bicg e(c);
+    spmv_any<W, MODE>(c->A, c->T, c->p, e);
 }
 __global__ void __launch_bounds__(kBlock) k2_bicg(SolveCtx* c) {
     if (c->done) return;
@@ -433,12 +459,12 @@ __global__ void __launch_bounds__(kBlock) k2_bicg(SolveCtx* c) {
     OpK2Bicg op{c, c->alpha};
     vec_body(c->A.n_rows, op);
 }
-template <int W>
-__global__ void __launch_bounds__(kBlock) k3_bicg(SolveCtx* c) {
+template <int W, int MODE>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k3_bicg(SolveCtx* c) {
     if (c->done) return;
     stamp_start<S_K3_BICG>(c);
-    EpiK3Bicg e{c};
-    spmv_body<W>(c->A, c->s, e);
+    EpiK3Bicg e(c);
+    spmv_any<W, MODE>(c->A, c->T, c->s, e);
 }
 __global__ void __launch_bounds__(kBlock) k4_bicg(SolveCtx* c) {
     const bool half = c->half != 0;
@@ -456,12 +482,12 @@ __global__ void __launch_bounds__(kBlock) k5_bicg(SolveCtx* c) {
     OpK5Bicg op{c, c->beta, c->omega};
     vec_body(c->A.n_rows, op);
 }
-template <int W>
-__global__ void __launch_bounds__(kBlock) k1_cg(SolveCtx* c) {
+template <int W, int MODE>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cg(SolveCtx* c) {
     if (c->done) return;
     stamp_start<S_K1_CG>(c);
-    EpiK1Cg e{c};
-    spmv_body<W>(c->A, c->p, e);
+    EpiK1Cg e(c);
+    spmv_any<W, MODE>(c->A, c->T, c->p, e);
 }
 __global__ void __launch_bounds__(kBlock) k2_cg(SolveCtx* c) {
     if (c->done) return;
@@ -481,22 +507,6 @@ __global__ void k_set_ctx(SolveCtx* c, SolveCtx h) {
 }
 
 // ------------------------------------------------------------------ host side
-template <class F>
-static zk_status with_w(int W, F&& f) {
-    switch (W) {
-        case 2: return f(std::integral_constant<int, 2>{});
-        case 4: return f(std::integral_constant<int, 4>{});
-        case 8: return f(std::integral_constant<int, 8>{});
-        case 16: return f(std::integral_constant<int, 16>{});
-        default: return f(std::integral_constant<int, 32>{});
-    }
-}
-
-static int spmv_grid(const zk_csr_s* A, const void* k, int W) {
-    int cap = A->dev.num_sms * blocks_per_sm(k);
-    if (cap > kMaxGrid) cap = kMaxGrid;
-    return grid_for(A->n_rows, kBlock / W, cap);
-}
 static int vec_grid(const zk_csr_s* A, const void* k) {
     int cap = A->dev.num_sms * blocks_per_sm(k);
     if (cap > kMaxGrid) cap = kMaxGrid;
@@ -518,18 +528,18 @@ static zk_status dist_finish(const zk_csr_s* A, SolveCtx* c, int count, cudaStre
 // enqueue one iteration of `method`
 static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc, int method, cudaStream_t s) {
     const bool dist = A->dist != nullptr;
-    return with_w(A->W, [&](auto wc) -> zk_status {
-        constexpr int W = decltype(wc)::value;
+    return with_spmv(A, [&](auto wc, auto mc) -> zk_status {
+        constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
         if (method == ZK_BICGSTAB) {
             if (dist) ZK_TRY(dist_halo(A, hc.p, s));
-            k1_bicg<W><<<spmv_grid(A, (const void*)k1_bicg<W>, W), kBlock, 0, s>>>(dc);
+            { auto kf = k1_bicg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); kf<<<L.grid, kBlock, L.smem, s>>>(dc); }
             ZK_CUDA(cudaGetLastError());
             if (dist) ZK_TRY((dist_finish<S_K1_BICG>(A, dc, 3, s)));
             k2_bicg<<<vec_grid(A, (const void*)k2_bicg), kBlock, 0, s>>>(dc);
             ZK_CUDA(cudaGetLastError());
             if (dist) ZK_TRY((dist_finish<S_K2_BICG>(A, dc, 1, s)));
             if (dist) ZK_TRY(dist_halo(A, hc.s, s));
-            k3_bicg<W><<<spmv_grid(A, (const void*)k3_bicg<W>, W), kBlock, 0, s>>>(dc);
+            { auto kf = k3_bicg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); kf<<<L.grid, kBlock, L.smem, s>>>(dc); }
             ZK_CUDA(cudaGetLastError());
             if (dist) ZK_TRY((dist_finish<S_K3_BICG>(A, dc, 3, s)));
             k4_bicg<<<vec_grid(A, (const void*)k4_bicg), kBlock, 0, s>>>(dc);
@@ -539,7 +549,7 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             ZK_CUDA(cudaGetLastError());
         } else {
             if (dist) ZK_TRY(dist_halo(A, hc.p, s));
-            k1_cg<W><<<spmv_grid(A, (const void*)k1_cg<W>, W), kBlock, 0, s>>>(dc);
+            { auto kf = k1_cg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); kf<<<L.grid, kBlock, L.smem, s>>>(dc); }
             ZK_CUDA(cudaGetLastError());
             if (dist) ZK_TRY((dist_finish<S_K1_CG>(A, dc, 2, s)));
             k2_cg<<<vec_grid(A, (const void*)k2_cg), kBlock, 0, s>>>(dc);
@@ -698,6 +708,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     }
     double2* xg = A->dist ? vec[L.nvec - 1] : nullptr;  // gather copy of x0 / x with halo slots
     hc.A = CsrDev{A->row_ptr, A->col, A->val, A->n_rows};
+    hc.T = A->tma;
     hc.tol = tol;
     hc.maxit = maxit;
     hc.status = ZK_MAXIT;
@@ -750,14 +761,16 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
             ZK_TRY(dist_halo(A, xg, s));
             g0 = xg;
         }
-        ZK_TRY(with_w(A->W, [&](auto wc) -> zk_status {
-            constexpr int W = decltype(wc)::value;
+        ZK_TRY(with_spmv(A, [&](auto wc, auto mc) -> zk_status {
+            constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
             if (bicg) {
-                auto k = k_init_x0<W, S_INIT_BICG>;
-                k<<<spmv_grid(A, (const void*)k, W), kBlock, 0, s>>>(dc, g0, 1);
+                auto k = k_init_x0<W, MODE, S_INIT_BICG>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)k, W, MODE);
+                k<<<L.grid, kBlock, L.smem, s>>>(dc, g0, 1);
             } else {
-                auto k = k_init_x0<W, S_INIT_CG>;
-                k<<<spmv_grid(A, (const void*)k, W), kBlock, 0, s>>>(dc, g0, 0);
+                auto k = k_init_x0<W, MODE, S_INIT_CG>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)k, W, MODE);
+                k<<<L.grid, kBlock, L.smem, s>>>(dc, g0, 0);
             }
             ZK_CUDA(cudaGetLastError());
             return ZK_OK;
@@ -802,9 +815,9 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         ZK_TRY(dist_halo(A, xg, s));
         gx = xg;
     }
-    ZK_TRY(with_w(A->W, [&](auto wc) -> zk_status {
-        constexpr int W = decltype(wc)::value;
-        k_true<W><<<spmv_grid(A, (const void*)k_true<W>, W), kBlock, 0, s>>>(dc, gx);
+    ZK_TRY(with_spmv(A, [&](auto wc, auto mc) -> zk_status {
+        constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
+        { auto kf = k_true<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); kf<<<L.grid, kBlock, L.smem, s>>>(dc, gx); }
         ZK_CUDA(cudaGetLastError());
         return ZK_OK;
     }));

@@ -1,14 +1,17 @@
 // spmv.cuh — the ZSpMV body (§3) and the BLAS-1 loop body,
 // both as __device__ templates so the solver kernels can fuse their epilogues into them.
 //
-// ZSpMV mapping: a sub-warp of W lanes per row, W chosen at create from the
-// mean row length (W = 8 for the 27-point FE rows).  A block of 256 threads owns 256/W
-// consecutive rows per step and walks its tiles grid-stride (a fixed static schedule, so the
-// fused reductions are deterministic).  Each lane issues up to 4 independent streaming loads
-// of (value, column) per chunk of 4W nonzeros before touching x, then the 4 gathers of x
-// (read-only path; x stays L1/L2-resident across neighbouring rows), then 4 complex FMAs; the
-// W partial sums are combined with xor-shuffles.  No tensor cores: this is not a contraction
-// (8 flops per 20+ bytes).
+// ZSpMV mapping: a sub-warp of W lanes per row, W chosen at create from the mean
+// row length (W = 8 for the 27-point FE rows).  A block of 256 threads owns 256/W consecutive
+// rows per step and walks its tiles grid-stride (a fixed static schedule, so the fused
+// reductions are deterministic).  Per row chunk of 4W nonzeros each lane issues 4 independent
+// (value, column) loads before touching x, then the 4 gathers of x (read-only path; x stays
+// L1/L2-resident across neighbouring rows), then 4 complex FMAs; the W partial sums are combined
+// with xor-shuffles.  The row bounds of the NEXT tile are loaded while the current tile computes
+// (one DRAM latency off each tile's dependency chain).  Matrix-stream loads carry an explicit
+// L2 evict_normal policy (LP 1): with the default evict-first treatment of no-allocate loads,
+// sectors shared by two row chunks were re-fetched (ncu: 1.25x DRAM reads; profiles/).
+// No tensor cores: this is not a contraction (8 flops per 20+ bytes).
 #pragma once
 #include "zk_internal.cuh"
 
@@ -16,14 +19,19 @@ namespace zk {
 
 // Epilogue concept:
 //   static constexpr int K;                         // doubles reduced over the grid (0..4)
-//   __device__ void row(int64_t i, double2 y, double (&acc)[K>0?K:1]);   // called once per row
+//   typename Pre; __device__ Pre pre(int64_t i);   // row i's own operands (loaded a tile ahead)
+//   __device__ void row(int64_t i, double2 y, const Pre&, double (&acc)[K>0?K:1]);   // once per row
 //   __device__ void finish(double (&acc)[K>0?K:1]); // called by every thread at the end
-template <int W, class Epi>
+#ifndef ZK_DEFAULT_LP
+#define ZK_DEFAULT_LP 1
+#endif
+template <int W, class Epi, int LP = ZK_DEFAULT_LP>
 __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
     static_assert(W >= 1 && W <= 32 && (W & (W - 1)) == 0, "W must be a power of two <= 32");
     constexpr int RPB = kBlock / W;  // rows per block step
     constexpr int U = 4;             // nonzeros per lane per chunk
     constexpr int KA = Epi::K > 0 ? Epi::K : 1;
+    const uint64_t pol = make_policy<LP>();
     double acc[KA];
 #pragma unroll
     for (int k = 0; k < KA; k++) acc[k] = 0.0;
@@ -31,11 +39,28 @@ __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __rest
     const int sub = threadIdx.x & (W - 1);
     const int grp = threadIdx.x / W;
     const int64_t n = A.n_rows;
-    for (int64_t tile = blockIdx.x; tile * RPB < n; tile += gridDim.x) {
-        const int64_t row = tile * RPB + grp;
+    const int64_t G = gridDim.x;
+    int64_t tile = blockIdx.x;
+    int64_t row = tile * RPB + grp;
+    int64_t rs = 0, re = 0;
+    typename Epi::Pre pre{};
+    if (row < n) {
+        rs = __ldg(A.row_ptr + row);
+        re = __ldg(A.row_ptr + row + 1);
+        if (sub == 0) pre = epi.pre(row);
+    }
+    for (; tile * RPB < n; tile += G) {
+        // bounds of this lane's row in the next tile, consumed one iteration later
+        const int64_t nrow = (tile + G) * RPB + grp;
+        int64_t nrs = 0, nre = 0;
+        typename Epi::Pre npre{};
+        if (nrow < n) {
+            nrs = __ldg(A.row_ptr + nrow);
+            nre = __ldg(A.row_ptr + nrow + 1);
+            if (sub == 0) npre = epi.pre(nrow);
+        }
         double2 sum = make_double2(0.0, 0.0);
         if (row < n) {
-            const int64_t rs = __ldg(A.row_ptr + row), re = __ldg(A.row_ptr + row + 1);
             for (int64_t base = rs; base < re; base += U * W) {
                 double2 v[U];
                 int c[U];
@@ -43,8 +68,8 @@ __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __rest
                 for (int u = 0; u < U; u++) {
                     const int64_t p = base + u * W + sub;
                     if (p < re) {
-                        v[u] = ld_stream(A.val + p);
-                        c[u] = ld_stream(A.col + p);
+                        v[u] = ld_mat<LP>(A.val + p, pol);
+                        c[u] = ld_mat<LP>(A.col + p, pol);
                     } else {
                         v[u] = make_double2(0.0, 0.0);
                         c[u] = -1;
@@ -62,7 +87,11 @@ __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __rest
             sum.x += __shfl_xor_sync(0xffffffffu, sum.x, o, W);
             sum.y += __shfl_xor_sync(0xffffffffu, sum.y, o, W);
         }
-        if (sub == 0 && row < n) epi.row(row, sum, acc);
+        if (sub == 0 && row < n) epi.row(row, sum, pre, acc);
+        row = nrow;
+        rs = nrs;
+        re = nre;
+        pre = npre;
     }
     epi.finish(acc);
 }

@@ -6,6 +6,7 @@
 #include <string>
 
 #include "../../include/zk.h"
+#include "spmv_tma.cuh"
 
 namespace zk {
 
@@ -31,8 +32,9 @@ struct DeviceInfo {
 };
 zk_status current_device(DeviceInfo* out);
 
-// cached blocks-per-SM for a kernel (occupancy API), computed once per kernel pointer
-int blocks_per_sm(const void* kernel);
+// cached blocks-per-SM for a kernel (occupancy API) at `smem` dynamic shared memory bytes; also
+// raises the kernel's dynamic shared memory limit when smem > 48 KB
+int blocks_per_sm(const void* kernel, int smem = 0);
 
 struct GraphCache {
     const void* ws = nullptr;
@@ -54,6 +56,8 @@ struct zk_csr_s {
     double2* val = nullptr;      // device
     bool owned = false;
     int W = 8;                   // SpMV lanes per row
+    int spmv_mode = 0;           // 0 = sub-warp kernel (spmv.cuh), 1 = TMA-staged tiles (spmv_tma.cuh)
+    zk::TmaPlan tma{};
     int max_len = 0;
     double mean_len = 0.0;
     zk::DeviceInfo dev;
@@ -63,3 +67,46 @@ struct zk_csr_s {
     // distributed: halo plan (see dist.cu)
     void* dist = nullptr;
 };
+
+#include <type_traits>
+
+namespace zk {
+// Call f(std::integral_constant<int, W>, std::integral_constant<int, MODE>) for the matrix's SpMV
+// mapping (instantiated combinations: sub-warp W ∈ {2,4,8,16,32}, TMA W ∈ {4,8,16}).
+template <class F>
+zk_status with_spmv(const zk_csr_s* A, F&& f) {
+    using std::integral_constant;
+    if (A->spmv_mode == 1) {
+        switch (A->W) {
+            case 4: return f(integral_constant<int, 4>{}, integral_constant<int, 1>{});
+            case 16: return f(integral_constant<int, 16>{}, integral_constant<int, 1>{});
+            default: return f(integral_constant<int, 8>{}, integral_constant<int, 1>{});
+        }
+    }
+    switch (A->W) {
+        case 2: return f(integral_constant<int, 2>{}, integral_constant<int, 0>{});
+        case 4: return f(integral_constant<int, 4>{}, integral_constant<int, 0>{});
+        case 8: return f(integral_constant<int, 8>{}, integral_constant<int, 0>{});
+        case 16: return f(integral_constant<int, 16>{}, integral_constant<int, 0>{});
+        default: return f(integral_constant<int, 32>{}, integral_constant<int, 0>{});
+    }
+}
+
+struct LaunchCfg {
+    int grid;
+    int smem;
+};
+// grid and dynamic smem for an SpMV kernel of A (TMA: one CTA per resident slot, ≤ n_tiles)
+inline LaunchCfg spmv_cfg(const zk_csr_s* A, const void* kernel, int W, int mode) {
+    if (mode == 1) {
+        const int smem = A->tma.smem_bytes;
+        int cap = A->dev.num_sms * blocks_per_sm(kernel, smem);
+        if (cap > kMaxGrid) cap = kMaxGrid;
+        int64_t g = A->tma.n_tiles < cap ? A->tma.n_tiles : cap;
+        return {(int)(g < 1 ? 1 : g), smem};
+    }
+    int cap = A->dev.num_sms * blocks_per_sm(kernel, 0);
+    if (cap > kMaxGrid) cap = kMaxGrid;
+    return {grid_for(A->n_rows, kBlock / W, cap), 0};
+}
+}  // namespace zk

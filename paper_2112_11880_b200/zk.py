@@ -38,7 +38,8 @@ class zk_csr_info_t(ctypes.Structure):
                 ("row_begin", ctypes.c_int64), ("n_global", ctypes.c_int64),
                 ("max_row_len", ctypes.c_int32), ("lanes_per_row", ctypes.c_int32),
                 ("mean_row_len", ctypes.c_double), ("n_halo", ctypes.c_int64),
-                ("borrowed", ctypes.c_int32), ("nranks", ctypes.c_int32)]
+                ("borrowed", ctypes.c_int32), ("nranks", ctypes.c_int32), ("spmv_mode", ctypes.c_int32),
+                ("rows_per_tile", ctypes.c_int32), ("tma_stages", ctypes.c_int32)]
 
 
 class zk_solve_info(ctypes.Structure):
@@ -80,10 +81,11 @@ def lib():
     """Load libzk.so (built by __graft_entry__.build() / paper_2112_11880_b200/build.py). Fails loudly."""
     global _lib
     if _lib is None:
-        if not os.path.exists(SO_PATH):
-            raise ImportError(f"libzk.so not built at {SO_PATH}: run `python __graft_entry__.py build` "
+        path = os.environ.get("ZK_LIB", SO_PATH)  # A/B builds of libzk (tools), default in-tree
+        if not os.path.exists(path):
+            raise ImportError(f"libzk.so not built at {path}: run `python __graft_entry__.py build` "
                               "(no CPU fallback exists)")
-        h = ctypes.CDLL(SO_PATH)
+        h = ctypes.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             f = getattr(h, name)
             f.restype, f.argtypes = res, args

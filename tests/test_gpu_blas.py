@@ -29,29 +29,42 @@ def row_scale(m, x):
     return A @ np.abs(x)
 
 
-def make_csr(m, W=None, **kw):
-    old = os.environ.get("ZK_SPMV_W")
+MAPPINGS = [(0, 2, None), (0, 4, None), (0, 8, None), (0, 16, None), (0, 32, None),
+            (1, 4, None), (1, 8, None), (1, 16, None), (1, 8, (2, 700)), (1, 4, (4, 640))]
+MAP_IDS = [f"{'tma' if m else 'subwarp'}-W{w}" + (f"-S{c[0]}-nnz{c[1]}" if c else "") for m, w, c in MAPPINGS]
+
+
+def make_csr(m, W=None, mode=None, tma=None, **kw):
+    """csr_create with the SpMV mapping forced through the env overrides read at create."""
+    env = {}
     if W is not None:
-        os.environ["ZK_SPMV_W"] = str(W)
+        env["ZK_SPMV_W"] = str(W)
+    if mode is not None:
+        env["ZK_SPMV_MODE"] = str(mode)
+    if tma is not None:
+        env["ZK_TMA_STAGES"], env["ZK_TMA_NNZ"] = str(tma[0]), str(tma[1])
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         return zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m.get("n_cols", m["n"]), **kw)
     finally:
-        if W is not None:
-            if old is None:
-                del os.environ["ZK_SPMV_W"]
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
             else:
-                os.environ["ZK_SPMV_W"] = old
+                os.environ[k] = v
 
 
 # ------------------------------------------------------------------ ZSpMV
-@pytest.mark.parametrize("W", [2, 4, 8, 16, 32])
+@pytest.mark.parametrize("mapping", MAPPINGS, ids=MAP_IDS)
 @pytest.mark.parametrize("alpha,beta", [(1, 0), (0.5 - 2j, 0), (1j, -0.25 + 1j)])
-def test_zcsrmv_random(W, alpha, beta):
+def test_zcsrmv_random(mapping, alpha, beta):
     """Random CSR with empty rows, 1-nnz rows and rows > 32 nnz; ragged n spanning many tiles."""
-    m = gen.random_csr(5003, seed=W, max_len=70)
+    mode, W, tma = mapping
+    m = gen.random_csr(5003, seed=W + 10 * mode, max_len=70)
     x, y0 = gen.rand_vector(5003, 1), gen.rand_vector(5003, 2)
-    A = make_csr(m, W)
-    assert A.info["lanes_per_row"] == W
+    A = make_csr(m, W, mode, tma)
+    assert A.info["lanes_per_row"] == W and A.info["spmv_mode"] == mode
     y = cuda(y0)
     zk.zcsrmv(A, alpha, cuda(x), beta, y)
     want = oracle.zcsrmv(m, x, alpha, beta, y0)
@@ -59,11 +72,12 @@ def test_zcsrmv_random(W, alpha, beta):
     assert np.all(np.abs(y.cpu().numpy() - want) <= tol)
 
 
-@pytest.mark.parametrize("W", [2, 8, 32])
-def test_zcsrmv_integer_exact_bitwise(W):
+@pytest.mark.parametrize("mapping", MAPPINGS, ids=MAP_IDS)
+def test_zcsrmv_integer_exact_bitwise(mapping):
+    mode, W, tma = mapping
     m = gen.random_csr(3001, seed=11, max_len=40, integer=True)
     x = gen.int_vector(3001, 3)
-    A = make_csr(m, W)
+    A = make_csr(m, W, mode, tma)
     y = torch.empty(3001, dtype=torch.complex128, device=DEV)
     zk.zcsrmv(A, 1, cuda(x), 0, y)
     assert np.array_equal(y.cpu().numpy(), oracle.zcsrmv(m, x))
@@ -79,11 +93,12 @@ def test_zcsrmv_beta_zero_ignores_nan_and_empty_rows():
     assert np.all(got[np.diff(m["row_ptr"]) == 0] == 0)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C3T"])
-def test_zcsrmv_paper_shapes(cfg):
+def test_zcsrmv_paper_shapes(cfg, mode):
     m = gen.make_matrix(cfg)
     x = gen.rand_vector(m["n"], 7)
-    A = make_csr(m)
+    A = make_csr(m, mode=mode)
     y = torch.empty(m["n"], dtype=torch.complex128, device=DEV)
     zk.zcsrmv(A, 1, cuda(x), 0, y)
     got = y.cpu().numpy()

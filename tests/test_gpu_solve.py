@@ -40,8 +40,10 @@ def relerr(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
+@pytest.mark.parametrize("spmv_mode", ["0", "1"])
 @pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
-def test_bicgstab_parity(cfg):
+def test_bicgstab_parity(cfg, spmv_mode, monkeypatch):
+    monkeypatch.setenv("ZK_SPMV_MODE", spmv_mode)
     m = gen.make_matrix(cfg)
     b = gen.make_rhs(m)
     r = gpu_solve(m, b, tol=1e-8, maxit=1000, method="bicgstab")
@@ -56,8 +58,10 @@ def test_bicgstab_parity(cfg):
     assert r["loop_mode"] == 1                          # device-resident WHILE graph
 
 
+@pytest.mark.parametrize("spmv_mode", ["0", "1"])
 @pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
-def test_cg_parity_twisted_hpd(cfg):
+def test_cg_parity_twisted_hpd(cfg, spmv_mode, monkeypatch):
+    monkeypatch.setenv("ZK_SPMV_MODE", spmv_mode)
     mg = gen.make_matrix(cfg, eta=0.0, twist_seed=gen.SEED_TWIST)
     b = np.exp(1j * mg["phase"]) * gen.make_rhs(mg)
     r = gpu_solve(mg, b, tol=1e-8, method="cg")
@@ -180,3 +184,27 @@ def test_x0_restart_and_alias():
     with pytest.raises(zk.ZkError) as e:
         zk.solve(A, B, x=B)
     assert e.value.code == -7
+
+
+def test_distributed_path_single_rank_comm():
+    """The row-partitioned code path (NCCL comm, halo plan, allreduce + finish kernels, direct
+    launches) on a 1-rank communicator gives bitwise the same solve as the local path."""
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    base = gpu_solve(m, b, tol=1e-8)
+    comm = zk.Comm(zk.Comm.unique_id(), 1, 0, 0)
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"], comm=comm, row_begin=0)
+    assert A.info["nranks"] == 1 and A.info["n_halo"] == 0
+    r = zk.solve(A, cuda(b), tol=1e-8)
+    assert r["loop_mode"] == 3
+    assert r["iters"] == base["iters"] and np.array_equal(r["x"].cpu().numpy(), base["x"])
+    x = cuda(gen.rand_vector(m["n"], 4))
+    y = torch.empty_like(x)
+    zk.zcsrmv(A, 1, x, 0, y)
+    y_local = torch.empty_like(x)
+    zk.zcsrmv(zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"]), 1, x, 0, y_local)
+    assert torch.equal(y, y_local)
+    d = zk.zdotc(x, y, comm=comm).cpu().numpy()[0]
+    assert d == zk.zdotc(x, y).cpu().numpy()[0]
+    A.close()
+    comm.close()
