@@ -48,6 +48,7 @@ def args_():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--spmv-reps", type=int, default=50)
+    p.add_argument("--no-shapes", action="store_true", help="skip the PAPER.md T1-shape latency runs")
     return p.parse_args()
 
 
@@ -278,6 +279,29 @@ def main():
             "frac_of_peak": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9 / peak,
             "lanes_per_row": A.info["lanes_per_row"]}
 
+    # the paper's own matrix shapes (PAPER.md T1; latency-bound on B200): BiCGStab per iteration
+    shapes = None
+    if world == 1 and not a.no_shapes:
+        shapes = {}
+        for cfg in ("C1", "C2", "C3", "C3T"):
+            ms_ = gen.make_matrix(cfg)
+            As = zk.csr_create(ms_["row_ptr"], ms_["col_idx"], ms_["values"], ms_["n"])
+            bs = torch.from_numpy(gen.make_rhs(ms_)).to(dev)
+            wss = zk.alloc_workspace(As, "bicgstab", a.maxit, dev)
+            for _ in range(2):
+                rs_ = zk.solve(As, bs, None, a.tol, a.maxit, "bicgstab", workspace=wss, stream=stream)
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(5):
+                rs_ = zk.solve(As, bs, None, a.tol, a.maxit, "bicgstab", workspace=wss, stream=stream)
+            g1.record(stream)
+            torch.cuda.synchronize()
+            t_ms = g0.elapsed_time(g1) / 5
+            shapes[cfg] = {"n": ms_["n"], "nnz": ms_["nnz"], "iters": rs_["iters"], "time_to_tol_ms": t_ms,
+                           "us_per_iteration": 1e3 * t_ms / max(rs_["iters"], 1),
+                           "gbs": step_bytes(ms_["n"], ms_["nnz"], rs_["iters"]) / (t_ms * 1e-3) / 1e9}
+            As.close()
+
     # end to end through the public API with HOST buffers (pinned): CSR upload + b H2D + solve + x D2H
     e2e = None
     if not a.no_e2e:
@@ -340,6 +364,7 @@ def main():
                          "spmv_share_of_solve": k_ms / sum(q["solve_ms"] for q in results),
                          "vector_kernels_ms_per_iter": vec_ms / a.steps / iters},
             "spmv": spmv,
+            "paper_shapes_bicgstab": shapes,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -139,7 +139,7 @@ template <int LP, int MINB>
 static zk_status launch_lp(const zk_csr_s* A, const double2* x, EpiAxpby e, cudaStream_t s) {
     const void* k = (const void*)zcsrmv_lp_kernel<8, LP, MINB>;
     const int G = grid_for(A->n_rows, kBlock / 8, A->dev.num_sms * blocks_per_sm(k, 0));
-    zcsrmv_lp_kernel<8, LP, MINB><<<G, kBlock, 0, s>>>(CsrDev{A->row_ptr, A->col, A->val, A->n_rows}, x, e);
+    zcsrmv_lp_kernel<8, LP, MINB><<<G, kBlock, 0, s>>>(csr_dev(A), x, e);
     ZK_CUDA(cudaGetLastError());
     return ZK_OK;
 }
@@ -164,7 +164,7 @@ zk_status zcsrmv_local(const zk_csr_s* A, double2 alpha, const double2* x, doubl
         constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
         const void* k = (const void*)zcsrmv_kernel<W, MODE>;
         const LaunchCfg L = spmv_cfg(A, k, W, MODE);
-        CsrDev d{A->row_ptr, A->col, A->val, A->n_rows};
+        const CsrDev d = csr_dev(A);
         EpiAxpby e{alpha, beta, y, beta.x == 0.0 && beta.y == 0.0};
         zcsrmv_kernel<W, MODE><<<L.grid, kBlock, L.smem, s>>>(d, A->tma, x, e);
         ZK_CUDA(cudaGetLastError());
@@ -173,8 +173,8 @@ zk_status zcsrmv_local(const zk_csr_s* A, double2 alpha, const double2* x, doubl
 }
 
 // SpMV mapping from the row statistics (env ZK_SPMV_MODE / ZK_SPMV_W override, for sweeps):
-//  TMA-staged tiles whenever rows are short enough to tile (max_len ≤ 128) and not nearly empty;
-//  lanes per row ≈ mean/4 (sub-warp) or 8 for the 27-point rows (TMA: W ∈ {4, 8, 16}).
+//  sub-warp kernel by default (measured faster than the TMA-staged variant on C4), lanes per row
+//  ≈ mean/8; the TMA-staged mode is available for rows ≤ 128 long (W ∈ {4, 8, 16}).
 static void choose_mapping(zk_csr_s* A) {
     int mode = -1, w = -1;
     if (const char* e = getenv("ZK_SPMV_MODE")) mode = atoi(e);
@@ -187,8 +187,10 @@ static void choose_mapping(zk_csr_s* A) {
     if (mode == 1 && !tma_ok) mode = 0;
     A->spmv_mode = mode;
     if (w != 2 && w != 4 && w != 8 && w != 16 && w != 32) {
+        // ≈ 8 nonzeros per lane (two chunks of U = 4): W = 4 for the 27-point rows (measured best
+        // on C4 in-loop: 925 µs vs 1027 µs for W = 8)
         w = 2;
-        while (w < 32 && 4.0 * w < A->mean_len) w *= 2;
+        while (w < 32 && 8.0 * w < A->mean_len) w *= 2;
     }
     if (mode == 1) w = w <= 4 ? 4 : (w >= 16 ? 16 : 8);
     A->W = w;
@@ -211,6 +213,7 @@ extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, 
     *out = nullptr;
     if (n_rows < 0 || n_cols < 0 || nnz < 0) return fail(ZK_ERR_INVALID_VALUE, "negative size");
     if (n_cols > INT32_MAX) return fail(ZK_ERR_INVALID_VALUE, "n_cols exceeds int32 column ids");
+    if (n_rows >= INT32_MAX) return fail(ZK_ERR_INVALID_VALUE, "n_rows must be < 2^31 per matrix (rank)");
     if (!row_ptr || (nnz > 0 && (!col_idx || !values))) return fail(ZK_ERR_INVALID_VALUE, "NULL array");
     if (n_rows == 0 && nnz != 0) return fail(ZK_ERR_INVALID_CSR, "n_rows = 0 but nnz > 0");
     const uint32_t where = flags & 3u;

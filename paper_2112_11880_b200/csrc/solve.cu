@@ -303,18 +303,24 @@ struct EpiK1Cg {  // q = A p ; {δ = ⟨p, q⟩}
     __device__ void finish(double (&acc)[2]) { reduce_finish<S_K1_CG, 2>(c, acc); }
 };
 
+// Vector ops: every pointer and scalar is copied out of the SolveCtx once per thread at kernel
+// start (reading c->x inside the loop would force a reload after every store through a
+// possibly-aliasing pointer).
 struct OpInitZero {  // x0 = 0: x = 0 ; r = r̂ = p = b ; {‖b‖², ‖r‖²}
     static constexpr int K = 2;
     struct In { double2 b; };
     SolveCtx* c;
+    const double2* __restrict__ b;
+    double2 *__restrict__ x, *__restrict__ r, *__restrict__ p, *__restrict__ rh;
     bool bicg;
-    int stage;
-    __device__ In load(int64_t i) const { return {ld_stream(c->b + i)}; }
+    __device__ OpInitZero(SolveCtx* c_, bool bicg_)
+        : c(c_), b(c_->b), x(c_->x), r(c_->r), p(c_->p), rh(c_->rh), bicg(bicg_) {}
+    __device__ In load(int64_t i) const { return {ld_stream(b + i)}; }
     __device__ void apply(int64_t i, const In& v, double (&acc)[2]) const {
-        c->x[i] = make_double2(0.0, 0.0);
-        c->r[i] = v.b;
-        c->p[i] = v.b;
-        if (bicg) c->rh[i] = v.b;
+        x[i] = make_double2(0.0, 0.0);
+        r[i] = v.b;
+        p[i] = v.b;
+        if (bicg) rh[i] = v.b;
         const double bb = cabs2(v.b);
         acc[0] += bb;
         acc[1] += bb;
@@ -329,51 +335,60 @@ struct OpK2Bicg {  // s = r − α v ; {‖s‖²}
     static constexpr int K = 1;
     struct In { double2 r, v; };
     SolveCtx* c;
+    const double2 *__restrict__ r, *__restrict__ v;
+    double2* __restrict__ s;
     double2 alpha;
-    __device__ In load(int64_t i) const { return {ld_stream(c->r + i), ld_stream(c->v + i)}; }
+    __device__ explicit OpK2Bicg(SolveCtx* c_) : c(c_), r(c_->r), v(c_->v), s(c_->s), alpha(c_->alpha) {}
+    __device__ In load(int64_t i) const { return {ld_stream(r + i), ld_stream(v + i)}; }
     __device__ void apply(int64_t i, const In& in, double (&acc)[1]) const {
-        double2 s = in.r;
-        s.x = fma(-alpha.x, in.v.x, fma(alpha.y, in.v.y, s.x));
-        s.y = fma(-alpha.x, in.v.y, fma(-alpha.y, in.v.x, s.y));
-        c->s[i] = s;
-        acc[0] += cabs2(s);
+        double2 o = in.r;
+        o.x = fma(-alpha.x, in.v.x, fma(alpha.y, in.v.y, o.x));
+        o.y = fma(-alpha.x, in.v.y, fma(-alpha.y, in.v.x, o.y));
+        s[i] = o;
+        acc[0] += cabs2(o);
     }
     __device__ void finish(double (&acc)[1]) const { reduce_finish<S_K2_BICG, 1>(c, acc); }
 };
 
 struct OpK4Bicg {  // x += αp + ωs ; r = s − ωt ; {‖r‖², ⟨r̂, r⟩}   (half: x += αp only)
     static constexpr int K = 3;
+    static constexpr int U = 1;  // 5 input streams: one element per thread per step keeps registers ≤ 64
     struct In { double2 x, p, s, t, rh; };
     SolveCtx* c;
+    double2 *__restrict__ x, *__restrict__ r;
+    const double2 *__restrict__ p, *__restrict__ s, *__restrict__ t, *__restrict__ rh;
     double2 alpha, omega;
     bool half;
+    __device__ OpK4Bicg(SolveCtx* c_, bool half_)
+        : c(c_), x(c_->x), r(c_->r), p(c_->p), s(c_->s), t(c_->t), rh(c_->rh), alpha(c_->alpha),
+          omega(c_->omega), half(half_) {}
     __device__ In load(int64_t i) const {
         In v;
-        v.x = ld_stream_rw(c->x + i);
-        v.p = ld_stream(c->p + i);
+        v.x = ld_stream_rw(x + i);
+        v.p = ld_stream(p + i);
         if (!half) {
-            v.s = ld_stream(c->s + i);
-            v.t = ld_stream(c->t + i);
-            v.rh = ld_stream(c->rh + i);
+            v.s = ld_stream(s + i);
+            v.t = ld_stream(t + i);
+            v.rh = ld_stream(rh + i);
         }
         return v;
     }
     __device__ void apply(int64_t i, const In& in, double (&acc)[3]) const {
-        double2 x = in.x;
-        cfma(x, alpha, in.p);
+        double2 xn = in.x;
+        cfma(xn, alpha, in.p);
         if (half) {
-            c->x[i] = x;
+            x[i] = xn;
             return;
         }
-        cfma(x, omega, in.s);
-        c->x[i] = x;
-        double2 r = in.s;
-        r.x = fma(-omega.x, in.t.x, fma(omega.y, in.t.y, r.x));
-        r.y = fma(-omega.x, in.t.y, fma(-omega.y, in.t.x, r.y));
-        c->r[i] = r;
-        acc[0] += cabs2(r);
-        acc[1] = fma(in.rh.x, r.x, fma(in.rh.y, r.y, acc[1]));
-        acc[2] = fma(in.rh.x, r.y, fma(-in.rh.y, r.x, acc[2]));
+        cfma(xn, omega, in.s);
+        x[i] = xn;
+        double2 rn = in.s;
+        rn.x = fma(-omega.x, in.t.x, fma(omega.y, in.t.y, rn.x));
+        rn.y = fma(-omega.x, in.t.y, fma(-omega.y, in.t.x, rn.y));
+        r[i] = rn;
+        acc[0] += cabs2(rn);
+        acc[1] = fma(in.rh.x, rn.x, fma(in.rh.y, rn.y, acc[1]));
+        acc[2] = fma(in.rh.x, rn.y, fma(-in.rh.y, rn.x, acc[2]));
     }
     __device__ void finish(double (&acc)[3]) const {
         if (half) return;  // no reduction on the half-step exit; K5 clears the flag
@@ -383,34 +398,41 @@ struct OpK4Bicg {  // x += αp + ωs ; r = s − ωt ; {‖r‖², ⟨r̂, r⟩}
 
 struct OpK5Bicg {  // p = r + β(p − ω v)
     static constexpr int K = 0;
+    static constexpr int U = 2;
     struct In { double2 r, p, v; };
-    SolveCtx* c;
+    const double2 *__restrict__ r, *__restrict__ v;
+    double2* __restrict__ p;
     double2 beta, omega;
-    __device__ In load(int64_t i) const { return {ld_stream(c->r + i), ld_stream_rw(c->p + i), ld_stream(c->v + i)}; }
+    __device__ explicit OpK5Bicg(SolveCtx* c) : r(c->r), v(c->v), p(c->p), beta(c->beta), omega(c->omega) {}
+    __device__ In load(int64_t i) const { return {ld_stream(r + i), ld_stream_rw(p + i), ld_stream(v + i)}; }
     __device__ void apply(int64_t i, const In& in, double (&)[1]) const {
         double2 d = in.p;  // p − ω v
         d.x = fma(-omega.x, in.v.x, fma(omega.y, in.v.y, d.x));
         d.y = fma(-omega.x, in.v.y, fma(-omega.y, in.v.x, d.y));
-        double2 p = in.r;
-        cfma(p, beta, d);
-        c->p[i] = p;
+        double2 o = in.r;
+        cfma(o, beta, d);
+        p[i] = o;
     }
     __device__ void finish(double (&)[1]) const {}
 };
 
 struct OpK2Cg {  // x += α p ; r −= α q ; {‖r‖²}
     static constexpr int K = 1;
+    static constexpr int U = 2;
     struct In { double2 x, p, r, q; };
     SolveCtx* c;
+    double2 *__restrict__ x, *__restrict__ r;
+    const double2 *__restrict__ p, *__restrict__ q;
     double alpha;
+    __device__ explicit OpK2Cg(SolveCtx* c_) : c(c_), x(c_->x), r(c_->r), p(c_->p), q(c_->q), alpha(c_->alpha_cg) {}
     __device__ In load(int64_t i) const {
-        return {ld_stream_rw(c->x + i), ld_stream(c->p + i), ld_stream_rw(c->r + i), ld_stream(c->q + i)};
+        return {ld_stream_rw(x + i), ld_stream(p + i), ld_stream_rw(r + i), ld_stream(q + i)};
     }
     __device__ void apply(int64_t i, const In& in, double (&acc)[1]) const {
-        c->x[i] = make_double2(fma(alpha, in.p.x, in.x.x), fma(alpha, in.p.y, in.x.y));
-        const double2 r = make_double2(fma(-alpha, in.q.x, in.r.x), fma(-alpha, in.q.y, in.r.y));
-        c->r[i] = r;
-        acc[0] += cabs2(r);
+        x[i] = make_double2(fma(alpha, in.p.x, in.x.x), fma(alpha, in.p.y, in.x.y));
+        const double2 rn = make_double2(fma(-alpha, in.q.x, in.r.x), fma(-alpha, in.q.y, in.r.y));
+        r[i] = rn;
+        acc[0] += cabs2(rn);
     }
     __device__ void finish(double (&acc)[1]) const { reduce_finish<S_K2_CG, 1>(c, acc); }
 };
@@ -418,88 +440,109 @@ struct OpK2Cg {  // x += α p ; r −= α q ; {‖r‖²}
 struct OpK3Cg {  // p = r + β p
     static constexpr int K = 0;
     struct In { double2 r, p; };
-    SolveCtx* c;
+    const double2* __restrict__ r;
+    double2* __restrict__ p;
     double beta;
-    __device__ In load(int64_t i) const { return {ld_stream(c->r + i), ld_stream_rw(c->p + i)}; }
+    __device__ explicit OpK3Cg(SolveCtx* c) : r(c->r), p(c->p), beta(c->beta_cg) {}
+    __device__ In load(int64_t i) const { return {ld_stream(r + i), ld_stream_rw(p + i)}; }
     __device__ void apply(int64_t i, const In& in, double (&)[1]) const {
-        c->p[i] = make_double2(fma(beta, in.p.x, in.r.x), fma(beta, in.p.y, in.r.y));
+        p[i] = make_double2(fma(beta, in.p.x, in.r.x), fma(beta, in.p.y, in.r.y));
     }
     __device__ void finish(double (&)[1]) const {}
 };
 
 // ------------------------------------------------------------------ kernels
+#ifndef ZK_VEC_MINB
+#define ZK_VEC_MINB 4  // fused vector kernels: ≤ 64 registers, 4 CTAs / 32 warps per SM
+#endif
+// The CSR view and TMA plan are copied into registers/locals once (not re-read from the ctx).
 template <int W, int MODE, int S>
-__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_init_x0(SolveCtx* c, const double2* __restrict__ xg, int bicg) {
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_init_x0(SolveCtx* c, const double2* __restrict__ xg,
+                                                                          int bicg) {
     stamp_start<S>(c);
+    const CsrDev A = c->A;
+    const TmaPlan T = c->T;
     EpiInit<S> e(c, xg, bicg != 0);
-    spmv_any<W, MODE>(c->A, c->T, xg, e);
+    spmv_any<W, MODE>(A, T, xg, e);
 }
-__global__ void __launch_bounds__(kBlock) k_init_zero(SolveCtx* c, int bicg) {
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k_init_zero(SolveCtx* c, int bicg) {
     stamp_start<S_INIT_BICG>(c);
-    OpInitZero op{c, bicg != 0, 0};
+    OpInitZero op(c, bicg != 0);
     vec_body(c->A.n_rows, op);
 }
 template <int W, int MODE>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_true(SolveCtx* c, const double2* __restrict__ xg) {
     if (c->status == ST_ZERO_RHS) return;
     stamp_start<S_TRUE>(c);
+    const CsrDev A = c->A;
+    const TmaPlan T = c->T;
     EpiTrue e(c);
-    spmv_any<W, MODE>(c->A, c->T, xg, e);
+    spmv_any<W, MODE>(A, T, xg, e);
 }
 template <int W, int MODE>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_bicg(SolveCtx* c) {
     if (c->done) return;
     stamp_start<S_K1_BICG>(c);
+    const CsrDev A = c->A;
+    const TmaPlan T = c->T;
+    const double2* p = c->p;
     EpiK1Bicg e(c);
-    spmv_any<W, MODE>(c->A, c->T, c->p, e);
+    spmv_any<W, MODE>(A, T, p, e);
 }
-__global__ void __launch_bounds__(kBlock) k2_bicg(SolveCtx* c) {
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_bicg(SolveCtx* c) {
     if (c->done) return;
     stamp_start<S_K2_BICG>(c);
-    OpK2Bicg op{c, c->alpha};
+    OpK2Bicg op(c);
     vec_body(c->A.n_rows, op);
 }
 template <int W, int MODE>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k3_bicg(SolveCtx* c) {
     if (c->done) return;
     stamp_start<S_K3_BICG>(c);
+    const CsrDev A = c->A;
+    const TmaPlan T = c->T;
+    const double2* s = c->s;
     EpiK3Bicg e(c);
-    spmv_any<W, MODE>(c->A, c->T, c->s, e);
+    spmv_any<W, MODE>(A, T, s, e);
 }
-__global__ void __launch_bounds__(kBlock) k4_bicg(SolveCtx* c) {
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k4_bicg(SolveCtx* c) {
     const bool half = c->half != 0;
     if (c->done && !half) return;
     if (!half) stamp_start<S_K4_BICG>(c);
-    OpK4Bicg op{c, c->alpha, c->omega, half};
+    OpK4Bicg op(c, half);
     vec_body(c->A.n_rows, op);
 }
-__global__ void __launch_bounds__(kBlock) k5_bicg(SolveCtx* c) {
-    set_cond(c);
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k5_bicg(SolveCtx* c) {
     if (c->done) {
         if (c->half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;  // K4 applied x += αp
-        return;
+    } else {
+        OpK5Bicg op(c);
+        vec_body(c->A.n_rows, op);
     }
-    OpK5Bicg op{c, c->beta, c->omega};
-    vec_body(c->A.n_rows, op);
+    set_cond(c);  // after the stream loop: the device-runtime call does not pressure its registers
 }
 template <int W, int MODE>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cg(SolveCtx* c) {
     if (c->done) return;
     stamp_start<S_K1_CG>(c);
+    const CsrDev A = c->A;
+    const TmaPlan T = c->T;
+    const double2* p = c->p;
     EpiK1Cg e(c);
-    spmv_any<W, MODE>(c->A, c->T, c->p, e);
+    spmv_any<W, MODE>(A, T, p, e);
 }
-__global__ void __launch_bounds__(kBlock) k2_cg(SolveCtx* c) {
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_cg(SolveCtx* c) {
     if (c->done) return;
     stamp_start<S_K2_CG>(c);
-    OpK2Cg op{c, c->alpha_cg};
+    OpK2Cg op(c);
     vec_body(c->A.n_rows, op);
 }
-__global__ void __launch_bounds__(kBlock) k3_cg(SolveCtx* c) {
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k3_cg(SolveCtx* c) {
+    if (!c->done) {
+        OpK3Cg op(c);
+        vec_body(c->A.n_rows, op);
+    }
     set_cond(c);
-    if (c->done) return;
-    OpK3Cg op{c, c->beta_cg};
-    vec_body(c->A.n_rows, op);
 }
 __global__ void k_set_ctx(SolveCtx* c, SolveCtx h) {
     *c = h;
@@ -707,7 +750,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         hc.r = vec[0]; hc.p = vec[1]; hc.q = vec[2];
     }
     double2* xg = A->dist ? vec[L.nvec - 1] : nullptr;  // gather copy of x0 / x with halo slots
-    hc.A = CsrDev{A->row_ptr, A->col, A->val, A->n_rows};
+    hc.A = csr_dev(A);
     hc.T = A->tma;
     hc.tol = tol;
     hc.maxit = maxit;

@@ -25,62 +25,68 @@ namespace zk {
 #ifndef ZK_DEFAULT_LP
 #define ZK_DEFAULT_LP 1
 #endif
+#ifndef ZK_SPMV_U
+#define ZK_SPMV_U 4
+#endif
 template <int W, class Epi, int LP = ZK_DEFAULT_LP>
 __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
     static_assert(W >= 1 && W <= 32 && (W & (W - 1)) == 0, "W must be a power of two <= 32");
     constexpr int RPB = kBlock / W;  // rows per block step
-    constexpr int U = 4;             // nonzeros per lane per chunk
+    constexpr int U = ZK_SPMV_U;     // nonzeros per lane per chunk
     constexpr int KA = Epi::K > 0 ? Epi::K : 1;
     const uint64_t pol = make_policy<LP>();
     double acc[KA];
 #pragma unroll
     for (int k = 0; k < KA; k++) acc[k] = 0.0;
 
+    // 32-bit row / in-row indices (n_rows < 2^31 is checked at create); nnz offsets stay 64-bit
+    // only in the per-row base pointers, so each chunk costs one address computation.
     const int sub = threadIdx.x & (W - 1);
     const int grp = threadIdx.x / W;
-    const int64_t n = A.n_rows;
-    const int64_t G = gridDim.x;
-    int64_t tile = blockIdx.x;
-    int64_t row = tile * RPB + grp;
-    int64_t rs = 0, re = 0;
+    const int n = (int)A.n_rows;
+    const int G = gridDim.x;
+    int row = blockIdx.x * RPB + grp;
+    int64_t rs = 0;
+    int len = 0;
     typename Epi::Pre pre{};
     if (row < n) {
         rs = __ldg(A.row_ptr + row);
-        re = __ldg(A.row_ptr + row + 1);
+        len = (int)(__ldg(A.row_ptr + row + 1) - rs);
         if (sub == 0) pre = epi.pre(row);
     }
-    for (; tile * RPB < n; tile += G) {
-        // bounds of this lane's row in the next tile, consumed one iteration later
-        const int64_t nrow = (tile + G) * RPB + grp;
-        int64_t nrs = 0, nre = 0;
+    for (int tile = blockIdx.x; tile * RPB < n; tile += G) {
+        // bounds (and epilogue operands) of this lane's row in the next tile, used next iteration
+        const int nrow = row + G * RPB;
+        int64_t nrs = 0;
+        int nlen = 0;
         typename Epi::Pre npre{};
         if (nrow < n) {
             nrs = __ldg(A.row_ptr + nrow);
-            nre = __ldg(A.row_ptr + nrow + 1);
+            nlen = (int)(__ldg(A.row_ptr + nrow + 1) - nrs);
             if (sub == 0) npre = epi.pre(nrow);
         }
         double2 sum = make_double2(0.0, 0.0);
-        if (row < n) {
-            for (int64_t base = rs; base < re; base += U * W) {
-                double2 v[U];
-                int c[U];
+        const double2* vr = A.val + rs;
+        const int* cr = A.col + rs;
+        for (int base = sub; base < len; base += U * W) {
+            double2 v[U];
+            int c[U];
 #pragma unroll
-                for (int u = 0; u < U; u++) {
-                    const int64_t p = base + u * W + sub;
-                    if (p < re) {
-                        v[u] = ld_mat<LP>(A.val + p, pol);
-                        c[u] = ld_mat<LP>(A.col + p, pol);
-                    } else {
-                        v[u] = make_double2(0.0, 0.0);
-                        c[u] = -1;
-                    }
+            for (int u = 0; u < U; u++) {
+                const int j = base + u * W;
+                if (j < len) {
+                    v[u] = ld_mat<LP>(vr + j, pol);
+                    c[u] = ld_mat<LP>(cr + j, pol);
+                } else {
+                    v[u] = make_double2(0.0, 0.0);
+                    c[u] = -1;
                 }
-                double2 xv[U];
-#pragma unroll
-                for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather(x + c[u]) : make_double2(0.0, 0.0);
-#pragma unroll
-                for (int u = 0; u < U; u++) cfma(sum, v[u], xv[u]);
             }
+            double2 xv[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather(x + c[u]) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < U; u++) cfma(sum, v[u], xv[u]);
         }
 #pragma unroll
         for (int o = W / 2; o > 0; o >>= 1) {
@@ -90,7 +96,7 @@ __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __rest
         if (sub == 0 && row < n) epi.row(row, sum, pre, acc);
         row = nrow;
         rs = nrs;
-        re = nre;
+        len = nlen;
         pre = npre;
     }
     epi.finish(acc);
@@ -99,8 +105,15 @@ __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __rest
 // Grid-stride elementwise body with U elements in flight per thread.
 //   Op::K, Op::In, In load(int64_t i), void apply(int64_t i, const In&, double (&acc)[K]), finish(acc)
 template <class Op>
+struct vec_unroll {
+    template <class T> static constexpr int get(decltype(T::U)*) { return T::U; }
+    template <class T> static constexpr int get(...) { return 4; }
+    static constexpr int value = get<Op>(nullptr);
+};
+
+template <class Op>
 __device__ __forceinline__ void vec_body(int64_t n, Op& op) {
-    constexpr int U = 4;
+    constexpr int U = vec_unroll<Op>::value;  // elements in flight per thread (Op::U, default 4)
     constexpr int KA = Op::K > 0 ? Op::K : 1;
     double acc[KA];
 #pragma unroll

@@ -132,58 +132,75 @@ __device__ __forceinline__ void spmv_tma_body(const CsrDev& A, const TmaPlan& T,
 
     if (warp == 0) {
         // ---------------- producer
-        if (lane == 0) {
-            int64_t k = 0;
-            TileBounds cur{0, 0};
-            if (blockIdx.x < T.n_tiles) cur = tile_bounds(A, T, blockIdx.x);
-            for (int64_t t = blockIdx.x; t < T.n_tiles; t += G, k++) {
-                const int s = (int)(k % S);
-                TileBounds nxt{0, 0};
-                if (t + G < T.n_tiles) nxt = tile_bounds(A, T, t + G);  // consumed next iteration
-                if (k >= S) mbar_wait(&empty[s], (uint32_t)(((k / S) - 1) & 1));
-                tma_issue(A, T, t, cur, zk_dyn_smem + s * T.stage_bytes, &full[s]);
-                cur = nxt;
+        // lane j holds the bounds of tile batch + j·G; the next batch of 32 is loaded while the
+        // current one is issued, so the row_ptr latency never sits on the issue path
+        auto load_batch = [&](int64_t tb, int64_t& ps, int64_t& pe) {
+            const int64_t t = tb + lane * G;
+            if (t < T.n_tiles) {
+                const TileBounds b = tile_bounds(A, T, t);
+                ps = b.ps;
+                pe = b.pe;
             }
+        };
+        int64_t cps = 0, cpe = 0, k = 0;
+        load_batch(blockIdx.x, cps, cpe);
+        for (int64_t tb = blockIdx.x; tb < T.n_tiles; tb += 32 * G) {
+            int64_t nps = 0, npe = 0;
+            load_batch(tb + 32 * G, nps, npe);
+            for (int j = 0; j < 32; j++, k++) {
+                const int64_t t = tb + j * G;
+                if (t >= T.n_tiles) break;
+                const TileBounds b{__shfl_sync(0xffffffffu, cps, j), __shfl_sync(0xffffffffu, cpe, j)};
+                if (lane == 0) {
+                    const int s = (int)(k % S);
+                    if (k >= S) mbar_wait(&empty[s], (uint32_t)(((k / S) - 1) & 1));
+                    tma_issue(A, T, t, b, zk_dyn_smem + s * T.stage_bytes, &full[s]);
+                }
+                __syncwarp();
+            }
+            cps = nps;
+            cpe = npe;
         }
-        __syncwarp();
     } else {
-        // ---------------- consumers
+        // ---------------- consumers (32-bit in-tile offsets; the ≤3 trailing columns past the
+        // last 16-B aligned column copy exist only in the matrix's final tile: uniform branch)
         const int ct = threadIdx.x - 32;     // consumer thread id
         const int sub = ct & (W - 1);
         const int grp = ct / W;
-        int64_t k = 0;
-        for (int64_t t = blockIdx.x; t < T.n_tiles; t += G, k++) {
-            const int s = (int)(k % S);
+        int k = 0;
+        for (int t = blockIdx.x; t < T.n_tiles; t += (int)G, k++) {
+            const int s = k % S;
             const char* stage = zk_dyn_smem + s * T.stage_bytes;
             mbar_wait(&full[s], (uint32_t)((k / S) & 1));
             const double2* sval = (const double2*)stage;
-            const int* scol = (const int*)(stage + T.off_col);
             const int64_t* srp = (const int64_t*)(stage + T.off_rp);
-            const int64_t r0 = t * T.R;
-            const int rows = (int)min((int64_t)T.R, A.n_rows - r0);
+            const int r0 = t * T.R;
+            const int rows = min(T.R, (int)A.n_rows - r0);
             const int64_t ps = srp[0];
-            const int64_t cs = ps & ~(int64_t)3;
-            const int64_t ce = min((srp[rows] + 3) & ~(int64_t)3, T.nnz4);
+            const int* scol = (const int*)(stage + T.off_col) + (int)(ps & 3);
+            const bool tail = srp[rows] > T.nnz4;
             for (int lr0 = 0; lr0 < rows; lr0 += GROUPS) {  // all consumer lanes iterate together
                 const int lr = lr0 + grp;
                 double2 sum = make_double2(0.0, 0.0);
                 if (lr < rows) {
-                    const int64_t rs = srp[lr], re = srp[lr + 1];
-                    for (int64_t base = rs; base < re; base += U * W) {
+                    const int rb = (int)(srp[lr] - ps);
+                    const int len = (int)(srp[lr + 1] - srp[lr]);
+                    const double2* sv = sval + rb;
+                    const int* sc = scol + rb;
+                    for (int j0 = sub; j0 < len; j0 += U * W) {
                         int c[U];
 #pragma unroll
                         for (int u = 0; u < U; u++) {
-                            const int64_t p = base + u * W + sub;
-                            c[u] = p < re ? (p < ce ? scol[p - cs] : __ldg(A.col + p)) : -1;
+                            const int j = j0 + u * W;
+                            c[u] = j < len ? sc[j] : -1;
+                            if (tail && j < len && ps + rb + j >= T.nnz4) c[u] = __ldg(A.col + ps + rb + j);
                         }
                         double2 xv[U];
 #pragma unroll
                         for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather(x + c[u]) : make_double2(0.0, 0.0);
 #pragma unroll
-                        for (int u = 0; u < U; u++) {
-                            const int64_t p = base + u * W + sub;
-                            if (c[u] >= 0) cfma(sum, sval[p - ps], xv[u]);
-                        }
+                        for (int u = 0; u < U; u++)
+                            if (c[u] >= 0) cfma(sum, sv[j0 + u * W], xv[u]);
                     }
                 }
 #pragma unroll
@@ -194,7 +211,7 @@ __device__ __forceinline__ void spmv_tma_body(const CsrDev& A, const TmaPlan& T,
                 if (sub == 0 && lr < rows) epi.row(r0 + lr, sum, epi.pre(r0 + lr), acc);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
         }
     }
     epi.finish(acc);
@@ -246,7 +263,7 @@ namespace zk {
 #define ZK_TMA_MINB 6
 #endif
 #ifndef ZK_SPMV_MINB
-#define ZK_SPMV_MINB 1
+#define ZK_SPMV_MINB 4
 #endif
 __host__ __device__ constexpr int spmv_min_blocks(int mode) { return mode == 1 ? ZK_TMA_MINB : ZK_SPMV_MINB; }
 }  // namespace zk

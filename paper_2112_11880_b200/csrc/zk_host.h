@@ -92,6 +92,10 @@ zk_status with_spmv(const zk_csr_s* A, F&& f) {
     }
 }
 
+inline CsrDev csr_dev(const zk_csr_s* A) {
+    return CsrDev{A->row_ptr, A->col, A->val, A->n_rows};
+}
+
 struct LaunchCfg {
     int grid;
     int smem;

@@ -47,12 +47,14 @@ def spmv(a):
     n, nnz = m["n"], m["nnz"]
     x = torch.from_numpy(gen.rand_vector(n, 1)).cuda()
     y = torch.empty_like(x)
-    for spec in a.maps.split(","):                      # mode:W[:stages:stage_nnz]
+    for spec in a.maps.split(","):                      # mode:W[:stages:stage_nnz[:span]]
         f = spec.split(":")
         env = {"ZK_SPMV_MODE": f[0], "ZK_SPMV_W": f[1]}
-        if len(f) > 2:
+        if len(f) > 3 and f[2]:
             env.update(ZK_TMA_STAGES=f[2], ZK_TMA_NNZ=f[3])
-        for k in ("ZK_TMA_STAGES", "ZK_TMA_NNZ"):
+        if len(f) > 4:
+            env["ZK_SPMV_SPAN"] = f[4]
+        for k in ("ZK_TMA_STAGES", "ZK_TMA_NNZ", "ZK_SPMV_SPAN"):
             os.environ.pop(k, None)
         os.environ.update(env)
         A = zk.csr_create(rp, ci, va, n, borrow=True)
