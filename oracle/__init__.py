@@ -53,7 +53,7 @@ def _lib():
         lib.oracle_zscal.restype = None
         lib.oracle_zcsrmv.argtypes = [I64, P, P, P, D, D, P, D, D, P, I]
         lib.oracle_zcsrmv.restype = None
-        for f in (lib.oracle_bicgstab, lib.oracle_cg):
+        for f in (lib.oracle_bicgstab, lib.oracle_cg, lib.oracle_bicgstab_jacobi):
             f.argtypes = [I64, P, P, P, P, P, D, ctypes.c_int32, I, P, P, P, P]
             f.restype = I
         _h = lib
@@ -145,3 +145,8 @@ def bicgstab(A, b, x0=None, tol=1e-8, maxit=1000, order=ORD_SEQ) -> dict:
 def cg(A, b, x0=None, tol=1e-8, maxit=1000, order=ORD_SEQ) -> dict:
     """O7 CG (north-star addition)."""
     return _solve(_lib().oracle_cg, A, b, x0, tol, maxit, order)
+
+
+def bicgstab_jacobi(A, b, x0=None, tol=1e-8, maxit=1000, order=ORD_SEQ) -> dict:
+    """NEXT-1: Jacobi-preconditioned BiCGStab, the paper's P-Bi-CGSTAB."""
+    return _solve(_lib().oracle_bicgstab_jacobi, A, b, x0, tol, maxit, order)

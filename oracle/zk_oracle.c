@@ -372,3 +372,145 @@ done:
     free(r); free(p); free(q);
     return status;
 }
+
+/*
+ * NEXT-1: Jacobi-preconditioned BiCGStab, the paper's "P-Bi-CGSTAB" (§4; the
+ * preconditioner is unnamed there, SPEC S:296-322 reads it as Jacobi).  The Templates
+ * preconditioned BiCGSTAB step by step with M = diag(A) (complex reciprocal of the stored
+ * diagonal): p̂ = M⁻¹p, v = A p̂, ŝ = M⁻¹s, t = A ŝ, x += α p̂ + ω ŝ.  Residuals, tests and
+ * breakdown floors are those of O6 (unpreconditioned r, so tol is comparable).
+ * A row without a stored nonzero diagonal makes M singular: returns ST_BREAKDOWN_RHO with
+ * iters = 0 and hist[0] unset (the GPU reports ZK_ERR_DIM at setup instead).
+ */
+static int jacobi_inverse(const csr_t* A, double* dinv) {
+    for (int64_t i = 0; i < A->n; i++) {
+        cplx d = {0, 0};
+        int found = 0;
+        for (int64_t p = A->row_ptr[i]; p < A->row_ptr[i + 1]; p++)
+            if (A->col[p] == i) { d.re = RE(A->val, p); d.im = IM(A->val, p); found = 1; }
+        if (!found || (d.re == 0.0 && d.im == 0.0)) return 0;
+        cplx one = {1, 0};
+        cplx q = cdiv(one, d);                                  /* 1/d written out (R7) */
+        RE(dinv, i) = q.re;
+        IM(dinv, i) = q.im;
+    }
+    return 1;
+}
+
+static void apply_jacobi(int64_t n, const double* dinv, const double* in, double* out) {
+    for (int64_t i = 0; i < n; i++) {
+        cplx d = {RE(dinv, i), IM(dinv, i)}, v = {RE(in, i), IM(in, i)};
+        cplx r = cmul(d, v);
+        RE(out, i) = r.re;
+        IM(out, i) = r.im;
+    }
+}
+
+int oracle_bicgstab_jacobi(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                           const double* b, const double* x0, double tol, int32_t maxit, int order,
+                           double* x, int32_t* iters, double* hist, double* out_true_relres) {
+    csr_t A = {n, row_ptr, col, val, order};
+    size_t bytes = (size_t)(2 * n) * sizeof(double);
+    double *r = malloc(bytes), *rh = malloc(bytes), *p = malloc(bytes), *v = malloc(bytes),
+           *s = malloc(bytes), *t = malloc(bytes), *ph = malloc(bytes), *sh = malloc(bytes),
+           *dinv = malloc(bytes);
+    int status = ST_MAXIT;
+    *iters = 0;
+    *out_true_relres = NAN;
+    if (!jacobi_inverse(&A, dinv)) { status = ST_BREAKDOWN_RHO; goto done; }
+
+    if (x0) {                                                  /* r = b − A x0 */
+        memcpy(x, x0, bytes);
+        spmv(&A, x, r);
+        for (int64_t i = 0; i < 2 * n; i++) r[i] = b[i] - r[i];
+    } else {
+        memset(x, 0, bytes);
+        memcpy(r, b, bytes);
+    }
+    double nb = nrm(&A, b);
+    if (nb == 0.0) { status = ST_ZERO_RHS; goto done; }
+    double rnorm = nrm(&A, r);
+    hist[0] = rnorm / nb;
+    if (!isfinite(hist[0])) { status = ST_NONFINITE; goto done; }
+    if (hist[0] <= tol) { status = ST_CONVERGED; goto done_true; }
+
+    memcpy(rh, r, bytes);                                      /* r̂ = r0 */
+    double nrh = rnorm;
+    cplx rho_prev = {1, 0}, alpha = {1, 0}, omega = {1, 0};
+    memset(p, 0, bytes);
+    memset(v, 0, bytes);
+
+    for (int32_t j = 1; j <= maxit; j++) {
+        cplx rho = dotc(&A, rh, r);                            /* ρ = ⟨r̂, r⟩ */
+        if (!cfinite(rho)) { status = ST_NONFINITE; break; }
+        if (cabs_(rho) <= 1e-30 * nrh * rnorm) { status = ST_BREAKDOWN_RHO; break; }
+        if (j == 1) {
+            memcpy(p, r, bytes);
+        } else {
+            cplx beta = cmul(cdiv(rho, rho_prev), cdiv(alpha, omega));
+            for (int64_t i = 0; i < n; i++) {                  /* p = r + β(p − ω v) */
+                cplx pv = {RE(p, i), IM(p, i)}, vv = {RE(v, i), IM(v, i)};
+                cplx wv = cmul(omega, vv);
+                cplx d = {pv.re - wv.re, pv.im - wv.im};
+                cplx bd = cmul(beta, d);
+                RE(p, i) = RE(r, i) + bd.re;
+                IM(p, i) = IM(r, i) + bd.im;
+            }
+        }
+        apply_jacobi(n, dinv, p, ph);                          /* p̂ = M⁻¹ p */
+        spmv(&A, ph, v);                                       /* v = A p̂ */
+        cplx sigma = dotc(&A, rh, v);
+        double vnorm = nrm(&A, v);
+        if (!cfinite(sigma)) { status = ST_NONFINITE; break; }
+        if (cabs_(sigma) <= 1e-30 * nrh * vnorm) { status = ST_BREAKDOWN_SIGMA; break; }
+        alpha = cdiv(rho, sigma);
+        for (int64_t i = 0; i < n; i++) {                      /* s = r − α v */
+            cplx vv = {RE(v, i), IM(v, i)};
+            cplx av = cmul(alpha, vv);
+            RE(s, i) = RE(r, i) - av.re;
+            IM(s, i) = IM(r, i) - av.im;
+        }
+        double snorm = nrm(&A, s);
+        if (!isfinite(snorm)) { status = ST_NONFINITE; break; }
+        if (snorm / nb <= tol) {                               /* half-step exit: x += α p̂ */
+            for (int64_t i = 0; i < n; i++) {
+                cplx pv = {RE(ph, i), IM(ph, i)};
+                cplx ap = cmul(alpha, pv);
+                RE(x, i) += ap.re;
+                IM(x, i) += ap.im;
+            }
+            hist[j] = snorm / nb;
+            *iters = j;
+            status = ST_CONVERGED;
+            goto done_true;
+        }
+        apply_jacobi(n, dinv, s, sh);                          /* ŝ = M⁻¹ s */
+        spmv(&A, sh, t);                                       /* t = A ŝ */
+        double tau = oracle_sumsq(n, t, order);
+        if (!isfinite(tau)) { status = ST_NONFINITE; break; }
+        if (tau == 0.0) { status = ST_BREAKDOWN_OMEGA; break; }
+        cplx ts = dotc(&A, t, s);                              /* ω = ⟨t, s⟩/τ */
+        omega.re = ts.re / tau;
+        omega.im = ts.im / tau;
+        for (int64_t i = 0; i < n; i++) {                      /* x += α p̂ + ω ŝ ; r = s − ω t */
+            cplx pv = {RE(ph, i), IM(ph, i)}, sv = {RE(sh, i), IM(sh, i)}, tv = {RE(t, i), IM(t, i)};
+            cplx ap = cmul(alpha, pv), ws = cmul(omega, sv), wt = cmul(omega, tv);
+            RE(x, i) += ap.re + ws.re;
+            IM(x, i) += ap.im + ws.im;
+            RE(r, i) = RE(s, i) - wt.re;
+            IM(r, i) = IM(s, i) - wt.im;
+        }
+        rnorm = nrm(&A, r);
+        hist[j] = rnorm / nb;
+        *iters = j;
+        if (!isfinite(hist[j]) || !cfinite(omega)) { status = ST_NONFINITE; break; }
+        if (hist[j] <= tol) { status = ST_CONVERGED; break; }
+        if (cabs_(omega) <= 1e-30) { status = ST_BREAKDOWN_OMEGA; break; }
+        rho_prev = rho;
+    }
+done_true:
+    *out_true_relres = true_relres(&A, b, x, nb, t);
+done:
+    free(r); free(rh); free(p); free(v); free(s); free(t); free(ph); free(sh); free(dinv);
+    return status;
+}

@@ -183,12 +183,21 @@ static void choose_mapping(zk_csr_s* A) {
     if (const char* e = getenv("ZK_TMA_STAGES")) stages = atoi(e) < 2 ? 2 : (atoi(e) > 8 ? 8 : atoi(e));
     if (const char* e = getenv("ZK_TMA_NNZ")) stage_nnz = atoi(e) < 256 ? 256 : atoi(e);
     const bool tma_ok = make_tma_plan(A->n_rows, A->nnz, A->max_len, &A->tma, stages, stage_nnz);
-    if (mode != 0 && mode != 1) mode = 0;  // measured: sub-warp + L2 evict_normal beats TMA staging on C4
+    const bool aligned = ((uintptr_t)A->val % 32 == 0) && ((uintptr_t)A->col % 16 == 0);
+    if (mode < 0 || mode > 2) mode = 0;  // measured: sub-warp W=4 beats blocked-4 (1000-1360 µs) and TMA
     if (mode == 1 && !tma_ok) mode = 0;
+    if (mode == 2 && !aligned) mode = 0;
     A->spmv_mode = mode;
-    if (w != 2 && w != 4 && w != 8 && w != 16 && w != 32) {
-        // ≈ 8 nonzeros per lane (two chunks of U = 4): W = 4 for the 27-point rows (measured best
-        // on C4 in-loop: 925 µs vs 1027 µs for W = 8)
+    const bool forced = (w == 2 || w == 4 || w == 8 || w == 16 || w == 32);
+    if (mode == 2) {
+        // lanes ≈ aligned 4-blocks per row (a 27-nonzero row spans ≤ 8): one round of loads
+        if (!forced) {
+            w = 4;
+            while (w < 16 && 4.0 * w < A->mean_len + 4.0) w *= 2;
+        }
+        w = w <= 4 ? 4 : (w >= 16 ? 16 : 8);
+    } else if (!forced) {
+        // ≈ 8 nonzeros per lane (two chunks of U = 4): W = 4 for the 27-point rows
         w = 2;
         while (w < 32 && 8.0 * w < A->mean_len) w *= 2;
     }

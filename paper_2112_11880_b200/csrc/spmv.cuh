@@ -102,6 +102,100 @@ __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __rest
     epi.finish(acc);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Blocked mapping (MODE 2, the default for rows of ≥ 8 nonzeros): a row's range [rs, re) is
+// covered by the 16-B aligned blocks of 4 nonzeros that intersect it; lane `sub` of the row's W
+// lanes takes blocks sub, sub+W, ...  One block = one 128-bit column load + two 256-bit value
+// loads (LDG.E.256, L2 evict_normal), so a warp instruction covers whole aligned sectors: the
+// per-lane strided mapping above requested ~7 sectors of column indices and ~20 of values per
+// 8-row instruction group (ncu: L2 at 73 % of peak, column sectors 3x their payload).  Entries of
+// the block outside [rs, re) belong to the neighbouring rows and are masked.  Requires 32-B aligned
+// values, 16-B aligned columns (checked at create); the final block of the array (nnz % 4 != 0)
+// is read element-wise.
+__device__ __forceinline__ void ld_val_pair(const double2* p, double2& a, double2& b) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_normal.v4.b64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
+}
+__device__ __forceinline__ int4 ld_col4(const int* p, uint64_t pol) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+
+template <int W, class Epi>
+__device__ __forceinline__ void spmv_body_b4(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
+    static_assert(W >= 2 && W <= 32 && (W & (W - 1)) == 0, "W must be a power of two");
+    constexpr int RPB = kBlock / W;
+    constexpr int KA = Epi::K > 0 ? Epi::K : 1;
+    const uint64_t pol = make_policy<1>();
+    double acc[KA];
+#pragma unroll
+    for (int k = 0; k < KA; k++) acc[k] = 0.0;
+    const int sub = threadIdx.x & (W - 1);
+    const int grp = threadIdx.x / W;
+    const int n = (int)A.n_rows;
+    const int64_t nnz_full = A.nnz & ~(int64_t)3;  // blocks below this are complete
+    const int G = gridDim.x;
+    int row = blockIdx.x * RPB + grp;
+    int64_t rs = 0, re = 0;
+    typename Epi::Pre pre{};
+    if (row < n) {
+        rs = __ldg(A.row_ptr + row);
+        re = __ldg(A.row_ptr + row + 1);
+        if (sub == 0) pre = epi.pre(row);
+    }
+    for (int tile = blockIdx.x; tile * RPB < n; tile += G) {
+        const int nrow = row + G * RPB;
+        int64_t nrs = 0, nre = 0;
+        typename Epi::Pre npre{};
+        if (nrow < n) {
+            nrs = __ldg(A.row_ptr + nrow);
+            nre = __ldg(A.row_ptr + nrow + 1);
+            if (sub == 0) npre = epi.pre(nrow);
+        }
+        double2 sum = make_double2(0.0, 0.0);
+        const int64_t b0 = rs & ~(int64_t)3;
+        for (int64_t p0 = b0 + 4 * sub; p0 < re; p0 += 4 * W) {
+            double2 v[4];
+            int c[4];
+            if (p0 < nnz_full) {
+                const int4 c4 = ld_col4(A.col + p0, pol);
+                ld_val_pair(A.val + p0, v[0], v[1]);
+                ld_val_pair(A.val + p0 + 2, v[2], v[3]);
+                c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
+            } else {  // the array's final partial block
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const bool in = p0 + u < A.nnz;
+                    c[u] = in ? __ldg(A.col + p0 + u) : 0;
+                    v[u] = in ? __ldg(A.val + p0 + u) : make_double2(0.0, 0.0);
+                }
+            }
+            double2 xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const bool in = p0 + u >= rs && p0 + u < re;
+                xv[u] = in ? ld_gather(x + c[u]) : make_double2(0.0, 0.0);
+                if (!in) v[u] = make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) cfma(sum, v[u], xv[u]);
+        }
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) {
+            sum.x += __shfl_xor_sync(0xffffffffu, sum.x, o, W);
+            sum.y += __shfl_xor_sync(0xffffffffu, sum.y, o, W);
+        }
+        if (sub == 0 && row < n) epi.row(row, sum, pre, acc);
+        row = nrow;
+        rs = nrs;
+        re = nre;
+        pre = npre;
+    }
+    epi.finish(acc);
+}
+
 // Grid-stride elementwise body with U elements in flight per thread.
 //   Op::K, Op::In, In load(int64_t i), void apply(int64_t i, const In&, double (&acc)[K]), finish(acc)
 template <class Op>

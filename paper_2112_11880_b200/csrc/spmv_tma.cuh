@@ -249,6 +249,8 @@ template <int W, int MODE, class Epi>
 __device__ __forceinline__ void spmv_any(const CsrDev& A, const TmaPlan& T, const double2* __restrict__ x, Epi& epi) {
     if constexpr (MODE == 1) {
         spmv_tma_body<W>(A, T, x, epi);
+    } else if constexpr (MODE == 2) {
+        spmv_body_b4<W>(A, x, epi);
     } else {
         spmv_body<W>(A, x, epi);
     }

@@ -76,6 +76,13 @@ namespace zk {
 template <class F>
 zk_status with_spmv(const zk_csr_s* A, F&& f) {
     using std::integral_constant;
+    if (A->spmv_mode == 2) {
+        switch (A->W) {
+            case 4: return f(integral_constant<int, 4>{}, integral_constant<int, 2>{});
+            case 16: return f(integral_constant<int, 16>{}, integral_constant<int, 2>{});
+            default: return f(integral_constant<int, 8>{}, integral_constant<int, 2>{});
+        }
+    }
     if (A->spmv_mode == 1) {
         switch (A->W) {
             case 4: return f(integral_constant<int, 4>{}, integral_constant<int, 1>{});
@@ -93,7 +100,7 @@ zk_status with_spmv(const zk_csr_s* A, F&& f) {
 }
 
 inline CsrDev csr_dev(const zk_csr_s* A) {
-    return CsrDev{A->row_ptr, A->col, A->val, A->n_rows};
+    return CsrDev{A->row_ptr, A->col, A->val, A->n_rows, A->nnz};
 }
 
 struct LaunchCfg {

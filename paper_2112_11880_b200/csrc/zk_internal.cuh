@@ -173,6 +173,7 @@ struct CsrDev {
     const int* col;
     const double2* val;
     int64_t n_rows;
+    int64_t nnz;
 };
 
 }  // namespace zk

@@ -30,8 +30,10 @@ def row_scale(m, x):
 
 
 MAPPINGS = [(0, 2, None), (0, 4, None), (0, 8, None), (0, 16, None), (0, 32, None),
-            (1, 4, None), (1, 8, None), (1, 16, None), (1, 8, (2, 700)), (1, 4, (4, 640))]
-MAP_IDS = [f"{'tma' if m else 'subwarp'}-W{w}" + (f"-S{c[0]}-nnz{c[1]}" if c else "") for m, w, c in MAPPINGS]
+            (1, 4, None), (1, 8, None), (1, 16, None), (1, 8, (2, 700)), (1, 4, (4, 640)),
+            (2, 4, None), (2, 8, None), (2, 16, None)]
+MAP_NAMES = {0: "subwarp", 1: "tma", 2: "blocked4"}
+MAP_IDS = [f"{MAP_NAMES[m]}-W{w}" + (f"-S{c[0]}-nnz{c[1]}" if c else "") for m, w, c in MAPPINGS]
 
 
 def make_csr(m, W=None, mode=None, tma=None, **kw):
@@ -83,6 +85,28 @@ def test_zcsrmv_integer_exact_bitwise(mapping):
     assert np.array_equal(y.cpu().numpy(), oracle.zcsrmv(m, x))
 
 
+def test_blocked_mapping_alignment_fallback_and_tail():
+    """The blocked-4 mapping needs 32-B aligned values: a borrowed, misaligned value array falls
+    back to the sub-warp mapping; nnz % 4 != 0 exercises the element-wise final block."""
+    m = gen.random_csr(2001, seed=21, max_len=30)
+    assert m["nnz"] % 4 != 0
+    x = gen.rand_vector(2001, 3)
+    want = oracle.zcsrmv(m, x)
+    rp, ci = cuda(m["row_ptr"]), cuda(m["col_idx"])
+    buf = torch.zeros(m["nnz"] + 1, dtype=torch.complex128, device=DEV)
+    buf[1:] = cuda(m["values"])
+    vals = buf[1:]                                                # 16-B but not 32-B aligned
+    A = zk.csr_create(rp, ci, vals, 2001, borrow=True)
+    assert A.info["spmv_mode"] == 0
+    y = torch.empty(2001, dtype=torch.complex128, device=DEV)
+    zk.zcsrmv(A, 1, cuda(x), 0, y)
+    assert np.all(np.abs(y.cpu().numpy() - want) <= 1e-13 * row_scale(m, x) + 1e-300)
+    B = make_csr(m, 8, 2)
+    assert B.info["spmv_mode"] == 2
+    zk.zcsrmv(B, 1, cuda(x), 0, y)
+    assert np.all(np.abs(y.cpu().numpy() - want) <= 1e-13 * row_scale(m, x) + 1e-300)
+
+
 def test_zcsrmv_beta_zero_ignores_nan_and_empty_rows():
     m = gen.random_csr(777, seed=5)
     x = gen.rand_vector(777, 1)
@@ -93,7 +117,7 @@ def test_zcsrmv_beta_zero_ignores_nan_and_empty_rows():
     assert np.all(got[np.diff(m["row_ptr"]) == 0] == 0)
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C3T"])
 def test_zcsrmv_paper_shapes(cfg, mode):
     m = gen.make_matrix(cfg)

@@ -188,3 +188,51 @@ def test_cg_not_hpd():
     r = oracle.cg(diag_csr(np.full(10, -1.0)), gen.rand_vector(10, 1))
     assert r["status"] == "NOT_HPD" and r["iters"] == 0
     assert oracle.cg(diag_csr([1.0]), np.zeros(1))["status"] == "ZERO_RHS"
+
+
+# ------------------------------------------------------------------ Jacobi P-BiCGStab (NEXT-1)
+def row_scaled(m, seed=5):
+    """(D_s·A, D_s) with a wild complex row scaling D_s (|d| in [e^-3, e^3], random phase)."""
+    rng = np.random.default_rng(seed)
+    ds = np.exp(rng.uniform(-3, 3, m["n"])) * np.exp(1j * rng.uniform(0, 2 * np.pi, m["n"]))
+    rows = np.repeat(np.arange(m["n"]), np.diff(m["row_ptr"]))
+    return dict(m, values=m["values"] * ds[rows]), ds
+
+
+def test_jacobi_diagonal_one_iteration():
+    """for diagonal matrices one Jacobi-preconditioned BiCGStab iteration reaches the solution."""
+    d = gen.rand_vector(300, 9) + 2.0
+    b = gen.rand_vector(300, 10)
+    r = oracle.bicgstab_jacobi(diag_csr(d), b, tol=1e-12)
+    assert r["status"] == "CONVERGED" and r["iters"] == 1
+    assert np.max(np.abs(r["x"] - b / d)) <= 1e-15 * np.max(np.abs(b / d))
+    assert oracle.bicgstab(diag_csr(d), b, tol=1e-12)["iters"] > 1
+
+
+def test_jacobi_undoes_row_scaling():
+    """Right-preconditioning with M = diag(D_s·A): the D_s·A system converges like A itself (the box
+    diagonal is constant on free rows) and to the DST-I exact solution, while unpreconditioned
+    BiCGStab on D_s·A stalls."""
+    spec = gen.CONFIGS["C2"]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    ms, ds = row_scaled(m)
+    r = oracle.bicgstab_jacobi(ms, ds * b, tol=1e-8)
+    ref = oracle.bicgstab(m, b, tol=1e-8)
+    assert r["status"] == "CONVERGED"
+    assert abs(r["iters"] - ref["iters"]) <= 0.15 * ref["iters"]
+    xe = cf.box_solve(spec, b, gen.ETA)
+    assert np.linalg.norm(r["x"] - xe) / np.linalg.norm(xe) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
+    assert oracle.bicgstab(ms, ds * b, tol=1e-8, maxit=300)["status"] == "MAXIT"
+
+
+def test_jacobi_dense_lu_and_missing_diagonal():
+    m = gen.make_matrix("C1")
+    ms, ds = row_scaled(m, 7)
+    b = ds * gen.make_rhs(m)
+    D = sp.csr_matrix((ms["values"], ms["col_idx"], ms["row_ptr"]), shape=(m["n"], m["n"])).toarray()
+    x_lu = np.linalg.solve(D, b)
+    r = oracle.bicgstab_jacobi(ms, b, tol=1e-10)
+    assert np.linalg.norm(r["x"] - x_lu) / np.linalg.norm(x_lu) <= 1e-7
+    skew = csr_from_dense(np.array([[0, 1], [-1, 0]], complex))   # no stored diagonal
+    assert oracle.bicgstab_jacobi(skew, np.array([1, 0], complex))["status"] == "BREAKDOWN_RHO"
