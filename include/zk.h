@@ -62,7 +62,12 @@ enum {
 };
 
 /* ---- solver methods and outcomes ---- */
-enum { ZK_BICGSTAB = 0, ZK_CG = 1 };
+enum {
+    ZK_BICGSTAB = 0,        /* unpreconditioned BiCGStab (O6) */
+    ZK_CG = 1,              /* CG, A Hermitian positive definite (O7) */
+    ZK_BICGSTAB_JACOBI = 2  /* Jacobi (M = diag A) right-preconditioned BiCGStab, the paper's P-Bi-CGSTAB
+                               (P:308); one GPU; a zero/missing diagonal fails with ZK_ERR_INVALID_CSR */
+};
 enum {
     ZK_CONVERGED = 0, ZK_MAXIT = 1, ZK_BREAKDOWN_RHO = 2, ZK_BREAKDOWN_SIGMA = 3,
     ZK_BREAKDOWN_OMEGA = 4, ZK_NOT_HPD = 5, ZK_NONFINITE = 6
@@ -80,7 +85,7 @@ typedef struct {
     int64_t n_halo;        /* off-rank x entries received per SpMV (0 on one GPU) */
     int32_t borrowed;      /* 1 if the arrays are borrowed (ZK_PTRS_DEVICE_BORROW) */
     int32_t nranks;
-    int32_t spmv_mode;     /* 0 = sub-warp rows, 1 = TMA bulk-copy staged row tiles */
+    int32_t spmv_mode;     /* 0 = sub-warp rows, 1 = TMA bulk-copy staged row tiles, 2 = aligned 4-blocks */
     int32_t rows_per_tile; /* TMA mode: rows per staged tile */
     int32_t tma_stages;    /* TMA mode: pipeline depth */
 } zk_csr_info_t;
@@ -91,7 +96,8 @@ typedef struct {
     double true_relres;    /* ||b - A x|| / ||b|| recomputed at exit */
     int64_t n_spmv;        /* SpMV applications performed (incl. initial residual and final check) */
     double solve_ms;       /* device time of the solve (CUDA events, entry to final check) */
-    int32_t loop_mode;     /* 1 = CUDA graph WHILE node, 2 = chunked graph launches, 3 = per-iteration launches */
+    int32_t loop_mode;     /* 1 = CUDA graph WHILE node, 2 = chunked graph launches, 3 = per-iteration launches,
+                              4 = one persistent cooperative kernel (opt-in: env ZK_LOOP_MODE=4) */
     int32_t gpu_launches;  /* libzk kernels launched by this solve */
     /* in-loop kernel timing from the device global timer (first block start -> last block end),
      * summed over launches: [0] SpMV kernels (BiCGStab K1+K3 / CG K1), [1] fused vector kernels
@@ -159,7 +165,8 @@ zk_status zk_zscal(int64_t n, zk_z alpha, zk_z* x, zk_stream s);
 
 /* ---- solve(A, b, x0, tol, maxit) (§4: Krylov solve with residual
  *      tolerance, initial guess, maximum iterations) ----
- * method     ZK_BICGSTAB (unpreconditioned BiCGStab, O6) or ZK_CG (Hermitian positive definite A, O7).
+ * method     ZK_BICGSTAB (unpreconditioned BiCGStab, O6), ZK_CG (Hermitian positive definite A, O7) or
+ *            ZK_BICGSTAB_JACOBI (P-BiCGStab with M = diag(A); the first call builds A·M⁻¹ in the handle).
  * b          device zk_z[n_rows]; must not alias x.
  * x0         device zk_z[n_rows] initial guess, or NULL for zero; may alias x.
  * tol        stop when the recurrence residual ||r_j||/||b|| <= tol (BiCGStab also tests the

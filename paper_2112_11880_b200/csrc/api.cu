@@ -210,6 +210,7 @@ void dist_destroy(zk_csr_s* A);                                                 
 zk_status dist_zcsrmv(const zk_csr_s* A, double2 alpha, const double2* x, double2 beta, double2* y,
                       cudaStream_t s);                                                           // dist.cu
 int64_t dist_n_halo(const zk_csr_s* A);                                                          // dist.cu
+void jacobi_destroy(zk_csr_s* A);                                                                // jacobi.cu
 int dist_nranks(const zk_csr_s* A);                                                              // dist.cu
 }  // namespace zk
 
@@ -314,6 +315,7 @@ extern "C" zk_status zk_csr_destroy(zk_csr A) {
         if (g.graph) cudaGraphDestroy(g.graph);
     }
     if (A->dist) dist_destroy(A);
+    jacobi_destroy(A);
     if (A->owned) {
         cudaFree(A->row_ptr);
         cudaFree(A->col);

@@ -18,6 +18,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "spmv.cuh"
 #include "zk_host.h"
 
@@ -229,7 +231,7 @@ struct EpiInit {  // r = b − A x0 ; x = x0 ; r̂ = p = r ; {‖b‖², ‖r‖
     double2 *r, *p, *rh, *x;
     __device__ EpiInit(SolveCtx* c_, const double2* x0_, bool bicg)
         : c(c_), x0(x0_), b(c_->b), r(c_->r), p(c_->p), rh(bicg ? c_->rh : nullptr), x(c_->x) {}
-    __device__ Pre pre(int64_t i) const { return {ld_stream(b + i), x != x0 ? ld_gather(x0 + i) : make_double2(0, 0)}; }
+    __device__ Pre pre(int64_t i) const { return {ld_vec(b + i), x != x0 ? ld_gather_coh(x0 + i) : make_double2(0, 0)}; }
     __device__ void row(int64_t i, double2 y, const Pre& q, double (&acc)[2]) {
         const double2 rr = csub(q.b, y);
         r[i] = rr;
@@ -248,7 +250,7 @@ struct EpiTrue {  // {‖b − A x‖²}
     SolveCtx* c;
     const double2* __restrict__ b;
     __device__ explicit EpiTrue(SolveCtx* c_) : c(c_), b(c_->b) {}
-    __device__ Pre pre(int64_t i) const { return ld_stream(b + i); }
+    __device__ Pre pre(int64_t i) const { return ld_vec(b + i); }
     __device__ void row(int64_t, double2 y, const Pre& bi, double (&acc)[1]) { acc[0] += cabs2(csub(bi, y)); }
     __device__ void finish(double (&acc)[1]) { reduce_finish<S_TRUE, 1>(c, acc); }
 };
@@ -260,7 +262,7 @@ struct EpiK1Bicg {  // v = A p ; {σ = ⟨r̂, v⟩, ‖v‖²}
     double2* __restrict__ v;
     const double2* __restrict__ rh;
     __device__ explicit EpiK1Bicg(SolveCtx* c_) : c(c_), v(c_->v), rh(c_->rh) {}
-    __device__ Pre pre(int64_t i) const { return ld_stream(rh + i); }
+    __device__ Pre pre(int64_t i) const { return ld_vec(rh + i); }
     __device__ void row(int64_t i, double2 y, const Pre& r, double (&acc)[3]) {
         v[i] = y;
         acc[0] = fma(r.x, y.x, fma(r.y, y.y, acc[0]));
@@ -277,7 +279,7 @@ struct EpiK3Bicg {  // t = A s ; {⟨t, s⟩, ⟨t, t⟩}
     double2* __restrict__ t;
     const double2* __restrict__ s;
     __device__ explicit EpiK3Bicg(SolveCtx* c_) : c(c_), t(c_->t), s(c_->s) {}
-    __device__ Pre pre(int64_t i) const { return ld_gather(s + i); }
+    __device__ Pre pre(int64_t i) const { return ld_gather_coh(s + i); }
     __device__ void row(int64_t i, double2 y, const Pre& si, double (&acc)[3]) {
         t[i] = y;
         acc[0] = fma(y.x, si.x, fma(y.y, si.y, acc[0]));
@@ -294,7 +296,7 @@ struct EpiK1Cg {  // q = A p ; {δ = ⟨p, q⟩}
     double2* __restrict__ q;
     const double2* __restrict__ p;
     __device__ explicit EpiK1Cg(SolveCtx* c_) : c(c_), q(c_->q), p(c_->p) {}
-    __device__ Pre pre(int64_t i) const { return ld_gather(p + i); }
+    __device__ Pre pre(int64_t i) const { return ld_gather_coh(p + i); }
     __device__ void row(int64_t i, double2 y, const Pre& pi, double (&acc)[2]) {
         q[i] = y;
         acc[0] = fma(pi.x, y.x, fma(pi.y, y.y, acc[0]));
@@ -315,7 +317,7 @@ struct OpInitZero {  // x0 = 0: x = 0 ; r = r̂ = p = b ; {‖b‖², ‖r‖²}
     bool bicg;
     __device__ OpInitZero(SolveCtx* c_, bool bicg_)
         : c(c_), b(c_->b), x(c_->x), r(c_->r), p(c_->p), rh(c_->rh), bicg(bicg_) {}
-    __device__ In load(int64_t i) const { return {ld_stream(b + i)}; }
+    __device__ In load(int64_t i) const { return {ld_vec(b + i)}; }
     __device__ void apply(int64_t i, const In& v, double (&acc)[2]) const {
         x[i] = make_double2(0.0, 0.0);
         r[i] = v.b;
@@ -339,7 +341,7 @@ struct OpK2Bicg {  // s = r − α v ; {‖s‖²}
     double2* __restrict__ s;
     double2 alpha;
     __device__ explicit OpK2Bicg(SolveCtx* c_) : c(c_), r(c_->r), v(c_->v), s(c_->s), alpha(c_->alpha) {}
-    __device__ In load(int64_t i) const { return {ld_stream(r + i), ld_stream(v + i)}; }
+    __device__ In load(int64_t i) const { return {ld_vec(r + i), ld_vec(v + i)}; }
     __device__ void apply(int64_t i, const In& in, double (&acc)[1]) const {
         double2 o = in.r;
         o.x = fma(-alpha.x, in.v.x, fma(alpha.y, in.v.y, o.x));
@@ -364,12 +366,12 @@ struct OpK4Bicg {  // x += αp + ωs ; r = s − ωt ; {‖r‖², ⟨r̂, r⟩}
           omega(c_->omega), half(half_) {}
     __device__ In load(int64_t i) const {
         In v;
-        v.x = ld_stream_rw(x + i);
-        v.p = ld_stream(p + i);
+        v.x = ld_vec(x + i);
+        v.p = ld_vec(p + i);
         if (!half) {
-            v.s = ld_stream(s + i);
-            v.t = ld_stream(t + i);
-            v.rh = ld_stream(rh + i);
+            v.s = ld_vec(s + i);
+            v.t = ld_vec(t + i);
+            v.rh = ld_vec(rh + i);
         }
         return v;
     }
@@ -404,7 +406,7 @@ struct OpK5Bicg {  // p = r + β(p − ω v)
     double2* __restrict__ p;
     double2 beta, omega;
     __device__ explicit OpK5Bicg(SolveCtx* c) : r(c->r), v(c->v), p(c->p), beta(c->beta), omega(c->omega) {}
-    __device__ In load(int64_t i) const { return {ld_stream(r + i), ld_stream_rw(p + i), ld_stream(v + i)}; }
+    __device__ In load(int64_t i) const { return {ld_vec(r + i), ld_vec(p + i), ld_vec(v + i)}; }
     __device__ void apply(int64_t i, const In& in, double (&)[1]) const {
         double2 d = in.p;  // p − ω v
         d.x = fma(-omega.x, in.v.x, fma(omega.y, in.v.y, d.x));
@@ -426,7 +428,7 @@ struct OpK2Cg {  // x += α p ; r −= α q ; {‖r‖²}
     double alpha;
     __device__ explicit OpK2Cg(SolveCtx* c_) : c(c_), x(c_->x), r(c_->r), p(c_->p), q(c_->q), alpha(c_->alpha_cg) {}
     __device__ In load(int64_t i) const {
-        return {ld_stream_rw(x + i), ld_stream(p + i), ld_stream_rw(r + i), ld_stream(q + i)};
+        return {ld_vec(x + i), ld_vec(p + i), ld_vec(r + i), ld_vec(q + i)};
     }
     __device__ void apply(int64_t i, const In& in, double (&acc)[1]) const {
         x[i] = make_double2(fma(alpha, in.p.x, in.x.x), fma(alpha, in.p.y, in.x.y));
@@ -444,7 +446,7 @@ struct OpK3Cg {  // p = r + β p
     double2* __restrict__ p;
     double beta;
     __device__ explicit OpK3Cg(SolveCtx* c) : r(c->r), p(c->p), beta(c->beta_cg) {}
-    __device__ In load(int64_t i) const { return {ld_stream(r + i), ld_stream_rw(p + i)}; }
+    __device__ In load(int64_t i) const { return {ld_vec(r + i), ld_vec(p + i)}; }
     __device__ void apply(int64_t i, const In& in, double (&)[1]) const {
         p[i] = make_double2(fma(beta, in.p.x, in.r.x), fma(beta, in.p.y, in.r.y));
     }
@@ -471,10 +473,11 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k_init_zero(SolveCtx* c, 
     vec_body(c->A.n_rows, op);
 }
 template <int W, int MODE>
-__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_true(SolveCtx* c, const double2* __restrict__ xg) {
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_true(SolveCtx* c, const double2* __restrict__ xg,
+                                                                       CsrDev A) {
+    // A: the ORIGINAL operator (the Jacobi path iterates on A·M⁻¹ but checks ‖b − A x‖)
     if (c->status == ST_ZERO_RHS) return;
     stamp_start<S_TRUE>(c);
-    const CsrDev A = c->A;
     const TmaPlan T = c->T;
     EpiTrue e(c);
     spmv_any<W, MODE>(A, T, xg, e);
@@ -544,6 +547,102 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k3_cg(SolveCtx* c) {
     }
     set_cond(c);
 }
+// ------------------------------------------------------------------ persistent solver (loop mode 4)
+// The whole iteration loop as ONE cooperative launch for latency-bound systems (the paper's
+// Audi3D/Twingo shapes: a WHILE-graph body of 5 launches costs ~40 µs per iteration there).  The
+// phases are the same fused bodies as the per-launch kernels, separated by grid-wide barriers
+// instead of kernel boundaries; the last-block scalar steps run unchanged.  Data written in one
+// phase and read in a later one is loaded coherently (ld_vec / ld_gather_coh; the barrier's
+// gpu-scope fences order it), never through the non-coherent read-only path.
+__device__ __forceinline__ int vol_int(const int* p) { return *(const volatile int*)p; }
+
+// The phases inline into one body, which needs ~128 registers without spilling (at the 64-register
+// cap of the per-launch kernels it spilled ~1.4 KB per thread): the persistent kernel runs 2 CTAs
+// per SM, which is plenty for the latency-bound sizes it is selected for.
+template <int W>
+__device__ __forceinline__ void ph_k1_bicg(SolveCtx* c) {
+    stamp_start<S_K1_BICG>(c);
+    const CsrDev A = c->A;
+    EpiK1Bicg e(c);
+    spmv_body<W, EpiK1Bicg, ZK_DEFAULT_LP, true>(A, c->p, e);
+}
+__device__ __forceinline__ void ph_k2_bicg(SolveCtx* c) {
+    stamp_start<S_K2_BICG>(c);
+    OpK2Bicg op(c);
+    vec_body(c->A.n_rows, op);
+}
+template <int W>
+__device__ __forceinline__ void ph_k3_bicg(SolveCtx* c) {
+    stamp_start<S_K3_BICG>(c);
+    const CsrDev A = c->A;
+    EpiK3Bicg e(c);
+    spmv_body<W, EpiK3Bicg, ZK_DEFAULT_LP, true>(A, c->s, e);
+}
+__device__ __forceinline__ void ph_k4_bicg(SolveCtx* c, bool half) {
+    if (!half) stamp_start<S_K4_BICG>(c);
+    OpK4Bicg op(c, half);
+    vec_body(c->A.n_rows, op);
+}
+__device__ __forceinline__ void ph_k5_bicg(SolveCtx* c) {
+    OpK5Bicg op(c);
+    vec_body(c->A.n_rows, op);
+}
+template <int W>
+__device__ __forceinline__ void ph_k1_cg(SolveCtx* c) {
+    stamp_start<S_K1_CG>(c);
+    const CsrDev A = c->A;
+    EpiK1Cg e(c);
+    spmv_body<W, EpiK1Cg, ZK_DEFAULT_LP, true>(A, c->p, e);
+}
+__device__ __forceinline__ void ph_k2_cg(SolveCtx* c) {
+    stamp_start<S_K2_CG>(c);
+    OpK2Cg op(c);
+    vec_body(c->A.n_rows, op);
+}
+__device__ __forceinline__ void ph_k3_cg(SolveCtx* c) {
+    OpK3Cg op(c);
+    vec_body(c->A.n_rows, op);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock, 2) k_persist_bicg(SolveCtx* c) {
+    namespace cg = cooperative_groups;
+    cg::grid_group g = cg::this_grid();
+    while (!vol_int(&c->done)) {
+        ph_k1_bicg<W>(c);
+        g.sync();
+        if (!vol_int(&c->done)) ph_k2_bicg(c);
+        g.sync();
+        if (!vol_int(&c->done)) ph_k3_bicg<W>(c);
+        g.sync();
+        const bool half = vol_int(&c->half) != 0;
+        if (!vol_int(&c->done) || half) ph_k4_bicg(c, half);
+        g.sync();
+        if (vol_int(&c->done)) {
+            if (half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;
+        } else {
+            ph_k5_bicg(c);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) c->bodies += 1;
+        g.sync();
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock, 2) k_persist_cg(SolveCtx* c) {
+    namespace cg = cooperative_groups;
+    cg::grid_group g = cg::this_grid();
+    while (!vol_int(&c->done)) {
+        ph_k1_cg<W>(c);
+        g.sync();
+        if (!vol_int(&c->done)) ph_k2_cg(c);
+        g.sync();
+        if (!vol_int(&c->done)) ph_k3_cg(c);
+        if (blockIdx.x == 0 && threadIdx.x == 0) c->bodies += 1;
+        g.sync();
+    }
+}
+
 __global__ void k_set_ctx(SolveCtx* c, SolveCtx h) {
     *c = h;
     for (int i = 0; i < 16; i++) h.tickets[i] = 0u;
@@ -555,6 +654,10 @@ static int vec_grid(const zk_csr_s* A, const void* k) {
     if (cap > kMaxGrid) cap = kMaxGrid;
     return grid_for(A->n_rows, (int64_t)kBlock * 4, cap);
 }
+
+// Jacobi hooks (jacobi.cu)
+zk_status jacobi_prepare(zk_csr_s* A, cudaStream_t s);
+zk_status cscale(const zk_csr_s* A, const double2* d, const double2* in, double2* out, cudaStream_t s);
 
 // distributed hooks (dist.cu)
 zk_status dist_halo(const zk_csr_s* A, double2* xg, cudaStream_t s);           // fill halo slots of xg
@@ -714,7 +817,8 @@ static WsLayout ws_layout(const zk_csr_s* A, int method, int32_t maxit) {
 using namespace zk;
 
 extern "C" size_t zk_solve_workspace_size(zk_csr A, int32_t method, int32_t maxit) {
-    if (!A || (method != ZK_BICGSTAB && method != ZK_CG)) return 0;
+    if (!A || (method != ZK_BICGSTAB && method != ZK_CG && method != ZK_BICGSTAB_JACOBI)) return 0;
+    if (method == ZK_BICGSTAB_JACOBI) method = ZK_BICGSTAB;
     return ws_layout(A, method, maxit).total;
 }
 
@@ -722,7 +826,13 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
                               zk_z* x, int32_t* iters, double* resid_hist, zk_solve_info* info, void* workspace,
                               size_t ws_bytes, zk_stream stream) {
     if (!A || !b || !x || !iters || !resid_hist || !workspace) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
-    if (method != ZK_BICGSTAB && method != ZK_CG) return fail(ZK_ERR_INVALID_VALUE, "unknown method");
+    if (method != ZK_BICGSTAB && method != ZK_CG && method != ZK_BICGSTAB_JACOBI)
+        return fail(ZK_ERR_INVALID_VALUE, "unknown method");
+    const bool jacobi = method == ZK_BICGSTAB_JACOBI;
+    if (jacobi) {
+        ZK_TRY(jacobi_prepare(A, (cudaStream_t)stream));  // A·M⁻¹ built once, cached in the handle
+        method = ZK_BICGSTAB;
+    }
     if (!(tol > 0.0)) return fail(ZK_ERR_INVALID_VALUE, "tol must be > 0");
     if (maxit < 1) return fail(ZK_ERR_INVALID_VALUE, "maxit must be >= 1");
     if (A->n_cols != A->n_global) return fail(ZK_ERR_DIM, "solve needs a square matrix");
@@ -751,6 +861,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     }
     double2* xg = A->dist ? vec[L.nvec - 1] : nullptr;  // gather copy of x0 / x with halo slots
     hc.A = csr_dev(A);
+    if (jacobi) hc.A.val = A->jac_val;  // iterate on A' = A·M⁻¹ (u = M x)
     hc.T = A->tma;
     hc.tol = tol;
     hc.maxit = maxit;
@@ -759,13 +870,34 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     hc.dist = A->dist ? 1 : 0;
     for (int i = 0; i < 4; i++) hc.t0[i] = ~0ull;
 
-    // ---- loop mode: 1 = WHILE graph (default on one GPU), 2 = chunked graphs, 3 = direct launches
+    // ---- loop mode: 1 = WHILE graph (default), 2 = chunked graphs, 3 = direct launches, 4 = one
+    //      persistent cooperative kernel.  Mode 4 measured SLOWER on every shape (C1 52 vs 39 µs per
+    //      iteration, C3 514 vs 184: the fused phases need 128 registers → half the warps, and
+    //      coherent gathers), so it is opt-in (ZK_LOOP_MODE=4) and parity-tested, not the default.
     int mode = A->dist ? 3 : 1;
     if (const char* e = getenv("ZK_LOOP_MODE")) {
         int m = atoi(e);
-        if (m >= 1 && m <= 3) mode = m;
+        if (m >= 1 && m <= 4) mode = m;
     }
-    if (A->dist && mode == 1) mode = 3;  // NCCL inside WHILE bodies is not used
+    if (A->dist && (mode == 1 || mode == 4)) mode = 3;  // NCCL inside WHILE bodies / persistent kernels is not used
+    int persist_grid = 0;
+    const void* kp = nullptr;
+    if (mode == 4) {
+        int dev_coop = 0;
+        cudaDeviceGetAttribute(&dev_coop, cudaDevAttrCooperativeLaunch, A->dev.device);
+        const int W = A->W == 2 || A->W == 4 || A->W == 8 ? A->W : 4;
+        kp = method == ZK_BICGSTAB
+                 ? (W == 2 ? (const void*)k_persist_bicg<2>
+                           : W == 8 ? (const void*)k_persist_bicg<8> : (const void*)k_persist_bicg<4>)
+                 : (W == 2 ? (const void*)k_persist_cg<2>
+                           : W == 8 ? (const void*)k_persist_cg<8> : (const void*)k_persist_cg<4>);
+        const int cap = A->dev.num_sms * blocks_per_sm(kp, 0);
+        // one row tile per block in the SpMV phases (a smaller grid serialises dependent load
+        // chains across tiles), capped at the co-resident limit
+        int64_t g = (A->n_rows + kBlock / W - 1) / (kBlock / W);
+        persist_grid = (int)(g < 1 ? 1 : (g > cap ? cap : g));
+        if (!dev_coop || cap < 1) mode = 1;
+    }
     GraphCache& gc = A->graph[method];
     if (mode <= 2 && (gc.ws != workspace || gc.mode != mode || gc.method != method || !gc.exec)) {
         drop_graph(gc);
@@ -799,6 +931,10 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     const bool bicg = method == ZK_BICGSTAB;
     if (x0) {
         const double2* g0 = (const double2*)x0;
+        if (jacobi) {  // u0 = M x0, in the output buffer (x may alias x0)
+            ZK_TRY(cscale(A, A->jac_diag, (const double2*)x0, (double2*)x, s));
+            g0 = (const double2*)x;
+        }
         if (A->dist) {
             ZK_CUDA(cudaMemcpyAsync(xg, x0, sizeof(double2) * A->n_rows, cudaMemcpyDeviceToDevice, s));
             ZK_TRY(dist_halo(A, xg, s));
@@ -829,6 +965,9 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     SolveCtx* hdone = nullptr;  // pinned copy of the ctx for the chunked modes
     if (mode == 1) {
         ZK_CUDA(cudaGraphLaunch(gc.exec, s));
+    } else if (mode == 4) {
+        void* args[] = {&dc};
+        ZK_CUDA(cudaLaunchCooperativeKernel(kp, dim3(persist_grid), dim3(kBlock), args, 0, s));
     } else {
         ZK_CUDA(cudaMallocHost(&hdone, sizeof(SolveCtx)));
         int launched = 0;
@@ -852,6 +991,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     }
 
     // ---- exit: true relative residual ‖b − A x‖/‖b‖ (one more SpMV)
+    if (jacobi) ZK_TRY(cscale(A, A->jac_dinv, (const double2*)x, (double2*)x, s));  // x = M⁻¹ u
     const double2* gx = (const double2*)x;
     if (A->dist) {
         ZK_CUDA(cudaMemcpyAsync(xg, x, sizeof(double2) * A->n_rows, cudaMemcpyDeviceToDevice, s));
@@ -860,7 +1000,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     }
     ZK_TRY(with_spmv(A, [&](auto wc, auto mc) -> zk_status {
         constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
-        { auto kf = k_true<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); kf<<<L.grid, kBlock, L.smem, s>>>(dc, gx); }
+        { auto kf = k_true<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); kf<<<L.grid, kBlock, L.smem, s>>>(dc, gx, csr_dev(A)); }
         ZK_CUDA(cudaGetLastError());
         return ZK_OK;
     }));
@@ -890,7 +1030,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         info->loop_mode = mode;
         const int per_body = method == ZK_BICGSTAB ? 5 : 3;
         const int fins = A->dist ? (method == ZK_BICGSTAB ? 4 : 2) : 0;  // dist: 1-thread finish kernels
-        info->gpu_launches = 3 + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);
+        info->gpu_launches = mode == 4 ? 4 : 3 + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);
         for (int i = 0; i < 4; i++) {
             info->kernel_ms[i] = out.tsum[i] * 1e-6;
             info->kernel_launches[i] = out.tcnt[i];

@@ -28,7 +28,8 @@ namespace zk {
 #ifndef ZK_SPMV_U
 #define ZK_SPMV_U 4
 #endif
-template <int W, class Epi, int LP = ZK_DEFAULT_LP>
+// GCOH: gather x with coherent loads (x written earlier in the same launch: persistent solver)
+template <int W, class Epi, int LP = ZK_DEFAULT_LP, bool GCOH = false>
 __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
     static_assert(W >= 1 && W <= 32 && (W & (W - 1)) == 0, "W must be a power of two <= 32");
     constexpr int RPB = kBlock / W;  // rows per block step
@@ -84,7 +85,8 @@ __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __rest
             }
             double2 xv[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather(x + c[u]) : make_double2(0.0, 0.0);
+            for (int u = 0; u < U; u++)
+                xv[u] = c[u] >= 0 ? (GCOH ? ld_gather_coh(x + c[u]) : ld_gather(x + c[u])) : make_double2(0.0, 0.0);
 #pragma unroll
             for (int u = 0; u < U; u++) cfma(sum, v[u], xv[u]);
         }

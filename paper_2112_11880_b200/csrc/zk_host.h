@@ -58,6 +58,10 @@ struct zk_csr_s {
     int W = 8;                   // SpMV lanes per row
     int spmv_mode = 0;           // 0 = sub-warp kernel (spmv.cuh), 1 = TMA-staged tiles (spmv_tma.cuh)
     zk::TmaPlan tma{};
+    // Jacobi right preconditioning (jacobi.cu), built on the first ZK_BICGSTAB_JACOBI solve
+    double2* jac_val = nullptr;   // a_ij / a_jj
+    double2* jac_diag = nullptr;  // a_ii
+    double2* jac_dinv = nullptr;  // 1 / a_ii
     int max_len = 0;
     double mean_len = 0.0;
     zk::DeviceInfo dev;

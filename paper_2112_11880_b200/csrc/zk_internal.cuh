@@ -99,6 +99,14 @@ __device__ __forceinline__ double2 ld_stream_rw(const double2* p) {
 }
 // Gather through the read-only path (L1 + L2 reuse of x across neighbouring rows).
 __device__ __forceinline__ double2 ld_gather(const double2* p) { return __ldg(p); }
+// Coherent loads for data written earlier in the SAME launch (the persistent solver phases,
+// separated by grid-wide barriers whose gpu-scope fences invalidate L1): never .nc.
+__device__ __forceinline__ double2 ld_gather_coh(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ double2 ld_vec(const double2* p) { return ld_stream_rw(p); }
 // Coherent L2 load (partials written by other blocks of the same launch).
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 

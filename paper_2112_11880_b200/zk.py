@@ -18,7 +18,8 @@ SO_PATH = os.path.join(_PKG, "libzk.so")
 
 ZK_PTRS_HOST, ZK_PTRS_DEVICE, ZK_PTRS_DEVICE_BORROW, ZK_SKIP_VALIDATE = 0, 1, 2, 4
 ZK_BICGSTAB, ZK_CG = 0, 1
-METHODS = {"bicgstab": ZK_BICGSTAB, "cg": ZK_CG}
+ZK_BICGSTAB_JACOBI = 2
+METHODS = {"bicgstab": ZK_BICGSTAB, "cg": ZK_CG, "bicgstab_jacobi": ZK_BICGSTAB_JACOBI}
 OUTCOMES = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN_RHO", 3: "BREAKDOWN_SIGMA", 4: "BREAKDOWN_OMEGA",
             5: "NOT_HPD", 6: "NONFINITE"}
 

@@ -112,6 +112,7 @@ def test_loop_modes_bitwise_identical(mode, monkeypatch):
     """WHILE graph, chunked graphs and direct launches run the same kernels: identical results."""
     m = gen.make_matrix("C2")
     b = gen.make_rhs(m)
+    monkeypatch.setenv("ZK_LOOP_MODE", "1")
     base = gpu_solve(m, b, tol=1e-8)
     monkeypatch.setenv("ZK_LOOP_MODE", mode)
     r = gpu_solve(m, b, tol=1e-8)
@@ -186,12 +187,15 @@ def test_x0_restart_and_alias():
     assert e.value.code == -7
 
 
-def test_distributed_path_single_rank_comm():
+def test_distributed_path_single_rank_comm(monkeypatch):
     """The row-partitioned code path (NCCL comm, halo plan, allreduce + finish kernels, direct
-    launches) on a 1-rank communicator gives bitwise the same solve as the local path."""
+    launches) on a 1-rank communicator gives bitwise the same solve as the local path running the
+    same per-iteration kernels."""
     m = gen.make_matrix("C2")
     b = gen.make_rhs(m)
+    monkeypatch.setenv("ZK_LOOP_MODE", "3")
     base = gpu_solve(m, b, tol=1e-8)
+    monkeypatch.delenv("ZK_LOOP_MODE")
     comm = zk.Comm(zk.Comm.unique_id(), 1, 0, 0)
     A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"], comm=comm, row_begin=0)
     assert A.info["nranks"] == 1 and A.info["n_halo"] == 0
@@ -208,3 +212,93 @@ def test_distributed_path_single_rank_comm():
     assert d == zk.zdotc(x, y).cpu().numpy()[0]
     A.close()
     comm.close()
+
+
+# ------------------------------------------------------------------ Jacobi P-BiCGStab (NEXT-1)
+def row_scaled(m, seed=5):
+    rng = np.random.default_rng(seed)
+    ds = np.exp(rng.uniform(-3, 3, m["n"])) * np.exp(1j * rng.uniform(0, 2 * np.pi, m["n"]))
+    rows = np.repeat(np.arange(m["n"]), np.diff(m["row_ptr"]))
+    return dict(m, values=m["values"] * ds[rows]), ds
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
+def test_bicgstab_jacobi_parity(cfg):
+    """P-BiCGStab (M = diag A) on the row-scaled system against the oracle's Templates recurrences:
+    count within the order envelope, hist prefix, solution 1e-6 (L11/L12)."""
+    m0 = gen.make_matrix(cfg)
+    m, ds = row_scaled(m0)
+    b = ds * gen.make_rhs(m0)
+    r = gpu_solve(m, b, tol=1e-8, method="bicgstab_jacobi")
+    refs = [oracle.bicgstab_jacobi(m, b, tol=1e-8, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    assert r["status"] == "CONVERGED" and all(q["status"] == "CONVERGED" for q in refs)
+    assert 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    k = min(12, r["iters"], refs[0]["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= 1e-10
+    assert relerr(r["x"], refs[0]["x"]) <= 1e-6
+    assert r["true_relres"] <= 2e-8
+
+
+def test_bicgstab_jacobi_cases():
+    # diagonal: one iteration (S:341)
+    n = 500
+    d = gen.rand_vector(n, 9) + 2.0
+    m = dict(row_ptr=np.arange(n + 1, dtype=np.int64), col_idx=np.arange(n, dtype=np.int32), values=d, n=n)
+    b = gen.rand_vector(n, 10)
+    r = gpu_solve(m, b, tol=1e-12, method="bicgstab_jacobi")
+    assert r["status"] == "CONVERGED" and r["iters"] == 1
+    assert np.max(np.abs(r["x"] - b / d)) <= 1e-14 * np.max(np.abs(b / d))
+    # x0 path (u0 = M x0) against the oracle
+    m0 = gen.make_matrix("C1")
+    ms, ds = row_scaled(m0, 3)
+    bb = ds * gen.make_rhs(m0)
+    x0 = gen.rand_vector(m0["n"], 4)
+    r = gpu_solve(ms, bb, x0=x0, tol=1e-8, method="bicgstab_jacobi")
+    ref = oracle.bicgstab_jacobi(ms, bb, x0=x0, tol=1e-8)
+    assert abs(r["iters"] - ref["iters"]) <= max(1, 0.05 * ref["iters"])
+    assert np.max(np.abs(r["hist"][:8] - ref["hist"][:8]) / ref["hist"][:8]) <= 1e-10
+    # missing diagonal → ZK_ERR_INVALID_CSR naming the row
+    skew = dict(row_ptr=np.array([0, 1, 2]), col_idx=np.array([1, 0], np.int32),
+                values=np.array([1, -1], np.complex128), n=2)
+    with pytest.raises(zk.ZkError) as e:
+        gpu_solve(skew, np.array([1, 0], np.complex128), method="bicgstab_jacobi")
+    assert e.value.code == -2 and "row 0" in str(e.value)
+
+
+def test_bicgstab_jacobi_c4():
+    """C4 in the bench configuration: Jacobi P-BiCGStab converges to the DST-I exact solution."""
+    spec = gen.CONFIGS["C4"]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    A = zk.csr_create(cuda(m["row_ptr"]), cuda(m["col_idx"]), cuda(m["values"]), m["n"], borrow=True)
+    r = zk.solve(A, cuda(b), tol=1e-8, maxit=2000, method="bicgstab_jacobi")
+    assert r["status"] == "CONVERGED" and r["true_relres"] <= 2e-8
+    xe = cf.box_solve(spec, b, gen.ETA)
+    assert relerr(r["x"].cpu().numpy(), xe) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "cg", "bicgstab_jacobi"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "A3"])
+def test_persistent_loop_parity(cfg, method, monkeypatch):
+    """Loop mode 4 (one cooperative kernel, grid barriers between the fused phases) against the
+    oracle, and bitwise reproducible run to run (fixed grid, fixed-order reductions)."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "4")
+    if method == "cg":
+        m = gen.make_matrix(cfg, eta=0.0, twist_seed=gen.SEED_TWIST)
+        b = np.exp(1j * m["phase"]) * gen.make_rhs(m)
+        refs = [oracle.cg(m, b, tol=1e-8)]
+    else:
+        m = gen.make_matrix(cfg)
+        b = gen.make_rhs(m)
+        fn = oracle.bicgstab if method == "bicgstab" else oracle.bicgstab_jacobi
+        refs = [fn(m, b, tol=1e-8, order=o) for o in ORDERS]
+    r = gpu_solve(m, b, tol=1e-8, method=method)
+    r2 = gpu_solve(m, b, tol=1e-8, method=method)
+    assert r["loop_mode"] == 4 and r["status"] == "CONVERGED"
+    assert np.array_equal(r["x"], r2["x"]) and np.array_equal(r["hist"], r2["hist"])
+    its = [q["iters"] for q in refs]
+    assert 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    k = min(12, r["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= 1e-10
+    assert relerr(r["x"], refs[0]["x"]) <= 1e-6
