@@ -66,6 +66,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+// Programmatic dependent launch: the loop kernels are launched with the PDL attribute so the
+// next kernel's blocks are scheduled while the previous one drains; each waits for the previous
+// grid's completion (and memory) before touching the context.  No-ops without the attribute.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void set_cond(SolveCtx* c) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         c->bodies += 1;
@@ -484,6 +492,7 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_true(SolveCtx
 }
 template <int W, int MODE>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_bicg(SolveCtx* c) {
+    pdl_enter();
     if (c->done) return;
     stamp_start<S_K1_BICG>(c);
     const CsrDev A = c->A;
@@ -493,6 +502,7 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_bicg(SolveCt
     spmv_any<W, MODE>(A, T, p, e);
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_bicg(SolveCtx* c) {
+    pdl_enter();
     if (c->done) return;
     stamp_start<S_K2_BICG>(c);
     OpK2Bicg op(c);
@@ -500,6 +510,7 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_bicg(SolveCtx* c) {
 }
 template <int W, int MODE>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k3_bicg(SolveCtx* c) {
+    pdl_enter();
     if (c->done) return;
     stamp_start<S_K3_BICG>(c);
     const CsrDev A = c->A;
@@ -509,6 +520,7 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k3_bicg(SolveCt
     spmv_any<W, MODE>(A, T, s, e);
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k4_bicg(SolveCtx* c) {
+    pdl_enter();
     const bool half = c->half != 0;
     if (c->done && !half) return;
     if (!half) stamp_start<S_K4_BICG>(c);
@@ -516,6 +528,7 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k4_bicg(SolveCtx* c) {
     vec_body(c->A.n_rows, op);
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k5_bicg(SolveCtx* c) {
+    pdl_enter();
     if (c->done) {
         if (c->half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;  // K4 applied x += αp
     } else {
@@ -526,6 +539,7 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k5_bicg(SolveCtx* c) {
 }
 template <int W, int MODE>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cg(SolveCtx* c) {
+    pdl_enter();
     if (c->done) return;
     stamp_start<S_K1_CG>(c);
     const CsrDev A = c->A;
@@ -535,12 +549,14 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cg(SolveCtx*
     spmv_any<W, MODE>(A, T, p, e);
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_cg(SolveCtx* c) {
+    pdl_enter();
     if (c->done) return;
     stamp_start<S_K2_CG>(c);
     OpK2Cg op(c);
     vec_body(c->A.n_rows, op);
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k3_cg(SolveCtx* c) {
+    pdl_enter();
     if (!c->done) {
         OpK3Cg op(c);
         vec_body(c->A.n_rows, op);
@@ -672,37 +688,49 @@ static zk_status dist_finish(const zk_csr_s* A, SolveCtx* c, int count, cudaStre
 }
 
 // enqueue one iteration of `method`
-static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc, int method, cudaStream_t s) {
+// loop-kernel launch, with the PDL attribute when `pdl`
+template <class... Args>
+static zk_status launch_loop(bool pdl, void (*k)(Args...), int grid, int smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBlock);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    ZK_CUDA(cudaLaunchKernelEx(&cfg, k, args...));
+    return ZK_OK;
+}
+
+static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc, int method, cudaStream_t s,
+                                   bool pdl = false) {
     const bool dist = A->dist != nullptr;
+    if (dist) pdl = false;
     return with_spmv(A, [&](auto wc, auto mc) -> zk_status {
         constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
         if (method == ZK_BICGSTAB) {
             if (dist) ZK_TRY(dist_halo(A, hc.p, s));
-            { auto kf = k1_bicg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); kf<<<L.grid, kBlock, L.smem, s>>>(dc); }
-            ZK_CUDA(cudaGetLastError());
+            { auto kf = k1_bicg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
             if (dist) ZK_TRY((dist_finish<S_K1_BICG>(A, dc, 3, s)));
-            k2_bicg<<<vec_grid(A, (const void*)k2_bicg), kBlock, 0, s>>>(dc);
-            ZK_CUDA(cudaGetLastError());
+            ZK_TRY(launch_loop(pdl, k2_bicg, vec_grid(A, (const void*)k2_bicg), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_K2_BICG>(A, dc, 1, s)));
             if (dist) ZK_TRY(dist_halo(A, hc.s, s));
-            { auto kf = k3_bicg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); kf<<<L.grid, kBlock, L.smem, s>>>(dc); }
-            ZK_CUDA(cudaGetLastError());
+            { auto kf = k3_bicg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
             if (dist) ZK_TRY((dist_finish<S_K3_BICG>(A, dc, 3, s)));
-            k4_bicg<<<vec_grid(A, (const void*)k4_bicg), kBlock, 0, s>>>(dc);
-            ZK_CUDA(cudaGetLastError());
+            ZK_TRY(launch_loop(pdl, k4_bicg, vec_grid(A, (const void*)k4_bicg), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_K4_BICG>(A, dc, 3, s)));
-            k5_bicg<<<vec_grid(A, (const void*)k5_bicg), kBlock, 0, s>>>(dc);
-            ZK_CUDA(cudaGetLastError());
+            ZK_TRY(launch_loop(pdl, k5_bicg, vec_grid(A, (const void*)k5_bicg), 0, s, dc));
         } else {
             if (dist) ZK_TRY(dist_halo(A, hc.p, s));
-            { auto kf = k1_cg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); kf<<<L.grid, kBlock, L.smem, s>>>(dc); }
-            ZK_CUDA(cudaGetLastError());
+            { auto kf = k1_cg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
             if (dist) ZK_TRY((dist_finish<S_K1_CG>(A, dc, 2, s)));
-            k2_cg<<<vec_grid(A, (const void*)k2_cg), kBlock, 0, s>>>(dc);
-            ZK_CUDA(cudaGetLastError());
+            ZK_TRY(launch_loop(pdl, k2_cg, vec_grid(A, (const void*)k2_cg), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_K2_CG>(A, dc, 1, s)));
-            k3_cg<<<vec_grid(A, (const void*)k3_cg), kBlock, 0, s>>>(dc);
-            ZK_CUDA(cudaGetLastError());
+            ZK_TRY(launch_loop(pdl, k3_cg, vec_grid(A, (const void*)k3_cg), 0, s, dc));
         }
         return ZK_OK;
     });
@@ -715,7 +743,8 @@ static void drop_graph(GraphCache& g) {
 }
 
 // WHILE-node graph: body = one iteration; condition written by the last kernel of the body.
-static zk_status build_while_graph(zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc, int method, GraphCache& g) {
+static zk_status build_while_graph(zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc, int method, GraphCache& g,
+                                   bool pdl) {
     cudaGraph_t graph = nullptr;
     ZK_CUDA(cudaGraphCreate(&graph, 0));
     cudaGraphConditionalHandle h;
@@ -743,7 +772,7 @@ static zk_status build_while_graph(zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc
         cudaGraphDestroy(graph);
         return cuda_fail(e, "cudaStreamBeginCaptureToGraph", __FILE__, __LINE__);
     }
-    zk_status st = enqueue_iteration(A, dc, hc, method, A->cap_stream);
+    zk_status st = enqueue_iteration(A, dc, hc, method, A->cap_stream, pdl);
     cudaGraph_t captured = nullptr;
     e = cudaStreamEndCapture(A->cap_stream, &captured);
     if (st != ZK_OK || e != cudaSuccess) {
@@ -901,7 +930,12 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     GraphCache& gc = A->graph[method];
     if (mode <= 2 && (gc.ws != workspace || gc.mode != mode || gc.method != method || !gc.exec)) {
         drop_graph(gc);
-        zk_status st = mode == 1 ? build_while_graph(A, dc, hc, method, gc) : build_chunk_graph(A, dc, hc, method, gc);
+        const bool pdl = !(getenv("ZK_PDL") && atoi(getenv("ZK_PDL")) == 0);
+        zk_status st = mode == 1 ? build_while_graph(A, dc, hc, method, gc, pdl) : build_chunk_graph(A, dc, hc, method, gc);
+        if (st != ZK_OK && mode == 1 && pdl) {  // PDL edges inside the WHILE body unavailable: retry without
+            drop_graph(gc);
+            st = build_while_graph(A, dc, hc, method, gc, false);
+        }
         if (st != ZK_OK && mode == 1) {  // conditional nodes unavailable: fall back to chunked graphs
             drop_graph(gc);
             mode = 2;
