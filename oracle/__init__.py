@@ -53,7 +53,11 @@ def _lib():
         lib.oracle_zscal.restype = None
         lib.oracle_zcsrmv.argtypes = [I64, P, P, P, D, D, P, D, D, P, I]
         lib.oracle_zcsrmv.restype = None
-        for f in (lib.oracle_bicgstab, lib.oracle_cg, lib.oracle_bicgstab_jacobi):
+        lib.oracle_zassign.argtypes = [I64, D, D, P]
+        lib.oracle_zassign.restype = None
+        lib.oracle_zaxmy.argtypes = [I64, P, P]
+        lib.oracle_zaxmy.restype = None
+        for f in (lib.oracle_bicgstab, lib.oracle_cg, lib.oracle_bicgstab_jacobi, lib.oracle_cocg):
             f.argtypes = [I64, P, P, P, P, P, D, ctypes.c_int32, I, P, P, P, P]
             f.restype = I
         _h = lib
@@ -150,3 +154,23 @@ def cg(A, b, x0=None, tol=1e-8, maxit=1000, order=ORD_SEQ) -> dict:
 def bicgstab_jacobi(A, b, x0=None, tol=1e-8, maxit=1000, order=ORD_SEQ) -> dict:
     """NEXT-1: Jacobi-preconditioned BiCGStab, the paper's P-Bi-CGSTAB."""
     return _solve(_lib().oracle_bicgstab_jacobi, A, b, x0, tol, maxit, order)
+
+
+def zassign(n: int, alpha) -> np.ndarray:
+    """NEXT-4 ZASSIGN: x_i ← α (PAPER.md T2 P:89-107, read as a fill, L16)."""
+    out = np.empty(n, np.complex128)
+    a = complex(alpha)
+    _lib().oracle_zassign(n, a.real, a.imag, _ptr(out))
+    return out
+
+
+def zaxmy(x, y) -> np.ndarray:
+    """NEXT-4 ZAXMY: returns x ⊙ y ("EWProduct", T5)."""
+    x, out = _c128(x), _c128(y).copy()
+    _lib().oracle_zaxmy(len(x), _ptr(x), _ptr(out))
+    return out
+
+
+def cocg(A, b, x0=None, tol=1e-8, maxit=1000, order=ORD_SEQ) -> dict:
+    """NEXT-4 COCG: CG with the unconjugated form, complex symmetric A (van der Vorst & Melissen)."""
+    return _solve(_lib().oracle_cocg, A, b, x0, tol, maxit, order)

@@ -514,3 +514,105 @@ done:
     free(r); free(rh); free(p); free(v); free(s); free(t); free(ph); free(sh); free(dinv);
     return status;
 }
+
+/* NEXT-4: ZASSIGN — "assign of a vector" (§3, T2), read as a fill x_i ← α
+   (T2's bytes per element imply a write-only pass). */
+void oracle_zassign(int64_t n, double ar, double ai, double* x) {
+    for (int64_t i = 0; i < n; i++) {
+        RE(x, i) = ar;
+        IM(x, i) = ai;
+    }
+}
+
+/* NEXT-4: ZAXMY — element-wise product y_i ← x_i · y_i ("EWProduct", T5;
+   the listing's unused α is ignored, L17). */
+void oracle_zaxmy(int64_t n, const double* x, double* y) {
+    for (int64_t i = 0; i < n; i++) {
+        double a = RE(x, i), b = IM(x, i), c = RE(y, i), d = IM(y, i);
+        RE(y, i) = a * c - b * d;
+        IM(y, i) = a * d + b * c;
+    }
+}
+
+/* unconjugated bilinear form Σ x_i·y_i (COCG) */
+static cplx dotu(const csr_t* A, const double* x, const double* y) {
+    /* Re Σ x y = Σ (xr·yr − xi·yi), Im = Σ (xr·yi + xi·yr), in the requested order via the
+       conjugated routine: Σ x y = Σ conj(conj(x)) y → conjugate x into a scratch copy. */
+    size_t bytes = (size_t)(2 * A->n) * sizeof(double);
+    double* xc = malloc(bytes);
+    for (int64_t i = 0; i < A->n; i++) { RE(xc, i) = RE(x, i); IM(xc, i) = -IM(x, i); }
+    cplx r = dotc(A, xc, y);
+    free(xc);
+    return r;
+}
+
+/*
+ * NEXT-4: COCG (van der Vorst & Melissen 1990) — CG with the unconjugated bilinear form for
+ * complex SYMMETRIC A (Aᵀ = A, the Helmholtz matrices with absorption, η > 0), where Hermitian
+ * CG does not apply (L9).  Step by step:
+ *   r = b − A x0; p = r; ρ = rᵀr; hist[0] = ‖r‖/‖b‖
+ *   loop: q = A p; μ = pᵀq (μ = 0 → BREAKDOWN_SIGMA); α = ρ/μ; x += α p; r −= α q;
+ *         hist[j] = ‖r‖/‖b‖ (tests as O7); ρ' = rᵀr (|ρ'| ≤ 1e-30‖r‖² → BREAKDOWN_RHO);
+ *         p = r + (ρ'/ρ) p; ρ = ρ'.
+ */
+int oracle_cocg(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val, const double* b,
+                const double* x0, double tol, int32_t maxit, int order, double* x, int32_t* iters,
+                double* hist, double* out_true_relres) {
+    csr_t A = {n, row_ptr, col, val, order};
+    size_t bytes = (size_t)(2 * n) * sizeof(double);
+    double *r = malloc(bytes), *p = malloc(bytes), *q = malloc(bytes);
+    int status = ST_MAXIT;
+    *iters = 0;
+    *out_true_relres = NAN;
+    if (x0) {
+        memcpy(x, x0, bytes);
+        spmv(&A, x, r);
+        for (int64_t i = 0; i < 2 * n; i++) r[i] = b[i] - r[i];
+    } else {
+        memset(x, 0, bytes);
+        memcpy(r, b, bytes);
+    }
+    double nb = nrm(&A, b);
+    if (nb == 0.0) { status = ST_ZERO_RHS; goto done; }
+    memcpy(p, r, bytes);
+    cplx rho = dotu(&A, r, r);
+    hist[0] = nrm(&A, r) / nb;
+    if (!isfinite(hist[0])) { status = ST_NONFINITE; goto done; }
+    if (hist[0] <= tol) { status = ST_CONVERGED; goto done_true; }
+    for (int32_t j = 1; j <= maxit; j++) {
+        spmv(&A, p, q);                                        /* q = A p */
+        cplx mu = dotu(&A, p, q);                              /* μ = pᵀ q */
+        if (!cfinite(mu)) { status = ST_NONFINITE; break; }
+        if (mu.re == 0.0 && mu.im == 0.0) { status = ST_BREAKDOWN_SIGMA; break; }
+        cplx alpha = cdiv(rho, mu);                            /* α = ρ/μ */
+        for (int64_t i = 0; i < n; i++) {                      /* x += α p ; r −= α q */
+            cplx pv = {RE(p, i), IM(p, i)}, qv = {RE(q, i), IM(q, i)};
+            cplx ap = cmul(alpha, pv), aq = cmul(alpha, qv);
+            RE(x, i) += ap.re;
+            IM(x, i) += ap.im;
+            RE(r, i) -= aq.re;
+            IM(r, i) -= aq.im;
+        }
+        double rn2 = oracle_sumsq(n, r, order);
+        hist[j] = sqrt(rn2) / nb;
+        *iters = j;
+        if (!isfinite(hist[j])) { status = ST_NONFINITE; break; }
+        if (hist[j] <= tol) { status = ST_CONVERGED; break; }
+        cplx rho_new = dotu(&A, r, r);                         /* ρ' = rᵀ r */
+        if (!cfinite(rho_new)) { status = ST_NONFINITE; break; }
+        if (cabs_(rho_new) <= 1e-30 * rn2) { status = ST_BREAKDOWN_RHO; break; }
+        cplx beta = cdiv(rho_new, rho);                        /* p = r + (ρ'/ρ) p */
+        for (int64_t i = 0; i < n; i++) {
+            cplx pv = {RE(p, i), IM(p, i)};
+            cplx bp = cmul(beta, pv);
+            RE(p, i) = RE(r, i) + bp.re;
+            IM(p, i) = IM(r, i) + bp.im;
+        }
+        rho = rho_new;
+    }
+done_true:
+    *out_true_relres = true_relres(&A, b, x, nb, q);
+done:
+    free(r); free(p); free(q);
+    return status;
+}

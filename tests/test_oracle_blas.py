@@ -198,3 +198,16 @@ def test_axpy_scal_spec_examples():
     want = np.array([complex(int(a.real * u.real - a.imag * u.imag + v.real),
                              int(a.real * u.imag + a.imag * u.real + v.imag)) for u, v in zip(xi, yi)])
     assert np.array_equal(oracle.zaxpy(a, xi, yi), want)
+
+
+# ---------------------------------------------------------------- ZASSIGN / ZAXMY (NEXT-4)
+def test_zassign_zaxmy():
+    assert np.array_equal(oracle.zassign(5, 1.5 - 2j), np.full(5, 1.5 - 2j))
+    assert oracle.zaxmy([1j], [1j])[0] == -1 + 0j                  # i·i = −1
+    x, y = gen.int_vector(10_000, 1), gen.int_vector(10_000, 2)
+    want = np.array([complex(int(a.real * b.real - a.imag * b.imag), int(a.real * b.imag + a.imag * b.real))
+                     for a, b in zip(x, y)])
+    assert np.array_equal(oracle.zaxmy(x, y), want)
+    ones = np.ones(100, np.complex128)
+    y = gen.rand_vector(100, 3)
+    assert np.array_equal(oracle.zaxmy(ones, y), y)                 # identity

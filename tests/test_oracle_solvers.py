@@ -236,3 +236,48 @@ def test_jacobi_dense_lu_and_missing_diagonal():
     assert np.linalg.norm(r["x"] - x_lu) / np.linalg.norm(x_lu) <= 1e-7
     skew = csr_from_dense(np.array([[0, 1], [-1, 0]], complex))   # no stored diagonal
     assert oracle.bicgstab_jacobi(skew, np.array([1, 0], complex))["status"] == "BREAKDOWN_RHO"
+
+
+# ------------------------------------------------------------------ COCG (NEXT-4)
+@pytest.mark.parametrize("c", [2.0, 1j, 0.3 - 2j])
+def test_cocg_scalar_identity(c):
+    b = gen.rand_vector(80, 1)
+    r = oracle.cocg(diag_csr(np.full(80, c)), b, tol=1e-12)
+    assert r["status"] == "CONVERGED" and r["iters"] == 1
+    assert np.max(np.abs(r["x"] - b / c)) <= 1e-15 * np.max(np.abs(b / c))
+
+
+def test_cocg_equals_cg_on_real_spd():
+    """For real symmetric positive definite A and real b the bilinear and sesquilinear forms agree:
+    COCG and CG produce the same iterates (same count, same history)."""
+    m = gen.make_matrix("C2", eta=0.0)
+    b = gen.make_rhs(m).real.astype(np.complex128)
+    r, rc = oracle.cocg(m, b), oracle.cg(m, b)
+    assert r["iters"] == rc["iters"]
+    assert np.max(np.abs(r["hist"] - rc["hist"]) / rc["hist"]) <= 1e-13
+    assert np.max(np.abs(r["x"] - rc["x"])) <= 1e-13 * np.max(np.abs(rc["x"]))
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "A3"])
+def test_cocg_complex_symmetric_closed_form(cfg):
+    """COCG on the absorbing (η = 0.05, complex symmetric) box: DST-I exact solution within 2κ·tol."""
+    spec = gen.CONFIGS[cfg]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    r = oracle.cocg(m, b, tol=1e-8)
+    assert r["status"] == "CONVERGED"
+    xe = cf.box_solve(spec, b, gen.ETA)
+    assert np.linalg.norm(r["x"] - xe) / np.linalg.norm(xe) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
+    assert abs(r["true_relres"] - r["hist"][-1]) <= 1e-8
+
+
+def test_cocg_dense_lu_and_breakdown():
+    m = gen.make_matrix("C1")
+    b = gen.make_rhs(m)
+    D = sp.csr_matrix((m["values"], m["col_idx"], m["row_ptr"]), shape=(m["n"], m["n"])).toarray()
+    x_lu = np.linalg.solve(D, b)
+    r = oracle.cocg(m, b, tol=1e-10)
+    assert np.linalg.norm(r["x"] - x_lu) / np.linalg.norm(x_lu) <= 1e-7
+    # b = (1, i): bᵀb = 0 → the bilinear form degenerates (quasi-null start): ρ = 0, μ = 0
+    A = diag_csr([1.0, 1.0])
+    assert oracle.cocg(A, np.array([1, 1j]))["status"] == "BREAKDOWN_SIGMA"
