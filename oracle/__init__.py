@@ -57,7 +57,7 @@ def _lib():
         lib.oracle_zassign.restype = None
         lib.oracle_zaxmy.argtypes = [I64, P, P]
         lib.oracle_zaxmy.restype = None
-        for f in (lib.oracle_bicgstab, lib.oracle_cg, lib.oracle_bicgstab_jacobi, lib.oracle_cocg):
+        for f in (lib.oracle_bicgstab, lib.oracle_cg, lib.oracle_bicgstab_jacobi, lib.oracle_cocg, lib.oracle_tfqmr):
             f.argtypes = [I64, P, P, P, P, P, D, ctypes.c_int32, I, P, P, P, P]
             f.restype = I
         _h = lib
@@ -174,3 +174,8 @@ def zaxmy(x, y) -> np.ndarray:
 def cocg(A, b, x0=None, tol=1e-8, maxit=1000, order=ORD_SEQ) -> dict:
     """NEXT-4 COCG: CG with the unconjugated form, complex symmetric A (van der Vorst & Melissen)."""
     return _solve(_lib().oracle_cocg, A, b, x0, tol, maxit, order)
+
+
+def tfqmr(A, b, x0=None, tol=1e-8, maxit=1000, order=ORD_SEQ) -> dict:
+    """NEXT-2 TFQMR (Freund; Kelley's two-half-step form), the paper's P-TFQMR without M."""
+    return _solve(_lib().oracle_tfqmr, A, b, x0, tol, maxit, order)

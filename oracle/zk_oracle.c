@@ -167,6 +167,7 @@ void oracle_zcsrmv(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, c
 /* complex scalar helpers (written out; no Annex-G handling)                 */
 /* ------------------------------------------------------------------------ */
 typedef struct { double re, im; } cplx;
+static cplx make_cplx_real(double a) { cplx r = {a, 0.0}; return r; }
 static cplx cmul(cplx a, cplx b) { cplx r = {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; return r; }
 static cplx cdiv(cplx a, cplx b) {
     double den = b.re * b.re + b.im * b.im;
@@ -614,5 +615,128 @@ done_true:
     *out_true_relres = true_relres(&A, b, x, nb, q);
 done:
     free(r); free(p); free(q);
+    return status;
+}
+
+/*
+ * NEXT-2: TFQMR (Freund 1993), the paper's "P-TFQMR" without preconditioner (§4 P:308,
+ * Tables 9/10), in Kelley's two-half-step form ("Iterative Methods for Linear and
+ * Nonlinear Equations", Alg. tfqmr), complex arithmetic with the Hermitian product, r̃ = r0:
+ *   w = y1 = r0; u1 = v = A y1; d = 0; τ = ‖r0‖; θ = η = 0; ρ = ⟨r̃, r0⟩
+ *   outer iteration k = 1, 2, ...:
+ *     σ = ⟨r̃, v⟩ (0 → BREAKDOWN_SIGMA); α = ρ/σ; y2 = y1 − α v; u2 = A y2
+ *     half steps j = 1, 2 (m = 2k − 2 + j):
+ *        w = w − α u_j; d = y_j + (θ² η / α) d; θ = ‖w‖/τ; c = (1 + θ²)^(-1/2); τ = τ θ c;
+ *        η = c² α; x = x + η d;  converged if τ √(m+1) / ‖b‖ ≤ tol (the quasi-residual bound, an
+ *        upper bound on ‖r_m‖/‖b‖) → iters = k (a first-half-step exit counts as one)
+ *     ρ' = ⟨r̃, w⟩ (|ρ'| ≤ 1e-30‖r̃‖‖w‖ → BREAKDOWN_RHO); β = ρ'/ρ; ρ = ρ'
+ *     y1 = w + β y2; u1 = A y1; v = u1 + β (u2 + β v)
+ *   hist[k] = τ √(2k+1)/‖b‖ after the second half step (hist[0] = 1 for x0 = 0... = ‖r0‖/‖b‖),
+ *   or the first half step's bound on a half-step exit.  θ, c, τ are real; α, β, ρ, σ, η complex.
+ */
+int oracle_tfqmr(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val, const double* b,
+                 const double* x0, double tol, int32_t maxit, int order, double* x, int32_t* iters,
+                 double* hist, double* out_true_relres) {
+    csr_t A = {n, row_ptr, col, val, order};
+    size_t bytes = (size_t)(2 * n) * sizeof(double);
+    double *r = malloc(bytes), *w = malloc(bytes), *y1 = malloc(bytes), *y2 = malloc(bytes), *u1 = malloc(bytes),
+           *u2 = malloc(bytes), *v = malloc(bytes), *d = malloc(bytes), *rt = malloc(bytes);
+    int status = ST_MAXIT;
+    *iters = 0;
+    *out_true_relres = NAN;
+    if (x0) {
+        memcpy(x, x0, bytes);
+        spmv(&A, x, r);
+        for (int64_t i = 0; i < 2 * n; i++) r[i] = b[i] - r[i];
+    } else {
+        memset(x, 0, bytes);
+        memcpy(r, b, bytes);
+    }
+    double nb = nrm(&A, b);
+    if (nb == 0.0) { status = ST_ZERO_RHS; goto done; }
+    double tau = nrm(&A, r);
+    hist[0] = tau / nb;
+    if (!isfinite(hist[0])) { status = ST_NONFINITE; goto done; }
+    if (hist[0] <= tol) { status = ST_CONVERGED; goto done_true; }
+    memcpy(w, r, bytes);
+    memcpy(y1, r, bytes);
+    memcpy(rt, r, bytes);
+    spmv(&A, y1, u1);                                          /* u1 = v = A y1 */
+    memcpy(v, u1, bytes);
+    memset(d, 0, bytes);
+    double theta = 0.0, nrt = tau;
+    cplx eta = {0, 0};
+    cplx rho = dotc(&A, rt, r);
+    for (int32_t k = 1; k <= maxit; k++) {
+        cplx sigma = dotc(&A, rt, v);                          /* σ = ⟨r̃, v⟩ */
+        if (!cfinite(sigma)) { status = ST_NONFINITE; break; }
+        if (sigma.re == 0.0 && sigma.im == 0.0) { status = ST_BREAKDOWN_SIGMA; break; }
+        cplx alpha = cdiv(rho, sigma);                         /* α = ρ/σ */
+        for (int64_t i = 0; i < n; i++) {                      /* y2 = y1 − α v */
+            cplx vv = {RE(v, i), IM(v, i)};
+            cplx av = cmul(alpha, vv);
+            RE(y2, i) = RE(y1, i) - av.re;
+            IM(y2, i) = IM(y1, i) - av.im;
+        }
+        spmv(&A, y2, u2);                                      /* u2 = A y2 */
+        int conv = 0;
+        for (int j = 1; j <= 2 && !conv; j++) {
+            const int m = 2 * k - 2 + j;
+            const double* yj = j == 1 ? y1 : y2;
+            const double* uj = j == 1 ? u1 : u2;
+            cplx coef = cdiv(make_cplx_real(theta * theta), alpha);   /* θ² η / α */
+            coef = cmul(coef, eta);
+            for (int64_t i = 0; i < n; i++) {                  /* w −= α u_j ; d = y_j + coef d */
+                cplx uv = {RE(uj, i), IM(uj, i)}, dv = {RE(d, i), IM(d, i)};
+                cplx au = cmul(alpha, uv), cd = cmul(coef, dv);
+                RE(w, i) -= au.re;
+                IM(w, i) -= au.im;
+                RE(d, i) = RE(yj, i) + cd.re;
+                IM(d, i) = IM(yj, i) + cd.im;
+            }
+            theta = nrm(&A, w) / tau;                          /* θ = ‖w‖/τ */
+            double c = 1.0 / sqrt(1.0 + theta * theta);
+            tau = tau * theta * c;
+            eta.re = c * c * alpha.re;                          /* η = c² α */
+            eta.im = c * c * alpha.im;
+            for (int64_t i = 0; i < n; i++) {                  /* x += η d */
+                cplx dv = {RE(d, i), IM(d, i)};
+                cplx ed = cmul(eta, dv);
+                RE(x, i) += ed.re;
+                IM(x, i) += ed.im;
+            }
+            double bound = tau * sqrt((double)m + 1.0) / nb;
+            if (!isfinite(bound)) { status = ST_NONFINITE; conv = 2; break; }
+            if (j == 2 || bound <= tol) hist[k] = bound;
+            if (bound <= tol) conv = 1;
+        }
+        *iters = k;
+        if (conv == 2) break;
+        if (conv == 1) { status = ST_CONVERGED; break; }
+        cplx rho_new = dotc(&A, rt, w);                        /* ρ' = ⟨r̃, w⟩ */
+        if (!cfinite(rho_new)) { status = ST_NONFINITE; break; }
+        if (cabs_(rho_new) <= 1e-30 * nrt * nrm(&A, w)) { status = ST_BREAKDOWN_RHO; break; }
+        cplx beta = cdiv(rho_new, rho);
+        rho = rho_new;
+        for (int64_t i = 0; i < n; i++) {                      /* y1 = w + β y2 */
+            cplx yv = {RE(y2, i), IM(y2, i)};
+            cplx by = cmul(beta, yv);
+            RE(y1, i) = RE(w, i) + by.re;
+            IM(y1, i) = IM(w, i) + by.im;
+        }
+        spmv(&A, y1, u1);                                      /* u1 = A y1 */
+        for (int64_t i = 0; i < n; i++) {                      /* v = u1 + β (u2 + β v) */
+            cplx vv = {RE(v, i), IM(v, i)}, u2v = {RE(u2, i), IM(u2, i)};
+            cplx bv = cmul(beta, vv);
+            cplx t = {u2v.re + bv.re, u2v.im + bv.im};
+            cplx bt = cmul(beta, t);
+            RE(v, i) = RE(u1, i) + bt.re;
+            IM(v, i) = IM(u1, i) + bt.im;
+        }
+    }
+done_true:
+    *out_true_relres = true_relres(&A, b, x, nb, u2);
+done:
+    free(r); free(w); free(y1); free(y2); free(u1); free(u2); free(v); free(d); free(rt);
     return status;
 }

@@ -49,7 +49,7 @@ def test_bicgstab_scalar_identity(c):
 
 @pytest.mark.parametrize("cfg", ["C1", "T0"])
 def test_bicgstab_dense_lu(cfg):
-    """‖x − x_LU‖/‖x_LU‖ ≤ 1e-7 at tol 1e-10 (S:389)."""
+    """‖x − x_LU‖/‖x_LU‖ ≤ 1e-7 at tol 1e-10 (S:388)."""
     m = gen.make_matrix(cfg)
     b = gen.make_rhs(m)
     D = sp.csr_matrix((m["values"], m["col_idx"], m["row_ptr"]), shape=(m["n"], m["n"])).toarray()
@@ -71,7 +71,7 @@ def test_bicgstab_dst_exact(cfg):
     kappa = cf.box_kappa(spec, gen.ETA)
     assert r["status"] == "CONVERGED"
     assert np.linalg.norm(r["x"] - xe) / np.linalg.norm(xe) <= 2 * kappa * tol
-    # true vs recurrence residual (S:388 allows 10·tol; we require tol)
+    # true vs recurrence residual (S:387 allows 10·tol; we require tol)
     assert abs(r["true_relres"] - r["hist"][-1]) <= tol
     assert r["true_relres"] <= 2 * tol
     # solution-agreement reading L12 is binding literally on C1/C2
@@ -281,3 +281,54 @@ def test_cocg_dense_lu_and_breakdown():
     # b = (1, i): bᵀb = 0 → the bilinear form degenerates (quasi-null start): ρ = 0, μ = 0
     A = diag_csr([1.0, 1.0])
     assert oracle.cocg(A, np.array([1, 1j]))["status"] == "BREAKDOWN_SIGMA"
+
+
+# ------------------------------------------------------------------ TFQMR (NEXT-2)
+@pytest.mark.parametrize("c", [2.0, -1.0, 1j, 0.3 - 2j])
+def test_tfqmr_scalar_identity(c):
+    """identity (scaled) → converges in 1 iteration."""
+    b = gen.rand_vector(60, 1)
+    r = oracle.tfqmr(diag_csr(np.full(60, c)), b, tol=1e-12)
+    assert r["status"] == "CONVERGED" and r["iters"] == 1
+    assert np.max(np.abs(r["x"] - b / c)) <= 1e-15 * np.max(np.abs(b / c))
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "A3"])
+def test_tfqmr_closed_form(cfg):
+    spec = gen.CONFIGS[cfg]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    r = oracle.tfqmr(m, b, tol=1e-8)
+    assert r["status"] == "CONVERGED"
+    xe = cf.box_solve(spec, b, gen.ETA)
+    assert np.linalg.norm(r["x"] - xe) / np.linalg.norm(xe) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
+    # the quasi-residual bound τ√(m+1) bounds the true residual (S:380; Freund 1993)
+    assert r["true_relres"] <= r["hist"][-1] * (1 + 1e-6)
+
+
+def test_tfqmr_bound_and_monotone_tau():
+    """Stopped after k iterations (MAXIT) the true residual never exceeds hist[k] = τ√(2k+1)/‖b‖,
+    and τ = hist[k]/√(2k+1)·‖b‖ is non-increasing (S:389 "monotone quasi-residual")."""
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    full = oracle.tfqmr(m, b, tol=1e-10)
+    k = np.arange(1, len(full["hist"]))
+    tau = full["hist"][1:] / np.sqrt(2 * k + 1)
+    assert np.all(np.diff(tau) <= 1e-15 * tau[:-1])
+    for kk in (1, 3, 7, 15):
+        r = oracle.tfqmr(m, b, tol=1e-14, maxit=kk)
+        assert r["status"] == "MAXIT"
+        assert r["true_relres"] <= r["hist"][kk] * (1 + 1e-9)
+
+
+def test_tfqmr_dense_lu_and_gauge():
+    m = gen.make_matrix("C1")
+    b = gen.make_rhs(m)
+    D = sp.csr_matrix((m["values"], m["col_idx"], m["row_ptr"]), shape=(m["n"], m["n"])).toarray()
+    x_lu = np.linalg.solve(D, b)
+    r = oracle.tfqmr(m, b, tol=1e-10)
+    assert np.linalg.norm(r["x"] - x_lu) / np.linalg.norm(x_lu) <= 1e-7   # S:385
+    mg, Dg = twisted(gen.CONFIGS["C1"], gen.ETA)
+    rg = oracle.tfqmr(mg, Dg * b, tol=1e-10)
+    assert rg["iters"] == r["iters"]
+    assert np.max(np.abs(rg["hist"] - r["hist"]) / r["hist"]) <= 1e-10
