@@ -65,8 +65,13 @@ enum {
 enum {
     ZK_BICGSTAB = 0,        /* unpreconditioned BiCGStab (O6) */
     ZK_CG = 1,              /* CG, A Hermitian positive definite (O7) */
-    ZK_BICGSTAB_JACOBI = 2  /* Jacobi (M = diag A) right-preconditioned BiCGStab, the paper's P-Bi-CGSTAB
+    ZK_BICGSTAB_JACOBI = 2, /* Jacobi (M = diag A) right-preconditioned BiCGStab, the paper's P-Bi-CGSTAB
                                (P:308); one GPU; a zero/missing diagonal fails with ZK_ERR_INVALID_CSR */
+    ZK_COCG = 3,            /* COCG: CG with the unconjugated form rᵀr for complex SYMMETRIC A (Aᵀ = A, the
+                               absorbing Helmholtz matrices); 1 SpMV per iteration */
+    ZK_TFQMR = 4            /* TFQMR (Freund 1993, two half-steps per iteration), the paper's P-TFQMR
+                               without preconditioner; 2 SpMV per iteration; the convergence test
+                               is the quasi-residual bound tau*sqrt(m+1)/||b|| */
 };
 enum {
     ZK_CONVERGED = 0, ZK_MAXIT = 1, ZK_BREAKDOWN_RHO = 2, ZK_BREAKDOWN_SIGMA = 3,
@@ -163,10 +168,22 @@ zk_status zk_dznrm2(int64_t n, const zk_z* x, double* result, zk_comm comm, zk_s
 zk_status zk_zaxpy(int64_t n, zk_z alpha, const zk_z* x, zk_z* y, zk_stream s);
 zk_status zk_zscal(int64_t n, zk_z alpha, zk_z* x, zk_stream s);
 
+/* ---- NEXT-4: the paper's remaining BLAS-1 operations ----
+ * zk_zassign: x_i <- alpha for i < n ("assign of a vector", §3, Table 2; a fill —
+ *             the table's bytes per element imply a write-only pass).
+ * zk_zaxmy:   y_i <- x_i * y_i (element-wise product "EWProduct"/ZAXMY, Table 5; the
+ *             listing's unused alpha is dropped, L17).  x and y device zk_z[n]; may alias. */
+zk_status zk_zassign(int64_t n, zk_z alpha, zk_z* x, zk_stream s);
+zk_status zk_zaxmy(int64_t n, const zk_z* x, zk_z* y, zk_stream s);
+
 /* ---- solve(A, b, x0, tol, maxit) (§4: Krylov solve with residual
  *      tolerance, initial guess, maximum iterations) ----
  * method     ZK_BICGSTAB (unpreconditioned BiCGStab, O6), ZK_CG (Hermitian positive definite A, O7) or
- *            ZK_BICGSTAB_JACOBI (P-BiCGStab with M = diag(A); the first call builds A·M⁻¹ in the handle).
+ *            ZK_BICGSTAB_JACOBI (P-BiCGStab with M = diag(A); the first call builds A·M⁻¹ in the handle)
+ *            or ZK_COCG (complex symmetric A; breakdowns: μ = pᵀAp = 0 → BREAKDOWN_SIGMA,
+ *            ρ = rᵀr ≈ 0 → BREAKDOWN_RHO) or ZK_TFQMR (σ = ⟨r̃,v⟩ = 0 → BREAKDOWN_SIGMA,
+ *            ρ = ⟨r̃,w⟩ ≈ 0 → BREAKDOWN_RHO; hist[j] is the quasi-residual bound τ_m·sqrt(m+1)/||b||
+ *            after the second half step m = 2j, or after the first m = 2j−1 when that converges).
  * b          device zk_z[n_rows]; must not alias x.
  * x0         device zk_z[n_rows] initial guess, or NULL for zero; may alias x.
  * tol        stop when the recurrence residual ||r_j||/||b|| <= tol (BiCGStab also tests the

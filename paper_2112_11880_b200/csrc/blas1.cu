@@ -35,6 +35,26 @@ struct OpScal {
     __device__ void finish(double (&)[1]) const {}
 };
 
+struct OpAssign {  // NEXT-4 ZASSIGN: x_i ← α (a fill: write-only, PAPER.md T2 / L16)
+    static constexpr int K = 0;
+    struct In {};
+    double2 a;
+    double2* __restrict__ x;
+    __device__ In load(int64_t) const { return {}; }
+    __device__ void apply(int64_t i, const In&, double (&)[1]) const { x[i] = a; }
+    __device__ void finish(double (&)[1]) const {}
+};
+
+struct OpAxmy {  // NEXT-4 ZAXMY: y_i ← x_i · y_i ("EWProduct", T5)
+    static constexpr int K = 0;
+    struct In { double2 x, y; };
+    const double2* __restrict__ x;
+    double2* __restrict__ y;
+    __device__ In load(int64_t i) const { return {ld_stream(x + i), ld_stream_rw(y + i)}; }
+    __device__ void apply(int64_t i, const In& v, double (&)[1]) const { y[i] = cmul(v.x, v.y); }
+    __device__ void finish(double (&)[1]) const {}
+};
+
 struct OpDotc {
     static constexpr int K = 2;
     struct In { double2 x, y; };
@@ -149,4 +169,18 @@ extern "C" zk_status zk_dznrm2(int64_t n, const zk_z* x, double* result, zk_comm
     ZK_TRY(sumsq_local(n, (const double2*)x, result, st));
     ZK_TRY(comm_allreduce_sum(comm, result, 1, st));
     return sqrt_inplace(result, st);
+}
+
+extern "C" zk_status zk_zassign(int64_t n, zk_z alpha, zk_z* x, zk_stream s) {
+    if (n < 0) return fail(ZK_ERR_INVALID_VALUE, "n < 0");
+    if (n == 0) return ZK_OK;
+    if (!x) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
+    return launch_vec(n, OpAssign{make_double2(alpha.re, alpha.im), (double2*)x}, (cudaStream_t)s);
+}
+
+extern "C" zk_status zk_zaxmy(int64_t n, const zk_z* x, zk_z* y, zk_stream s) {
+    if (n < 0) return fail(ZK_ERR_INVALID_VALUE, "n < 0");
+    if (n == 0) return ZK_OK;
+    if (!x || !y) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
+    return launch_vec(n, OpAxmy{(const double2*)x, (double2*)y}, (cudaStream_t)s);
 }

@@ -14,6 +14,14 @@
 //   K5  p = r + β(p − ωv)                             (writes the WHILE condition)
 // CG: K1 q = A p ; δ = ⟨p,q⟩ → α = γ/Re δ (NOT_HPD) ; K2 x += αp ; r −= αq ; γ' → hist, β ;
 //     K3 p = r + βp.
+// TFQMR (NEXT-2; Freund 1993 in the two-half-step form of oracle_tfqmr), iteration k:
+//   T1  y2 = y1 − αv ; w −= αu1 ; d1 = y1 + c1·d2 ; ‖w‖²    → θ,c,τ,η1 (half step m = 2k−1), test
+//   T2  u2 = A y2 ; d2 = y2 + c2·d1 ; w −= αu2 ; ‖w‖², ⟨r̃,w⟩
+//                                                          → half step m = 2k, hist[k], ρ', β
+//   T3  x += η1·d1 + η2·d2 ; y1 = w + βy2
+// (d is double-buffered so both x updates of an iteration land in T3: the SpMV epilogue of T2
+//  then carries 4 row operands instead of 5, and x is read and written once per iteration)
+//   T4  u1 = A y1 ; v = u1 + β(u2 + βv) ; σ = ⟨r̃,v⟩        → α = ρ/σ, c1 (writes the WHILE condition)
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -32,6 +40,7 @@ struct SolveCtx {
     double2* x;
     const double2* b;
     double2 *r, *rh, *p, *v, *s, *t, *q;
+    double2 *w, *y1, *y2, *u1, *u2, *d1, *d2, *rt;  // TFQMR (r/p/rh alias w/y1/rt for the shared init)
     double* hist;
     double* partials;       // [kMaxRed][kMaxGrid]
     unsigned int* tickets;  // [8]
@@ -40,11 +49,14 @@ struct SolveCtx {
     // scalars
     double2 rho, alpha, omega, beta;
     double nb, nrh, rnorm, gamma, alpha_cg, beta_cg;
+    double2 eta, eta1, coef;  // TFQMR η (η1: first half step's) and the next half step's d coefficient (θ²/α)·η
+    double theta, tau;      // TFQMR θ, τ
     double tol;
     int maxit;
     int j;       // iteration being executed (1-based)
     int done;    // loop finished (any outcome)
-    int half;    // BiCGStab half-step exit pending (K4 applies x += αp)
+    int half;    // BiCGStab half-step exit pending (K4 applies x += αp); TFQMR exit inside an
+                 // iteration: 1 → T2 applies x += η1·d1 only, 2 → T3 applies its x update only
     int status;  // ZK_CONVERGED ... / ST_ZERO_RHS
     int iters;
     double true_relres;
@@ -166,16 +178,109 @@ __device__ void fin_k2_cg(SolveCtx* c, const double* tot) {  // {γ'}
     c->gamma = g;
     c->j = j + 1;
 }
+// NEXT-4 COCG (van der Vorst & Melissen): CG with the unconjugated form for complex symmetric A
+__device__ void fin_init_cocg(SolveCtx* c, const double* tot) {  // {‖b‖², ‖r0‖², Re r0ᵀr0, Im r0ᵀr0}
+    c->iters = 0;
+    c->nb = sqrt(tot[0]);
+    if (c->nb == 0.0) { c->status = ST_ZERO_RHS; c->done = 1; return; }
+    c->rho = make_double2(tot[2], tot[3]);
+    c->hist[0] = sqrt(tot[1]) / c->nb;
+    if (!isfinite(c->hist[0])) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (c->hist[0] <= c->tol) { c->status = ZK_CONVERGED; c->done = 1; return; }
+    c->j = 1;
+}
+__device__ void fin_k1_cocg(SolveCtx* c, const double* tot) {  // {Re μ, Im μ}, μ = pᵀq
+    const double2 mu = make_double2(tot[0], tot[1]);
+    if (!cfinite(mu)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (mu.x == 0.0 && mu.y == 0.0) { c->status = ZK_BREAKDOWN_SIGMA; c->done = 1; return; }
+    c->alpha = cdiv(c->rho, mu);
+}
+__device__ void fin_k2_cocg(SolveCtx* c, const double* tot) {  // {‖r‖², Re ρ', Im ρ'}, ρ' = rᵀr
+    const int j = c->j;
+    const double rn2 = tot[0];
+    c->hist[j] = sqrt(rn2) / c->nb;
+    c->iters = j;
+    if (!isfinite(c->hist[j])) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (c->hist[j] <= c->tol) { c->status = ZK_CONVERGED; c->done = 1; return; }
+    if (j >= c->maxit) { c->status = ZK_MAXIT; c->done = 1; return; }
+    const double2 rho = make_double2(tot[1], tot[2]);
+    if (!cfinite(rho)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (cabs_(rho) <= 1e-30 * rn2) { c->status = ZK_BREAKDOWN_RHO; c->done = 1; return; }
+    c->beta = cdiv(rho, c->rho);
+    c->rho = rho;
+    c->j = j + 1;
+}
+// NEXT-2 TFQMR — the scalar steps of oracle_tfqmr in its order (θ, c, τ, η, bound; ρ', β; σ, α)
+__device__ void fin_init_tfqmr(SolveCtx* c, const double* tot) {  // {‖b‖², ‖r0‖², ·, ·}
+    c->iters = 0;
+    c->nb = sqrt(tot[0]);
+    if (c->nb == 0.0) { c->status = ST_ZERO_RHS; c->done = 1; return; }
+    c->tau = sqrt(tot[1]);
+    c->hist[0] = c->tau / c->nb;
+    if (!isfinite(c->hist[0])) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (c->hist[0] <= c->tol) { c->status = ZK_CONVERGED; c->done = 1; return; }
+    c->nrh = c->tau;                     // ‖r̃‖, r̃ = r0
+    c->rho = make_double2(tot[1], 0.0);  // ρ = ⟨r̃, r0⟩ = ‖r0‖²
+    c->theta = 0.0;
+    c->eta = make_double2(0.0, 0.0);
+    c->j = 1;
+}
+__device__ void fin_sigma_tfqmr(SolveCtx* c, const double* tot) {  // {Re σ, Im σ}, σ = ⟨r̃, v⟩
+    const double2 sigma = make_double2(tot[0], tot[1]);
+    if (!cfinite(sigma)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (sigma.x == 0.0 && sigma.y == 0.0) { c->status = ZK_BREAKDOWN_SIGMA; c->done = 1; return; }
+    c->alpha = cdiv(c->rho, sigma);
+    c->coef = cmul(cdiv(make_double2(c->theta * c->theta, 0.0), c->alpha), c->eta);  // for half step 1
+}
+// one half step's scalars from ‖w‖²; returns false when the loop ends (x += η·d still pending)
+__device__ bool half_tfqmr(SolveCtx* c, double ww, int m, bool second) {
+    c->theta = sqrt(ww) / c->tau;
+    const double cc = 1.0 / sqrt(1.0 + c->theta * c->theta);
+    c->tau = c->tau * c->theta * cc;
+    c->eta = make_double2(cc * cc * c->alpha.x, cc * cc * c->alpha.y);
+    const double bound = c->tau * sqrt((double)m + 1.0) / c->nb;
+    if (!isfinite(bound)) { c->status = ZK_NONFINITE; c->iters = c->j; c->done = 1; return false; }
+    if (second || bound <= c->tol) c->hist[c->j] = bound;
+    if (bound <= c->tol) { c->status = ZK_CONVERGED; c->iters = c->j; c->done = 1; return false; }
+    return true;
+}
+// Any exit inside an iteration leaves the x update of its half steps to the next kernel (the
+// oracle applies it before testing): c->half = 1 (T2 does x += η1·d1) or 2 (T3 does its update).
+__device__ void fin_t1_tfqmr(SolveCtx* c, const double* tot) {  // {‖w‖²}
+    const bool go = half_tfqmr(c, tot[0], 2 * c->j - 1, false);
+    c->eta1 = c->eta;
+    if (!go) { c->half = 1; return; }
+    c->coef = cmul(cdiv(make_double2(c->theta * c->theta, 0.0), c->alpha), c->eta);  // for half step 2
+}
+__device__ void fin_t2_steps(SolveCtx* c, const double* tot) {
+    const int j = c->j;
+    if (!half_tfqmr(c, tot[0], 2 * j, true)) return;
+    c->iters = j;
+    const double2 rho = make_double2(tot[1], tot[2]);
+    if (!cfinite(rho)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (cabs_(rho) <= 1e-30 * c->nrh * sqrt(tot[0])) { c->status = ZK_BREAKDOWN_RHO; c->done = 1; return; }
+    c->beta = cdiv(rho, c->rho);
+    c->rho = rho;
+    if (j >= c->maxit) { c->status = ZK_MAXIT; c->done = 1; return; }
+    c->j = j + 1;
+}
+__device__ void fin_t2_tfqmr(SolveCtx* c, const double* tot) {  // {‖w‖², Re ρ', Im ρ'}
+    fin_t2_steps(c, tot);
+    if (c->done) c->half = 2;
+}
 __device__ void fin_true(SolveCtx* c, const double* tot) {  // {‖b − Ax‖²}
     c->true_relres = c->nb > 0.0 ? sqrt(tot[0]) / c->nb : NAN;
 }
 
-enum Stage { S_INIT_BICG, S_K1_BICG, S_K2_BICG, S_K3_BICG, S_K4_BICG, S_INIT_CG, S_K1_CG, S_K2_CG, S_TRUE };
+enum Stage { S_INIT_BICG, S_K1_BICG, S_K2_BICG, S_K3_BICG, S_K4_BICG, S_INIT_CG, S_K1_CG, S_K2_CG, S_TRUE,
+             S_INIT_COCG, S_K1_COCG, S_K2_COCG, S_INIT_TFQMR, S_K0_TFQMR, S_T1_TFQMR, S_T2_TFQMR,
+             S_T4_TFQMR };
 
 // timer class of a stage: 0 SpMV in the loop, 1 fused vector kernels, 2 init, 3 true residual
 __host__ __device__ constexpr int timer_of(int S) {
-    return (S == S_K1_BICG || S == S_K3_BICG || S == S_K1_CG) ? 0
-           : (S == S_K2_BICG || S == S_K4_BICG || S == S_K2_CG) ? 1
+    return (S == S_K1_BICG || S == S_K3_BICG || S == S_K1_CG || S == S_K1_COCG || S == S_T2_TFQMR ||
+            S == S_T4_TFQMR) ? 0
+           : (S == S_K2_BICG || S == S_K4_BICG || S == S_K2_CG || S == S_K2_COCG || S == S_T1_TFQMR) ? 1
            : (S == S_TRUE) ? 3 : 2;
 }
 template <int S>
@@ -194,6 +299,13 @@ __device__ __forceinline__ void finish_stage(SolveCtx* c, const double* tot) {
     if (S == S_K1_CG) fin_k1_cg(c, tot);
     if (S == S_K2_CG) fin_k2_cg(c, tot);
     if (S == S_TRUE) fin_true(c, tot);
+    if (S == S_INIT_COCG) fin_init_cocg(c, tot);
+    if (S == S_K1_COCG) fin_k1_cocg(c, tot);
+    if (S == S_K2_COCG) fin_k2_cocg(c, tot);
+    if (S == S_INIT_TFQMR) fin_init_tfqmr(c, tot);
+    if (S == S_K0_TFQMR || S == S_T4_TFQMR) fin_sigma_tfqmr(c, tot);
+    if (S == S_T1_TFQMR) fin_t1_tfqmr(c, tot);
+    if (S == S_T2_TFQMR) fin_t2_tfqmr(c, tot);
 }
 
 // grid reduction of K values, then (single GPU) the stage's scalar step in the last block, or
@@ -219,7 +331,7 @@ template <int S>
 __global__ void fin_kernel(SolveCtx* c) {
     // the reducing kernel skipped its work (loop already finished): nothing to finish — the
     // chunked loop launches whole iterations past convergence (regression: tools/debug/dist1.py)
-    if (S != S_TRUE && S != S_INIT_BICG && S != S_INIT_CG && c->done) return;
+    if (S != S_TRUE && S != S_INIT_BICG && S != S_INIT_CG && S != S_INIT_COCG && S != S_INIT_TFQMR && c->done) return;
     double tot[kMaxRed];
     for (int k = 0; k < kMaxRed; k++) tot[k] = c->red[k];
     finish_stage<S>(c, tot);
@@ -230,26 +342,29 @@ __global__ void fin_kernel(SolveCtx* c) {
 // load is off the critical path); row(i, y, pre, acc) consumes them.  Pointers are cached from
 // the SolveCtx at kernel start.
 template <int S>
-struct EpiInit {  // r = b − A x0 ; x = x0 ; r̂ = p = r ; {‖b‖², ‖r‖²}
-    static constexpr int K = 2;
+struct EpiInit {  // r = b − A x0 ; x = x0 ; r̂ = p = r ; {‖b‖², ‖r‖², Re rᵀr, Im rᵀr}
+    static constexpr int K = 4;
     struct Pre { double2 b, x0; };
     SolveCtx* c;
     const double2* __restrict__ x0;
     const double2* __restrict__ b;
-    double2 *r, *p, *rh, *x;
+    double2 *r, *p, *rh, *x, *d;
     __device__ EpiInit(SolveCtx* c_, const double2* x0_, bool bicg)
-        : c(c_), x0(x0_), b(c_->b), r(c_->r), p(c_->p), rh(bicg ? c_->rh : nullptr), x(c_->x) {}
+        : c(c_), x0(x0_), b(c_->b), r(c_->r), p(c_->p), rh(bicg ? c_->rh : nullptr), x(c_->x), d(c_->d2) {}
     __device__ Pre pre(int64_t i) const { return {ld_vec(b + i), x != x0 ? ld_gather_coh(x0 + i) : make_double2(0, 0)}; }
-    __device__ void row(int64_t i, double2 y, const Pre& q, double (&acc)[2]) {
+    __device__ void row(int64_t i, double2 y, const Pre& q, double (&acc)[4]) {
         const double2 rr = csub(q.b, y);
         r[i] = rr;
         p[i] = rr;
         if (rh) rh[i] = rr;
         if (x != x0) x[i] = q.x0;
+        if (d) d[i] = make_double2(0.0, 0.0);
         acc[0] += cabs2(q.b);
         acc[1] += cabs2(rr);
+        acc[2] = fma(rr.x, rr.x, fma(-rr.y, rr.y, acc[2]));  // rᵀr (COCG's ρ0)
+        acc[3] = fma(2.0 * rr.x, rr.y, acc[3]);
     }
-    __device__ void finish(double (&acc)[2]) { reduce_finish<S, 2>(c, acc); }
+    __device__ void finish(double (&acc)[4]) { reduce_finish<S, 4>(c, acc); }
 };
 
 struct EpiTrue {  // {‖b − A x‖²}
@@ -316,28 +431,33 @@ struct EpiK1Cg {  // q = A p ; {δ = ⟨p, q⟩}
 // Vector ops: every pointer and scalar is copied out of the SolveCtx once per thread at kernel
 // start (reading c->x inside the loop would force a reload after every store through a
 // possibly-aliasing pointer).
-struct OpInitZero {  // x0 = 0: x = 0 ; r = r̂ = p = b ; {‖b‖², ‖r‖²}
-    static constexpr int K = 2;
+struct OpInitZero {  // x0 = 0: x = 0 ; r = r̂ = p = b ; {‖b‖², ‖r‖², Re bᵀb, Im bᵀb}
+    static constexpr int K = 4;
     struct In { double2 b; };
     SolveCtx* c;
     const double2* __restrict__ b;
-    double2 *__restrict__ x, *__restrict__ r, *__restrict__ p, *__restrict__ rh;
-    bool bicg;
-    __device__ OpInitZero(SolveCtx* c_, bool bicg_)
-        : c(c_), b(c_->b), x(c_->x), r(c_->r), p(c_->p), rh(c_->rh), bicg(bicg_) {}
+    double2 *__restrict__ x, *__restrict__ r, *__restrict__ p, *__restrict__ rh, *__restrict__ d;
+    int kind;  // 0 BiCGStab, 1 CG, 3 COCG, 4 TFQMR
+    __device__ OpInitZero(SolveCtx* c_, int kind_)
+        : c(c_), b(c_->b), x(c_->x), r(c_->r), p(c_->p), rh(c_->rh), d(c_->d2), kind(kind_) {}
     __device__ In load(int64_t i) const { return {ld_vec(b + i)}; }
-    __device__ void apply(int64_t i, const In& v, double (&acc)[2]) const {
+    __device__ void apply(int64_t i, const In& v, double (&acc)[4]) const {
         x[i] = make_double2(0.0, 0.0);
         r[i] = v.b;
         p[i] = v.b;
-        if (bicg) rh[i] = v.b;
+        if (kind == 0 || kind == 4) rh[i] = v.b;
+    if (kind == 4) d[i] = make_double2(0.0, 0.0);
         const double bb = cabs2(v.b);
         acc[0] += bb;
         acc[1] += bb;
+        acc[2] = fma(v.b.x, v.b.x, fma(-v.b.y, v.b.y, acc[2]));
+        acc[3] = fma(2.0 * v.b.x, v.b.y, acc[3]);
     }
-    __device__ void finish(double (&acc)[2]) const {
-        if (bicg) reduce_finish<S_INIT_BICG, 2>(c, acc);
-        else reduce_finish<S_INIT_CG, 2>(c, acc);
+    __device__ void finish(double (&acc)[4]) const {
+        if (kind == 0) reduce_finish<S_INIT_BICG, 4>(c, acc);
+        else if (kind == 1) reduce_finish<S_INIT_CG, 4>(c, acc);
+        else if (kind == 3) reduce_finish<S_INIT_COCG, 4>(c, acc);
+        else reduce_finish<S_INIT_TFQMR, 4>(c, acc);
     }
 };
 
@@ -461,6 +581,189 @@ struct OpK3Cg {  // p = r + β p
     __device__ void finish(double (&)[1]) const {}
 };
 
+struct EpiK1Cocg {  // q = A p ; {μ = pᵀ q} (unconjugated)
+    static constexpr int K = 2;
+    using Pre = double2;
+    SolveCtx* c;
+    double2* __restrict__ q;
+    const double2* __restrict__ p;
+    __device__ explicit EpiK1Cocg(SolveCtx* c_) : c(c_), q(c_->q), p(c_->p) {}
+    __device__ Pre pre(int64_t i) const { return ld_gather_coh(p + i); }
+    __device__ void row(int64_t i, double2 y, const Pre& pi, double (&acc)[2]) {
+        q[i] = y;
+        acc[0] = fma(pi.x, y.x, fma(-pi.y, y.y, acc[0]));
+        acc[1] = fma(pi.x, y.y, fma(pi.y, y.x, acc[1]));
+    }
+    __device__ void finish(double (&acc)[2]) { reduce_finish<S_K1_COCG, 2>(c, acc); }
+};
+
+struct OpK2Cocg {  // x += α p ; r −= α q ; {‖r‖², rᵀr}
+    static constexpr int K = 3;
+    static constexpr int U = 2;
+    struct In { double2 x, p, r, q; };
+    SolveCtx* c;
+    double2 *__restrict__ x, *__restrict__ r;
+    const double2 *__restrict__ p, *__restrict__ q;
+    double2 alpha;
+    __device__ explicit OpK2Cocg(SolveCtx* c_) : c(c_), x(c_->x), r(c_->r), p(c_->p), q(c_->q), alpha(c_->alpha) {}
+    __device__ In load(int64_t i) const { return {ld_vec(x + i), ld_vec(p + i), ld_vec(r + i), ld_vec(q + i)}; }
+    __device__ void apply(int64_t i, const In& in, double (&acc)[3]) const {
+        double2 xn = in.x;
+        cfma(xn, alpha, in.p);
+        x[i] = xn;
+        double2 rn = in.r;
+        rn.x = fma(-alpha.x, in.q.x, fma(alpha.y, in.q.y, rn.x));
+        rn.y = fma(-alpha.x, in.q.y, fma(-alpha.y, in.q.x, rn.y));
+        r[i] = rn;
+        acc[0] += cabs2(rn);
+        acc[1] = fma(rn.x, rn.x, fma(-rn.y, rn.y, acc[1]));
+        acc[2] = fma(2.0 * rn.x, rn.y, acc[2]);
+    }
+    __device__ void finish(double (&acc)[3]) const { reduce_finish<S_K2_COCG, 3>(c, acc); }
+};
+
+struct OpK3Cocg {  // p = r + β p (complex β)
+    static constexpr int K = 0;
+    struct In { double2 r, p; };
+    const double2* __restrict__ r;
+    double2* __restrict__ p;
+    double2 beta;
+    __device__ explicit OpK3Cocg(SolveCtx* c) : r(c->r), p(c->p), beta(c->beta) {}
+    __device__ In load(int64_t i) const { return {ld_vec(r + i), ld_vec(p + i)}; }
+    __device__ void apply(int64_t i, const In& in, double (&)[1]) const {
+        double2 o = in.r;
+        cfma(o, beta, in.p);
+        p[i] = o;
+    }
+    __device__ void finish(double (&)[1]) const {}
+};
+
+// TFQMR epilogues and vector ops (the loops of oracle_tfqmr, fused per kernel T1..T4)
+struct OpT1Tfqmr {  // y2 = y1 − α v ; w −= α u1 ; d1 = y1 + c1·d2 ; {‖w‖²}
+    static constexpr int K = 1;
+    static constexpr int U = 1;  // 5 input streams (as OpK4Bicg)
+    struct In { double2 y1, v, w, u1, d; };
+    SolveCtx* c;
+    const double2 *__restrict__ y1, *__restrict__ v, *__restrict__ u1, *__restrict__ d2;
+    double2 *__restrict__ y2, *__restrict__ w, *__restrict__ d;
+    double2 alpha, coef;
+    __device__ explicit OpT1Tfqmr(SolveCtx* c_)
+        : c(c_), y1(c_->y1), v(c_->v), u1(c_->u1), d2(c_->d2), y2(c_->y2), w(c_->w), d(c_->d1), alpha(c_->alpha),
+          coef(c_->coef) {}
+    __device__ In load(int64_t i) const {
+        return {ld_vec(y1 + i), ld_vec(v + i), ld_vec(w + i), ld_vec(u1 + i), ld_vec(d2 + i)};
+    }
+    __device__ void apply(int64_t i, const In& in, double (&acc)[1]) const {
+        double2 o = in.y1;
+        o.x = fma(-alpha.x, in.v.x, fma(alpha.y, in.v.y, o.x));
+        o.y = fma(-alpha.x, in.v.y, fma(-alpha.y, in.v.x, o.y));
+        y2[i] = o;
+        double2 wn = in.w;
+        wn.x = fma(-alpha.x, in.u1.x, fma(alpha.y, in.u1.y, wn.x));
+        wn.y = fma(-alpha.x, in.u1.y, fma(-alpha.y, in.u1.x, wn.y));
+        w[i] = wn;
+        double2 dn = in.y1;
+        cfma(dn, coef, in.d);
+        d[i] = dn;
+        acc[0] += cabs2(wn);
+    }
+    __device__ void finish(double (&acc)[1]) const { reduce_finish<S_T1_TFQMR, 1>(c, acc); }
+};
+
+struct EpiT2Tfqmr {  // u2 = A y2 ; d2 = y2 + c2·d1 ; w −= α u2 ; {‖w‖², ⟨r̃, w⟩}
+    static constexpr int K = 3;
+    static constexpr bool kAhead = false;  // 4 row operands: one copy in registers (no spill at 64)
+    struct Pre { double2 d, w, rt, y2; };
+    SolveCtx* c;
+    double2 *__restrict__ u2, *__restrict__ d2, *__restrict__ w;
+    const double2 *__restrict__ d1, *__restrict__ rt, *__restrict__ y2;
+    double2 coef, alpha;
+    __device__ explicit EpiT2Tfqmr(SolveCtx* c_)
+        : c(c_), u2(c_->u2), d2(c_->d2), w(c_->w), d1(c_->d1), rt(c_->rt), y2(c_->y2), coef(c_->coef),
+          alpha(c_->alpha) {}
+    __device__ Pre pre(int64_t i) const {
+        return {ld_vec(d1 + i), ld_vec(w + i), ld_vec(rt + i), ld_gather_coh(y2 + i)};
+    }
+    __device__ void row(int64_t i, double2 y, const Pre& q, double (&acc)[3]) {
+        u2[i] = y;
+        double2 dn = q.y2;
+        cfma(dn, coef, q.d);
+        d2[i] = dn;
+        double2 wn = q.w;
+        wn.x = fma(-alpha.x, y.x, fma(alpha.y, y.y, wn.x));
+        wn.y = fma(-alpha.x, y.y, fma(-alpha.y, y.x, wn.y));
+        w[i] = wn;
+        acc[0] += cabs2(wn);
+        acc[1] = fma(q.rt.x, wn.x, fma(q.rt.y, wn.y, acc[1]));
+        acc[2] = fma(q.rt.x, wn.y, fma(-q.rt.y, wn.x, acc[2]));
+    }
+    __device__ void finish(double (&acc)[3]) { reduce_finish<S_T2_TFQMR, 3>(c, acc); }
+};
+
+struct OpT3Tfqmr {  // x += η1·d1 + η2·d2 ; y1 = w + β y2   (exit: the x update only)
+    static constexpr int K = 0;
+    static constexpr int U = 1;  // 5 input streams
+    struct In { double2 x, d1, d2, w, y2; };
+    double2 *__restrict__ x, *__restrict__ y1;
+    const double2 *__restrict__ d1, *__restrict__ d2, *__restrict__ w, *__restrict__ y2;
+    double2 eta1, eta2, beta;
+    bool only_x;
+    __device__ OpT3Tfqmr(SolveCtx* c, bool only_x_)
+        : x(c->x), y1(c->y1), d1(c->d1), d2(c->d2), w(c->w), y2(c->y2), eta1(c->eta1), eta2(c->eta), beta(c->beta),
+          only_x(only_x_) {}
+    __device__ In load(int64_t i) const {
+        In v;
+        v.x = ld_vec(x + i);
+        v.d1 = ld_vec(d1 + i);
+        v.d2 = ld_vec(d2 + i);
+        if (!only_x) {
+            v.w = ld_vec(w + i);
+            v.y2 = ld_vec(y2 + i);
+        }
+        return v;
+    }
+    __device__ void apply(int64_t i, const In& in, double (&)[1]) const {
+        double2 xn = in.x;  // oracle order: (x + η1·d1) + η2·d2
+        cfma(xn, eta1, in.d1);
+        cfma(xn, eta2, in.d2);
+        x[i] = xn;
+        if (only_x) return;
+        double2 o = in.w;
+        cfma(o, beta, in.y2);
+        y1[i] = o;
+    }
+    __device__ void finish(double (&)[1]) const {}
+};
+
+template <int S>
+struct EpiT4Tfqmr {  // u1 = A y1 ; v = u1 + β(u2 + β v) (first: v = u1) ; {σ = ⟨r̃, v⟩}
+    static constexpr int K = 2;
+    struct Pre { double2 u2, v, rt; };
+    SolveCtx* c;
+    double2 *__restrict__ u1, *__restrict__ v;
+    const double2 *__restrict__ u2, *__restrict__ rt;
+    double2 beta;
+    __device__ explicit EpiT4Tfqmr(SolveCtx* c_)
+        : c(c_), u1(c_->u1), v(c_->v), u2(c_->u2), rt(c_->rt), beta(c_->beta) {}
+    __device__ Pre pre(int64_t i) const {
+        if (S == S_K0_TFQMR) return {make_double2(0, 0), make_double2(0, 0), ld_vec(rt + i)};
+        return {ld_vec(u2 + i), ld_vec(v + i), ld_vec(rt + i)};
+    }
+    __device__ void row(int64_t i, double2 y, const Pre& q, double (&acc)[2]) {
+        u1[i] = y;
+        double2 vn = y;
+        if (S != S_K0_TFQMR) {
+            double2 t = q.u2;
+            cfma(t, beta, q.v);
+            cfma(vn, beta, t);
+        }
+        v[i] = vn;
+        acc[0] = fma(q.rt.x, vn.x, fma(q.rt.y, vn.y, acc[0]));
+        acc[1] = fma(q.rt.x, vn.y, fma(-q.rt.y, vn.x, acc[1]));
+    }
+    __device__ void finish(double (&acc)[2]) { reduce_finish<S, 2>(c, acc); }
+};
+
 // ------------------------------------------------------------------ kernels
 #ifndef ZK_VEC_MINB
 #define ZK_VEC_MINB 4  // fused vector kernels: ≤ 64 registers, 4 CTAs / 32 warps per SM
@@ -472,12 +775,12 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_init_x0(Solve
     stamp_start<S>(c);
     const CsrDev A = c->A;
     const TmaPlan T = c->T;
-    EpiInit<S> e(c, xg, bicg != 0);
+    EpiInit<S> e(c, xg, bicg == 1);
     spmv_any<W, MODE>(A, T, xg, e);
 }
-__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k_init_zero(SolveCtx* c, int bicg) {
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k_init_zero(SolveCtx* c, int kind) {
     stamp_start<S_INIT_BICG>(c);
-    OpInitZero op(c, bicg != 0);
+    OpInitZero op(c, kind);
     vec_body(c->A.n_rows, op);
 }
 template <int W, int MODE>
@@ -538,6 +841,32 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k5_bicg(SolveCtx* c) {
     set_cond(c);  // after the stream loop: the device-runtime call does not pressure its registers
 }
 template <int W, int MODE>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cocg(SolveCtx* c) {
+    pdl_enter();
+    if (c->done) return;
+    stamp_start<S_K1_COCG>(c);
+    const CsrDev A = c->A;
+    const TmaPlan T = c->T;
+    const double2* p = c->p;
+    EpiK1Cocg e(c);
+    spmv_any<W, MODE>(A, T, p, e);
+}
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_cocg(SolveCtx* c) {
+    pdl_enter();
+    if (c->done) return;
+    stamp_start<S_K2_COCG>(c);
+    OpK2Cocg op(c);
+    vec_body(c->A.n_rows, op);
+}
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k3_cocg(SolveCtx* c) {
+    pdl_enter();
+    if (!c->done) {
+        OpK3Cocg op(c);
+        vec_body(c->A.n_rows, op);
+    }
+    set_cond(c);
+}
+template <int W, int MODE>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cg(SolveCtx* c) {
     pdl_enter();
     if (c->done) return;
@@ -560,6 +889,69 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k3_cg(SolveCtx* c) {
     if (!c->done) {
         OpK3Cg op(c);
         vec_body(c->A.n_rows, op);
+    }
+    set_cond(c);
+}
+template <int W, int MODE>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k0_tfqmr(SolveCtx* c) {  // u1 = v = A y1, σ
+    if (c->done) return;
+    stamp_start<S_K0_TFQMR>(c);
+    const CsrDev A = c->A;
+    const TmaPlan T = c->T;
+    const double2* y1 = c->y1;
+    EpiT4Tfqmr<S_K0_TFQMR> e(c);
+    spmv_any<W, MODE>(A, T, y1, e);
+}
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t1_tfqmr(SolveCtx* c) {
+    pdl_enter();
+    if (c->done) return;
+    stamp_start<S_T1_TFQMR>(c);
+    OpT1Tfqmr op(c);
+    vec_body(c->A.n_rows, op);
+}
+template <int W, int MODE>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) t2_tfqmr(SolveCtx* c) {
+    pdl_enter();
+    if (c->done) {
+        if (c->half != 1) return;
+        // the first half step ended the loop: only its x += η1·d1 remains
+        double2* __restrict__ x = c->x;
+        const double2* __restrict__ d = c->d1;
+        const double2 eta = c->eta1;
+        const int64_t n = c->A.n_rows;
+        for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+            double2 xn = x[i];
+            cfma(xn, eta, d[i]);
+            x[i] = xn;
+        }
+        return;
+    }
+    stamp_start<S_T2_TFQMR>(c);
+    const CsrDev A = c->A;
+    const TmaPlan T = c->T;
+    const double2* y2 = c->y2;
+    EpiT2Tfqmr e(c);
+    spmv_any<W, MODE>(A, T, y2, e);
+}
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t3_tfqmr(SolveCtx* c) {
+    pdl_enter();
+    const bool done = c->done != 0;
+    if (done && c->half != 2) return;
+    OpT3Tfqmr op(c, done);
+    vec_body(c->A.n_rows, op);
+}
+template <int W, int MODE>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) t4_tfqmr(SolveCtx* c) {
+    pdl_enter();
+    if (c->done) {
+        if (c->half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;  // T2/T3 applied the last x += η·d
+    } else {
+        stamp_start<S_T4_TFQMR>(c);
+        const CsrDev A = c->A;
+        const TmaPlan T = c->T;
+        const double2* y1 = c->y1;
+        EpiT4Tfqmr<S_T4_TFQMR> e(c);
+        spmv_any<W, MODE>(A, T, y1, e);
     }
     set_cond(c);
 }
@@ -724,6 +1116,23 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             ZK_TRY(launch_loop(pdl, k4_bicg, vec_grid(A, (const void*)k4_bicg), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_K4_BICG>(A, dc, 3, s)));
             ZK_TRY(launch_loop(pdl, k5_bicg, vec_grid(A, (const void*)k5_bicg), 0, s, dc));
+        } else if (method == ZK_TFQMR) {
+            ZK_TRY(launch_loop(pdl, t1_tfqmr, vec_grid(A, (const void*)t1_tfqmr), 0, s, dc));
+            if (dist) ZK_TRY((dist_finish<S_T1_TFQMR>(A, dc, 1, s)));
+            if (dist) ZK_TRY(dist_halo(A, hc.y2, s));
+            { auto kf = t2_tfqmr<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
+            if (dist) ZK_TRY((dist_finish<S_T2_TFQMR>(A, dc, 3, s)));
+            ZK_TRY(launch_loop(pdl, t3_tfqmr, vec_grid(A, (const void*)t3_tfqmr), 0, s, dc));
+            if (dist) ZK_TRY(dist_halo(A, hc.y1, s));
+            { auto kf = t4_tfqmr<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
+            if (dist) ZK_TRY((dist_finish<S_T4_TFQMR>(A, dc, 2, s)));
+        } else if (method == ZK_COCG) {
+            if (dist) ZK_TRY(dist_halo(A, hc.p, s));
+            { auto kf = k1_cocg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
+            if (dist) ZK_TRY((dist_finish<S_K1_COCG>(A, dc, 2, s)));
+            ZK_TRY(launch_loop(pdl, k2_cocg, vec_grid(A, (const void*)k2_cocg), 0, s, dc));
+            if (dist) ZK_TRY((dist_finish<S_K2_COCG>(A, dc, 3, s)));
+            ZK_TRY(launch_loop(pdl, k3_cocg, vec_grid(A, (const void*)k3_cocg), 0, s, dc));
         } else {
             if (dist) ZK_TRY(dist_halo(A, hc.p, s));
             { auto kf = k1_cg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
@@ -834,8 +1243,9 @@ static WsLayout ws_layout(const zk_csr_s* A, int method, int32_t maxit) {
     L.vec0 = off;
     const int64_t len = A->dist ? dist_gather_len(A) : A->n_rows;
     L.vec_bytes = up256(sizeof(double2) * (size_t)(len > 0 ? len : 1));
-    // BiCGStab: r r̂ p v s t (+ xg gather copy on >1 GPU) ; CG: r p q (+ xg)
-    L.nvec = (method == ZK_BICGSTAB ? 6 : 3) + (A->dist ? 1 : 0);
+    // BiCGStab: r r̂ p v s t (+ xg gather copy on >1 GPU) ; CG/COCG: r p q (+ xg) ;
+    // TFQMR: w y1 y2 u1 u2 v d1 d2 r̃ (+ xg)
+    L.nvec = (method == ZK_BICGSTAB ? 6 : method == ZK_TFQMR ? 9 : 3) + (A->dist ? 1 : 0);
     off += L.vec_bytes * L.nvec;
     L.total = off;
     return L;
@@ -846,7 +1256,7 @@ static WsLayout ws_layout(const zk_csr_s* A, int method, int32_t maxit) {
 using namespace zk;
 
 extern "C" size_t zk_solve_workspace_size(zk_csr A, int32_t method, int32_t maxit) {
-    if (!A || (method != ZK_BICGSTAB && method != ZK_CG && method != ZK_BICGSTAB_JACOBI)) return 0;
+    if (!A || method < ZK_BICGSTAB || method > ZK_TFQMR) return 0;
     if (method == ZK_BICGSTAB_JACOBI) method = ZK_BICGSTAB;
     return ws_layout(A, method, maxit).total;
 }
@@ -855,7 +1265,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
                               zk_z* x, int32_t* iters, double* resid_hist, zk_solve_info* info, void* workspace,
                               size_t ws_bytes, zk_stream stream) {
     if (!A || !b || !x || !iters || !resid_hist || !workspace) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
-    if (method != ZK_BICGSTAB && method != ZK_CG && method != ZK_BICGSTAB_JACOBI)
+    if (method < ZK_BICGSTAB || method > ZK_TFQMR)
         return fail(ZK_ERR_INVALID_VALUE, "unknown method");
     const bool jacobi = method == ZK_BICGSTAB_JACOBI;
     if (jacobi) {
@@ -881,10 +1291,14 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     hc.partials = (double*)(ws + L.partials);
     hc.tickets = (unsigned int*)(ws + L.tickets);
     hc.hist = (double*)(ws + L.hist);
-    double2* vec[8];
+    double2* vec[10];
     for (int i = 0; i < L.nvec; i++) vec[i] = (double2*)(ws + L.vec0 + L.vec_bytes * i);
     if (method == ZK_BICGSTAB) {
         hc.r = vec[0]; hc.rh = vec[1]; hc.p = vec[2]; hc.v = vec[3]; hc.s = vec[4]; hc.t = vec[5];
+    } else if (method == ZK_TFQMR) {
+        hc.w = vec[0]; hc.y1 = vec[1]; hc.y2 = vec[2]; hc.u1 = vec[3]; hc.u2 = vec[4]; hc.v = vec[5];
+        hc.d1 = vec[6]; hc.d2 = vec[7]; hc.rt = vec[8];
+        hc.r = hc.w; hc.p = hc.y1; hc.rh = hc.rt;  // the shared init writes r0 into w, y1 and r̃
     } else {
         hc.r = vec[0]; hc.p = vec[1]; hc.q = vec[2];
     }
@@ -911,6 +1325,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     if (A->dist && (mode == 1 || mode == 4)) mode = 3;  // NCCL inside WHILE bodies / persistent kernels is not used
     int persist_grid = 0;
     const void* kp = nullptr;
+    if (mode == 4 && (method == ZK_COCG || method == ZK_TFQMR)) mode = 1;  // persistent: BiCGStab and CG only
     if (mode == 4) {
         int dev_coop = 0;
         cudaDeviceGetAttribute(&dev_coop, cudaDevAttrCooperativeLaunch, A->dev.device);
@@ -962,7 +1377,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     // ---- init: context, r0 = b − A x0 (or b), ‖b‖, hist[0]
     k_set_ctx<<<1, 1, 0, s>>>(dc, hc);
     ZK_CUDA(cudaGetLastError());
-    const bool bicg = method == ZK_BICGSTAB;
+    const int kind = method == ZK_BICGSTAB ? 0 : method == ZK_CG ? 1 : method == ZK_COCG ? 3 : 4;
     if (x0) {
         const double2* g0 = (const double2*)x0;
         if (jacobi) {  // u0 = M x0, in the output buffer (x may alias x0)
@@ -976,24 +1391,49 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         }
         ZK_TRY(with_spmv(A, [&](auto wc, auto mc) -> zk_status {
             constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
-            if (bicg) {
+            if (kind == 0) {
                 auto k = k_init_x0<W, MODE, S_INIT_BICG>;
                 const LaunchCfg L = spmv_cfg(A, (const void*)k, W, MODE);
                 k<<<L.grid, kBlock, L.smem, s>>>(dc, g0, 1);
-            } else {
+            } else if (kind == 1) {
                 auto k = k_init_x0<W, MODE, S_INIT_CG>;
                 const LaunchCfg L = spmv_cfg(A, (const void*)k, W, MODE);
                 k<<<L.grid, kBlock, L.smem, s>>>(dc, g0, 0);
+            } else if (kind == 3) {
+                auto k = k_init_x0<W, MODE, S_INIT_COCG>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)k, W, MODE);
+                k<<<L.grid, kBlock, L.smem, s>>>(dc, g0, 0);
+            } else {
+                auto k = k_init_x0<W, MODE, S_INIT_TFQMR>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)k, W, MODE);
+                k<<<L.grid, kBlock, L.smem, s>>>(dc, g0, 1);
             }
             ZK_CUDA(cudaGetLastError());
             return ZK_OK;
         }));
         n_spmv++;
     } else {
-        k_init_zero<<<vec_grid(A, (const void*)k_init_zero), kBlock, 0, s>>>(dc, bicg ? 1 : 0);
+        k_init_zero<<<vec_grid(A, (const void*)k_init_zero), kBlock, 0, s>>>(dc, kind);
         ZK_CUDA(cudaGetLastError());
     }
-    if (A->dist) ZK_TRY(bicg ? dist_finish<S_INIT_BICG>(A, dc, 2, s) : dist_finish<S_INIT_CG>(A, dc, 2, s));
+    if (A->dist)
+        ZK_TRY(kind == 0   ? dist_finish<S_INIT_BICG>(A, dc, 4, s)
+               : kind == 1 ? dist_finish<S_INIT_CG>(A, dc, 4, s)
+               : kind == 3 ? dist_finish<S_INIT_COCG>(A, dc, 4, s)
+                           : dist_finish<S_INIT_TFQMR>(A, dc, 4, s));
+    if (method == ZK_TFQMR) {  // u1 = v = A y1 and σ = ⟨r̃, v⟩ → α for iteration 1
+        if (A->dist) ZK_TRY(dist_halo(A, hc.y1, s));
+        ZK_TRY(with_spmv(A, [&](auto wc, auto mc) -> zk_status {
+            constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
+            auto k = k0_tfqmr<W, MODE>;
+            const LaunchCfg L = spmv_cfg(A, (const void*)k, W, MODE);
+            k<<<L.grid, kBlock, L.smem, s>>>(dc);
+            ZK_CUDA(cudaGetLastError());
+            return ZK_OK;
+        }));
+        if (A->dist) ZK_TRY(dist_finish<S_K0_TFQMR>(A, dc, 2, s));
+        n_spmv++;
+    }
 
     // ---- the loop
     SolveCtx* hdone = nullptr;  // pinned copy of the ctx for the chunked modes
@@ -1054,7 +1494,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
 
     *iters = out.iters;
     const int passes = out.iters;
-    n_spmv += (int64_t)passes * (method == ZK_BICGSTAB ? 2 : 1) + 1;
+    n_spmv += (int64_t)passes * (method == ZK_BICGSTAB || method == ZK_TFQMR ? 2 : 1) + 1;
     if (info) {
         info->status = out.status == ST_ZERO_RHS ? ZK_CONVERGED : out.status;
         info->iters = out.iters;
@@ -1062,9 +1502,10 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         info->n_spmv = n_spmv;
         info->solve_ms = ms;
         info->loop_mode = mode;
-        const int per_body = method == ZK_BICGSTAB ? 5 : 3;
-        const int fins = A->dist ? (method == ZK_BICGSTAB ? 4 : 2) : 0;  // dist: 1-thread finish kernels
-        info->gpu_launches = mode == 4 ? 4 : 3 + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);
+        const int per_body = method == ZK_BICGSTAB ? 5 : method == ZK_TFQMR ? 4 : 3;
+        const int fins = A->dist ? (method == ZK_BICGSTAB ? 4 : method == ZK_TFQMR ? 3 : 2) : 0;  // dist: 1-thread finish kernels
+        const int pre = method == ZK_TFQMR ? (A->dist ? 2 : 1) : 0;                               // TFQMR: K0 (+ its finish)
+        info->gpu_launches = mode == 4 ? 4 : 3 + pre + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);
         for (int i = 0; i < 4; i++) {
             info->kernel_ms[i] = out.tsum[i] * 1e-6;
             info->kernel_launches[i] = out.tcnt[i];

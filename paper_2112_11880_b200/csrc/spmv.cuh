@@ -22,6 +22,15 @@ namespace zk {
 //   typename Pre; __device__ Pre pre(int64_t i);   // row i's own operands (loaded a tile ahead)
 //   __device__ void row(int64_t i, double2 y, const Pre&, double (&acc)[K>0?K:1]);   // once per row
 //   __device__ void finish(double (&acc)[K>0?K:1]); // called by every thread at the end
+//   optional static constexpr bool kAhead = false;  // load pre() at the start of the row's own tile
+//                                                   // instead of one tile ahead (wide Pre: one copy
+//                                                   // in registers instead of two)
+template <class E>
+struct pre_ahead {
+    template <class T> static constexpr bool get(decltype(T::kAhead)*) { return T::kAhead; }
+    template <class T> static constexpr bool get(...) { return true; }
+    static constexpr bool value = get<E>(nullptr);
+};
 #ifndef ZK_DEFAULT_LP
 #define ZK_DEFAULT_LP 1
 #endif
@@ -35,6 +44,7 @@ __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __rest
     constexpr int RPB = kBlock / W;  // rows per block step
     constexpr int U = ZK_SPMV_U;     // nonzeros per lane per chunk
     constexpr int KA = Epi::K > 0 ? Epi::K : 1;
+    constexpr bool AHEAD = pre_ahead<Epi>::value;
     const uint64_t pol = make_policy<LP>();
     double acc[KA];
 #pragma unroll
@@ -53,7 +63,7 @@ __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __rest
     if (row < n) {
         rs = __ldg(A.row_ptr + row);
         len = (int)(__ldg(A.row_ptr + row + 1) - rs);
-        if (sub == 0) pre = epi.pre(row);
+        if (AHEAD && sub == 0) pre = epi.pre(row);
     }
     for (int tile = blockIdx.x; tile * RPB < n; tile += G) {
         // bounds (and epilogue operands) of this lane's row in the next tile, used next iteration
@@ -61,10 +71,11 @@ __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __rest
         int64_t nrs = 0;
         int nlen = 0;
         typename Epi::Pre npre{};
+        if (!AHEAD && sub == 0 && row < n) pre = epi.pre(row);
         if (nrow < n) {
             nrs = __ldg(A.row_ptr + nrow);
             nlen = (int)(__ldg(A.row_ptr + nrow + 1) - nrs);
-            if (sub == 0) npre = epi.pre(nrow);
+            if (AHEAD && sub == 0) npre = epi.pre(nrow);
         }
         double2 sum = make_double2(0.0, 0.0);
         const double2* vr = A.val + rs;
@@ -99,7 +110,7 @@ __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __rest
         row = nrow;
         rs = nrs;
         len = nlen;
-        pre = npre;
+        if (AHEAD) pre = npre;
     }
     epi.finish(acc);
 }

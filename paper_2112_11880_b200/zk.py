@@ -18,8 +18,8 @@ SO_PATH = os.path.join(_PKG, "libzk.so")
 
 ZK_PTRS_HOST, ZK_PTRS_DEVICE, ZK_PTRS_DEVICE_BORROW, ZK_SKIP_VALIDATE = 0, 1, 2, 4
 ZK_BICGSTAB, ZK_CG = 0, 1
-ZK_BICGSTAB_JACOBI = 2
-METHODS = {"bicgstab": ZK_BICGSTAB, "cg": ZK_CG, "bicgstab_jacobi": ZK_BICGSTAB_JACOBI}
+ZK_BICGSTAB_JACOBI, ZK_COCG, ZK_TFQMR = 2, 3, 4
+METHODS = {"bicgstab": ZK_BICGSTAB, "cg": ZK_CG, "bicgstab_jacobi": ZK_BICGSTAB_JACOBI, "cocg": ZK_COCG, "tfqmr": ZK_TFQMR}
 OUTCOMES = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN_RHO", 3: "BREAKDOWN_SIGMA", 4: "BREAKDOWN_OMEGA",
             5: "NOT_HPD", 6: "NONFINITE"}
 
@@ -67,6 +67,8 @@ SIGNATURES = {
     "zk_dznrm2": (I32, [I64, P, P, P, P]),
     "zk_zaxpy": (I32, [I64, zk_z, P, P, P]),
     "zk_zscal": (I32, [I64, zk_z, P, P]),
+    "zk_zassign": (I32, [I64, zk_z, P, P]),
+    "zk_zaxmy": (I32, [I64, P, P, P]),
     "zk_solve_workspace_size": (SZ, [P, I32, I32]),
     "zk_solve": (I32, [P, P, P, D, I32, I32, P, ctypes.POINTER(I32), P, ctypes.POINTER(zk_solve_info), P, SZ, P]),
     # include/zk_dist.h (host-only)
@@ -248,6 +250,20 @@ def zscal(alpha, x: torch.Tensor, stream=None) -> torch.Tensor:
     """x ← αx (zk_zscal)."""
     _check(lib().zk_zscal(x.numel(), _z(alpha), _dev_c128(x, "x"), _stream(stream)))
     return x
+
+
+def zassign(alpha, x: torch.Tensor, stream=None) -> torch.Tensor:
+    """x ← α (zk_zassign; the paper's ZASSIGN fill)."""
+    _check(lib().zk_zassign(x.numel(), _z(alpha), _dev_c128(x, "x"), _stream(stream)))
+    return x
+
+
+def zaxmy(x: torch.Tensor, y: torch.Tensor, stream=None) -> torch.Tensor:
+    """y ← x ⊙ y (zk_zaxmy; the paper's ZAXMY / EWProduct)."""
+    if x.numel() != y.numel():
+        raise ValueError("length mismatch")
+    _check(lib().zk_zaxmy(x.numel(), _dev_c128(x, "x"), _dev_c128(y, "y"), _stream(stream)))
+    return y
 
 
 def workspace_size(A: Csr, method: str = "bicgstab", maxit: int = 1000) -> int:

@@ -273,3 +273,22 @@ def test_zaxpy_zscal_exact_alphas():
     Y = cuda(yi)
     zk.zaxpy(3 - 2j, cuda(xi), Y)
     assert np.array_equal(Y.cpu().numpy(), oracle.zaxpy(3 - 2j, xi, yi))
+
+
+# ------------------------------------------------------------------ ZASSIGN / ZAXMY (NEXT-4)
+def test_zassign_zaxmy():
+    x = torch.empty(1_000_003, dtype=torch.complex128, device=DEV)
+    zk.zassign(1.5 - 2j, x)
+    assert np.array_equal(x.cpu().numpy(), oracle.zassign(1_000_003, 1.5 - 2j))
+    a, b = gen.rand_vector(1 << 20, 1), gen.rand_vector(1 << 20, 2)
+    Y = cuda(b)
+    zk.zaxmy(cuda(a), Y)
+    want = oracle.zaxmy(a, b)
+    assert np.all(np.abs(Y.cpu().numpy() - want) <= 1e-15 * np.abs(a) * np.abs(b))
+    ai, bi = gen.int_vector(100_001, 3), gen.int_vector(100_001, 4)
+    Y = cuda(bi)
+    zk.zaxmy(cuda(ai), Y)
+    assert np.array_equal(Y.cpu().numpy(), oracle.zaxmy(ai, bi))    # integer-exact: bitwise
+    one_i = cuda(np.array([1j]))
+    zk.zaxmy(one_i, one_i)
+    assert one_i.cpu().numpy()[0] == -1

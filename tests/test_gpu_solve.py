@@ -302,3 +302,54 @@ def test_persistent_loop_parity(cfg, method, monkeypatch):
     k = min(12, r["iters"]) + 1
     assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= 1e-10
     assert relerr(r["x"], refs[0]["x"]) <= 1e-6
+
+
+# ------------------------------------------------------------------ COCG (NEXT-4)
+@pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
+def test_cocg_parity(cfg):
+    """COCG on the absorbing complex-symmetric Helmholtz matrices: ±5 % of the oracle's count
+    (like CG, the recurrences are order-insensitive), hist prefix, solution 1e-6."""
+    m = gen.make_matrix(cfg)
+    b = gen.make_rhs(m)
+    r = gpu_solve(m, b, tol=1e-8, method="cocg")
+    ref = oracle.cocg(m, b, tol=1e-8)
+    assert r["status"] == ref["status"] == "CONVERGED"
+    assert abs(r["iters"] - ref["iters"]) <= 0.05 * ref["iters"], (r["iters"], ref["iters"])
+    k = min(12, r["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-10
+    assert relerr(r["x"], ref["x"]) <= 1e-6
+    assert r["true_relres"] <= 2e-8
+
+
+def test_cocg_cases():
+    n = 200
+    c = 0.3 - 2j
+    m = dict(row_ptr=np.arange(n + 1, dtype=np.int64), col_idx=np.arange(n, dtype=np.int32),
+             values=np.full(n, c, np.complex128), n=n)
+    b = gen.rand_vector(n, 1)
+    r = gpu_solve(m, b, tol=1e-12, method="cocg")
+    assert r["status"] == "CONVERGED" and r["iters"] == 1
+    # quasi-null start bᵀb = 0 → BREAKDOWN_SIGMA, as the oracle
+    m2 = dict(row_ptr=np.arange(3, dtype=np.int64), col_idx=np.arange(2, dtype=np.int32),
+              values=np.ones(2, np.complex128), n=2)
+    bb = np.array([1, 1j])
+    assert gpu_solve(m2, bb, method="cocg")["status"] == oracle.cocg(m2, bb)["status"] == "BREAKDOWN_SIGMA"
+    # x0 path and MAXIT history against the oracle
+    mc = gen.make_matrix("C2")
+    bc = gen.make_rhs(mc)
+    x0 = gen.rand_vector(mc["n"], 5)
+    r = gpu_solve(mc, bc, x0=x0, tol=1e-14, maxit=7, method="cocg")
+    ref = oracle.cocg(mc, bc, x0=x0, tol=1e-14, maxit=7)
+    assert r["status"] == ref["status"] == "MAXIT" and r["iters"] == 7
+    assert np.max(np.abs(r["hist"] - ref["hist"]) / ref["hist"]) <= 1e-10
+
+
+def test_cocg_c4():
+    spec = gen.CONFIGS["C4"]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    A = zk.csr_create(cuda(m["row_ptr"]), cuda(m["col_idx"]), cuda(m["values"]), m["n"], borrow=True)
+    r = zk.solve(A, cuda(b), tol=1e-8, maxit=2000, method="cocg")
+    assert r["status"] == "CONVERGED" and r["true_relres"] <= 2e-8
+    xe = cf.box_solve(spec, b, gen.ETA)
+    assert relerr(r["x"].cpu().numpy(), xe) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
