@@ -60,6 +60,8 @@ def _lib():
         for f in (lib.oracle_bicgstab, lib.oracle_cg, lib.oracle_bicgstab_jacobi, lib.oracle_cocg, lib.oracle_tfqmr):
             f.argtypes = [I64, P, P, P, P, P, D, ctypes.c_int32, I, P, P, P, P]
             f.restype = I
+        lib.oracle_bicgstab_l.argtypes = [I64, P, P, P, P, P, D, ctypes.c_int32, I, I, P, P, P, P]
+        lib.oracle_bicgstab_l.restype = I
         _h = lib
     return _h
 
@@ -123,7 +125,7 @@ def zscal(alpha, x) -> np.ndarray:
     return out
 
 
-def _solve(fn, A, b, x0, tol, maxit, order):
+def _solve(fn, A, b, x0, tol, maxit, order, *extra):
     rp = np.ascontiguousarray(A["row_ptr"], dtype=np.int64)
     col = np.ascontiguousarray(A["col_idx"], dtype=np.int32)
     val = _c128(A["values"])
@@ -134,7 +136,7 @@ def _solve(fn, A, b, x0, tol, maxit, order):
     iters = ctypes.c_int32(0)
     hist = np.full(maxit + 1, np.nan)
     tr = ctypes.c_double(0.0)
-    st = fn(n, _ptr(rp), _ptr(col), _ptr(val), _ptr(b), _ptr(x0), float(tol), int(maxit), order,
+    st = fn(n, _ptr(rp), _ptr(col), _ptr(val), _ptr(b), _ptr(x0), float(tol), int(maxit), order, *extra,
             _ptr(x), ctypes.addressof(iters), _ptr(hist), ctypes.addressof(tr))
     it = iters.value
     return dict(x=x, iters=it, hist=hist[: it + 1].copy(), status=STATUS[st],
@@ -179,3 +181,10 @@ def cocg(A, b, x0=None, tol=1e-8, maxit=1000, order=ORD_SEQ) -> dict:
 def tfqmr(A, b, x0=None, tol=1e-8, maxit=1000, order=ORD_SEQ) -> dict:
     """NEXT-2 TFQMR (Freund; Kelley's two-half-step form), the paper's P-TFQMR without M."""
     return _solve(_lib().oracle_tfqmr, A, b, x0, tol, maxit, order)
+
+
+def bicgstab_l(A, b, x0=None, tol=1e-8, maxit=1000, ell=8, order=ORD_SEQ) -> dict:
+    """NEXT-3 BiCGStab(ℓ) (Sleijpen & Fokkema 1993), the paper's P-BiCGSTAB(8) without M (P:308;
+    S:367-371); iters and hist count outer cycles of 2ℓ SpMVs."""
+    assert 1 <= ell <= 8
+    return _solve(_lib().oracle_bicgstab_l, A, b, x0, tol, maxit, order, int(ell))

@@ -740,3 +740,185 @@ done:
     free(r); free(w); free(y1); free(y2); free(u1); free(u2); free(v); free(d); free(rt);
     return status;
 }
+
+/*
+ * NEXT-3: BiCGStab(ℓ) (Sleijpen & Fokkema 1993), the paper's "P-BiCGSTAB parametered (l)" /
+ * "P-BiCGSTAB(8)" without preconditioner (§4, T9/T10 headers),
+ * complex arithmetic with the Hermitian product ⟨x, y⟩ = Σ conj(x_i) y_i, r̃ = r0.
+ * One outer cycle k (2ℓ SpMVs; hist/iters count cycles, SURVEY.md §8 A2 / T9-T10 "#iter"):
+ *   ρ0 = −ω ρ0
+ *   BiCG part, j = 0..ℓ−1:
+ *     ρ1 = ⟨r̃, r̂_j⟩ (|ρ1| ≤ 1e-30‖r̃‖‖r̂_j‖ → BREAKDOWN_RHO); β = α ρ1 / ρ0; ρ0 = ρ1
+ *     û_i = r̂_i − β û_i (i = 0..j);  û_{j+1} = A û_j
+ *     γ = ⟨r̃, û_{j+1}⟩ (|γ| ≤ 1e-30‖r̃‖‖û_{j+1}‖ → BREAKDOWN_SIGMA); α = ρ0 / γ
+ *     r̂_i = r̂_i − α û_{i+1} (i = 0..j);  x̂ = x̂ + α û_0
+ *     ‖r̂_0‖/‖b‖ ≤ tol → CONVERGED inside the cycle (BiCGStab's half-step test, L6)
+ *     r̂_{j+1} = A r̂_j
+ *   MR part ("coefficients solve the l×l least-squares system of inner products"):
+ *     G_ij = ⟨r̂_i, r̂_j⟩ (i, j = 0..ℓ); solve G[1..ℓ,1..ℓ] γ = G[1..ℓ,0] by Cholesky (a non-positive
+ *     or non-finite pivot → BREAKDOWN_OMEGA); ω = γ_ℓ
+ *     x̂ = x̂ + Σ_j γ_j r̂_{j−1};  r̂_0 = r̂_0 − Σ_j γ_j r̂_j;  û_0 = û_0 − Σ_j γ_j û_j   (j = 1..ℓ)
+ *   hist[k] = ‖r̂_0‖/‖b‖; converged if ≤ tol; |ω| ≤ 1e-30 → BREAKDOWN_OMEGA.
+ * Start: x̂ = x0, r̂_0 = b − A x0, û_0 = 0, ρ0 = 1, α = 0, ω = 1.  *iters = the cycle in which the
+ * loop ended (an exit inside a cycle, convergence or breakdown, counts that cycle).  With ℓ = 1 this is BiCGStab
+ * (O6) up to rounding (pinned in tests/test_oracle_solvers.py).  ℓ ∈ [1, 8].
+ */
+int oracle_bicgstab_l(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val, const double* b,
+                      const double* x0, double tol, int32_t maxit, int order, int ell, double* x, int32_t* iters,
+                      double* hist, double* out_true_relres) {
+    csr_t A = {n, row_ptr, col, val, order};
+    if (ell < 1 || ell > 8) return -1;
+    size_t bytes = (size_t)(2 * n) * sizeof(double);
+    double* rr[9];
+    double* uu[9];
+    for (int i = 0; i <= ell; i++) {
+        rr[i] = malloc(bytes);
+        uu[i] = calloc((size_t)(2 * n), sizeof(double));
+    }
+    double* rt = malloc(bytes);
+    int status = ST_MAXIT;
+    *iters = 0;
+    *out_true_relres = NAN;
+    double* r = rr[0];
+    if (x0) {
+        memcpy(x, x0, bytes);
+        spmv(&A, x, r);
+        for (int64_t i = 0; i < 2 * n; i++) r[i] = b[i] - r[i];
+    } else {
+        memset(x, 0, bytes);
+        memcpy(r, b, bytes);
+    }
+    double nb = nrm(&A, b);
+    if (nb == 0.0) { status = ST_ZERO_RHS; goto done; }
+    double rnorm = nrm(&A, r);
+    hist[0] = rnorm / nb;
+    if (!isfinite(hist[0])) { status = ST_NONFINITE; goto done; }
+    if (hist[0] <= tol) { status = ST_CONVERGED; goto done_true; }
+    memcpy(rt, r, bytes);
+    double nrt = rnorm;
+    cplx rho0 = {1, 0}, alpha = {0, 0}, omega = {1, 0};
+    for (int32_t k = 1; k <= maxit; k++) {
+        *iters = k;                                                 /* an exit inside a cycle counts it */
+        cplx mw = {-omega.re, -omega.im};
+        rho0 = cmul(mw, rho0);                                      /* ρ0 = −ω ρ0 */
+        for (int j = 0; j < ell; j++) {
+            cplx rho1 = dotc(&A, rt, rr[j]);                        /* ρ1 = ⟨r̃, r̂_j⟩ */
+            if (!cfinite(rho1)) { status = ST_NONFINITE; goto done_true; }
+            if (cabs_(rho1) <= 1e-30 * nrt * nrm(&A, rr[j])) { status = ST_BREAKDOWN_RHO; goto done_true; }
+            cplx beta = cdiv(cmul(alpha, rho1), rho0);              /* β = α ρ1 / ρ0 */
+            rho0 = rho1;
+            for (int i = 0; i <= j; i++)                            /* û_i = r̂_i − β û_i */
+                for (int64_t e = 0; e < n; e++) {
+                    cplx uv = {RE(uu[i], e), IM(uu[i], e)};
+                    cplx bu = cmul(beta, uv);
+                    RE(uu[i], e) = RE(rr[i], e) - bu.re;
+                    IM(uu[i], e) = IM(rr[i], e) - bu.im;
+                }
+            spmv(&A, uu[j], uu[j + 1]);                             /* û_{j+1} = A û_j */
+            cplx gam = dotc(&A, rt, uu[j + 1]);                     /* γ = ⟨r̃, û_{j+1}⟩ */
+            if (!cfinite(gam)) { status = ST_NONFINITE; goto done_true; }
+            if (cabs_(gam) <= 1e-30 * nrt * nrm(&A, uu[j + 1])) { status = ST_BREAKDOWN_SIGMA; goto done_true; }
+            alpha = cdiv(rho0, gam);                                /* α = ρ0 / γ */
+            for (int i = 0; i <= j; i++)                            /* r̂_i = r̂_i − α û_{i+1} */
+                for (int64_t e = 0; e < n; e++) {
+                    cplx uv = {RE(uu[i + 1], e), IM(uu[i + 1], e)};
+                    cplx au = cmul(alpha, uv);
+                    RE(rr[i], e) -= au.re;
+                    IM(rr[i], e) -= au.im;
+                }
+            for (int64_t e = 0; e < n; e++) {                       /* x̂ = x̂ + α û_0 */
+                cplx uv = {RE(uu[0], e), IM(uu[0], e)};
+                cplx au = cmul(alpha, uv);
+                RE(x, e) += au.re;
+                IM(x, e) += au.im;
+            }
+            double rn = nrm(&A, rr[0]);
+            if (!isfinite(rn)) { status = ST_NONFINITE; goto done_true; }
+            if (rn / nb <= tol) {                                   /* exit inside the cycle */
+                hist[k] = rn / nb;
+                status = ST_CONVERGED;
+                goto done_true;
+            }
+            spmv(&A, rr[j], rr[j + 1]);                             /* r̂_{j+1} = A r̂_j */
+        }
+        /* MR part: G_ij = ⟨r̂_i, r̂_j⟩ ; M γ = g with M = G[1..ℓ,1..ℓ], g_i = G[i][0] */
+        cplx G[9][9];
+        for (int i = 0; i <= ell; i++)
+            for (int j = i; j <= ell; j++) {
+                G[i][j] = dotc(&A, rr[i], rr[j]);
+                cplx c = {G[i][j].re, -G[i][j].im};
+                G[j][i] = c;
+            }
+        /* Cholesky M = L Lᴴ (L lower, real positive diagonal), written out */
+        cplx L[8][8];
+        int bad = 0;
+        for (int j = 0; j < ell && !bad; j++) {
+            double dsum = G[j + 1][j + 1].re;
+            for (int q = 0; q < j; q++) dsum -= L[j][q].re * L[j][q].re + L[j][q].im * L[j][q].im;
+            if (!(dsum > 0.0) || !isfinite(dsum)) { bad = 1; break; }
+            double ljj = sqrt(dsum);
+            L[j][j] = make_cplx_real(ljj);
+            for (int i = j + 1; i < ell; i++) {
+                cplx s = G[i + 1][j + 1];
+                for (int q = 0; q < j; q++) {                       /* s −= L_iq conj(L_jq) */
+                    cplx cj = {L[j][q].re, -L[j][q].im};
+                    cplx t = cmul(L[i][q], cj);
+                    s.re -= t.re;
+                    s.im -= t.im;
+                }
+                L[i][j].re = s.re / ljj;
+                L[i][j].im = s.im / ljj;
+            }
+        }
+        if (bad) { status = ST_BREAKDOWN_OMEGA; goto done_true; }
+        cplx y[8], gm[9];
+        for (int i = 0; i < ell; i++) {                             /* L y = g */
+            cplx s = G[i + 1][0];
+            for (int q = 0; q < i; q++) {
+                cplx t = cmul(L[i][q], y[q]);
+                s.re -= t.re;
+                s.im -= t.im;
+            }
+            y[i].re = s.re / L[i][i].re;
+            y[i].im = s.im / L[i][i].re;
+        }
+        for (int i = ell - 1; i >= 0; i--) {                        /* Lᴴ γ = y */
+            cplx s = y[i];
+            for (int q = i + 1; q < ell; q++) {                     /* s −= conj(L_qi) γ_q */
+                cplx cq = {L[q][i].re, -L[q][i].im};
+                cplx t = cmul(cq, gm[q + 1]);
+                s.re -= t.re;
+                s.im -= t.im;
+            }
+            gm[i + 1].re = s.re / L[i][i].re;
+            gm[i + 1].im = s.im / L[i][i].re;
+        }
+        omega = gm[ell];                                            /* ω = γ_ℓ */
+        for (int64_t e = 0; e < n; e++) {
+            double xr = RE(x, e), xi = IM(x, e), r0r = RE(rr[0], e), r0i = IM(rr[0], e);
+            double u0r = RE(uu[0], e), u0i = IM(uu[0], e);
+            for (int j = 1; j <= ell; j++) {
+                cplx rp = {RE(rr[j - 1], e), IM(rr[j - 1], e)}, rj = {RE(rr[j], e), IM(rr[j], e)};
+                cplx uj = {RE(uu[j], e), IM(uu[j], e)};
+                cplx a = cmul(gm[j], rp), c = cmul(gm[j], rj), d = cmul(gm[j], uj);
+                xr += a.re; xi += a.im;                             /* x̂ += γ_j r̂_{j−1} */
+                r0r -= c.re; r0i -= c.im;                           /* r̂_0 −= γ_j r̂_j   */
+                u0r -= d.re; u0i -= d.im;                           /* û_0 −= γ_j û_j   */
+            }
+            RE(x, e) = xr; IM(x, e) = xi;
+            RE(rr[0], e) = r0r; IM(rr[0], e) = r0i;
+            RE(uu[0], e) = u0r; IM(uu[0], e) = u0i;
+        }
+        rnorm = nrm(&A, rr[0]);
+        hist[k] = rnorm / nb;
+        if (!isfinite(hist[k]) || !cfinite(omega)) { status = ST_NONFINITE; break; }
+        if (hist[k] <= tol) { status = ST_CONVERGED; break; }
+        if (cabs_(omega) <= 1e-30) { status = ST_BREAKDOWN_OMEGA; break; }
+    }
+done_true:
+    *out_true_relres = true_relres(&A, b, x, nb, uu[1]);
+done:
+    for (int i = 0; i <= ell; i++) { free(rr[i]); free(uu[i]); }
+    free(rt);
+    return status;
+}

@@ -49,7 +49,7 @@ def test_bicgstab_scalar_identity(c):
 
 @pytest.mark.parametrize("cfg", ["C1", "T0"])
 def test_bicgstab_dense_lu(cfg):
-    """‖x − x_LU‖/‖x_LU‖ ≤ 1e-7 at tol 1e-10 (S:388)."""
+    """‖x − x_LU‖/‖x_LU‖ ≤ 1e-7 at tol 1e-10 (S:389)."""
     m = gen.make_matrix(cfg)
     b = gen.make_rhs(m)
     D = sp.csr_matrix((m["values"], m["col_idx"], m["row_ptr"]), shape=(m["n"], m["n"])).toarray()
@@ -71,7 +71,7 @@ def test_bicgstab_dst_exact(cfg):
     kappa = cf.box_kappa(spec, gen.ETA)
     assert r["status"] == "CONVERGED"
     assert np.linalg.norm(r["x"] - xe) / np.linalg.norm(xe) <= 2 * kappa * tol
-    # true vs recurrence residual (S:387 allows 10·tol; we require tol)
+    # true vs recurrence residual (S:388 allows 10·tol; we require tol)
     assert abs(r["true_relres"] - r["hist"][-1]) <= tol
     assert r["true_relres"] <= 2 * tol
     # solution-agreement reading L12 is binding literally on C1/C2
@@ -308,7 +308,7 @@ def test_tfqmr_closed_form(cfg):
 
 def test_tfqmr_bound_and_monotone_tau():
     """Stopped after k iterations (MAXIT) the true residual never exceeds hist[k] = τ√(2k+1)/‖b‖,
-    and τ = hist[k]/√(2k+1)·‖b‖ is non-increasing (S:389 "monotone quasi-residual")."""
+    and τ = hist[k]/√(2k+1)·‖b‖ is non-increasing (S:390 "monotone quasi-residual")."""
     m = gen.make_matrix("C2")
     b = gen.make_rhs(m)
     full = oracle.tfqmr(m, b, tol=1e-10)
@@ -332,3 +332,105 @@ def test_tfqmr_dense_lu_and_gauge():
     rg = oracle.tfqmr(mg, Dg * b, tol=1e-10)
     assert rg["iters"] == r["iters"]
     assert np.max(np.abs(rg["hist"] - r["hist"]) / r["hist"]) <= 1e-10
+
+
+# ------------------------------------------------------------------ BiCGStab(ℓ) (NEXT-3)
+@pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
+def test_bicgstab_l1_is_bicgstab(cfg):
+    """ℓ = 1 reduces to BiCGStab: the independently pinned O6 gives the same count, the
+    same residual history (to rounding, first 12 iterations) and the same solution."""
+    m = gen.make_matrix(cfg)
+    b = gen.make_rhs(m)
+    r1 = oracle.bicgstab_l(m, b, tol=1e-8, ell=1)
+    r0 = oracle.bicgstab(m, b, tol=1e-8)
+    assert r1["status"] == r0["status"] == "CONVERGED" and r1["iters"] == r0["iters"]
+    k = min(12, r0["iters"]) + 1
+    assert np.max(np.abs(r1["hist"][:k] - r0["hist"][:k]) / r0["hist"][:k]) <= 1e-9
+    assert np.linalg.norm(r1["x"] - r0["x"]) / np.linalg.norm(r0["x"]) <= 1e-6
+
+
+@pytest.mark.parametrize("ell", [1, 2, 8])
+@pytest.mark.parametrize("c", [2.0, -1.0, 1j, 0.3 - 2j])
+def test_bicgstab_l_scalar_identity(c, ell):
+    """One-step exactness: A = cI converges in the first cycle, x = b/c."""
+    b = gen.rand_vector(60, 1)
+    r = oracle.bicgstab_l(diag_csr(np.full(60, c)), b, tol=1e-12, ell=ell)
+    assert r["status"] == "CONVERGED" and r["iters"] == 1
+    assert np.max(np.abs(r["x"] - b / c)) <= 1e-15 * np.max(np.abs(b / c))
+
+
+@pytest.mark.parametrize("ell,neig", [(2, 2), (4, 3), (8, 5)])
+def test_bicgstab_l_finite_termination(ell, neig):
+    """BiCG with r̃ = r0 terminates after as many steps as A has distinct eigenvalues: with
+    ℓ ≥ that number the first cycle's BiCG part already reaches the solution."""
+    n = 120
+    eig = np.array([1.5, -2.0 + 0.5j, 3.0j, 0.7, 4.0 - 1j])[:neig]
+    d = eig[np.arange(n) % neig]
+    b = gen.rand_vector(n, 2)
+    r = oracle.bicgstab_l(diag_csr(d), b, tol=1e-10, ell=ell)
+    assert r["status"] == "CONVERGED" and r["iters"] == 1
+    assert np.max(np.abs(r["x"] - b / d)) <= 1e-12 * np.max(np.abs(b / d))
+
+
+@pytest.mark.parametrize("ell", [2, 4, 8])
+def test_bicgstab_l_dense_lu_and_gauge(ell):
+    """ℓ = 8 matches the dense LU solution within 1e-7; gauge invariance D·A·Dᴴ,
+    D·b (a missing conjugate in the Gram matrix or the BiCG products breaks it)."""
+    m = gen.make_matrix("C1")
+    b = gen.make_rhs(m)
+    D = sp.csr_matrix((m["values"], m["col_idx"], m["row_ptr"]), shape=(m["n"], m["n"])).toarray()
+    x_lu = np.linalg.solve(D, b)
+    r = oracle.bicgstab_l(m, b, tol=1e-10, ell=ell)
+    assert r["status"] == "CONVERGED"
+    assert np.linalg.norm(r["x"] - x_lu) / np.linalg.norm(x_lu) <= 1e-7
+    mg, Dg = twisted(gen.CONFIGS["C1"], gen.ETA)
+    rg = oracle.bicgstab_l(mg, Dg * b, tol=1e-10, ell=ell)
+    assert rg["iters"] == r["iters"]
+    # ℓ = 8: the Gram matrix of A^j r̂ (j ≤ 8) is ill-conditioned, rounding differences of the
+    # twisted run are amplified in the last cycle's tiny residual
+    htol = 1e-8 if ell < 8 else 1e-3
+    assert np.max(np.abs(rg["hist"] - r["hist"]) / r["hist"]) <= htol
+    assert np.linalg.norm(rg["x"] - Dg * r["x"]) / np.linalg.norm(r["x"]) <= 1e-8
+
+
+@pytest.mark.parametrize("ell", [2, 8])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "A3"])
+def test_bicgstab_l_closed_form_and_residual_consistency(cfg, ell):
+    """DST-I exact solution within 2κ·tol; the recurrence residual (hist) and the true residual
+    agree — a wrong x update in the MR part (e.g. γ_j r̂_j instead of γ_j r̂_{j−1}) breaks
+    the second, a wrong Gram system slows or stops convergence."""
+    spec = gen.CONFIGS[cfg]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    r = oracle.bicgstab_l(m, b, tol=1e-8, ell=ell)
+    assert r["status"] == "CONVERGED"
+    xe = cf.box_solve(spec, b, gen.ETA)
+    assert np.linalg.norm(r["x"] - xe) / np.linalg.norm(xe) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
+    assert abs(r["true_relres"] - r["hist"][-1]) <= 1e-3 * 1e-8 * max(1, ell)
+
+
+def test_bicgstab_l_cycle_count_scales():
+    """A cycle holds ℓ BiCG steps (2ℓ SpMVs): on C2 the cycle count is at most 1.5× BiCGStab's
+    iteration count / ℓ (+1) — a wrong MR polynomial (sign, conjugate, index) loses this."""
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    n_bicg = oracle.bicgstab(m, b, tol=1e-8)["iters"]
+    for ell in (2, 4, 8):
+        r = oracle.bicgstab_l(m, b, tol=1e-8, ell=ell)
+        assert r["status"] == "CONVERGED" and r["iters"] <= 1.5 * n_bicg / ell + 1
+
+
+def test_bicgstab_l_outcomes():
+    # BREAKDOWN_SIGMA: γ = ⟨r̃, A r0⟩ = 0 on a real skew matrix
+    m = dict(row_ptr=np.array([0, 1, 2]), col_idx=np.array([1, 0], np.int32),
+             values=np.array([1, -1], np.complex128), n=2)
+    assert oracle.bicgstab_l(m, np.array([1, 0], np.complex128), ell=2)["status"] == "BREAKDOWN_SIGMA"
+    mc = gen.make_matrix("C2")
+    bc = gen.make_rhs(mc)
+    r = oracle.bicgstab_l(mc, bc, tol=1e-14, maxit=3, ell=4)
+    assert r["status"] == "MAXIT" and r["iters"] == 3 and np.all(np.isfinite(r["hist"]))
+    assert r["true_relres"] == pytest.approx(r["hist"][-1], rel=1e-6)
+    assert oracle.bicgstab_l(mc, np.zeros(mc["n"]), ell=2)["status"] == "ZERO_RHS"
+    bn = bc.copy()
+    bn[0] = np.nan
+    assert oracle.bicgstab_l(mc, bn, ell=2)["status"] == "NONFINITE"
