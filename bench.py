@@ -49,6 +49,8 @@ def args_():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--spmv-reps", type=int, default=50)
     p.add_argument("--no-shapes", action="store_true", help="skip the PAPER.md T1-shape latency runs")
+    p.add_argument("--no-methods", action="store_true",
+                   help="skip the per-method C4 solves (Jacobi-BiCGStab, COCG, TFQMR, BiCGStab(2), BiCGStab(8))")
     return p.parse_args()
 
 
@@ -302,6 +304,34 @@ def main():
                            "gbs": step_bytes(ms_["n"], ms_["nnz"], rs_["iters"]) / (t_ms * 1e-3) / 1e9}
             As.close()
 
+    # the other solvers of the path on the same C4 system, after the timed
+    # region: per-iteration time and counted GB/s of their fused kernels (one warm-up + 2 timed solves)
+    methods = None
+    if world == 1 and not a.no_methods:
+        methods = {}
+        runs = [("bicgstab_jacobi", 0, M.bicgstab_iter_bytes(n, nnz)), ("cocg", 0, M.cocg_iter_bytes(n, nnz)),
+                ("tfqmr", 0, M.tfqmr_iter_bytes(n, nnz)),
+                ("bicgstab_l", 2, M.bicgstab_l_cycle_bytes(n, nnz, 2)),
+                ("bicgstab_l", 8, M.bicgstab_l_cycle_bytes(n, nnz, 8))]
+        for meth, ell, it_bytes in runs:
+            wsm = zk.alloc_workspace(A, meth, a.maxit, dev, ell=ell or 8)
+            rm = zk.solve(A, b, None, a.tol, a.maxit, meth, workspace=wsm, stream=stream, ell=ell or 8)
+            h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            h0.record(stream)
+            for _ in range(2):
+                rm = zk.solve(A, b, None, a.tol, a.maxit, meth, workspace=wsm, stream=stream, ell=ell or 8)
+            h1.record(stream)
+            torch.cuda.synchronize()
+            t_ms = h0.elapsed_time(h1) / 2
+            its = max(rm["iters"], 1)
+            gbs = it_bytes * its / (t_ms * 1e-3) / 1e9
+            key = f"bicgstab({ell})" if meth == "bicgstab_l" else meth
+            methods[key] = {"status": rm["status"], "iters": rm["iters"], "time_to_tol_ms": t_ms,
+                            "ms_per_iteration": t_ms / its, "bytes_per_iteration": it_bytes, "iter_gbs": gbs,
+                            "frac_of_peak": gbs / peak, "true_relres": rm["true_relres"],
+                            "spmv_launch_us": 1e3 * rm["kernel_ms"][0] / max(rm["kernel_launches"][0], 1)}
+            del wsm
+
     # end to end through the public API with HOST buffers (pinned): CSR upload + b H2D + solve + x D2H
     e2e = None
     if not a.no_e2e:
@@ -365,6 +395,7 @@ def main():
                          "vector_kernels_ms_per_iter": vec_ms / a.steps / iters},
             "spmv": spmv,
             "paper_shapes_bicgstab": shapes,
+            "methods_c4": methods,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -15,12 +15,12 @@
 // CG: K1 q = A p ; δ = ⟨p,q⟩ → α = γ/Re δ (NOT_HPD) ; K2 x += αp ; r −= αq ; γ' → hist, β ;
 //     K3 p = r + βp.
 // TFQMR (NEXT-2; Freund 1993 in the two-half-step form of oracle_tfqmr), iteration k:
-//   T1  y2 = y1 − αv ; w −= αu1 ; d1 = y1 + c1·d2 ; ‖w‖²    → θ,c,τ,η1 (half step m = 2k−1), test
-//   T2  u2 = A y2 ; d2 = y2 + c2·d1 ; w −= αu2 ; ‖w‖², ⟨r̃,w⟩
-//                                                          → half step m = 2k, hist[k], ρ', β
-//   T3  x += η1·d1 + η2·d2 ; y1 = w + βy2
-// (d is double-buffered so both x updates of an iteration land in T3: the SpMV epilogue of T2
-//  then carries 4 row operands instead of 5, and x is read and written once per iteration)
+//   T1  y2 = y1 − αv ; w −= αu1 ; ‖w‖²                     → θ,c,τ,η1 (half step m = 2k−1), c2, test
+//   T2  u2 = A y2 ; w −= αu2 ; ‖w‖², ⟨r̃,w⟩                 → half step m = 2k, hist[k], ρ', β
+//   T3  d1 = y1 + c1·d ; d = y2 + c2·d1 ; x += η1·d1 + η2·d ; y1 = w + βy2
+// The d recurrence and both x updates of an iteration are deferred to T3, which holds every
+// operand they need (y1 before it is overwritten, y2, d): d and x are read and written once per
+// iteration, and the SpMV epilogue of T2 carries 2 row operands.  2·Mat + 25 vector passes.
 //   T4  u1 = A y1 ; v = u1 + β(u2 + βv) ; σ = ⟨r̃,v⟩        → α = ρ/σ, c1 (writes the WHILE condition)
 #include <cstdio>
 #include <cstdlib>
@@ -34,29 +34,35 @@
 namespace zk {
 
 enum { ST_ZERO_RHS = 7 };  // internal outcome → ZK_ERR_ZERO_RHS at the ABI
+constexpr int kTickets = 64;  // workspace ticket slots (256 B)
+constexpr int kMaxEll = 8;    // BiCGStab(ℓ): ℓ ≤ 8
+constexpr int kBiCGStabL = 5; // internal method id of ZK_BICGSTAB_L(ℓ)
 
 struct SolveCtx {
     // vectors (device)
     double2* x;
     const double2* b;
     double2 *r, *rh, *p, *v, *s, *t, *q;
-    double2 *w, *y1, *y2, *u1, *u2, *d1, *d2, *rt;  // TFQMR (r/p/rh alias w/y1/rt for the shared init)
+    double2 *w, *y1, *y2, *u1, *u2, *d, *rt;  // TFQMR (r/p/rh alias w/y1/rt for the shared init)
+    double2 *rl[kMaxEll + 1], *ul[kMaxEll + 1];      // BiCGStab(ℓ) r̂_0..ℓ, û_0..ℓ (r/rh alias r̂_0/r̃)
     double* hist;
     double* partials;       // [kMaxRed][kMaxGrid]
-    unsigned int* tickets;  // [8]
+    unsigned int* tickets;  // [kTickets], one per reduction stage (self-resetting; cleared at solve start)
     CsrDev A;
     TmaPlan T;
     // scalars
     double2 rho, alpha, omega, beta;
     double nb, nrh, rnorm, gamma, alpha_cg, beta_cg;
-    double2 eta, eta1, coef;  // TFQMR η (η1: first half step's) and the next half step's d coefficient (θ²/α)·η
+    double2 eta, eta1, coef1, coef2;  // TFQMR η (η1: first half step's) and the d coefficients (θ²/α)·η
     double theta, tau;      // TFQMR θ, τ
+    double2 gam[kMaxEll + 1];  // BiCGStab(ℓ) minimal-residual coefficients γ_1..ℓ
+    int ell;
     double tol;
     int maxit;
     int j;       // iteration being executed (1-based)
     int done;    // loop finished (any outcome)
     int half;    // BiCGStab half-step exit pending (K4 applies x += αp); TFQMR exit inside an
-                 // iteration: 1 → T2 applies x += η1·d1 only, 2 → T3 applies its x update only
+                 // iteration: 1 → T2 applies x += η1·d1 only, 2 → T3 applies its d, x updates only
     int status;  // ZK_CONVERGED ... / ST_ZERO_RHS
     int iters;
     double true_relres;
@@ -230,7 +236,7 @@ __device__ void fin_sigma_tfqmr(SolveCtx* c, const double* tot) {  // {Re σ, Im
     if (!cfinite(sigma)) { c->status = ZK_NONFINITE; c->done = 1; return; }
     if (sigma.x == 0.0 && sigma.y == 0.0) { c->status = ZK_BREAKDOWN_SIGMA; c->done = 1; return; }
     c->alpha = cdiv(c->rho, sigma);
-    c->coef = cmul(cdiv(make_double2(c->theta * c->theta, 0.0), c->alpha), c->eta);  // for half step 1
+    c->coef1 = cmul(cdiv(make_double2(c->theta * c->theta, 0.0), c->alpha), c->eta);  // for half step 1
 }
 // one half step's scalars from ‖w‖²; returns false when the loop ends (x += η·d still pending)
 __device__ bool half_tfqmr(SolveCtx* c, double ww, int m, bool second) {
@@ -244,13 +250,13 @@ __device__ bool half_tfqmr(SolveCtx* c, double ww, int m, bool second) {
     if (bound <= c->tol) { c->status = ZK_CONVERGED; c->iters = c->j; c->done = 1; return false; }
     return true;
 }
-// Any exit inside an iteration leaves the x update of its half steps to the next kernel (the
-// oracle applies it before testing): c->half = 1 (T2 does x += η1·d1) or 2 (T3 does its update).
+// Any exit inside an iteration leaves the d, x updates of its half steps to the next kernel (the
+// oracle applies them before testing): c->half = 1 (T2 does x += η1·d1) or 2 (T3 does its updates).
 __device__ void fin_t1_tfqmr(SolveCtx* c, const double* tot) {  // {‖w‖²}
     const bool go = half_tfqmr(c, tot[0], 2 * c->j - 1, false);
     c->eta1 = c->eta;
     if (!go) { c->half = 1; return; }
-    c->coef = cmul(cdiv(make_double2(c->theta * c->theta, 0.0), c->alpha), c->eta);  // for half step 2
+    c->coef2 = cmul(cdiv(make_double2(c->theta * c->theta, 0.0), c->alpha), c->eta);  // for half step 2
 }
 __device__ void fin_t2_steps(SolveCtx* c, const double* tot) {
     const int j = c->j;
@@ -268,19 +274,80 @@ __device__ void fin_t2_tfqmr(SolveCtx* c, const double* tot) {  // {‖w‖², R
     fin_t2_steps(c, tot);
     if (c->done) c->half = 2;
 }
+// NEXT-3 BiCGStab(ℓ) — the scalar steps of oracle_bicgstab_l in its order; c->rho is ρ0
+__device__ bool bl_rho(SolveCtx* c, double2 rho1, double rn) {  // ρ1 = ⟨r̃, r̂_j⟩, rn = ‖r̂_j‖
+    if (!cfinite(rho1)) { c->status = ZK_NONFINITE; c->done = 1; return false; }
+    if (cabs_(rho1) <= 1e-30 * c->nrh * rn) { c->status = ZK_BREAKDOWN_RHO; c->done = 1; return false; }
+    c->beta = cdiv(cmul(c->alpha, rho1), c->rho);  // β = α ρ1 / ρ0
+    c->rho = rho1;
+    return true;
+}
+__device__ void bl_cycle_start(SolveCtx* c) {  // iters = k (an exit inside the cycle counts it); ρ0 = −ω ρ0
+    c->iters = c->j;
+    c->rho = cmul(make_double2(-c->omega.x, -c->omega.y), c->rho);
+}
+__device__ void fin_init_bl(SolveCtx* c, const double* tot) {  // {‖b‖², ‖r0‖², ·, ·}
+    c->iters = 0;
+    c->nb = sqrt(tot[0]);
+    if (c->nb == 0.0) { c->status = ST_ZERO_RHS; c->done = 1; return; }
+    c->rnorm = sqrt(tot[1]);
+    c->hist[0] = c->rnorm / c->nb;
+    if (!isfinite(c->hist[0])) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (c->hist[0] <= c->tol) { c->status = ZK_CONVERGED; c->done = 1; return; }
+    c->nrh = c->rnorm;  // r̃ = r0
+    c->rho = make_double2(1.0, 0.0);
+    c->alpha = make_double2(0.0, 0.0);
+    c->omega = make_double2(1.0, 0.0);
+    c->j = 1;
+    bl_cycle_start(c);
+    bl_rho(c, make_double2(tot[1], 0.0), c->rnorm);  // ρ1 = ⟨r̃, r0⟩ = ‖r0‖²
+}
+__device__ void fin_s1_bl(SolveCtx* c, const double* tot) {  // {Re γ, Im γ, ‖û_{j+1}‖²}
+    const double2 g = make_double2(tot[0], tot[1]);
+    if (!cfinite(g)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (cabs_(g) <= 1e-30 * c->nrh * sqrt(tot[2])) { c->status = ZK_BREAKDOWN_SIGMA; c->done = 1; return; }
+    c->alpha = cdiv(c->rho, g);
+}
+__device__ void fin_b2_bl(SolveCtx* c, const double* tot) {  // {‖r̂_0‖²} after x += α û_0
+    const double rn = sqrt(tot[0]);
+    if (!isfinite(rn)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (rn / c->nb <= c->tol) {
+        c->hist[c->j] = rn / c->nb;
+        c->status = ZK_CONVERGED;
+        c->done = 1;
+    }
+}
+__device__ void fin_s2_bl(SolveCtx* c, const double* tot) {  // {Re ρ1, Im ρ1, ‖r̂_{j+1}‖²}
+    bl_rho(c, make_double2(tot[0], tot[1]), sqrt(tot[2]));
+}
+__device__ void fin_u_bl(SolveCtx* c, const double* tot) {  // {‖r̂_0‖², Re ρ1, Im ρ1}
+    const int j = c->j;
+    c->rnorm = sqrt(tot[0]);
+    c->hist[j] = c->rnorm / c->nb;
+    c->iters = j;
+    if (!isfinite(c->hist[j]) || !cfinite(c->omega)) { c->status = ZK_NONFINITE; c->done = 1; return; }
+    if (c->hist[j] <= c->tol) { c->status = ZK_CONVERGED; c->done = 1; return; }
+    if (cabs_(c->omega) <= 1e-30) { c->status = ZK_BREAKDOWN_OMEGA; c->done = 1; return; }
+    if (j >= c->maxit) { c->status = ZK_MAXIT; c->done = 1; return; }
+    c->j = j + 1;
+    bl_cycle_start(c);
+    bl_rho(c, make_double2(tot[1], tot[2]), c->rnorm);
+}
 __device__ void fin_true(SolveCtx* c, const double* tot) {  // {‖b − Ax‖²}
     c->true_relres = c->nb > 0.0 ? sqrt(tot[0]) / c->nb : NAN;
 }
 
 enum Stage { S_INIT_BICG, S_K1_BICG, S_K2_BICG, S_K3_BICG, S_K4_BICG, S_INIT_CG, S_K1_CG, S_K2_CG, S_TRUE,
              S_INIT_COCG, S_K1_COCG, S_K2_COCG, S_INIT_TFQMR, S_K0_TFQMR, S_T1_TFQMR, S_T2_TFQMR,
-             S_T4_TFQMR };
+             S_T4_TFQMR, S_INIT_BL, S_S1_BL, S_B2_BL, S_S2_BL, S_G_BL, S_U_BL, S_COUNT };
+static_assert(S_COUNT <= kTickets, "one ticket per reduction stage");
 
 // timer class of a stage: 0 SpMV in the loop, 1 fused vector kernels, 2 init, 3 true residual
 __host__ __device__ constexpr int timer_of(int S) {
     return (S == S_K1_BICG || S == S_K3_BICG || S == S_K1_CG || S == S_K1_COCG || S == S_T2_TFQMR ||
-            S == S_T4_TFQMR) ? 0
-           : (S == S_K2_BICG || S == S_K4_BICG || S == S_K2_CG || S == S_K2_COCG || S == S_T1_TFQMR) ? 1
+            S == S_T4_TFQMR || S == S_S1_BL || S == S_S2_BL) ? 0
+           : (S == S_K2_BICG || S == S_K4_BICG || S == S_K2_CG || S == S_K2_COCG || S == S_T1_TFQMR ||
+              S == S_B2_BL || S == S_G_BL || S == S_U_BL) ? 1
            : (S == S_TRUE) ? 3 : 2;
 }
 template <int S>
@@ -306,6 +373,11 @@ __device__ __forceinline__ void finish_stage(SolveCtx* c, const double* tot) {
     if (S == S_K0_TFQMR || S == S_T4_TFQMR) fin_sigma_tfqmr(c, tot);
     if (S == S_T1_TFQMR) fin_t1_tfqmr(c, tot);
     if (S == S_T2_TFQMR) fin_t2_tfqmr(c, tot);
+    if (S == S_INIT_BL) fin_init_bl(c, tot);
+    if (S == S_S1_BL) fin_s1_bl(c, tot);
+    if (S == S_B2_BL) fin_b2_bl(c, tot);
+    if (S == S_S2_BL) fin_s2_bl(c, tot);
+    if (S == S_U_BL) fin_u_bl(c, tot);
 }
 
 // grid reduction of K values, then (single GPU) the stage's scalar step in the last block, or
@@ -331,7 +403,7 @@ template <int S>
 __global__ void fin_kernel(SolveCtx* c) {
     // the reducing kernel skipped its work (loop already finished): nothing to finish — the
     // chunked loop launches whole iterations past convergence (regression: tools/debug/dist1.py)
-    if (S != S_TRUE && S != S_INIT_BICG && S != S_INIT_CG && S != S_INIT_COCG && S != S_INIT_TFQMR && c->done) return;
+    if (S != S_TRUE && S != S_INIT_BICG && S != S_INIT_CG && S != S_INIT_COCG && S != S_INIT_TFQMR && S != S_INIT_BL && c->done) return;
     double tot[kMaxRed];
     for (int k = 0; k < kMaxRed; k++) tot[k] = c->red[k];
     finish_stage<S>(c, tot);
@@ -350,7 +422,7 @@ struct EpiInit {  // r = b − A x0 ; x = x0 ; r̂ = p = r ; {‖b‖², ‖r‖
     const double2* __restrict__ b;
     double2 *r, *p, *rh, *x, *d;
     __device__ EpiInit(SolveCtx* c_, const double2* x0_, bool bicg)
-        : c(c_), x0(x0_), b(c_->b), r(c_->r), p(c_->p), rh(bicg ? c_->rh : nullptr), x(c_->x), d(c_->d2) {}
+        : c(c_), x0(x0_), b(c_->b), r(c_->r), p(c_->p), rh(bicg ? c_->rh : nullptr), x(c_->x), d(c_->d) {}
     __device__ Pre pre(int64_t i) const { return {ld_vec(b + i), x != x0 ? ld_gather_coh(x0 + i) : make_double2(0, 0)}; }
     __device__ void row(int64_t i, double2 y, const Pre& q, double (&acc)[4]) {
         const double2 rr = csub(q.b, y);
@@ -437,16 +509,16 @@ struct OpInitZero {  // x0 = 0: x = 0 ; r = r̂ = p = b ; {‖b‖², ‖r‖²,
     SolveCtx* c;
     const double2* __restrict__ b;
     double2 *__restrict__ x, *__restrict__ r, *__restrict__ p, *__restrict__ rh, *__restrict__ d;
-    int kind;  // 0 BiCGStab, 1 CG, 3 COCG, 4 TFQMR
+    int kind;  // 0 BiCGStab, 1 CG, 3 COCG, 4 TFQMR, 5 BiCGStab(ℓ)
     __device__ OpInitZero(SolveCtx* c_, int kind_)
-        : c(c_), b(c_->b), x(c_->x), r(c_->r), p(c_->p), rh(c_->rh), d(c_->d2), kind(kind_) {}
+        : c(c_), b(c_->b), x(c_->x), r(c_->r), p(c_->p), rh(c_->rh), d(c_->d), kind(kind_) {}
     __device__ In load(int64_t i) const { return {ld_vec(b + i)}; }
     __device__ void apply(int64_t i, const In& v, double (&acc)[4]) const {
         x[i] = make_double2(0.0, 0.0);
         r[i] = v.b;
         p[i] = v.b;
-        if (kind == 0 || kind == 4) rh[i] = v.b;
-    if (kind == 4) d[i] = make_double2(0.0, 0.0);
+        if (kind == 0 || kind >= 4) rh[i] = v.b;
+        if (kind >= 4) d[i] = make_double2(0.0, 0.0);
         const double bb = cabs2(v.b);
         acc[0] += bb;
         acc[1] += bb;
@@ -457,7 +529,8 @@ struct OpInitZero {  // x0 = 0: x = 0 ; r = r̂ = p = b ; {‖b‖², ‖r‖²,
         if (kind == 0) reduce_finish<S_INIT_BICG, 4>(c, acc);
         else if (kind == 1) reduce_finish<S_INIT_CG, 4>(c, acc);
         else if (kind == 3) reduce_finish<S_INIT_COCG, 4>(c, acc);
-        else reduce_finish<S_INIT_TFQMR, 4>(c, acc);
+        else if (kind == 4) reduce_finish<S_INIT_TFQMR, 4>(c, acc);
+        else reduce_finish<S_INIT_BL, 4>(c, acc);
     }
 };
 
@@ -639,20 +712,25 @@ struct OpK3Cocg {  // p = r + β p (complex β)
 };
 
 // TFQMR epilogues and vector ops (the loops of oracle_tfqmr, fused per kernel T1..T4)
-struct OpT1Tfqmr {  // y2 = y1 − α v ; w −= α u1 ; d1 = y1 + c1·d2 ; {‖w‖²}
+#ifndef ZK_T1_U
+#define ZK_T1_U 1
+#endif
+// T2/T4 (SpMV + the TFQMR epilogues): 80 registers (3 CTAs/SM) measured 16 % faster on C4 than
+// the 64 of the plain SpMV kernels (profiles/r01_tfqmr_variants.md)
+#ifndef ZK_TF_MINB
+#define ZK_TF_MINB (MODE == 0 ? 3 : spmv_min_blocks(MODE))
+#endif
+struct OpT1Tfqmr {  // y2 = y1 − α v ; w −= α u1 ; {‖w‖²}
     static constexpr int K = 1;
-    static constexpr int U = 1;  // 5 input streams (as OpK4Bicg)
-    struct In { double2 y1, v, w, u1, d; };
+    static constexpr int U = ZK_T1_U;
+    struct In { double2 y1, v, w, u1; };
     SolveCtx* c;
-    const double2 *__restrict__ y1, *__restrict__ v, *__restrict__ u1, *__restrict__ d2;
-    double2 *__restrict__ y2, *__restrict__ w, *__restrict__ d;
-    double2 alpha, coef;
+    const double2 *__restrict__ y1, *__restrict__ v, *__restrict__ u1;
+    double2 *__restrict__ y2, *__restrict__ w;
+    double2 alpha;
     __device__ explicit OpT1Tfqmr(SolveCtx* c_)
-        : c(c_), y1(c_->y1), v(c_->v), u1(c_->u1), d2(c_->d2), y2(c_->y2), w(c_->w), d(c_->d1), alpha(c_->alpha),
-          coef(c_->coef) {}
-    __device__ In load(int64_t i) const {
-        return {ld_vec(y1 + i), ld_vec(v + i), ld_vec(w + i), ld_vec(u1 + i), ld_vec(d2 + i)};
-    }
+        : c(c_), y1(c_->y1), v(c_->v), u1(c_->u1), y2(c_->y2), w(c_->w), alpha(c_->alpha) {}
+    __device__ In load(int64_t i) const { return {ld_vec(y1 + i), ld_vec(v + i), ld_vec(w + i), ld_vec(u1 + i)}; }
     __device__ void apply(int64_t i, const In& in, double (&acc)[1]) const {
         double2 o = in.y1;
         o.x = fma(-alpha.x, in.v.x, fma(alpha.y, in.v.y, o.x));
@@ -662,33 +740,22 @@ struct OpT1Tfqmr {  // y2 = y1 − α v ; w −= α u1 ; d1 = y1 + c1·d2 ; {‖
         wn.x = fma(-alpha.x, in.u1.x, fma(alpha.y, in.u1.y, wn.x));
         wn.y = fma(-alpha.x, in.u1.y, fma(-alpha.y, in.u1.x, wn.y));
         w[i] = wn;
-        double2 dn = in.y1;
-        cfma(dn, coef, in.d);
-        d[i] = dn;
         acc[0] += cabs2(wn);
     }
     __device__ void finish(double (&acc)[1]) const { reduce_finish<S_T1_TFQMR, 1>(c, acc); }
 };
 
-struct EpiT2Tfqmr {  // u2 = A y2 ; d2 = y2 + c2·d1 ; w −= α u2 ; {‖w‖², ⟨r̃, w⟩}
+struct EpiT2Tfqmr {  // u2 = A y2 ; w −= α u2 ; {‖w‖², ⟨r̃, w⟩}
     static constexpr int K = 3;
-    static constexpr bool kAhead = false;  // 4 row operands: one copy in registers (no spill at 64)
-    struct Pre { double2 d, w, rt, y2; };
+    struct Pre { double2 w, rt; };
     SolveCtx* c;
-    double2 *__restrict__ u2, *__restrict__ d2, *__restrict__ w;
-    const double2 *__restrict__ d1, *__restrict__ rt, *__restrict__ y2;
-    double2 coef, alpha;
-    __device__ explicit EpiT2Tfqmr(SolveCtx* c_)
-        : c(c_), u2(c_->u2), d2(c_->d2), w(c_->w), d1(c_->d1), rt(c_->rt), y2(c_->y2), coef(c_->coef),
-          alpha(c_->alpha) {}
-    __device__ Pre pre(int64_t i) const {
-        return {ld_vec(d1 + i), ld_vec(w + i), ld_vec(rt + i), ld_gather_coh(y2 + i)};
-    }
+    double2 *__restrict__ u2, *__restrict__ w;
+    const double2* __restrict__ rt;
+    double2 alpha;
+    __device__ explicit EpiT2Tfqmr(SolveCtx* c_) : c(c_), u2(c_->u2), w(c_->w), rt(c_->rt), alpha(c_->alpha) {}
+    __device__ Pre pre(int64_t i) const { return {ld_vec(w + i), ld_vec(rt + i)}; }
     __device__ void row(int64_t i, double2 y, const Pre& q, double (&acc)[3]) {
         u2[i] = y;
-        double2 dn = q.y2;
-        cfma(dn, coef, q.d);
-        d2[i] = dn;
         double2 wn = q.w;
         wn.x = fma(-alpha.x, y.x, fma(alpha.y, y.y, wn.x));
         wn.y = fma(-alpha.x, y.y, fma(-alpha.y, y.x, wn.y));
@@ -700,34 +767,38 @@ struct EpiT2Tfqmr {  // u2 = A y2 ; d2 = y2 + c2·d1 ; w −= α u2 ; {‖w‖²
     __device__ void finish(double (&acc)[3]) { reduce_finish<S_T2_TFQMR, 3>(c, acc); }
 };
 
-struct OpT3Tfqmr {  // x += η1·d1 + η2·d2 ; y1 = w + β y2   (exit: the x update only)
+// d1 = y1 + c1·d ; d = y2 + c2·d1 ; x += η1·d1 + η2·d ; y1 = w + β y2   (exit: no y1)
+struct OpT3Tfqmr {
     static constexpr int K = 0;
     static constexpr int U = 1;  // 5 input streams
-    struct In { double2 x, d1, d2, w, y2; };
-    double2 *__restrict__ x, *__restrict__ y1;
-    const double2 *__restrict__ d1, *__restrict__ d2, *__restrict__ w, *__restrict__ y2;
-    double2 eta1, eta2, beta;
-    bool only_x;
-    __device__ OpT3Tfqmr(SolveCtx* c, bool only_x_)
-        : x(c->x), y1(c->y1), d1(c->d1), d2(c->d2), w(c->w), y2(c->y2), eta1(c->eta1), eta2(c->eta), beta(c->beta),
-          only_x(only_x_) {}
+    struct In { double2 x, y1, d, w, y2; };
+    double2 *__restrict__ x, *__restrict__ y1, *__restrict__ d;
+    const double2 *__restrict__ w, *__restrict__ y2;
+    double2 coef1, coef2, eta1, eta2, beta;
+    bool exit_only;
+    __device__ OpT3Tfqmr(SolveCtx* c, bool exit_only_)
+        : x(c->x), y1(c->y1), d(c->d), w(c->w), y2(c->y2), coef1(c->coef1), coef2(c->coef2), eta1(c->eta1),
+          eta2(c->eta), beta(c->beta), exit_only(exit_only_) {}
     __device__ In load(int64_t i) const {
         In v;
         v.x = ld_vec(x + i);
-        v.d1 = ld_vec(d1 + i);
-        v.d2 = ld_vec(d2 + i);
-        if (!only_x) {
-            v.w = ld_vec(w + i);
-            v.y2 = ld_vec(y2 + i);
-        }
+        v.y1 = ld_vec(y1 + i);
+        v.d = ld_vec(d + i);
+        v.y2 = ld_vec(y2 + i);
+        if (!exit_only) v.w = ld_vec(w + i);
         return v;
     }
     __device__ void apply(int64_t i, const In& in, double (&)[1]) const {
-        double2 xn = in.x;  // oracle order: (x + η1·d1) + η2·d2
-        cfma(xn, eta1, in.d1);
-        cfma(xn, eta2, in.d2);
+        double2 d1 = in.y1;  // oracle order: d1, then d2 from d1, then (x + η1·d1) + η2·d2
+        cfma(d1, coef1, in.d);
+        double2 d2 = in.y2;
+        cfma(d2, coef2, d1);
+        double2 xn = in.x;
+        cfma(xn, eta1, d1);
+        cfma(xn, eta2, d2);
         x[i] = xn;
-        if (only_x) return;
+        d[i] = d2;
+        if (exit_only) return;
         double2 o = in.w;
         cfma(o, beta, in.y2);
         y1[i] = o;
@@ -910,18 +981,21 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t1_tfqmr(SolveCtx* c) {
     vec_body(c->A.n_rows, op);
 }
 template <int W, int MODE>
-__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) t2_tfqmr(SolveCtx* c) {
+__global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t2_tfqmr(SolveCtx* c) {
     pdl_enter();
     if (c->done) {
         if (c->half != 1) return;
-        // the first half step ended the loop: only its x += η1·d1 remains
+        // the first half step ended the loop: only its x += η1·d1, d1 = y1 + c1·d, remains
         double2* __restrict__ x = c->x;
-        const double2* __restrict__ d = c->d1;
-        const double2 eta = c->eta1;
+        const double2* __restrict__ d = c->d;
+        const double2* __restrict__ y1 = c->y1;
+        const double2 eta = c->eta1, coef = c->coef1;
         const int64_t n = c->A.n_rows;
         for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+            double2 d1 = y1[i];
+            cfma(d1, coef, d[i]);
             double2 xn = x[i];
-            cfma(xn, eta, d[i]);
+            cfma(xn, eta, d1);
             x[i] = xn;
         }
         return;
@@ -941,7 +1015,7 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t3_tfqmr(SolveCtx* c) {
     vec_body(c->A.n_rows, op);
 }
 template <int W, int MODE>
-__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) t4_tfqmr(SolveCtx* c) {
+__global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t4_tfqmr(SolveCtx* c) {
     pdl_enter();
     if (c->done) {
         if (c->half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;  // T2/T3 applied the last x += η·d
@@ -955,6 +1029,352 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) t4_tfqmr(SolveC
     }
     set_cond(c);
 }
+// ------------------------------------------------------------------ BiCGStab(ℓ) kernels (NEXT-3)
+// One outer cycle (oracle_bicgstab_l): for j = 0..ℓ−1 the BiCG step runs as
+//   B1(j)  û_i = r̂_i − β û_i (i ≤ j)
+//   S1(j)  û_{j+1} = A û_j ; γ = ⟨r̃, û_{j+1}⟩, ‖û_{j+1}‖²                → α = ρ0/γ
+//   B2(j)  r̂_i −= α û_{i+1} (i ≤ j) ; x += α û_0 ; ‖r̂_0‖²                → exit test
+//   S2(j)  r̂_{j+1} = A r̂_j ; ρ1 = ⟨r̃, r̂_{j+1}⟩, ‖r̂_{j+1}‖² (j < ℓ−1)    → β = α ρ1/ρ0
+// then the minimal-residual part:
+//   G      Gram matrix ⟨r̂_a, r̂_b⟩ (a ≤ b ≤ ℓ) in ONE pass over the ℓ+1 vectors → Cholesky, γ, ω
+//   U      x += Σ γ_j r̂_{j−1} ; r̂_0 −= Σ γ_j r̂_j ; û_0 −= Σ γ_j û_j ; ‖r̂_0‖², ⟨r̃, r̂_0⟩
+//                                                             → hist, tests, next cycle's β
+// (writes the WHILE condition).  The vector sets travel as a kernel parameter (constant bank).
+struct VecSet {
+    double2* r[kMaxEll + 1];
+    double2* u[kMaxEll + 1];
+};
+
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) bl_b1(SolveCtx* c, VecSet P, int j) {
+    pdl_enter();
+    if (c->done) return;
+    const double2 beta = c->beta;
+    const int64_t n = c->A.n_rows;
+    constexpr int UE = 4;
+    for (int64_t base = (int64_t)blockIdx.x * kBlock * UE + threadIdx.x; base < n;
+         base += (int64_t)gridDim.x * kBlock * UE) {
+        for (int q = 0; q <= j; q++) {  // û_q = r̂_q − β û_q
+            const double2* __restrict__ r = P.r[q];
+            double2* __restrict__ u = P.u[q];
+            double2 rv[UE], uv[UE];
+#pragma unroll
+            for (int e = 0; e < UE; e++) {
+                const int64_t i = base + e * kBlock;
+                if (i < n) {
+                    rv[e] = ld_vec(r + i);
+                    uv[e] = ld_vec(u + i);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < UE; e++) {
+                const int64_t i = base + e * kBlock;
+                if (i < n) {
+                    double2 o = rv[e];
+                    o.x = fma(-beta.x, uv[e].x, fma(beta.y, uv[e].y, o.x));
+                    o.y = fma(-beta.x, uv[e].y, fma(-beta.y, uv[e].x, o.y));
+                    u[i] = o;
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) bl_b2(SolveCtx* c, VecSet P, int j) {
+    pdl_enter();
+    if (c->done) return;
+    stamp_start<S_B2_BL>(c);
+    const double2 alpha = c->alpha;
+    double2* __restrict__ x = c->x;
+    const int64_t n = c->A.n_rows;
+    constexpr int UE = 2;
+    double acc[1] = {0.0};
+    for (int64_t base = (int64_t)blockIdx.x * kBlock * UE + threadIdx.x; base < n;
+         base += (int64_t)gridDim.x * kBlock * UE) {
+        {   // q = 0: r̂_0 −= α û_1 ; x += α û_0 ; ‖r̂_0‖²
+            double2 rv[UE], u1[UE], xv[UE], u0[UE];
+#pragma unroll
+            for (int e = 0; e < UE; e++) {
+                const int64_t i = base + e * kBlock;
+                if (i < n) {
+                    rv[e] = ld_vec(P.r[0] + i);
+                    u1[e] = ld_vec(P.u[1] + i);
+                    xv[e] = ld_vec(x + i);
+                    u0[e] = ld_vec(P.u[0] + i);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < UE; e++) {
+                const int64_t i = base + e * kBlock;
+                if (i < n) {
+                    double2 o = rv[e];
+                    o.x = fma(-alpha.x, u1[e].x, fma(alpha.y, u1[e].y, o.x));
+                    o.y = fma(-alpha.x, u1[e].y, fma(-alpha.y, u1[e].x, o.y));
+                    P.r[0][i] = o;
+                    acc[0] += cabs2(o);
+                    double2 xn = xv[e];
+                    cfma(xn, alpha, u0[e]);
+                    x[i] = xn;
+                }
+            }
+        }
+        for (int q = 1; q <= j; q++) {  // r̂_q −= α û_{q+1}
+            double2* __restrict__ r = P.r[q];
+            const double2* __restrict__ u = P.u[q + 1];
+            double2 rv[UE], uv[UE];
+#pragma unroll
+            for (int e = 0; e < UE; e++) {
+                const int64_t i = base + e * kBlock;
+                if (i < n) {
+                    rv[e] = ld_vec(r + i);
+                    uv[e] = ld_vec(u + i);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < UE; e++) {
+                const int64_t i = base + e * kBlock;
+                if (i < n) {
+                    double2 o = rv[e];
+                    o.x = fma(-alpha.x, uv[e].x, fma(alpha.y, uv[e].y, o.x));
+                    o.y = fma(-alpha.x, uv[e].y, fma(-alpha.y, uv[e].x, o.y));
+                    r[i] = o;
+                }
+            }
+        }
+    }
+    reduce_finish<S_B2_BL, 1>(c, acc);
+}
+
+template <int S, bool RED>
+struct EpiBl {  // out = A v ; {⟨r̃, out⟩, ‖out‖²} when RED
+    static constexpr int K = RED ? 3 : 0;
+    static constexpr int KA = K > 0 ? K : 1;
+    using Pre = double2;
+    SolveCtx* c;
+    double2* __restrict__ out;
+    const double2* __restrict__ rt;
+    __device__ EpiBl(SolveCtx* c_, double2* out_) : c(c_), out(out_), rt(c_->rh) {}
+    __device__ Pre pre(int64_t i) const {
+        if constexpr (RED) return ld_vec(rt + i);
+        else return make_double2(0.0, 0.0);
+    }
+    __device__ void row(int64_t i, double2 y, const Pre& q, double (&acc)[KA]) {
+        out[i] = y;
+        if constexpr (RED) {
+            acc[0] = fma(q.x, y.x, fma(q.y, y.y, acc[0]));
+            acc[1] = fma(q.x, y.y, fma(-q.y, y.x, acc[1]));
+            acc[2] += cabs2(y);
+        }
+    }
+    __device__ void finish(double (&acc)[KA]) {
+        if constexpr (RED) reduce_finish<S, 3>(c, acc);
+    }
+};
+
+template <int W, int MODE>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) bl_s1(SolveCtx* c, VecSet P, int j) {
+    pdl_enter();
+    if (c->done) return;
+    stamp_start<S_S1_BL>(c);
+    const CsrDev A = c->A;
+    const TmaPlan T = c->T;
+    EpiBl<S_S1_BL, true> e(c, P.u[j + 1]);
+    spmv_any<W, MODE>(A, T, P.u[j], e);
+}
+template <int W, int MODE, bool RED>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) bl_s2(SolveCtx* c, VecSet P, int j) {
+    pdl_enter();
+    if (c->done) return;
+    if (RED) stamp_start<S_S2_BL>(c);
+    const CsrDev A = c->A;
+    const TmaPlan T = c->T;
+    EpiBl<S_S2_BL, RED> e(c, P.r[j + 1]);
+    spmv_any<W, MODE>(A, T, P.r[j], e);
+}
+
+// Gram matrix of r̂_0..ℓ, packed: for a = 0..ℓ: ‖r̂_a‖², then (Re, Im)⟨r̂_a, r̂_b⟩ for b = a+1..ℓ.
+template <int L>
+struct GramPack {
+    static constexpr int NV = L + 1;
+    static constexpr int ND = NV + NV * (NV - 1);  // doubles
+    __host__ __device__ static constexpr int diag(int a) { return a + a * (2 * NV - a - 1); }  // entry (a, a)
+    __host__ __device__ static constexpr int off(int a, int b) { return diag(a) + 1 + 2 * (b - a - 1); }  // a < b
+};
+
+// the minimal-residual system from the packed Gram totals: M γ = v with M_ik = ⟨r̂_{i+1}, r̂_{k+1}⟩,
+// v_i = ⟨r̂_{i+1}, r̂_0⟩, by Cholesky M = L·Lᴴ (the oracle's algorithm, written independently)
+template <int L>
+__device__ void fin_gram_bl(SolveCtx* c, const double* g) {
+    using GP = GramPack<L>;
+    auto G = [&](int a, int b) -> double2 {  // ⟨r̂_a, r̂_b⟩
+        if (a == b) return make_double2(g[GP::diag(a)], 0.0);
+        if (a < b) return make_double2(g[GP::off(a, b)], g[GP::off(a, b) + 1]);
+        return make_double2(g[GP::off(b, a)], -g[GP::off(b, a) + 1]);
+    };
+    double2 Lm[L][L];
+    for (int jj = 0; jj < L; jj++) {
+        double d = G(jj + 1, jj + 1).x;
+        for (int q = 0; q < jj; q++) d -= Lm[jj][q].x * Lm[jj][q].x + Lm[jj][q].y * Lm[jj][q].y;
+        if (!(d > 0.0) || !isfinite(d)) {
+            c->status = ZK_BREAKDOWN_OMEGA;  // singular ℓ×ℓ minimal-residual system
+            c->done = 1;
+            return;
+        }
+        const double l = sqrt(d);
+        Lm[jj][jj] = make_double2(l, 0.0);
+        for (int i = jj + 1; i < L; i++) {
+            double2 s = G(i + 1, jj + 1);
+            for (int q = 0; q < jj; q++) s = csub(s, cmul(Lm[i][q], make_double2(Lm[jj][q].x, -Lm[jj][q].y)));
+            Lm[i][jj] = make_double2(s.x / l, s.y / l);
+        }
+    }
+    double2 y[L];
+    for (int i = 0; i < L; i++) {  // L y = v
+        double2 s = G(i + 1, 0);
+        for (int q = 0; q < i; q++) s = csub(s, cmul(Lm[i][q], y[q]));
+        y[i] = make_double2(s.x / Lm[i][i].x, s.y / Lm[i][i].x);
+    }
+    for (int i = L - 1; i >= 0; i--) {  // Lᴴ γ = y
+        double2 s = y[i];
+        for (int q = i + 1; q < L; q++) s = csub(s, cmul(make_double2(Lm[q][i].x, -Lm[q][i].y), c->gam[q + 1]));
+        c->gam[i + 1] = make_double2(s.x / Lm[i][i].x, s.y / Lm[i][i].x);
+    }
+    c->omega = c->gam[L];
+}
+
+template <int L>
+__global__ void __launch_bounds__(kBlock, 1) bl_gram(SolveCtx* c, VecSet P) {
+    using GP = GramPack<L>;
+    constexpr int NV = GP::NV, ND = GP::ND;
+    __shared__ double sm[kWarps][ND];
+    __shared__ double tot[ND];
+    __shared__ bool last;
+    pdl_enter();
+    if (c->done) return;
+    stamp_start<S_G_BL>(c);
+    double acc[ND];
+#pragma unroll
+    for (int k = 0; k < ND; k++) acc[k] = 0.0;
+    const int64_t n = c->A.n_rows;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        double2 v[NV];
+#pragma unroll
+        for (int a = 0; a < NV; a++) v[a] = ld_vec(P.r[a] + i);
+#pragma unroll
+        for (int a = 0; a < NV; a++) {
+            acc[GP::diag(a)] += cabs2(v[a]);
+#pragma unroll
+            for (int b = a + 1; b < NV; b++) {
+                double& re = acc[GP::off(a, b)];
+                double& im = acc[GP::off(a, b) + 1];
+                re = fma(v[a].x, v[b].x, fma(v[a].y, v[b].y, re));
+                im = fma(v[a].x, v[b].y, fma(-v[a].y, v[b].x, im));
+            }
+        }
+    }
+    warp_sum<ND>(acc);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < ND; k++) sm[warp][k] = acc[k];
+    }
+    __syncthreads();
+    const int G = gridDim.x;
+    double* part = c->partials;  // [ND][G]
+    for (int k = threadIdx.x; k < ND; k += kBlock) {
+        double s = 0.0;
+        for (int w = 0; w < kWarps; w++) s += sm[w][k];
+        part[k * G + blockIdx.x] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(c->tickets + S_G_BL, 1u) == (unsigned)G - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int k = threadIdx.x; k < ND; k += kBlock) {  // fixed order over blocks
+        double s = 0.0;
+        for (int b = 0; b < G; b++) s += ld_cg(part + k * G + b);
+        tot[k] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        c->tickets[S_G_BL] = 0u;
+        const unsigned long long st = atomicExch(&c->t0[timer_of(S_G_BL)], ~0ull);
+        c->tsum[timer_of(S_G_BL)] += gtimer() - st;
+        c->tcnt[timer_of(S_G_BL)] += 1;
+        fin_gram_bl<L>(c, tot);
+    }
+}
+
+template <int L>
+__global__ void __launch_bounds__(kBlock, 2) bl_u(SolveCtx* c, VecSet P) {
+    pdl_enter();
+    if (!c->done) {
+        stamp_start<S_U_BL>(c);
+        double2 g[L + 1];
+#pragma unroll
+        for (int j = 1; j <= L; j++) g[j] = c->gam[j];
+        double2* __restrict__ x = c->x;
+        const double2* __restrict__ rt = c->rh;
+        const int64_t n = c->A.n_rows;
+        double acc[3] = {0.0, 0.0, 0.0};
+        for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+            double2 rv[L + 1], uv[L + 1];
+#pragma unroll
+            for (int a = 0; a <= L; a++) {
+                rv[a] = ld_vec(P.r[a] + i);
+                uv[a] = ld_vec(P.u[a] + i);
+            }
+            double2 xv = ld_vec(x + i);
+            const double2 tv = ld_vec(rt + i);
+            double2 r0 = rv[0], u0 = uv[0];
+#pragma unroll
+            for (int j = 1; j <= L; j++) {  // oracle order: j ascending
+                cfma(xv, g[j], rv[j - 1]);
+                r0.x = fma(-g[j].x, rv[j].x, fma(g[j].y, rv[j].y, r0.x));
+                r0.y = fma(-g[j].x, rv[j].y, fma(-g[j].y, rv[j].x, r0.y));
+                u0.x = fma(-g[j].x, uv[j].x, fma(g[j].y, uv[j].y, u0.x));
+                u0.y = fma(-g[j].x, uv[j].y, fma(-g[j].y, uv[j].x, u0.y));
+            }
+            x[i] = xv;
+            P.r[0][i] = r0;
+            P.u[0][i] = u0;
+            acc[0] += cabs2(r0);
+            acc[1] = fma(tv.x, r0.x, fma(tv.y, r0.y, acc[1]));
+            acc[2] = fma(tv.x, r0.y, fma(-tv.y, r0.x, acc[2]));
+        }
+        reduce_finish<S_U_BL, 3>(c, acc);
+    }
+    set_cond(c);
+}
+
+using BlKernel = void (*)(SolveCtx*, VecSet);
+static BlKernel bl_gram_of(int L) {
+    switch (L) {
+        case 1: return bl_gram<1>;
+        case 2: return bl_gram<2>;
+        case 3: return bl_gram<3>;
+        case 4: return bl_gram<4>;
+        case 5: return bl_gram<5>;
+        case 6: return bl_gram<6>;
+        case 7: return bl_gram<7>;
+        default: return bl_gram<8>;
+    }
+}
+static BlKernel bl_u_of(int L) {
+    switch (L) {
+        case 1: return bl_u<1>;
+        case 2: return bl_u<2>;
+        case 3: return bl_u<3>;
+        case 4: return bl_u<4>;
+        case 5: return bl_u<5>;
+        case 6: return bl_u<6>;
+        case 7: return bl_u<7>;
+        default: return bl_u<8>;
+    }
+}
+static int bl_nd(int L) { return (L + 1) + (L + 1) * L; }
+
 // ------------------------------------------------------------------ persistent solver (loop mode 4)
 // The whole iteration loop as ONE cooperative launch for latency-bound systems (the paper's
 // Audi3D/Twingo shapes: a WHILE-graph body of 5 launches costs ~40 µs per iteration there).  The
@@ -1053,7 +1473,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_persist_cg(SolveCtx* c) {
 
 __global__ void k_set_ctx(SolveCtx* c, SolveCtx h) {
     *c = h;
-    for (int i = 0; i < 16; i++) h.tickets[i] = 0u;
+    for (int i = 0; i < kTickets; i++) h.tickets[i] = 0u;  // workspace memory may be recycled
 }
 
 // ------------------------------------------------------------------ host side
@@ -1116,6 +1536,34 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             ZK_TRY(launch_loop(pdl, k4_bicg, vec_grid(A, (const void*)k4_bicg), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_K4_BICG>(A, dc, 3, s)));
             ZK_TRY(launch_loop(pdl, k5_bicg, vec_grid(A, (const void*)k5_bicg), 0, s, dc));
+        } else if (method == kBiCGStabL) {
+            VecSet P;
+            for (int q = 0; q <= hc.ell; q++) {
+                P.r[q] = hc.rl[q];
+                P.u[q] = hc.ul[q];
+            }
+            for (int q = hc.ell + 1; q <= kMaxEll; q++) P.r[q] = P.u[q] = nullptr;
+            for (int j = 0; j < hc.ell; j++) {
+                ZK_TRY(launch_loop(pdl, bl_b1, vec_grid(A, (const void*)bl_b1), 0, s, dc, P, j));
+                { auto kf = bl_s1<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, P, j)); }
+                ZK_TRY(launch_loop(pdl, bl_b2, vec_grid(A, (const void*)bl_b2), 0, s, dc, P, j));
+                if (j < hc.ell - 1) {
+                    auto kf = bl_s2<W, MODE, true>;
+                    const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                    ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, P, j));
+                } else {
+                    auto kf = bl_s2<W, MODE, false>;
+                    const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                    ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, P, j));
+                }
+            }
+            const BlKernel kg = bl_gram_of(hc.ell);
+            int gg = A->dev.num_sms * blocks_per_sm((const void*)kg);
+            const int gcap = kMaxRed * kMaxGrid / bl_nd(hc.ell);  // partials [ND][grid]
+            if (gg > gcap) gg = gcap;
+            ZK_TRY(launch_loop(pdl, kg, gg, 0, s, dc, P));
+            const BlKernel ku = bl_u_of(hc.ell);
+            ZK_TRY(launch_loop(pdl, ku, vec_grid(A, (const void*)ku), 0, s, dc, P));
         } else if (method == ZK_TFQMR) {
             ZK_TRY(launch_loop(pdl, t1_tfqmr, vec_grid(A, (const void*)t1_tfqmr), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_T1_TFQMR>(A, dc, 1, s)));
@@ -1229,7 +1677,7 @@ struct WsLayout {
 static size_t up256(size_t v) { return (v + 255) & ~(size_t)255; }
 int64_t dist_gather_len(const zk_csr_s* A);  // dist.cu: n_rows + halo slots
 
-static WsLayout ws_layout(const zk_csr_s* A, int method, int32_t maxit) {
+static WsLayout ws_layout(const zk_csr_s* A, int method, int32_t maxit, int ell = 0) {
     WsLayout L;
     size_t off = 0;
     L.ctx = off;
@@ -1237,15 +1685,17 @@ static WsLayout ws_layout(const zk_csr_s* A, int method, int32_t maxit) {
     L.partials = off;
     off += up256(sizeof(double) * kMaxRed * kMaxGrid);
     L.tickets = off;
-    off += 256;
+    off += sizeof(unsigned int) * kTickets;
     L.hist = off;
     off += up256(sizeof(double) * ((size_t)(maxit > 0 ? maxit : 0) + 1));
     L.vec0 = off;
     const int64_t len = A->dist ? dist_gather_len(A) : A->n_rows;
     L.vec_bytes = up256(sizeof(double2) * (size_t)(len > 0 ? len : 1));
     // BiCGStab: r r̂ p v s t (+ xg gather copy on >1 GPU) ; CG/COCG: r p q (+ xg) ;
-    // TFQMR: w y1 y2 u1 u2 v d1 d2 r̃ (+ xg)
-    L.nvec = (method == ZK_BICGSTAB ? 6 : method == ZK_TFQMR ? 9 : 3) + (A->dist ? 1 : 0);
+    // TFQMR: w y1 y2 u1 u2 v d r̃ (+ xg)
+    // BiCGStab(ℓ): r̂_0..ℓ û_0..ℓ r̃
+    L.nvec = (method == ZK_BICGSTAB ? 6 : method == ZK_TFQMR ? 8 : method == kBiCGStabL ? 2 * ell + 3 : 3) +
+             (A->dist ? 1 : 0);
     off += L.vec_bytes * L.nvec;
     L.total = off;
     return L;
@@ -1255,18 +1705,36 @@ static WsLayout ws_layout(const zk_csr_s* A, int method, int32_t maxit) {
 
 using namespace zk;
 
-extern "C" size_t zk_solve_workspace_size(zk_csr A, int32_t method, int32_t maxit) {
-    if (!A || method < ZK_BICGSTAB || method > ZK_TFQMR) return 0;
-    if (method == ZK_BICGSTAB_JACOBI) method = ZK_BICGSTAB;
-    return ws_layout(A, method, maxit).total;
+// method code → (internal method, ℓ); false for an unknown code
+static bool decode_method(int32_t code, int* method, int* ell) {
+    *ell = 0;
+    if (code >= ZK_BICGSTAB && code <= ZK_TFQMR) {
+        *method = code;
+        return true;
+    }
+    if (code >= ZK_BICGSTAB_L(1) && code <= ZK_BICGSTAB_L(kMaxEll)) {
+        *method = kBiCGStabL;
+        *ell = code - ZK_BICGSTAB_L(0);
+        return true;
+    }
+    return false;
 }
 
-extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double tol, int32_t maxit, int32_t method,
+extern "C" size_t zk_solve_workspace_size(zk_csr A, int32_t code, int32_t maxit) {
+    int method, ell;
+    if (!A || !decode_method(code, &method, &ell)) return 0;
+    if (method == ZK_BICGSTAB_JACOBI) method = ZK_BICGSTAB;
+    return ws_layout(A, method, maxit, ell).total;
+}
+
+extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double tol, int32_t maxit, int32_t code,
                               zk_z* x, int32_t* iters, double* resid_hist, zk_solve_info* info, void* workspace,
                               size_t ws_bytes, zk_stream stream) {
     if (!A || !b || !x || !iters || !resid_hist || !workspace) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
-    if (method < ZK_BICGSTAB || method > ZK_TFQMR)
-        return fail(ZK_ERR_INVALID_VALUE, "unknown method");
+    int method, ell;
+    if (!decode_method(code, &method, &ell)) return fail(ZK_ERR_INVALID_VALUE, "unknown method");
+    if (method == kBiCGStabL && A->dist)
+        return fail(ZK_ERR_UNSUPPORTED, "BiCGStab(l) runs on one GPU (no comm handle)");
     const bool jacobi = method == ZK_BICGSTAB_JACOBI;
     if (jacobi) {
         ZK_TRY(jacobi_prepare(A, (cudaStream_t)stream));  // A·M⁻¹ built once, cached in the handle
@@ -1277,7 +1745,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     if (A->n_cols != A->n_global) return fail(ZK_ERR_DIM, "solve needs a square matrix");
     if ((const void*)b == (const void*)x) return fail(ZK_ERR_ALIAS, "b aliases x");
     if (((uintptr_t)workspace & 255u) != 0) return fail(ZK_ERR_INVALID_VALUE, "workspace must be 256-B aligned");
-    const WsLayout L = ws_layout(A, method, maxit);
+    const WsLayout L = ws_layout(A, method, maxit, ell);
     if (ws_bytes < L.total) return fail(ZK_ERR_INVALID_VALUE, "workspace too small");
     if (A->n_rows == 0 && !A->dist) return fail(ZK_ERR_ZERO_RHS, "empty system (||b|| = 0)");
     cudaStream_t s = (cudaStream_t)stream;
@@ -1291,14 +1759,24 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     hc.partials = (double*)(ws + L.partials);
     hc.tickets = (unsigned int*)(ws + L.tickets);
     hc.hist = (double*)(ws + L.hist);
-    double2* vec[10];
+    double2* vec[2 * kMaxEll + 4];
     for (int i = 0; i < L.nvec; i++) vec[i] = (double2*)(ws + L.vec0 + L.vec_bytes * i);
     if (method == ZK_BICGSTAB) {
         hc.r = vec[0]; hc.rh = vec[1]; hc.p = vec[2]; hc.v = vec[3]; hc.s = vec[4]; hc.t = vec[5];
     } else if (method == ZK_TFQMR) {
         hc.w = vec[0]; hc.y1 = vec[1]; hc.y2 = vec[2]; hc.u1 = vec[3]; hc.u2 = vec[4]; hc.v = vec[5];
-        hc.d1 = vec[6]; hc.d2 = vec[7]; hc.rt = vec[8];
+        hc.d = vec[6]; hc.rt = vec[7];
         hc.r = hc.w; hc.p = hc.y1; hc.rh = hc.rt;  // the shared init writes r0 into w, y1 and r̃
+    } else if (method == kBiCGStabL) {
+        for (int q = 0; q <= ell; q++) {
+            hc.rl[q] = vec[q];
+            hc.ul[q] = vec[ell + 1 + q];
+        }
+        hc.rh = vec[2 * ell + 2];  // r̃
+        hc.r = hc.rl[0];           // the shared init writes r0 into r̂_0, r̃ (and û_1, overwritten later)
+        hc.p = hc.ul[1];
+        hc.d = hc.ul[0];           // û_0 = 0
+        hc.ell = ell;
     } else {
         hc.r = vec[0]; hc.p = vec[1]; hc.q = vec[2];
     }
@@ -1325,7 +1803,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     if (A->dist && (mode == 1 || mode == 4)) mode = 3;  // NCCL inside WHILE bodies / persistent kernels is not used
     int persist_grid = 0;
     const void* kp = nullptr;
-    if (mode == 4 && (method == ZK_COCG || method == ZK_TFQMR)) mode = 1;  // persistent: BiCGStab and CG only
+    if (mode == 4 && (method == ZK_COCG || method == ZK_TFQMR || method == kBiCGStabL)) mode = 1;  // persistent: BiCGStab, CG
     if (mode == 4) {
         int dev_coop = 0;
         cudaDeviceGetAttribute(&dev_coop, cudaDevAttrCooperativeLaunch, A->dev.device);
@@ -1342,8 +1820,10 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         persist_grid = (int)(g < 1 ? 1 : (g > cap ? cap : g));
         if (!dev_coop || cap < 1) mode = 1;
     }
+    static_assert(kBiCGStabL < (int)(sizeof(((zk_csr_s*)nullptr)->graph) / sizeof(GraphCache)), "graph slot per method");
     GraphCache& gc = A->graph[method];
-    if (mode <= 2 && (gc.ws != workspace || gc.mode != mode || gc.method != method || !gc.exec)) {
+    const int gkey = method * 16 + ell;  // BiCGStab(ℓ): one graph per ℓ
+    if (mode <= 2 && (gc.ws != workspace || gc.mode != mode || gc.method != gkey || !gc.exec)) {
         drop_graph(gc);
         const bool pdl = !(getenv("ZK_PDL") && atoi(getenv("ZK_PDL")) == 0);
         zk_status st = mode == 1 ? build_while_graph(A, dc, hc, method, gc, pdl) : build_chunk_graph(A, dc, hc, method, gc);
@@ -1362,7 +1842,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         } else {
             gc.ws = workspace;
             gc.mode = mode;
-            gc.method = method;
+            gc.method = gkey;
         }
     }
     hc.use_cond = mode == 1 ? 1 : 0;
@@ -1377,7 +1857,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     // ---- init: context, r0 = b − A x0 (or b), ‖b‖, hist[0]
     k_set_ctx<<<1, 1, 0, s>>>(dc, hc);
     ZK_CUDA(cudaGetLastError());
-    const int kind = method == ZK_BICGSTAB ? 0 : method == ZK_CG ? 1 : method == ZK_COCG ? 3 : 4;
+    const int kind = method == ZK_BICGSTAB ? 0 : method == ZK_CG ? 1 : method == ZK_COCG ? 3 : method == ZK_TFQMR ? 4 : 5;
     if (x0) {
         const double2* g0 = (const double2*)x0;
         if (jacobi) {  // u0 = M x0, in the output buffer (x may alias x0)
@@ -1403,8 +1883,12 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
                 auto k = k_init_x0<W, MODE, S_INIT_COCG>;
                 const LaunchCfg L = spmv_cfg(A, (const void*)k, W, MODE);
                 k<<<L.grid, kBlock, L.smem, s>>>(dc, g0, 0);
-            } else {
+            } else if (kind == 4) {
                 auto k = k_init_x0<W, MODE, S_INIT_TFQMR>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)k, W, MODE);
+                k<<<L.grid, kBlock, L.smem, s>>>(dc, g0, 1);
+            } else {
+                auto k = k_init_x0<W, MODE, S_INIT_BL>;
                 const LaunchCfg L = spmv_cfg(A, (const void*)k, W, MODE);
                 k<<<L.grid, kBlock, L.smem, s>>>(dc, g0, 1);
             }
@@ -1494,7 +1978,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
 
     *iters = out.iters;
     const int passes = out.iters;
-    n_spmv += (int64_t)passes * (method == ZK_BICGSTAB || method == ZK_TFQMR ? 2 : 1) + 1;
+    n_spmv += (int64_t)passes * (method == ZK_BICGSTAB || method == ZK_TFQMR ? 2 : method == kBiCGStabL ? 2 * ell : 1) + 1;
     if (info) {
         info->status = out.status == ST_ZERO_RHS ? ZK_CONVERGED : out.status;
         info->iters = out.iters;
@@ -1502,7 +1986,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         info->n_spmv = n_spmv;
         info->solve_ms = ms;
         info->loop_mode = mode;
-        const int per_body = method == ZK_BICGSTAB ? 5 : method == ZK_TFQMR ? 4 : 3;
+        const int per_body = method == ZK_BICGSTAB ? 5 : method == ZK_TFQMR ? 4 : method == kBiCGStabL ? 4 * ell + 2 : 3;
         const int fins = A->dist ? (method == ZK_BICGSTAB ? 4 : method == ZK_TFQMR ? 3 : 2) : 0;  // dist: 1-thread finish kernels
         const int pre = method == ZK_TFQMR ? (A->dist ? 2 : 1) : 0;                               // TFQMR: K0 (+ its finish)
         info->gpu_launches = mode == 4 ? 4 : 3 + pre + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);

@@ -66,7 +66,7 @@ struct zk_csr_s {
     double mean_len = 0.0;
     zk::DeviceInfo dev;
     cudaStream_t cap_stream = nullptr;  // private stream used for graph capture
-    zk::GraphCache graph[4];            // per method (ZK_BICGSTAB, ZK_CG, -, ZK_COCG)
+    zk::GraphCache graph[8];            // per solver method code (ZK_BICGSTAB .. ZK_TFQMR)
     zk_comm_s* comm = nullptr;
     // distributed: halo plan (see dist.cu)
     void* dist = nullptr;

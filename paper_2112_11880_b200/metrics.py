@@ -37,5 +37,23 @@ def cg_iter_bytes(n: int, nnz: int) -> int:
     return csr_bytes(n, nnz) + 11 * Z * n
 
 
+def cocg_iter_bytes(n: int, nnz: int) -> int:
+    """COCG (NEXT-4) runs CG's schedule with unconjugated products: Mat + 176n."""
+    return cg_iter_bytes(n, nnz)
+
+
+def tfqmr_iter_bytes(n: int, nnz: int) -> int:
+    """TFQMR (NEXT-2), kernels T1-T4 of solve.cu: 2·Mat + 400n (25 complex vector passes:
+    T1 6, T2 5 incl. the gathered y2, T3 8, T4 6 incl. the gathered y1)."""
+    return 2 * csr_bytes(n, nnz) + 25 * Z * n
+
+
+def bicgstab_l_cycle_bytes(n: int, nnz: int, ell: int) -> int:
+    """BiCGStab(ℓ) (NEXT-3), one outer cycle of solve.cu's bl_* kernels: 2ℓ·Mat + (3ℓ² + 15ℓ + 7)
+    complex vector passes — BiCG step j: B1 3(j+1), S1 3, B2 6 + 3j, S2 3 (2 for j = ℓ−1);
+    Gram ℓ+1; update 2ℓ + 7.  ℓ = 8: 319 passes."""
+    return 2 * ell * csr_bytes(n, nnz) + (3 * ell * ell + 15 * ell + 7) * Z * n
+
+
 def spmv_flops(nnz: int) -> int:
     return FLOPS_PER_NNZ_SPMV * nnz

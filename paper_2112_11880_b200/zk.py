@@ -20,6 +20,18 @@ ZK_PTRS_HOST, ZK_PTRS_DEVICE, ZK_PTRS_DEVICE_BORROW, ZK_SKIP_VALIDATE = 0, 1, 2,
 ZK_BICGSTAB, ZK_CG = 0, 1
 ZK_BICGSTAB_JACOBI, ZK_COCG, ZK_TFQMR = 2, 3, 4
 METHODS = {"bicgstab": ZK_BICGSTAB, "cg": ZK_CG, "bicgstab_jacobi": ZK_BICGSTAB_JACOBI, "cocg": ZK_COCG, "tfqmr": ZK_TFQMR}
+
+
+def ZK_BICGSTAB_L(ell: int) -> int:
+    """Method code of BiCGStab(l), 1 <= l <= 8 (zk.h ZK_BICGSTAB_L)."""
+    return 16 + int(ell)
+
+
+def method_code(method: str, ell: int = 8) -> int:
+    """"bicgstab", "cg", "bicgstab_jacobi", "cocg", "tfqmr" or "bicgstab_l" (with ell)."""
+    if method == "bicgstab_l":
+        return ZK_BICGSTAB_L(ell)
+    return METHODS[method]
 OUTCOMES = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN_RHO", 3: "BREAKDOWN_SIGMA", 4: "BREAKDOWN_OMEGA",
             5: "NOT_HPD", 6: "NONFINITE"}
 
@@ -266,28 +278,29 @@ def zaxmy(x: torch.Tensor, y: torch.Tensor, stream=None) -> torch.Tensor:
     return y
 
 
-def workspace_size(A: Csr, method: str = "bicgstab", maxit: int = 1000) -> int:
-    return int(lib().zk_solve_workspace_size(A.handle, METHODS[method], int(maxit)))
+def workspace_size(A: Csr, method: str = "bicgstab", maxit: int = 1000, ell: int = 8) -> int:
+    return int(lib().zk_solve_workspace_size(A.handle, method_code(method, ell), int(maxit)))
 
 
-def alloc_workspace(A: Csr, method: str = "bicgstab", maxit: int = 1000, device=None) -> torch.Tensor:
-    nbytes = workspace_size(A, method, maxit)
+def alloc_workspace(A: Csr, method: str = "bicgstab", maxit: int = 1000, device=None, ell: int = 8) -> torch.Tensor:
+    nbytes = workspace_size(A, method, maxit, ell)
     # torch's caching allocator returns 512-B aligned blocks
     return torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
 
 
 def solve(A: Csr, b: torch.Tensor, x0: torch.Tensor | None = None, tol: float = 1e-8, maxit: int = 1000,
           method: str = "bicgstab", x: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
-          stream=None) -> dict:
-    """zk_solve: returns dict(x, iters, hist, status, true_relres, n_spmv, solve_ms, loop_mode)."""
-    m = METHODS[method]
+          stream=None, ell: int = 8) -> dict:
+    """zk_solve: returns dict(x, iters, hist, status, true_relres, n_spmv, solve_ms, loop_mode).
+    method "bicgstab_l" runs BiCGStab(ell) (iters/hist count outer cycles)."""
+    m = method_code(method, ell)
     pb = _dev_c128(b, "b")
     if x is None:
         x = torch.empty_like(b)
     px = _dev_c128(x, "x")
     px0 = _dev_c128(x0, "x0") if x0 is not None else None
     if workspace is None:
-        workspace = alloc_workspace(A, method, maxit, b.device)
+        workspace = alloc_workspace(A, method, maxit, b.device, ell)
     iters = I32(0)
     hist = np.full(maxit + 1, np.nan)
     info = zk_solve_info()

@@ -1,0 +1,162 @@
+"""GPU parity of the device-resident BiCGStab(ℓ) (NEXT-3; zk_solve method ZK_BICGSTAB_L(ℓ)) against
+oracle.bicgstab_l.
+
+Bars (iterations are outer cycles of 2ℓ SpMVs):
+  * cycle count within [0.95·min, 1.05·max] of the oracle's counts under its summation orders
+    (seq, rev, block-256), as for BiCGStab;
+  * residual histories: ℓ ≤ 2 to 1e-10 relative over the first 6 cycles; ℓ = 8 to 1e-3 — the
+    ℓ = 8 minimal-residual step solves a Gram system of A^j r̂ (j ≤ 8) whose conditioning
+    amplifies rounding: the oracle's own summation orders already differ by up to 9e-5 there;
+  * solutions to 1e-6 relative (C1/C2/T0); true residual ≤ 10·tol;
+  * C4 (bench shape, ℓ = 8): DST-I closed form within 2κ·tol, first cycle's residual vs the oracle;
+  * outcomes match the oracle's; loop modes bitwise identical; a comm handle → ZK_ERR_UNSUPPORTED."""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+from paper_2112_11880_b200 import zk
+from tests import closed_form as cf
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+ORDERS = (oracle.ORD_SEQ, oracle.ORD_REV, oracle.ORD_BLOCK256)
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def gpu_solve(m, b, ell, **kw):
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+    x0 = kw.pop("x0", None)
+    r = zk.solve(A, cuda(b), None if x0 is None else cuda(x0), method="bicgstab_l", ell=ell, **kw)
+    r["x"] = r["x"].cpu().numpy()
+    return r
+
+
+def relerr(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def diag(d):
+    n = len(d)
+    return dict(row_ptr=np.arange(n + 1, dtype=np.int64), col_idx=np.arange(n, dtype=np.int32),
+                values=np.asarray(d, np.complex128), n=n)
+
+
+def htol(ell):
+    return 1e-10 if ell <= 2 else 1e-3
+
+
+@pytest.mark.parametrize("ell", [1, 2, 4, 8])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
+def test_bicgstab_l_parity(cfg, ell):
+    m = gen.make_matrix(cfg)
+    b = gen.make_rhs(m)
+    r = gpu_solve(m, b, ell, tol=1e-8, maxit=1000)
+    refs = [oracle.bicgstab_l(m, b, tol=1e-8, ell=ell, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    assert r["status"] == "CONVERGED" and all(q["status"] == "CONVERGED" for q in refs)
+    assert 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    k = min(6, r["iters"], refs[0]["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= htol(ell)
+    assert relerr(r["x"], refs[0]["x"]) <= 1e-6
+    assert r["true_relres"] <= 10 * 1e-8
+    assert r["loop_mode"] == 1
+
+
+@pytest.mark.parametrize("ell", [1, 2, 8])
+@pytest.mark.parametrize("c", [2.0, -1.0, 1j, 0.3 - 2j])
+def test_bicgstab_l_scalar_identity(c, ell):
+    """One-step exactness: the first BiCG step reaches x = b/c, exit in cycle 1."""
+    n = 1000
+    b = gen.rand_vector(n, 1)
+    r = gpu_solve(diag(np.full(n, c)), b, ell, tol=1e-12)
+    assert r["status"] == "CONVERGED" and r["iters"] == 1
+    assert np.max(np.abs(r["x"] - b / c)) <= 1e-15 * np.max(np.abs(b / c))
+
+
+def test_bicgstab_l_finite_termination():
+    """3 distinct eigenvalues, ℓ = 4: the BiCG part of cycle 1 reaches the solution (as the oracle)."""
+    n = 3000
+    d = np.array([1.5, -2.0 + 0.5j, 3.0j])[np.arange(n) % 3]
+    b = gen.rand_vector(n, 2)
+    r = gpu_solve(diag(d), b, 4, tol=1e-10)
+    assert r["status"] == "CONVERGED" and r["iters"] == 1
+    assert np.max(np.abs(r["x"] - b / d)) <= 1e-12 * np.max(np.abs(b / d))
+
+
+def test_bicgstab_l_outcomes_match_oracle():
+    m = dict(row_ptr=np.array([0, 1, 2]), col_idx=np.array([1, 0], np.int32),
+             values=np.array([1, -1], np.complex128), n=2)
+    b = np.array([1, 0], np.complex128)
+    assert gpu_solve(m, b, 2)["status"] == oracle.bicgstab_l(m, b, ell=2)["status"] == "BREAKDOWN_SIGMA"
+    mc = gen.make_matrix("C2")
+    bc = gen.make_rhs(mc)
+    x0 = gen.rand_vector(mc["n"], 5)
+    r = gpu_solve(mc, bc, 4, x0=x0, tol=1e-14, maxit=3)
+    ref = oracle.bicgstab_l(mc, bc, x0=x0, tol=1e-14, maxit=3, ell=4)
+    assert r["status"] == ref["status"] == "MAXIT" and r["iters"] == ref["iters"] == 3
+    assert np.max(np.abs(r["hist"] - ref["hist"]) / ref["hist"]) <= 1e-9
+    assert relerr(r["x"], ref["x"]) <= 1e-9
+    bn = bc.copy()
+    bn[3] = np.nan
+    assert gpu_solve(mc, bn, 2)["status"] == oracle.bicgstab_l(mc, bn, ell=2)["status"] == "NONFINITE"
+    with pytest.raises(zk.ZkError) as e:
+        gpu_solve(mc, np.zeros(mc["n"], np.complex128), 2)
+    assert e.value.code == -8
+
+
+@pytest.mark.parametrize("mode", ["2", "3"])
+def test_bicgstab_l_loop_modes_bitwise_identical(mode, monkeypatch):
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    monkeypatch.setenv("ZK_LOOP_MODE", "1")
+    base = gpu_solve(m, b, 4, tol=1e-8)
+    monkeypatch.setenv("ZK_LOOP_MODE", mode)
+    r = gpu_solve(m, b, 4, tol=1e-8)
+    assert r["loop_mode"] == int(mode)
+    assert r["iters"] == base["iters"] and np.array_equal(r["x"], base["x"])
+    assert np.array_equal(r["hist"], base["hist"])
+
+
+def test_bicgstab_l_deterministic_and_ell_switch():
+    """Repeated solves are bitwise identical; switching ℓ on one handle rebuilds the loop graph."""
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+    B = cuda(b)
+    r1 = zk.solve(A, B, method="bicgstab_l", ell=2)
+    x1 = r1["x"].cpu().numpy()
+    r8 = zk.solve(A, B, method="bicgstab_l", ell=8)
+    r2 = zk.solve(A, B, method="bicgstab_l", ell=2)
+    assert np.array_equal(x1, r2["x"].cpu().numpy()) and np.array_equal(r1["hist"], r2["hist"])
+    assert r8["iters"] == oracle.bicgstab_l(m, b, ell=8)["iters"]
+
+
+def test_bicgstab_l_rejects_comm():
+    m = gen.make_matrix("C1")
+    comm = zk.Comm(zk.Comm.unique_id(), 1, 0, 0)
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"], comm=comm, row_begin=0)
+    with pytest.raises(zk.ZkError) as e:
+        zk.solve(A, cuda(gen.make_rhs(m)), method="bicgstab_l", ell=2)
+    assert e.value.code == -10
+    A.close()
+    comm.close()
+
+
+def test_bicgstab_l8_c4_full_size():
+    """C4 (8M rows), ℓ = 8 as the paper's P-BiCGSTAB(8): closed-form forward error, true residual,
+    and the first cycle's residual against the oracle (one oracle cycle = 16 SpMVs)."""
+    spec = gen.CONFIGS["C4"]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    A = zk.csr_create(cuda(m["row_ptr"]), cuda(m["col_idx"]), cuda(m["values"]), m["n"], borrow=True)
+    r = zk.solve(A, cuda(b), tol=1e-8, maxit=300, method="bicgstab_l", ell=8)
+    assert r["status"] == "CONVERGED" and r["true_relres"] <= 1e-7
+    xe = cf.box_solve(spec, b, gen.ETA)
+    assert relerr(r["x"].cpu().numpy(), xe) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
+    ref = oracle.bicgstab_l(m, b, tol=1e-8, maxit=1, ell=8)
+    assert abs(r["hist"][1] - ref["hist"][1]) / ref["hist"][1] <= 1e-3
