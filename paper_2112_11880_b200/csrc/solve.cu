@@ -712,6 +712,9 @@ struct OpK3Cocg {  // p = r + β p (complex β)
 };
 
 // TFQMR epilogues and vector ops (the loops of oracle_tfqmr, fused per kernel T1..T4)
+#ifndef ZK_TF_AHEAD
+#define ZK_TF_AHEAD true
+#endif
 #ifndef ZK_T1_U
 #define ZK_T1_U 1
 #endif
@@ -747,6 +750,7 @@ struct OpT1Tfqmr {  // y2 = y1 − α v ; w −= α u1 ; {‖w‖²}
 
 struct EpiT2Tfqmr {  // u2 = A y2 ; w −= α u2 ; {‖w‖², ⟨r̃, w⟩}
     static constexpr int K = 3;
+    static constexpr bool kAhead = ZK_TF_AHEAD;
     struct Pre { double2 w, rt; };
     SolveCtx* c;
     double2 *__restrict__ u2, *__restrict__ w;
@@ -809,6 +813,7 @@ struct OpT3Tfqmr {
 template <int S>
 struct EpiT4Tfqmr {  // u1 = A y1 ; v = u1 + β(u2 + β v) (first: v = u1) ; {σ = ⟨r̃, v⟩}
     static constexpr int K = 2;
+    static constexpr bool kAhead = ZK_TF_AHEAD;
     struct Pre { double2 u2, v, rt; };
     SolveCtx* c;
     double2 *__restrict__ u1, *__restrict__ v;

@@ -2,7 +2,7 @@
 // both as __device__ templates so the solver kernels can fuse their epilogues into them.
 //
 // ZSpMV mapping: a sub-warp of W lanes per row, W chosen at create from the mean
-// row length (W = 8 for the 27-point FE rows).  A block of 256 threads owns 256/W consecutive
+// row length (W = 4 for the 27-point FE rows: ≈ 7 nonzeros per lane).  A block of 256 threads owns 256/W consecutive
 // rows per step and walks its tiles grid-stride (a fixed static schedule, so the fused
 // reductions are deterministic).  Per row chunk of 4W nonzeros each lane issues 4 independent
 // (value, column) loads before touching x, then the 4 gathers of x (read-only path; x stays

@@ -92,9 +92,12 @@ __device__ __forceinline__ int ld_mat(const int* p, uint64_t pol) {
     }
 }
 // Streaming load of data this kernel also writes (coherent path, no L1 allocation).
+#ifndef ZK_LD_CLOBBER
+#define ZK_LD_CLOBBER : "memory"
+#endif
 __device__ __forceinline__ double2 ld_stream_rw(const double2* p) {
     double2 v;
-    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) ZK_LD_CLOBBER);
     return v;
 }
 // Gather through the read-only path (L1 + L2 reuse of x across neighbouring rows).
@@ -103,7 +106,7 @@ __device__ __forceinline__ double2 ld_gather(const double2* p) { return __ldg(p)
 // separated by grid-wide barriers whose gpu-scope fences invalidate L1): never .nc.
 __device__ __forceinline__ double2 ld_gather_coh(const double2* p) {
     double2 v;
-    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) ZK_LD_CLOBBER);
     return v;
 }
 __device__ __forceinline__ double2 ld_vec(const double2* p) { return ld_stream_rw(p); }
