@@ -95,9 +95,13 @@ typedef struct {
     int64_t n_halo;        /* off-rank x entries received per SpMV (0 on one GPU) */
     int32_t borrowed;      /* 1 if the arrays are borrowed (ZK_PTRS_DEVICE_BORROW) */
     int32_t nranks;
-    int32_t spmv_mode;     /* 0 = sub-warp rows, 1 = TMA bulk-copy staged row tiles, 2 = aligned 4-blocks */
+    int32_t spmv_mode;     /* 0 = sub-warp rows, 1 = TMA bulk-copy staged row tiles, 2 = aligned 4-blocks,
+                              3 = sliced ELL (SELL-32 copy of the matrix, the default unless its padding
+                              exceeds 10 % of nnz; a library-owned copy, also for borrowed arrays) */
     int32_t rows_per_tile; /* TMA mode: rows per staged tile */
     int32_t tma_stages;    /* TMA mode: pipeline depth */
+    int64_t sell_entries;  /* mode 3: stored entries incl. padding (slices of 32 rows, each padded to
+                              its longest row); 0 otherwise */
 } zk_csr_info_t;
 
 typedef struct {

@@ -175,16 +175,22 @@ zk_status zcsrmv_local(const zk_csr_s* A, double2 alpha, const double2* x, doubl
 // SpMV mapping from the row statistics (env ZK_SPMV_MODE / ZK_SPMV_W override, for sweeps):
 //  sub-warp kernel by default (measured faster than the TMA-staged variant on C4), lanes per row
 //  ≈ mean/8; the TMA-staged mode is available for rows ≤ 128 long (W ∈ {4, 8, 16}).
-static void choose_mapping(zk_csr_s* A) {
+// SpMV mapping.  Default: the sliced-ELL copy (mode 3) — on C4 zk_zcsrmv 647 µs vs 812 µs for the
+// best CSR mapping (profiles/r01_sell.md) — unless its padding exceeds kSellMaxPad of the nonzeros
+// (checked after the build; then the sub-warp CSR kernel).  ZK_SPMV_MODE forces a mapping.
+constexpr double kSellMaxPad = 0.10;
+static void choose_mapping(zk_csr_s* A, int force_mode = -1) {
     int mode = -1, w = -1;
     if (const char* e = getenv("ZK_SPMV_MODE")) mode = atoi(e);
+    else mode = 3;
+    if (force_mode >= 0) mode = force_mode;
     if (const char* e = getenv("ZK_SPMV_W")) w = atoi(e);
     int stages = 4, stage_nnz = 756;
     if (const char* e = getenv("ZK_TMA_STAGES")) stages = atoi(e) < 2 ? 2 : (atoi(e) > 8 ? 8 : atoi(e));
     if (const char* e = getenv("ZK_TMA_NNZ")) stage_nnz = atoi(e) < 256 ? 256 : atoi(e);
     const bool tma_ok = make_tma_plan(A->n_rows, A->nnz, A->max_len, &A->tma, stages, stage_nnz);
     const bool aligned = ((uintptr_t)A->val % 32 == 0) && ((uintptr_t)A->col % 16 == 0);
-    if (mode < 0 || mode > 2) mode = 0;  // measured: sub-warp W=4 beats blocked-4 (1000-1360 µs) and TMA
+    if (mode < 0 || mode > 3) mode = 0;  // measured: sub-warp W=4 beats blocked-4 (1000-1360 µs) and TMA
     if (mode == 1 && !tma_ok) mode = 0;
     if (mode == 2 && !aligned) mode = 0;
     A->spmv_mode = mode;
@@ -202,6 +208,7 @@ static void choose_mapping(zk_csr_s* A) {
         while (w < 32 && 8.0 * w < A->mean_len) w *= 2;
     }
     if (mode == 1) w = w <= 4 ? 4 : (w >= 16 ? 16 : 8);
+    if (mode == 3) w = 32;  // a warp per 32-row slice (sell.cu)
     A->W = w;
 }
 
@@ -211,6 +218,8 @@ zk_status dist_zcsrmv(const zk_csr_s* A, double2 alpha, const double2* x, double
                       cudaStream_t s);                                                           // dist.cu
 int64_t dist_n_halo(const zk_csr_s* A);                                                          // dist.cu
 void jacobi_destroy(zk_csr_s* A);                                                                // jacobi.cu
+zk_status sell_build(zk_csr_s* A, cudaStream_t s);                                               // sell.cu
+void sell_destroy(zk_csr_s* A);                                                                  // sell.cu
 int dist_nranks(const zk_csr_s* A);                                                              // dist.cu
 }  // namespace zk
 
@@ -304,6 +313,15 @@ extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, 
         st = dist_setup(A, nullptr, nullptr, s);
         if (st != ZK_OK) return cleanup(st);
     }
+    if (A->spmv_mode == 3) {  // after the halo renumbering: the copy holds the final column ids
+        st = sell_build(A, s);
+        if (st != ZK_OK) return cleanup(st);
+        const char* forced = getenv("ZK_SPMV_MODE");
+        if (!forced && (double)A->sl_nnz > (1.0 + kSellMaxPad) * (double)A->nnz) {
+            sell_destroy(A);  // too much padding (irregular rows): CSR sub-warp kernel
+            choose_mapping(A, 0);
+        }
+    }
     *out = A;
     return ZK_OK;
 }
@@ -316,6 +334,7 @@ extern "C" zk_status zk_csr_destroy(zk_csr A) {
     }
     if (A->dist) dist_destroy(A);
     jacobi_destroy(A);
+    sell_destroy(A);
     if (A->owned) {
         cudaFree(A->row_ptr);
         cudaFree(A->col);
@@ -342,6 +361,7 @@ extern "C" zk_status zk_csr_info(zk_csr A, zk_csr_info_t* info) {
     info->spmv_mode = A->spmv_mode;
     info->rows_per_tile = A->spmv_mode == 1 ? A->tma.R : 0;
     info->tma_stages = A->spmv_mode == 1 ? A->tma.S : 0;
+    info->sell_entries = A->spmv_mode == 3 ? A->sl_nnz : 0;
     return ZK_OK;
 }
 

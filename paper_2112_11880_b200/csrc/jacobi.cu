@@ -31,8 +31,10 @@ __global__ void jacobi_diag_kernel(const int64_t* __restrict__ row_ptr, const in
 __global__ void jacobi_scale_kernel(const int* __restrict__ col, const double2* __restrict__ val,
                                     const double2* __restrict__ dinv, int64_t nnz, double2* __restrict__ out) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += stride)
-        out[p] = cmul(val[p], __ldg(dinv + col[p]));
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += stride) {
+        const int c = col[p];
+        out[p] = c >= 0 ? cmul(val[p], __ldg(dinv + c)) : make_double2(0.0, 0.0);  // c < 0: SELL padding
+    }
 }
 
 // out_i = d_i · in_i (x0 → u0 = M x0, u → x = M⁻¹ u); out may alias in
@@ -75,6 +77,22 @@ zk_status jacobi_prepare(zk_csr_s* A, cudaStream_t s) {
         snprintf(buf, sizeof buf, "row %lld has no nonzero stored diagonal (Jacobi preconditioner)",
                  (long long)hbad + (long long)A->row_begin);
         return fail(ZK_ERR_INVALID_CSR, buf);
+    }
+    if (A->sl_val) {  // the same scaling of the sliced-ELL copy (SpMV mode 3)
+        e = cudaMalloc(&A->jac_sl_val, sizeof(double2) * (size_t)(A->sl_nnz > 0 ? A->sl_nnz : 1));
+        if (e == cudaSuccess && A->sl_nnz > 0) {
+            jacobi_scale_kernel<<<grid_for(A->sl_nnz, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(
+                A->sl_col, A->sl_val, dinv, A->sl_nnz, A->jac_sl_val);
+            e = cudaGetLastError();
+        }
+        if (e != cudaSuccess) {
+            cudaFree(val);
+            cudaFree(diag);
+            cudaFree(dinv);
+            cudaFree(A->jac_sl_val);
+            A->jac_sl_val = nullptr;
+            return cuda_fail(e, "jacobi_prepare (sliced ELL)", __FILE__, __LINE__);
+        }
     }
     A->jac_val = val;
     A->jac_diag = diag;

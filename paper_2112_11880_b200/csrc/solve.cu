@@ -721,7 +721,7 @@ struct OpK3Cocg {  // p = r + β p (complex β)
 // T2/T4 (SpMV + the TFQMR epilogues): 80 registers (3 CTAs/SM) measured 16 % faster on C4 than
 // the 64 of the plain SpMV kernels (profiles/r01_tfqmr_variants.md)
 #ifndef ZK_TF_MINB
-#define ZK_TF_MINB (MODE == 0 ? 3 : spmv_min_blocks(MODE))
+#define ZK_TF_MINB ((MODE == 0 || MODE == 3) ? 3 : spmv_min_blocks(MODE))
 #endif
 struct OpT1Tfqmr {  // y2 = y1 − α v ; w −= α u1 ; {‖w‖²}
     static constexpr int K = 1;
@@ -1787,7 +1787,10 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     }
     double2* xg = A->dist ? vec[L.nvec - 1] : nullptr;  // gather copy of x0 / x with halo slots
     hc.A = csr_dev(A);
-    if (jacobi) hc.A.val = A->jac_val;  // iterate on A' = A·M⁻¹ (u = M x)
+    if (jacobi) {  // iterate on A' = A·M⁻¹ (u = M x)
+        hc.A.val = A->jac_val;
+        hc.A.sl_val = A->jac_sl_val;
+    }
     hc.T = A->tma;
     hc.tol = tol;
     hc.maxit = maxit;

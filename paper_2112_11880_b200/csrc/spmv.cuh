@@ -209,6 +209,81 @@ __device__ __forceinline__ void spmv_body_b4(const CsrDev& A, const double2* __r
     epi.finish(acc);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Sliced-ELL mapping (MODE 3, built at create by sell.cu): one warp per slice of 32 consecutive
+// rows, lane = row.  The slice's entries are stored column-major (entry k of the slice's rows at
+// k·32 + lane), so every value / column load instruction of a warp reads 512 / 128 contiguous
+// bytes, the gathers of x for neighbouring rows are adjacent, and the epilogue runs on all 32
+// lanes with coalesced loads and stores.  Each lane sums its row's entries in stored order (the
+// oracle's order).  U entries per lane are in flight per step; padding (col −1) is skipped.
+#ifndef ZK_SELL_U
+#define ZK_SELL_U 9
+#endif
+template <class Epi, int LP = ZK_DEFAULT_LP>
+__device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
+    constexpr int U = ZK_SELL_U;
+    constexpr int KA = Epi::K > 0 ? Epi::K : 1;
+    constexpr bool AHEAD = pre_ahead<Epi>::value;
+    const uint64_t pol = make_policy<LP>();
+    double acc[KA];
+#pragma unroll
+    for (int k = 0; k < KA; k++) acc[k] = 0.0;
+    const int lane = threadIdx.x & 31;
+    const int n = (int)A.n_rows;
+    const int n_sl = (n + 31) >> 5;
+    const int nw = gridDim.x * kWarps;
+    int s = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    int64_t base = 0;
+    int width = 0;
+    typename Epi::Pre pre{};
+    if (s < n_sl) {
+        base = __ldg(A.sl_ptr + s);
+        width = (int)((__ldg(A.sl_ptr + s + 1) - base) >> 5);
+        if (AHEAD && s * 32 + lane < n) pre = epi.pre(s * 32 + lane);
+    }
+    for (; s < n_sl; s += nw) {
+        const int row = s * 32 + lane;
+        const int ns = s + nw;  // next slice: bounds and epilogue operands one step ahead
+        int64_t nbase = 0;
+        int nwidth = 0;
+        typename Epi::Pre npre{};
+        if (!AHEAD && row < n) pre = epi.pre(row);
+        if (ns < n_sl) {
+            nbase = __ldg(A.sl_ptr + ns);
+            nwidth = (int)((__ldg(A.sl_ptr + ns + 1) - nbase) >> 5);
+            if (AHEAD && ns * 32 + lane < n) npre = epi.pre(ns * 32 + lane);
+        }
+        const double2* vr = A.sl_val + base + lane;
+        const int* cr = A.sl_col + base + lane;
+        double2 sum = make_double2(0.0, 0.0);
+        for (int k0 = 0; k0 < width; k0 += U) {
+            double2 v[U];
+            int c[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (k0 + u < width) {
+                    v[u] = ld_mat<LP>(vr + (k0 + u) * 32, pol);
+                    c[u] = ld_mat<LP>(cr + (k0 + u) * 32, pol);
+                } else {
+                    v[u] = make_double2(0.0, 0.0);
+                    c[u] = -1;
+                }
+            }
+            double2 xv[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather(x + c[u]) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (c[u] >= 0) cfma(sum, v[u], xv[u]);
+        }
+        if (row < n) epi.row(row, sum, pre, acc);
+        base = nbase;
+        width = nwidth;
+        if (AHEAD) pre = npre;
+    }
+    epi.finish(acc);
+}
+
 // Grid-stride elementwise body with U elements in flight per thread.
 //   Op::K, Op::In, In load(int64_t i), void apply(int64_t i, const In&, double (&acc)[K]), finish(acc)
 template <class Op>

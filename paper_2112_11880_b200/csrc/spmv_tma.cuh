@@ -251,6 +251,8 @@ __device__ __forceinline__ void spmv_any(const CsrDev& A, const TmaPlan& T, cons
         spmv_tma_body<W>(A, T, x, epi);
     } else if constexpr (MODE == 2) {
         spmv_body_b4<W>(A, x, epi);
+    } else if constexpr (MODE == 3) {
+        spmv_body_sell(A, x, epi);
     } else {
         spmv_body<W>(A, x, epi);
     }
@@ -267,5 +269,10 @@ namespace zk {
 #ifndef ZK_SPMV_MINB
 #define ZK_SPMV_MINB 4
 #endif
-__host__ __device__ constexpr int spmv_min_blocks(int mode) { return mode == 1 ? ZK_TMA_MINB : ZK_SPMV_MINB; }
+#ifndef ZK_SELL_MINB
+#define ZK_SELL_MINB 3  // 80 registers: U = 9 entries in flight per lane without spilling (C4: 647 vs 869 µs at 64)
+#endif
+__host__ __device__ constexpr int spmv_min_blocks(int mode) {
+    return mode == 1 ? ZK_TMA_MINB : mode == 3 ? ZK_SELL_MINB : ZK_SPMV_MINB;
+}
 }  // namespace zk

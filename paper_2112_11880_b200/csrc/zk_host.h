@@ -56,12 +56,18 @@ struct zk_csr_s {
     double2* val = nullptr;      // device
     bool owned = false;
     int W = 8;                   // SpMV lanes per row
-    int spmv_mode = 0;           // 0 = sub-warp kernel (spmv.cuh), 1 = TMA-staged tiles (spmv_tma.cuh)
+    int spmv_mode = 0;           // 0 sub-warp CSR (spmv.cuh), 1 TMA-staged tiles, 2 blocked-4, 3 sliced ELL (sell.cu)
     zk::TmaPlan tma{};
     // Jacobi right preconditioning (jacobi.cu), built on the first ZK_BICGSTAB_JACOBI solve
     double2* jac_val = nullptr;   // a_ij / a_jj
     double2* jac_diag = nullptr;  // a_ii
     double2* jac_dinv = nullptr;  // 1 / a_ii
+    double2* jac_sl_val = nullptr;  // A·M⁻¹ in the sliced-ELL layout (SpMV mode 3)
+    // sliced-ELL (SELL-32) copy of the matrix, SpMV mode 3 (sell.cu)
+    int64_t* sl_ptr = nullptr;
+    int* sl_col = nullptr;
+    double2* sl_val = nullptr;
+    int64_t n_slices = 0, sl_nnz = 0;
     int max_len = 0;
     double mean_len = 0.0;
     zk::DeviceInfo dev;
@@ -80,6 +86,7 @@ namespace zk {
 template <class F>
 zk_status with_spmv(const zk_csr_s* A, F&& f) {
     using std::integral_constant;
+    if (A->spmv_mode == 3) return f(integral_constant<int, 32>{}, integral_constant<int, 3>{});
     if (A->spmv_mode == 2) {
         switch (A->W) {
             case 4: return f(integral_constant<int, 4>{}, integral_constant<int, 2>{});
@@ -104,7 +111,7 @@ zk_status with_spmv(const zk_csr_s* A, F&& f) {
 }
 
 inline CsrDev csr_dev(const zk_csr_s* A) {
-    return CsrDev{A->row_ptr, A->col, A->val, A->n_rows, A->nnz};
+    return CsrDev{A->row_ptr, A->col, A->val, A->n_rows, A->nnz, A->sl_ptr, A->sl_col, A->sl_val};
 }
 
 struct LaunchCfg {
@@ -122,6 +129,7 @@ inline LaunchCfg spmv_cfg(const zk_csr_s* A, const void* kernel, int W, int mode
     }
     int cap = A->dev.num_sms * blocks_per_sm(kernel, 0);
     if (cap > kMaxGrid) cap = kMaxGrid;
+    if (mode == 3) return {grid_for(A->n_slices, kWarps, cap), 0};  // one warp per 32-row slice
     return {grid_for(A->n_rows, kBlock / W, cap), 0};
 }
 }  // namespace zk

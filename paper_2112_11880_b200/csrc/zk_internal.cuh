@@ -185,6 +185,11 @@ struct CsrDev {
     const double2* val;
     int64_t n_rows;
     int64_t nnz;
+    // sliced-ELL copy (SpMV mode 3, sell.cu): slice s of 32 rows holds its entries column-major at
+    // [sl_ptr[s], sl_ptr[s+1]), width = (sl_ptr[s+1] − sl_ptr[s]) / 32; padding has col −1, val 0
+    const int64_t* sl_ptr;
+    const int* sl_col;
+    const double2* sl_val;
 };
 
 }  // namespace zk

@@ -52,7 +52,7 @@ class zk_csr_info_t(ctypes.Structure):
                 ("max_row_len", ctypes.c_int32), ("lanes_per_row", ctypes.c_int32),
                 ("mean_row_len", ctypes.c_double), ("n_halo", ctypes.c_int64),
                 ("borrowed", ctypes.c_int32), ("nranks", ctypes.c_int32), ("spmv_mode", ctypes.c_int32),
-                ("rows_per_tile", ctypes.c_int32), ("tma_stages", ctypes.c_int32)]
+                ("rows_per_tile", ctypes.c_int32), ("tma_stages", ctypes.c_int32), ("sell_entries", ctypes.c_int64)]
 
 
 class zk_solve_info(ctypes.Structure):

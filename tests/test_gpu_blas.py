@@ -31,8 +31,8 @@ def row_scale(m, x):
 
 MAPPINGS = [(0, 2, None), (0, 4, None), (0, 8, None), (0, 16, None), (0, 32, None),
             (1, 4, None), (1, 8, None), (1, 16, None), (1, 8, (2, 700)), (1, 4, (4, 640)),
-            (2, 4, None), (2, 8, None), (2, 16, None)]
-MAP_NAMES = {0: "subwarp", 1: "tma", 2: "blocked4"}
+            (2, 4, None), (2, 8, None), (2, 16, None), (3, 32, None)]
+MAP_NAMES = {0: "subwarp", 1: "tma", 2: "blocked4", 3: "sell32"}
 MAP_IDS = [f"{MAP_NAMES[m]}-W{w}" + (f"-S{c[0]}-nnz{c[1]}" if c else "") for m, w, c in MAPPINGS]
 
 
@@ -85,9 +85,10 @@ def test_zcsrmv_integer_exact_bitwise(mapping):
     assert np.array_equal(y.cpu().numpy(), oracle.zcsrmv(m, x))
 
 
-def test_blocked_mapping_alignment_fallback_and_tail():
+def test_blocked_mapping_alignment_fallback_and_tail(monkeypatch):
     """The blocked-4 mapping needs 32-B aligned values: a borrowed, misaligned value array falls
     back to the sub-warp mapping; nnz % 4 != 0 exercises the element-wise final block."""
+    monkeypatch.setenv("ZK_SPMV_MODE", "2")
     m = gen.random_csr(2001, seed=21, max_len=30)
     assert m["nnz"] % 4 != 0
     x = gen.rand_vector(2001, 3)
@@ -117,7 +118,7 @@ def test_zcsrmv_beta_zero_ignores_nan_and_empty_rows():
     assert np.all(got[np.diff(m["row_ptr"]) == 0] == 0)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C3T"])
 def test_zcsrmv_paper_shapes(cfg, mode):
     m = gen.make_matrix(cfg)
@@ -132,9 +133,11 @@ def test_zcsrmv_paper_shapes(cfg, mode):
     assert np.array_equal(got[ident], want[ident])
 
 
-def test_zcsrmv_c4_full_size_sampled():
+@pytest.mark.parametrize("mode", ["0", "3"])
+def test_zcsrmv_c4_full_size_sampled(mode, monkeypatch):
     """C4 (8M rows, 214M nnz) in the bench's launch configuration: sampled rows against the
     oracle computed row by row, and the closed-form eigenvector identity A·v = λ·v on all rows."""
+    monkeypatch.setenv("ZK_SPMV_MODE", mode)
     spec = gen.CONFIGS["C4"]
     m = gen.make_matrix(spec)
     n = m["n"]

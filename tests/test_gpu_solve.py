@@ -40,7 +40,7 @@ def relerr(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-@pytest.mark.parametrize("spmv_mode", ["0", "1", "2"])
+@pytest.mark.parametrize("spmv_mode", ["0", "1", "2", "3"])
 @pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
 def test_bicgstab_parity(cfg, spmv_mode, monkeypatch):
     monkeypatch.setenv("ZK_SPMV_MODE", spmv_mode)
@@ -58,7 +58,7 @@ def test_bicgstab_parity(cfg, spmv_mode, monkeypatch):
     assert r["loop_mode"] == 1                          # device-resident WHILE graph
 
 
-@pytest.mark.parametrize("spmv_mode", ["0", "1", "2"])
+@pytest.mark.parametrize("spmv_mode", ["0", "1", "2", "3"])
 @pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
 def test_cg_parity_twisted_hpd(cfg, spmv_mode, monkeypatch):
     monkeypatch.setenv("ZK_SPMV_MODE", spmv_mode)

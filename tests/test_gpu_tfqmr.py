@@ -45,7 +45,7 @@ def diag(n, c):
                 values=np.full(n, c, np.complex128), n=n)
 
 
-@pytest.mark.parametrize("spmv_mode", ["0", "1", "2"])
+@pytest.mark.parametrize("spmv_mode", ["0", "1", "2", "3"])
 @pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
 def test_tfqmr_parity(cfg, spmv_mode, monkeypatch):
     monkeypatch.setenv("ZK_SPMV_MODE", spmv_mode)
