@@ -57,7 +57,8 @@ enum {
 enum {
     ZK_PTRS_HOST = 0,          /* arrays are host memory: copied to the device (H2D inside the call) */
     ZK_PTRS_DEVICE = 1,        /* arrays are device memory: copied device-to-device */
-    ZK_PTRS_DEVICE_BORROW = 2, /* arrays are device memory and are used in place; they must outlive A */
+    ZK_PTRS_DEVICE_BORROW = 2, /* arrays are device memory and are used in place; they must outlive A (the
+                                  SpMV may also keep a library-owned sliced-ELL copy, see spmv_mode) */
     ZK_SKIP_VALIDATE = 4       /* trust the input (no validation pass) */
 };
 

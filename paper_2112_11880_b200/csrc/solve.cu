@@ -751,6 +751,7 @@ struct OpT1Tfqmr {  // y2 = y1 − α v ; w −= α u1 ; {‖w‖²}
 struct EpiT2Tfqmr {  // u2 = A y2 ; w −= α u2 ; {‖w‖², ⟨r̃, w⟩}
     static constexpr int K = 3;
     static constexpr bool kAhead = ZK_TF_AHEAD;
+    static constexpr int kPrePlace = 2;  // SELL: after the row sums (T2+T4 489 vs 547 ms on C4)
     struct Pre { double2 w, rt; };
     SolveCtx* c;
     double2 *__restrict__ u2, *__restrict__ w;
@@ -814,6 +815,7 @@ template <int S>
 struct EpiT4Tfqmr {  // u1 = A y1 ; v = u1 + β(u2 + β v) (first: v = u1) ; {σ = ⟨r̃, v⟩}
     static constexpr int K = 2;
     static constexpr bool kAhead = ZK_TF_AHEAD;
+    static constexpr int kPrePlace = 2;
     struct Pre { double2 u2, v, rt; };
     SolveCtx* c;
     double2 *__restrict__ u1, *__restrict__ v;

@@ -22,9 +22,19 @@ namespace zk {
 //   typename Pre; __device__ Pre pre(int64_t i);   // row i's own operands (loaded a tile ahead)
 //   __device__ void row(int64_t i, double2 y, const Pre&, double (&acc)[K>0?K:1]);   // once per row
 //   __device__ void finish(double (&acc)[K>0?K:1]); // called by every thread at the end
+//   optional static constexpr int kPrePlace;        // SELL kernel: 0 / 1 / 2, see spmv_body_sell
 //   optional static constexpr bool kAhead = false;  // load pre() at the start of the row's own tile
 //                                                   // instead of one tile ahead (wide Pre: one copy
 //                                                   // in registers instead of two)
+#ifndef ZK_SELL_PRE
+#define ZK_SELL_PRE 0
+#endif
+template <class E>
+struct pre_place {
+    template <class T> static constexpr int get(decltype(T::kPrePlace)*) { return T::kPrePlace; }
+    template <class T> static constexpr int get(...) { return ZK_SELL_PRE; }
+    static constexpr int value = get<E>(nullptr);
+};
 template <class E>
 struct pre_ahead {
     template <class T> static constexpr bool get(decltype(T::kAhead)*) { return T::kAhead; }
@@ -219,15 +229,47 @@ __device__ __forceinline__ void spmv_body_b4(const CsrDev& A, const double2* __r
 #ifndef ZK_SELL_U
 #define ZK_SELL_U 9
 #endif
+#ifndef ZK_SELL_PIPE
+#define ZK_SELL_PIPE 0
+#endif
+#ifndef ZK_SELL_SMEM_ACC
+#define ZK_SELL_SMEM_ACC 0
+#endif
+// ZK_SELL_VGATHER: gathers as volatile asm, so they stay behind ALL the batch's matrix loads in
+// program order (the compiler otherwise interleaves load column → wait → gather per entry)
+#ifndef ZK_SELL_VGATHER
+#define ZK_SELL_VGATHER 0
+#endif
+__device__ __forceinline__ double2 ld_gather_ord(const double2* p) {
+#if ZK_SELL_VGATHER
+    double2 v;
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+#else
+    return ld_gather(p);
+#endif
+}
 template <class Epi, int LP = ZK_DEFAULT_LP>
 __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
     constexpr int U = ZK_SELL_U;
     constexpr int KA = Epi::K > 0 ? Epi::K : 1;
-    constexpr bool AHEAD = pre_ahead<Epi>::value;
+    // where the epilogue's row operands are loaded: 0 one slice ahead (registers held across the
+    // whole slice), 1 with the slice's last batch of matrix loads, 2 after the row sums.  Per
+    // epilogue (Epi::kPrePlace): wide epilogues (TFQMR T2/T4: 2-3 operands) measured faster at 2,
+    // the one-operand BiCGStab epilogues at 0 (profiles/r01_sell.md)
+    constexpr int PRE = pre_place<Epi>::value;
+    constexpr bool AHEAD = PRE == 0 && pre_ahead<Epi>::value;
     const uint64_t pol = make_policy<LP>();
     double acc[KA];
 #pragma unroll
     for (int k = 0; k < KA; k++) acc[k] = 0.0;
+#if ZK_SELL_SMEM_ACC
+    // the epilogue's running sums live in per-thread shared-memory slots, not in registers held
+    // across the whole kernel (the row loop runs at the 80-register cap)
+    __shared__ double sacc[KA][kBlock];
+#pragma unroll
+    for (int k = 0; k < KA; k++) sacc[k][threadIdx.x] = 0.0;
+#endif
     const int lane = threadIdx.x & 31;
     const int n = (int)A.n_rows;
     const int n_sl = (n + 31) >> 5;
@@ -247,7 +289,7 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
         int64_t nbase = 0;
         int nwidth = 0;
         typename Epi::Pre npre{};
-        if (!AHEAD && row < n) pre = epi.pre(row);
+        if (PRE == 0 && !AHEAD && row < n) pre = epi.pre(row);
         if (ns < n_sl) {
             nbase = __ldg(A.sl_ptr + ns);
             nwidth = (int)((__ldg(A.sl_ptr + ns + 1) - nbase) >> 5);
@@ -256,6 +298,47 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
         const double2* vr = A.sl_val + base + lane;
         const int* cr = A.sl_col + base + lane;
         double2 sum = make_double2(0.0, 0.0);
+#if ZK_SELL_PIPE
+        // one batch of lookahead: the (value, column) loads of batch k0 + U are issued before the
+        // gathers of batch k0 wait, so the matrix stream's DRAM latency hides behind the gathers'
+        double2 v[U];
+        int c[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (u < width) {
+                v[u] = ld_mat<LP>(vr + u * 32, pol);
+                c[u] = ld_mat<LP>(cr + u * 32, pol);
+            } else {
+                v[u] = make_double2(0.0, 0.0);
+                c[u] = -1;
+            }
+        }
+        for (int k0 = 0; k0 < width; k0 += U) {
+            double2 nv[U];
+            int nc[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (k0 + U + u < width) {
+                    nv[u] = ld_mat<LP>(vr + (k0 + U + u) * 32, pol);
+                    nc[u] = ld_mat<LP>(cr + (k0 + U + u) * 32, pol);
+                } else {
+                    nv[u] = make_double2(0.0, 0.0);
+                    nc[u] = -1;
+                }
+            }
+            double2 xv[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather_ord(x + c[u]) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (c[u] >= 0) cfma(sum, v[u], xv[u]);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                v[u] = nv[u];
+                c[u] = nc[u];
+            }
+        }
+#else
         for (int k0 = 0; k0 < width; k0 += U) {
             double2 v[U];
             int c[U];
@@ -269,18 +352,37 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
                     c[u] = -1;
                 }
             }
+            if (PRE == 1 && k0 + U >= width && row < n) pre = epi.pre(row);
             double2 xv[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather(x + c[u]) : make_double2(0.0, 0.0);
+            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather_ord(x + c[u]) : make_double2(0.0, 0.0);
 #pragma unroll
             for (int u = 0; u < U; u++)
                 if (c[u] >= 0) cfma(sum, v[u], xv[u]);
         }
+#endif
+        if (PRE == 1 && width == 0 && row < n) pre = epi.pre(row);
+        if (PRE == 2 && row < n) pre = epi.pre(row);
+#if ZK_SELL_SMEM_ACC
+        if (row < n) {
+            double racc[KA];
+#pragma unroll
+            for (int k = 0; k < KA; k++) racc[k] = sacc[k][threadIdx.x];
+            epi.row(row, sum, pre, racc);
+#pragma unroll
+            for (int k = 0; k < KA; k++) sacc[k][threadIdx.x] = racc[k];
+        }
+#else
         if (row < n) epi.row(row, sum, pre, acc);
+#endif
         base = nbase;
         width = nwidth;
         if (AHEAD) pre = npre;
     }
+#if ZK_SELL_SMEM_ACC
+#pragma unroll
+    for (int k = 0; k < KA; k++) acc[k] = sacc[k][threadIdx.x];
+#endif
     epi.finish(acc);
 }
 

@@ -1,7 +1,7 @@
 #!/bin/bash
 # microbench.py spmv for each lib in $LIBS with maps $MAPS, printing lib, map, µs, GB/s only
 for L in $LIBS; do
-  ZK_LIB=$L python tools/microbench.py spmv --config ${CFG:-C4} --maps ${MAPS:-0:4,3:32} --reps ${REPS:-30} 2>/dev/null |
+  ZK_LIB=$L python tools/microbench.py spmv --config ${CFG:-C4} --maps ${MAPS:-0:4,3:32} --reps ${REPS:-30} --beta ${BETA:-0} 2>/dev/null |
   python3 -c "
 import sys, json
 for l in sys.stdin:

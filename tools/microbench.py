@@ -58,8 +58,8 @@ def spmv(a):
             os.environ.pop(k, None)
         os.environ.update(env)
         A = zk.csr_create(rp, ci, va, n, borrow=True)
-        us = timeit(lambda: zk.zcsrmv(A, 1.0, x, 0.0, y), a.reps)
-        gbs = M.spmv_bytes(n, nnz) / (us * 1e-6) / 1e9
+        us = timeit(lambda: zk.zcsrmv(A, 1.0, x, a.beta, y), a.reps)
+        gbs = M.spmv_bytes(n, nnz, a.beta != 0) / (us * 1e-6) / 1e9
         print(json.dumps({"kernel": "zcsrmv", "config": a.config, "map": spec, "info": A.info, "us": us,
                           "gbs": gbs, "gflops": M.spmv_flops(nnz) / (us * 1e-6) / 1e9}), flush=True)
         A.close()
@@ -111,6 +111,7 @@ if __name__ == "__main__":
     p.add_argument("--config", default="C4")
     p.add_argument("--maps", default="0:8,1:4,1:8,1:16,1:8:2:1792,1:8:4:1792,1:8:2:896,1:8:4:896,1:8:3:896,1:4:3:3584,1:8:2:3584")
     p.add_argument("--reps", type=int, default=50)
+    p.add_argument("--beta", type=float, default=0.0)
     p.add_argument("--n", type=int, default=1 << 28)
     a = p.parse_args()
     {"spmv": spmv, "blas1": blas1, "ncu-spmv": ncu_spmv, "solve": solve}[a.what](a)
