@@ -279,7 +279,10 @@ def main():
     spmv = {"us": spmv_us, "gbs": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9,
             "gflops": M.spmv_flops(nnz) / (spmv_us * 1e-6) / 1e9,
             "frac_of_peak": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9 / peak,
-            "lanes_per_row": A.info["lanes_per_row"]}
+            "lanes_per_row": A.info["lanes_per_row"],
+            "mapping": {0: "CSR sub-warp", 1: "CSR TMA-staged", 2: "CSR blocked-4",
+                        3: "sliced ELL (SELL-32 device copy)"}[A.info["spmv_mode"]],
+            "stored_entries": A.info["sell_entries"] or nnz}
 
     # the paper's own matrix shapes (PAPER.md T1; latency-bound on B200): BiCGStab per iteration
     shapes = None

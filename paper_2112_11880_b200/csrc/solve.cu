@@ -484,6 +484,70 @@ struct EpiK3Bicg {  // t = A s ; {⟨t, s⟩, ⟨t, t⟩}
     __device__ void finish(double (&acc)[3]) { reduce_finish<S_K3_BICG, 3>(c, acc); }
 };
 
+// Split reductions (large systems): the SpMV of BiCGStab K1/K3 and CG/COCG K1 only stores its
+// product and a following vector pass (r1/r3/rq) forms the dot products.  The fused epilogue's
+// operand load and running sums cost the SELL kernel ≈ 140 µs per launch on C4 (its batch of 18
+// matrix loads gets interleaved with the gathers at the 80-register cap), the extra pass over
+// two vectors ≈ 40 µs: BiCGStab 1.83 vs 1.90 ms per iteration.  Below kSplitRows the two extra
+// launches per iteration cost more than they save (latency-bound sizes), so the fused kernels stay.
+constexpr int64_t kSplitRows = 1 << 20;
+struct EpiStore {  // out = A x
+    static constexpr int K = 0;
+    using Pre = double2;
+    double2* __restrict__ out;
+    __device__ explicit EpiStore(double2* o) : out(o) {}
+    __device__ Pre pre(int64_t) const { return make_double2(0.0, 0.0); }
+    __device__ void row(int64_t i, double2 y, const Pre&, double (&)[1]) { out[i] = y; }
+    __device__ void finish(double (&)[1]) {}
+};
+struct OpRed1Bicg {  // {⟨r̂, v⟩, ‖v‖²}
+    static constexpr int K = 3;
+    struct In { double2 r, v; };
+    SolveCtx* c;
+    const double2 *__restrict__ rh, *__restrict__ v;
+    __device__ explicit OpRed1Bicg(SolveCtx* c_) : c(c_), rh(c_->rh), v(c_->v) {}
+    __device__ In load(int64_t i) const { return {ld_vec(rh + i), ld_vec(v + i)}; }
+    __device__ void apply(int64_t, const In& in, double (&acc)[3]) const {
+        acc[0] = fma(in.r.x, in.v.x, fma(in.r.y, in.v.y, acc[0]));
+        acc[1] = fma(in.r.x, in.v.y, fma(-in.r.y, in.v.x, acc[1]));
+        acc[2] += cabs2(in.v);
+    }
+    __device__ void finish(double (&acc)[3]) const { reduce_finish<S_K1_BICG, 3>(c, acc); }
+};
+template <bool CONJ, int S>
+struct OpRedPq {  // {⟨p, q⟩} (CG, CONJ) or {pᵀq} (COCG)
+    static constexpr int K = 2;
+    struct In { double2 p, q; };
+    SolveCtx* c;
+    const double2 *__restrict__ p, *__restrict__ q;
+    __device__ explicit OpRedPq(SolveCtx* c_) : c(c_), p(c_->p), q(c_->q) {}
+    __device__ In load(int64_t i) const { return {ld_vec(p + i), ld_vec(q + i)}; }
+    __device__ void apply(int64_t, const In& in, double (&acc)[2]) const {
+        if (CONJ) {
+            acc[0] = fma(in.p.x, in.q.x, fma(in.p.y, in.q.y, acc[0]));
+            acc[1] = fma(in.p.x, in.q.y, fma(-in.p.y, in.q.x, acc[1]));
+        } else {
+            acc[0] = fma(in.p.x, in.q.x, fma(-in.p.y, in.q.y, acc[0]));
+            acc[1] = fma(in.p.x, in.q.y, fma(in.p.y, in.q.x, acc[1]));
+        }
+    }
+    __device__ void finish(double (&acc)[2]) const { reduce_finish<S, 2>(c, acc); }
+};
+struct OpRed3Bicg {  // {⟨t, s⟩, ‖t‖²}
+    static constexpr int K = 3;
+    struct In { double2 t, s; };
+    SolveCtx* c;
+    const double2 *__restrict__ t, *__restrict__ s;
+    __device__ explicit OpRed3Bicg(SolveCtx* c_) : c(c_), t(c_->t), s(c_->s) {}
+    __device__ In load(int64_t i) const { return {ld_vec(t + i), ld_vec(s + i)}; }
+    __device__ void apply(int64_t, const In& in, double (&acc)[3]) const {
+        acc[0] = fma(in.t.x, in.s.x, fma(in.t.y, in.s.y, acc[0]));
+        acc[1] = fma(in.t.x, in.s.y, fma(-in.t.y, in.s.x, acc[1]));
+        acc[2] += cabs2(in.t);
+    }
+    __device__ void finish(double (&acc)[3]) const { reduce_finish<S_K3_BICG, 3>(c, acc); }
+};
+
 struct EpiK1Cg {  // q = A p ; {δ = ⟨p, q⟩}
     static constexpr int K = 2;
     using Pre = double2;
@@ -811,6 +875,50 @@ struct OpT3Tfqmr {
     __device__ void finish(double (&)[1]) const {}
 };
 
+// split schedule (large systems): T2/T4 store A·y only, these passes do the rest
+struct OpT2bTfqmr {  // w −= α u2 ; {‖w‖², ⟨r̃, w⟩}
+    static constexpr int K = 3;
+    static constexpr int U = 2;
+    struct In { double2 w, u2, rt; };
+    SolveCtx* c;
+    double2* __restrict__ w;
+    const double2 *__restrict__ u2, *__restrict__ rt;
+    double2 alpha;
+    __device__ explicit OpT2bTfqmr(SolveCtx* c_) : c(c_), w(c_->w), u2(c_->u2), rt(c_->rt), alpha(c_->alpha) {}
+    __device__ In load(int64_t i) const { return {ld_vec(w + i), ld_vec(u2 + i), ld_vec(rt + i)}; }
+    __device__ void apply(int64_t i, const In& in, double (&acc)[3]) const {
+        double2 wn = in.w;
+        wn.x = fma(-alpha.x, in.u2.x, fma(alpha.y, in.u2.y, wn.x));
+        wn.y = fma(-alpha.x, in.u2.y, fma(-alpha.y, in.u2.x, wn.y));
+        w[i] = wn;
+        acc[0] += cabs2(wn);
+        acc[1] = fma(in.rt.x, wn.x, fma(in.rt.y, wn.y, acc[1]));
+        acc[2] = fma(in.rt.x, wn.y, fma(-in.rt.y, wn.x, acc[2]));
+    }
+    __device__ void finish(double (&acc)[3]) const { reduce_finish<S_T2_TFQMR, 3>(c, acc); }
+};
+struct OpT4bTfqmr {  // v = u1 + β(u2 + β v) ; {σ = ⟨r̃, v⟩}
+    static constexpr int K = 2;
+    static constexpr int U = 1;
+    struct In { double2 u1, u2, v, rt; };
+    SolveCtx* c;
+    double2* __restrict__ v;
+    const double2 *__restrict__ u1, *__restrict__ u2, *__restrict__ rt;
+    double2 beta;
+    __device__ explicit OpT4bTfqmr(SolveCtx* c_) : c(c_), v(c_->v), u1(c_->u1), u2(c_->u2), rt(c_->rt), beta(c_->beta) {}
+    __device__ In load(int64_t i) const { return {ld_vec(u1 + i), ld_vec(u2 + i), ld_vec(v + i), ld_vec(rt + i)}; }
+    __device__ void apply(int64_t i, const In& in, double (&acc)[2]) const {
+        double2 t = in.u2;
+        cfma(t, beta, in.v);
+        double2 vn = in.u1;
+        cfma(vn, beta, t);
+        v[i] = vn;
+        acc[0] = fma(in.rt.x, vn.x, fma(in.rt.y, vn.y, acc[0]));
+        acc[1] = fma(in.rt.x, vn.y, fma(-in.rt.y, vn.x, acc[1]));
+    }
+    __device__ void finish(double (&acc)[2]) const { reduce_finish<S_T4_TFQMR, 2>(c, acc); }
+};
+
 template <int S>
 struct EpiT4Tfqmr {  // u1 = A y1 ; v = u1 + β(u2 + β v) (first: v = u1) ; {σ = ⟨r̃, v⟩}
     static constexpr int K = 2;
@@ -871,16 +979,33 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_true(SolveCtx
     EpiTrue e(c);
     spmv_any<W, MODE>(A, T, xg, e);
 }
-template <int W, int MODE>
-__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_bicg(SolveCtx* c) {
+template <int W, int MODE, bool SP>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_bicg(SolveCtx* c, const CsrDev A) {
+    constexpr bool SPLIT = SP;  // products only; r1_bicg reduces
     pdl_enter();
     if (c->done) return;
     stamp_start<S_K1_BICG>(c);
-    const CsrDev A = c->A;
     const TmaPlan T = c->T;
     const double2* p = c->p;
-    EpiK1Bicg e(c);
-    spmv_any<W, MODE>(A, T, p, e);
+    if constexpr (SPLIT) {
+        EpiStore e(c->v);
+        spmv_any<W, MODE>(A, T, p, e);
+    } else {
+        EpiK1Bicg e(c);
+        spmv_any<W, MODE>(A, T, p, e);
+    }
+}
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) r1_bicg(SolveCtx* c) {
+    pdl_enter();
+    if (c->done) return;
+    OpRed1Bicg op(c);
+    vec_body(c->A.n_rows, op);
+}
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) r3_bicg(SolveCtx* c) {
+    pdl_enter();
+    if (c->done) return;
+    OpRed3Bicg op(c);
+    vec_body(c->A.n_rows, op);
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_bicg(SolveCtx* c) {
     pdl_enter();
@@ -889,16 +1014,20 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_bicg(SolveCtx* c) {
     OpK2Bicg op(c);
     vec_body(c->A.n_rows, op);
 }
-template <int W, int MODE>
-__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k3_bicg(SolveCtx* c) {
+template <int W, int MODE, bool SPLIT>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k3_bicg(SolveCtx* c, const CsrDev A) {
     pdl_enter();
     if (c->done) return;
     stamp_start<S_K3_BICG>(c);
-    const CsrDev A = c->A;
     const TmaPlan T = c->T;
     const double2* s = c->s;
-    EpiK3Bicg e(c);
-    spmv_any<W, MODE>(A, T, s, e);
+    if constexpr (SPLIT) {
+        EpiStore e(c->t);
+        spmv_any<W, MODE>(A, T, s, e);
+    } else {
+        EpiK3Bicg e(c);
+        spmv_any<W, MODE>(A, T, s, e);
+    }
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k4_bicg(SolveCtx* c) {
     pdl_enter();
@@ -918,16 +1047,20 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k5_bicg(SolveCtx* c) {
     }
     set_cond(c);  // after the stream loop: the device-runtime call does not pressure its registers
 }
-template <int W, int MODE>
-__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cocg(SolveCtx* c) {
+template <int W, int MODE, bool SPLIT>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cocg(SolveCtx* c, const CsrDev A) {
     pdl_enter();
     if (c->done) return;
     stamp_start<S_K1_COCG>(c);
-    const CsrDev A = c->A;
     const TmaPlan T = c->T;
     const double2* p = c->p;
-    EpiK1Cocg e(c);
-    spmv_any<W, MODE>(A, T, p, e);
+    if constexpr (SPLIT) {
+        EpiStore e(c->q);
+        spmv_any<W, MODE>(A, T, p, e);
+    } else {
+        EpiK1Cocg e(c);
+        spmv_any<W, MODE>(A, T, p, e);
+    }
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_cocg(SolveCtx* c) {
     pdl_enter();
@@ -944,16 +1077,27 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k3_cocg(SolveCtx* c) {
     }
     set_cond(c);
 }
-template <int W, int MODE>
-__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cg(SolveCtx* c) {
+template <int W, int MODE, bool SPLIT>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cg(SolveCtx* c, const CsrDev A) {
     pdl_enter();
     if (c->done) return;
     stamp_start<S_K1_CG>(c);
-    const CsrDev A = c->A;
     const TmaPlan T = c->T;
     const double2* p = c->p;
-    EpiK1Cg e(c);
-    spmv_any<W, MODE>(A, T, p, e);
+    if constexpr (SPLIT) {
+        EpiStore e(c->q);
+        spmv_any<W, MODE>(A, T, p, e);
+    } else {
+        EpiK1Cg e(c);
+        spmv_any<W, MODE>(A, T, p, e);
+    }
+}
+template <bool CONJ, int S>
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) rq_kernel(SolveCtx* c) {
+    pdl_enter();
+    if (c->done) return;
+    OpRedPq<CONJ, S> op(c);
+    vec_body(c->A.n_rows, op);
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_cg(SolveCtx* c) {
     pdl_enter();
@@ -971,10 +1115,9 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k3_cg(SolveCtx* c) {
     set_cond(c);
 }
 template <int W, int MODE>
-__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k0_tfqmr(SolveCtx* c) {  // u1 = v = A y1, σ
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k0_tfqmr(SolveCtx* c, const CsrDev A) {  // u1 = v = A y1, σ
     if (c->done) return;
     stamp_start<S_K0_TFQMR>(c);
-    const CsrDev A = c->A;
     const TmaPlan T = c->T;
     const double2* y1 = c->y1;
     EpiT4Tfqmr<S_K0_TFQMR> e(c);
@@ -987,8 +1130,8 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t1_tfqmr(SolveCtx* c) {
     OpT1Tfqmr op(c);
     vec_body(c->A.n_rows, op);
 }
-template <int W, int MODE>
-__global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t2_tfqmr(SolveCtx* c) {
+template <int W, int MODE, bool SPLIT>
+__global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t2_tfqmr(SolveCtx* c, const CsrDev A) {
     pdl_enter();
     if (c->done) {
         if (c->half != 1) return;
@@ -1008,11 +1151,31 @@ __global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t2_tfqmr(SolveCtx* c) {
         return;
     }
     stamp_start<S_T2_TFQMR>(c);
-    const CsrDev A = c->A;
     const TmaPlan T = c->T;
     const double2* y2 = c->y2;
-    EpiT2Tfqmr e(c);
-    spmv_any<W, MODE>(A, T, y2, e);
+    if constexpr (SPLIT) {
+        EpiStore e(c->u2);
+        spmv_any<W, MODE>(A, T, y2, e);
+    } else {
+        EpiT2Tfqmr e(c);
+        spmv_any<W, MODE>(A, T, y2, e);
+    }
+}
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t2b_tfqmr(SolveCtx* c) {
+    pdl_enter();
+    if (c->done) return;
+    OpT2bTfqmr op(c);
+    vec_body(c->A.n_rows, op);
+}
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t4b_tfqmr(SolveCtx* c) {
+    pdl_enter();
+    if (c->done) {
+        if (c->half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;
+    } else {
+        OpT4bTfqmr op(c);
+        vec_body(c->A.n_rows, op);
+    }
+    set_cond(c);
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t3_tfqmr(SolveCtx* c) {
     pdl_enter();
@@ -1021,20 +1184,24 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t3_tfqmr(SolveCtx* c) {
     OpT3Tfqmr op(c, done);
     vec_body(c->A.n_rows, op);
 }
-template <int W, int MODE>
-__global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t4_tfqmr(SolveCtx* c) {
+template <int W, int MODE, bool SPLIT>
+__global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t4_tfqmr(SolveCtx* c, const CsrDev A) {
     pdl_enter();
     if (c->done) {
-        if (c->half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;  // T2/T3 applied the last x += η·d
+        if (!SPLIT && c->half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;  // T2/T3 applied the last x update
     } else {
         stamp_start<S_T4_TFQMR>(c);
-        const CsrDev A = c->A;
         const TmaPlan T = c->T;
         const double2* y1 = c->y1;
-        EpiT4Tfqmr<S_T4_TFQMR> e(c);
-        spmv_any<W, MODE>(A, T, y1, e);
+        if constexpr (SPLIT) {
+            EpiStore e(c->u1);
+            spmv_any<W, MODE>(A, T, y1, e);
+        } else {
+            EpiT4Tfqmr<S_T4_TFQMR> e(c);
+            spmv_any<W, MODE>(A, T, y1, e);
+        }
     }
-    set_cond(c);
+    if (!SPLIT) set_cond(c);  // split: t4b_tfqmr is the body's last kernel
 }
 // ------------------------------------------------------------------ BiCGStab(ℓ) kernels (NEXT-3)
 // One outer cycle (oracle_bicgstab_l): for j = 0..ℓ−1 the BiCG step runs as
@@ -1177,25 +1344,47 @@ struct EpiBl {  // out = A v ; {⟨r̃, out⟩, ‖out‖²} when RED
     }
 };
 
-template <int W, int MODE>
-__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) bl_s1(SolveCtx* c, VecSet P, int j) {
+template <int W, int MODE, bool RED>
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) bl_s1(SolveCtx* c, const CsrDev A, VecSet P, int j) {
     pdl_enter();
     if (c->done) return;
-    stamp_start<S_S1_BL>(c);
-    const CsrDev A = c->A;
+    stamp_start<S_S1_BL>(c);  // RED = false (split): bl_r<S_S1_BL> reduces and closes the timer
     const TmaPlan T = c->T;
-    EpiBl<S_S1_BL, true> e(c, P.u[j + 1]);
+    EpiBl<S_S1_BL, RED> e(c, P.u[j + 1]);
     spmv_any<W, MODE>(A, T, P.u[j], e);
 }
 template <int W, int MODE, bool RED>
-__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) bl_s2(SolveCtx* c, VecSet P, int j) {
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) bl_s2(SolveCtx* c, const CsrDev A, VecSet P, int j,
+                                                                    int stamp) {
     pdl_enter();
     if (c->done) return;
-    if (RED) stamp_start<S_S2_BL>(c);
-    const CsrDev A = c->A;
+    if (stamp) stamp_start<S_S2_BL>(c);
     const TmaPlan T = c->T;
     EpiBl<S_S2_BL, RED> e(c, P.r[j + 1]);
     spmv_any<W, MODE>(A, T, P.r[j], e);
+}
+
+template <int S>
+struct OpRedBl {  // {⟨r̃, y⟩, ‖y‖²} of the vector y just produced by S1/S2 (split schedule)
+    static constexpr int K = 3;
+    struct In { double2 r, y; };
+    SolveCtx* c;
+    const double2 *__restrict__ rt, *__restrict__ y;
+    __device__ OpRedBl(SolveCtx* c_, const double2* y_) : c(c_), rt(c_->rh), y(y_) {}
+    __device__ In load(int64_t i) const { return {ld_vec(rt + i), ld_vec(y + i)}; }
+    __device__ void apply(int64_t, const In& in, double (&acc)[3]) const {
+        acc[0] = fma(in.r.x, in.y.x, fma(in.r.y, in.y.y, acc[0]));
+        acc[1] = fma(in.r.x, in.y.y, fma(-in.r.y, in.y.x, acc[1]));
+        acc[2] += cabs2(in.y);
+    }
+    __device__ void finish(double (&acc)[3]) const { reduce_finish<S, 3>(c, acc); }
+};
+template <int S>
+__global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) bl_r(SolveCtx* c, const double2* y) {
+    pdl_enter();
+    if (c->done) return;
+    OpRedBl<S> op(c, y);
+    vec_body(c->A.n_rows, op);
 }
 
 // Gram matrix of r̂_0..ℓ, packed: for a = 0..ℓ: ‖r̂_a‖², then (Re, Im)⟨r̂_a, r̂_b⟩ for b = a+1..ℓ.
@@ -1506,6 +1695,11 @@ static zk_status dist_finish(const zk_csr_s* A, SolveCtx* c, int count, cudaStre
     return ZK_OK;
 }
 
+static bool split_reductions(const zk_csr_s* A) {
+    if (const char* e = getenv("ZK_SPLIT_RED")) return atoi(e) != 0;
+    return A->n_rows >= kSplitRows;
+}
+
 // enqueue one iteration of `method`
 // loop-kernel launch, with the PDL attribute when `pdl`
 template <class... Args>
@@ -1529,16 +1723,35 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
                                    bool pdl = false) {
     const bool dist = A->dist != nullptr;
     if (dist) pdl = false;
+    const bool split = split_reductions(A);
     return with_spmv(A, [&](auto wc, auto mc) -> zk_status {
         constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
         if (method == ZK_BICGSTAB) {
             if (dist) ZK_TRY(dist_halo(A, hc.p, s));
-            { auto kf = k1_bicg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
+            if (split) {
+                auto kf = k1_bicg<W, MODE, true>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+                ZK_TRY(launch_loop(pdl, r1_bicg, vec_grid(A, (const void*)r1_bicg), 0, s, dc));
+            } else {
+                auto kf = k1_bicg<W, MODE, false>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+            }
             if (dist) ZK_TRY((dist_finish<S_K1_BICG>(A, dc, 3, s)));
             ZK_TRY(launch_loop(pdl, k2_bicg, vec_grid(A, (const void*)k2_bicg), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_K2_BICG>(A, dc, 1, s)));
             if (dist) ZK_TRY(dist_halo(A, hc.s, s));
-            { auto kf = k3_bicg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
+            if (split) {
+                auto kf = k3_bicg<W, MODE, true>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+                ZK_TRY(launch_loop(pdl, r3_bicg, vec_grid(A, (const void*)r3_bicg), 0, s, dc));
+            } else {
+                auto kf = k3_bicg<W, MODE, false>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+            }
             if (dist) ZK_TRY((dist_finish<S_K3_BICG>(A, dc, 3, s)));
             ZK_TRY(launch_loop(pdl, k4_bicg, vec_grid(A, (const void*)k4_bicg), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_K4_BICG>(A, dc, 3, s)));
@@ -1552,16 +1765,30 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             for (int q = hc.ell + 1; q <= kMaxEll; q++) P.r[q] = P.u[q] = nullptr;
             for (int j = 0; j < hc.ell; j++) {
                 ZK_TRY(launch_loop(pdl, bl_b1, vec_grid(A, (const void*)bl_b1), 0, s, dc, P, j));
-                { auto kf = bl_s1<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, P, j)); }
+                if (split) {
+                    auto kf = bl_s1<W, MODE, false>;
+                    const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                    ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A, P, j));
+                    auto kr = bl_r<S_S1_BL>;
+                    ZK_TRY(launch_loop(pdl, kr, vec_grid(A, (const void*)kr), 0, s, dc, (const double2*)P.u[j + 1]));
+                } else {
+                    auto kf = bl_s1<W, MODE, true>;
+                    const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                    ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A, P, j));
+                }
                 ZK_TRY(launch_loop(pdl, bl_b2, vec_grid(A, (const void*)bl_b2), 0, s, dc, P, j));
-                if (j < hc.ell - 1) {
+                if (j < hc.ell - 1 && !split) {
                     auto kf = bl_s2<W, MODE, true>;
                     const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
-                    ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, P, j));
+                    ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A, P, j, 1));
                 } else {
                     auto kf = bl_s2<W, MODE, false>;
                     const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
-                    ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, P, j));
+                    ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A, P, j, j < hc.ell - 1 ? 1 : 0));
+                    if (j < hc.ell - 1) {
+                        auto kr = bl_r<S_S2_BL>;
+                        ZK_TRY(launch_loop(pdl, kr, vec_grid(A, (const void*)kr), 0, s, dc, (const double2*)P.r[j + 1]));
+                    }
                 }
             }
             const BlKernel kg = bl_gram_of(hc.ell);
@@ -1575,22 +1802,60 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             ZK_TRY(launch_loop(pdl, t1_tfqmr, vec_grid(A, (const void*)t1_tfqmr), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_T1_TFQMR>(A, dc, 1, s)));
             if (dist) ZK_TRY(dist_halo(A, hc.y2, s));
-            { auto kf = t2_tfqmr<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
+            if (split) {
+                auto kf = t2_tfqmr<W, MODE, true>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+                ZK_TRY(launch_loop(pdl, t2b_tfqmr, vec_grid(A, (const void*)t2b_tfqmr), 0, s, dc));
+            } else {
+                auto kf = t2_tfqmr<W, MODE, false>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+            }
             if (dist) ZK_TRY((dist_finish<S_T2_TFQMR>(A, dc, 3, s)));
             ZK_TRY(launch_loop(pdl, t3_tfqmr, vec_grid(A, (const void*)t3_tfqmr), 0, s, dc));
             if (dist) ZK_TRY(dist_halo(A, hc.y1, s));
-            { auto kf = t4_tfqmr<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
+            if (split) {
+                auto kf = t4_tfqmr<W, MODE, true>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+                ZK_TRY(launch_loop(pdl, t4b_tfqmr, vec_grid(A, (const void*)t4b_tfqmr), 0, s, dc));
+            } else {
+                auto kf = t4_tfqmr<W, MODE, false>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+            }
             if (dist) ZK_TRY((dist_finish<S_T4_TFQMR>(A, dc, 2, s)));
         } else if (method == ZK_COCG) {
             if (dist) ZK_TRY(dist_halo(A, hc.p, s));
-            { auto kf = k1_cocg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
+            if (split) {
+                auto kf = k1_cocg<W, MODE, true>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+                auto kr = rq_kernel<false, S_K1_COCG>;
+                ZK_TRY(launch_loop(pdl, kr, vec_grid(A, (const void*)kr), 0, s, dc));
+            } else {
+                auto kf = k1_cocg<W, MODE, false>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+            }
             if (dist) ZK_TRY((dist_finish<S_K1_COCG>(A, dc, 2, s)));
             ZK_TRY(launch_loop(pdl, k2_cocg, vec_grid(A, (const void*)k2_cocg), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_K2_COCG>(A, dc, 3, s)));
             ZK_TRY(launch_loop(pdl, k3_cocg, vec_grid(A, (const void*)k3_cocg), 0, s, dc));
         } else {
             if (dist) ZK_TRY(dist_halo(A, hc.p, s));
-            { auto kf = k1_cg<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc)); }
+            if (split) {
+                auto kf = k1_cg<W, MODE, true>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+                auto kr = rq_kernel<true, S_K1_CG>;
+                ZK_TRY(launch_loop(pdl, kr, vec_grid(A, (const void*)kr), 0, s, dc));
+            } else {
+                auto kf = k1_cg<W, MODE, false>;
+                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
+                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+            }
             if (dist) ZK_TRY((dist_finish<S_K1_CG>(A, dc, 2, s)));
             ZK_TRY(launch_loop(pdl, k2_cg, vec_grid(A, (const void*)k2_cg), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_K2_CG>(A, dc, 1, s)));
@@ -1832,7 +2097,9 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     }
     static_assert(kBiCGStabL < (int)(sizeof(((zk_csr_s*)nullptr)->graph) / sizeof(GraphCache)), "graph slot per method");
     GraphCache& gc = A->graph[method];
-    const int gkey = method * 16 + ell;  // BiCGStab(ℓ): one graph per ℓ
+    // one graph per (method, ℓ, Jacobi): the SpMV kernels take the CSR view (A or A·M⁻¹) as a
+    // launch parameter baked into the graph
+    const int gkey = (method * 16 + ell) * 2 + (jacobi ? 1 : 0);
     if (mode <= 2 && (gc.ws != workspace || gc.mode != mode || gc.method != gkey || !gc.exec)) {
         drop_graph(gc);
         const bool pdl = !(getenv("ZK_PDL") && atoi(getenv("ZK_PDL")) == 0);
@@ -1921,7 +2188,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
             constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
             auto k = k0_tfqmr<W, MODE>;
             const LaunchCfg L = spmv_cfg(A, (const void*)k, W, MODE);
-            k<<<L.grid, kBlock, L.smem, s>>>(dc);
+            k<<<L.grid, kBlock, L.smem, s>>>(dc, hc.A);
             ZK_CUDA(cudaGetLastError());
             return ZK_OK;
         }));
@@ -1996,7 +2263,10 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         info->n_spmv = n_spmv;
         info->solve_ms = ms;
         info->loop_mode = mode;
-        const int per_body = method == ZK_BICGSTAB ? 5 : method == ZK_TFQMR ? 4 : method == kBiCGStabL ? 4 * ell + 2 : 3;
+        int per_body = method == ZK_BICGSTAB ? 5 : method == ZK_TFQMR ? 4 : method == kBiCGStabL ? 4 * ell + 2 : 3;
+        if (split_reductions(A) && mode != 4)  // the separate reduction / update passes
+            per_body += method == ZK_BICGSTAB ? 2 : (method == ZK_CG || method == ZK_COCG) ? 1
+                        : method == ZK_TFQMR ? 2 : method == kBiCGStabL ? 2 * ell - 1 : 0;
         const int fins = A->dist ? (method == ZK_BICGSTAB ? 4 : method == ZK_TFQMR ? 3 : 2) : 0;  // dist: 1-thread finish kernels
         const int pre = method == ZK_TFQMR ? (A->dist ? 2 : 1) : 0;                               // TFQMR: K0 (+ its finish)
         info->gpu_launches = mode == 4 ? 4 : 3 + pre + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);

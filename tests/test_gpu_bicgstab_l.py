@@ -160,3 +160,20 @@ def test_bicgstab_l8_c4_full_size():
     assert relerr(r["x"].cpu().numpy(), xe) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
     ref = oracle.bicgstab_l(m, b, tol=1e-8, maxit=1, ell=8)
     assert abs(r["hist"][1] - ref["hist"][1]) / ref["hist"][1] <= 1e-3
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+@pytest.mark.parametrize("ell", [1, 3])
+def test_bicgstab_l_split_schedule(split, ell, monkeypatch):
+    """Both BiCGStab(ℓ) schedules (fused SpMV reductions; split: SpMV stores, a vector pass
+    reduces — the default from 2^20 rows) against the oracle on C2."""
+    monkeypatch.setenv("ZK_SPLIT_RED", split)
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    r = gpu_solve(m, b, ell, tol=1e-8)
+    refs = [oracle.bicgstab_l(m, b, tol=1e-8, ell=ell, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    assert r["status"] == "CONVERGED" and 0.95 * min(its) <= r["iters"] <= 1.05 * max(its)
+    k = min(6, r["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= htol(ell) * 10
+    assert relerr(r["x"], refs[0]["x"]) <= 1e-6

@@ -295,3 +295,21 @@ def test_zassign_zaxmy():
     one_i = cuda(np.array([1j]))
     zk.zaxmy(one_i, one_i)
     assert one_i.cpu().numpy()[0] == -1
+
+
+def test_sell_default_and_padding_fallback(monkeypatch):
+    """The sliced-ELL copy is the default for regular FE rows (C2: 6.5 % padding) and is dropped
+    for irregular rows (random lengths 0-70: padding far above 10 %), falling back to the CSR
+    sub-warp kernel; both give the oracle's product."""
+    monkeypatch.delenv("ZK_SPMV_MODE", raising=False)
+    m = gen.make_matrix("C2")
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+    assert A.info["spmv_mode"] == 3 and m["nnz"] <= A.info["sell_entries"] <= 1.1 * m["nnz"]
+    r = gen.random_csr(4099, seed=5, max_len=70)
+    B = zk.csr_create(r["row_ptr"], r["col_idx"], r["values"], 4099)
+    assert B.info["spmv_mode"] == 0 and B.info["sell_entries"] == 0
+    for mat, M in ((m, A), (r, B)):
+        x = gen.rand_vector(mat["n"], 4)
+        y = torch.empty(mat["n"], dtype=torch.complex128, device=DEV)
+        zk.zcsrmv(M, 1, cuda(x), 0, y)
+        assert np.all(np.abs(y.cpu().numpy() - oracle.zcsrmv(mat, x)) <= 1e-13 * row_scale(mat, x) + 1e-300)

@@ -183,3 +183,23 @@ def test_tfqmr_c4_full_size():
     assert relerr(r["x"].cpu().numpy(), xe) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
     ref = oracle.tfqmr(m, b, tol=1e-8, maxit=3)
     assert np.max(np.abs(r["hist"][:4] - ref["hist"][:4]) / ref["hist"][:4]) <= 1e-10
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_tfqmr_split_schedule(split, monkeypatch):
+    """Both TFQMR schedules (fused epilogues; split: T2/T4 store A·y and vector passes finish —
+    the default from 2^20 rows) against the oracle on C2, and their MAXIT exits."""
+    monkeypatch.setenv("ZK_SPLIT_RED", split)
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    r = gpu_solve(m, b, tol=1e-8)
+    refs = [oracle.tfqmr(m, b, tol=1e-8, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    assert r["status"] == "CONVERGED" and 0.95 * min(its) <= r["iters"] <= 1.05 * max(its)
+    k = min(12, r["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= 1e-10
+    assert relerr(r["x"], refs[0]["x"]) <= 1e-6
+    for kk in (1, 2, 5):
+        q = gpu_solve(m, b, tol=1e-14, maxit=kk)
+        ref = oracle.tfqmr(m, b, tol=1e-14, maxit=kk)
+        assert q["status"] == "MAXIT" and relerr(q["x"], ref["x"]) <= 1e-11
