@@ -47,7 +47,7 @@ def args_():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=2)
-    p.add_argument("--spmv-reps", type=int, default=50)
+    p.add_argument("--spmv-reps", type=int, default=100)
     p.add_argument("--no-shapes", action="store_true", help="skip the PAPER.md T1-shape latency runs")
     p.add_argument("--no-methods", action="store_true",
                    help="skip the per-method C4 solves (Jacobi-BiCGStab, COCG, TFQMR, BiCGStab(2), BiCGStab(8))")
@@ -269,14 +269,31 @@ def main():
     y = torch.empty_like(b)
     for _ in range(3):
         zk.zcsrmv(A, 1.0, b, 0.0, y, stream)
-    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s0.record(stream)
-    for _ in range(a.spmv_reps):
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(a.spmv_reps + 1)]
+    evs[0].record(stream)
+    for i in range(a.spmv_reps):                     # back to back; per-launch events
         zk.zcsrmv(A, 1.0, b, 0.0, y, stream)
-    s1.record(stream)
+        evs[i + 1].record(stream)
     torch.cuda.synchronize()
-    spmv_us = 1e3 * s0.elapsed_time(s1) / a.spmv_reps
-    spmv = {"us": spmv_us, "gbs": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9,
+    per = sorted(1e3 * evs[i].elapsed_time(evs[i + 1]) for i in range(a.spmv_reps))
+    spmv_us = 1e3 * evs[0].elapsed_time(evs[-1]) / a.spmv_reps
+    # measured read-only stream peak (SURVEY.md §8(d) "Reporting"): zk_dznrm2 over a 4 GiB vector
+    big = torch.ones(1 << 28, dtype=torch.complex128, device=dev)
+    for _ in range(2):
+        zk.dznrm2(big, stream=stream)
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q0.record(stream)
+    for _ in range(10):
+        zk.dznrm2(big, stream=stream)
+    q1.record(stream)
+    torch.cuda.synchronize()
+    read_gbs = 16.0 * (1 << 28) * 10 / (q0.elapsed_time(q1) * 1e-3) / 1e9
+    del big
+    roofline["read_stream_gbs"] = read_gbs
+    roofline["frac_of_read_stream"] = spmv_gbs / read_gbs
+    spmv = {"us": spmv_us, "us_median": per[len(per) // 2], "us_min": per[0], "reps": a.spmv_reps,
+            "gbs": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9,
+            "frac_of_read_stream": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9 / read_gbs,
             "gflops": M.spmv_flops(nnz) / (spmv_us * 1e-6) / 1e9,
             "frac_of_peak": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9 / peak,
             "lanes_per_row": A.info["lanes_per_row"],

@@ -210,3 +210,41 @@ def int_vector(n: int, seed: int, lo: int = -8, hi: int = 8) -> np.ndarray:
     """Gaussian-integer vector with parts in [lo, hi] (exactness pins)."""
     rng = np.random.default_rng(seed)
     return (rng.integers(lo, hi + 1, size=n) + 1j * rng.integers(lo, hi + 1, size=n)).astype(np.complex128)
+
+
+def add_long_rows(mat: dict, frac: float = 0.02, target_len: int = 39, scale: float = 1e-3,
+                  seed: int = 44) -> dict:
+    """NEXT-4 irregular-row stress input (Twingo's max row lengths 33/39, PAPER.md
+    T1, which conforming hexes cannot produce): a copy of `mat` in which a random `frac` of the
+    free rows gets extra entries at random columns (sorted, unique) until it holds `target_len`,
+    with values U[−1,1]² · scale · |diagonal| (weak couplings keep the system well posed).
+    Free-row mask, phase and row_begin are carried over; rhs generation is unchanged."""
+    rng = np.random.default_rng(seed)
+    rp, col, val = mat["row_ptr"], mat["col_idx"], mat["values"]
+    n = len(rp) - 1
+    n_cols = mat.get("n_cols", mat["n"])
+    free = np.flatnonzero(mat["free_mask"]) if "free_mask" in mat else np.arange(n)
+    pick = np.zeros(n, dtype=bool)
+    pick[rng.choice(free, size=max(1, int(frac * len(free))), replace=False)] = True
+    rows_c, rows_v = [], []
+    for i in range(n):
+        c = col[rp[i]:rp[i + 1]]
+        v = val[rp[i]:rp[i + 1]]
+        if pick[i] and len(c) < target_len:
+            d = np.abs(v[c == i + mat.get("row_begin", 0)]).max() if np.any(c == i + mat.get("row_begin", 0)) else 1.0
+            extra = rng.choice(np.setdiff1d(np.arange(n_cols, dtype=np.int64), c), size=target_len - len(c),
+                               replace=False).astype(np.int32)
+            ev = (rng.uniform(-1, 1, len(extra)) + 1j * rng.uniform(-1, 1, len(extra))) * scale * d
+            c = np.concatenate([c, extra])
+            v = np.concatenate([v, ev])
+            o = np.argsort(c, kind="stable")
+            c, v = c[o], v[o]
+        rows_c.append(c)
+        rows_v.append(v)
+    lens = np.array([len(c) for c in rows_c], dtype=np.int64)
+    out = dict(mat)
+    out["row_ptr"] = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    out["col_idx"] = np.concatenate(rows_c).astype(np.int32)
+    out["values"] = np.concatenate(rows_v).astype(np.complex128)
+    out["nnz"] = int(out["row_ptr"][-1])
+    return out

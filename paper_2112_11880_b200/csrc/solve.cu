@@ -1667,6 +1667,273 @@ __global__ void __launch_bounds__(kBlock, 2) k_persist_cg(SolveCtx* c) {
     }
 }
 
+// ------------------------------------------------------------------ cluster solver (loop mode 5)
+// Small systems (the paper's Audi/Twingo shapes) are latency-bound: a WHILE-graph
+// iteration of 5 kernels costs ≈ 40 µs there, mostly dependent global-memory round trips of the
+// grid reductions and kernel boundaries.  Mode 5 runs the whole BiCGStab loop in ONE thread-block
+// cluster (up to 16 CTAs × 1024 threads on one GPC): each thread owns fixed rows/elements in every
+// phase (so own-row data needs no cross-CTA ordering), gathers of vectors written by other CTAs go
+// through L2 (ld.global.cg) after a cluster barrier, every reduction is a block reduction into a
+// shared-memory slot + one cluster barrier + a rank-ordered sum of the slots over distributed
+// shared memory, and every CTA runs the scalar step (the same fin_* functions) on its own
+// shared-memory copy of the context — identical totals in identical order give identical scalars,
+// so nothing is broadcast and the loop never touches global memory for control.
+#ifndef ZK_CBLOCK
+#define ZK_CBLOCK 512
+#endif
+constexpr int kCBlock = ZK_CBLOCK;
+constexpr int kCWarps = kCBlock / 32;
+constexpr int64_t kClusterRows = 65536;   // mode 5 possible up to this size (ZK_LOOP_MODE=5)
+constexpr int64_t kClusterDefaultRows = 4096;  // and the default up to this size: measured per
+// iteration (incl. init/true-residual overhead) C1 33.7 vs 40.1 µs for the WHILE graph, but C2
+// 43.1 vs 39.3 and T0 36.4 vs 34.3 — the thread-per-row SpMV's dependent L2 round trips (7 chunks
+// of 4 entries per row) outweigh the saved kernel boundaries once rows exceed one round
+
+struct ClusterRed {
+    double slot[2][kMaxRed];      // this CTA's partial sums, double-buffered across reductions
+    double warp_part[kMaxRed][kCWarps];
+    double tot[kMaxRed];
+    int parity;
+};
+
+// cluster-wide sum of K doubles; result in R.tot (valid after return, all threads)
+template <int K>
+__device__ __forceinline__ void cl_sum(double (&v)[K], ClusterRed& R) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    warp_sum<K>(v);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) R.warp_part[k][warp] = v[k];
+    }
+    __syncthreads();
+    const int par = R.parity;
+    if (warp == 0) {
+        double w[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) w[k] = lane < kCWarps ? R.warp_part[k][lane] : 0.0;
+        warp_sum<K>(w);
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < K; k++) R.slot[par][k] = w[k];
+        }
+    }
+    cl.sync();  // release/acquire at cluster scope: slots (and this phase's global writes) visible
+    if (threadIdx.x == 0) {
+        const unsigned ncta = cl.num_blocks();
+        double t[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) t[k] = 0.0;
+        for (unsigned r = 0; r < ncta; r++) {  // fixed rank order
+            const double* rs = cl.map_shared_rank(&R.slot[par][0], r);
+#pragma unroll
+            for (int k = 0; k < K; k++) t[k] += rs[k];
+        }
+#pragma unroll
+        for (int k = 0; k < K; k++) R.tot[k] = t[k];
+        R.parity = par ^ 1;
+    }
+}
+
+// y_i = Σ val·x[col] for row i (CSR, stored order, 4 entries in flight); x gathered through L2
+__device__ __forceinline__ double2 cl_row(const CsrDev& A, const double2* x, int64_t i) {
+    const int64_t rs = A.row_ptr[i], re = A.row_ptr[i + 1];
+    double2 sum = make_double2(0.0, 0.0);
+    for (int64_t p = rs; p < re; p += 4) {
+        double2 v[4];
+        int c[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            if (p + u < re) {
+                v[u] = __ldg(A.val + p + u);
+                c[u] = __ldg(A.col + p + u);
+            } else {
+                c[u] = -1;
+            }
+        }
+        double2 xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) xv[u] = c[u] >= 0 ? __ldcg(x + c[u]) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (c[u] >= 0) cfma(sum, v[u], xv[u]);
+    }
+    return sum;
+}
+
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, const CsrDev A) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ SolveCtx cs;
+    __shared__ ClusterRed R;
+    if (threadIdx.x == 0) {
+        cs = *gctx;
+        R.parity = 0;
+    }
+    __syncthreads();
+    SolveCtx* c = &cs;
+    const int64_t n = A.n_rows;
+    const int64_t nt = (int64_t)cl.num_blocks() * kCBlock;
+    const int64_t g0 = (int64_t)cl.block_rank() * kCBlock + threadIdx.x;
+    double2 *x = cs.x, *r = cs.r, *p = cs.p, *v = cs.v, *s = cs.s, *t = cs.t;
+    const double2* rh = cs.rh;
+    int bodies = 0;
+    while (!c->done) {
+        {   // K1: v = A p ; σ = ⟨r̂, v⟩, ‖v‖²
+            double acc[3] = {0.0, 0.0, 0.0};
+            for (int64_t i = g0; i < n; i += nt) {
+                const double2 y = cl_row(A, p, i);
+                v[i] = y;
+                const double2 q = rh[i];
+                acc[0] = fma(q.x, y.x, fma(q.y, y.y, acc[0]));
+                acc[1] = fma(q.x, y.y, fma(-q.y, y.x, acc[1]));
+                acc[2] += cabs2(y);
+            }
+            cl_sum<3>(acc, R);
+            if (threadIdx.x == 0) fin_k1_bicg(c, R.tot);
+            __syncthreads();
+            if (c->done) break;
+        }
+        {   // K2: s = r − α v ; ‖s‖²
+            const double2 al = c->alpha;
+            double acc[1] = {0.0};
+            for (int64_t i = g0; i < n; i += nt) {
+                const double2 vi = v[i];
+                double2 o = r[i];
+                o.x = fma(-al.x, vi.x, fma(al.y, vi.y, o.x));
+                o.y = fma(-al.x, vi.y, fma(-al.y, vi.x, o.y));
+                s[i] = o;
+                acc[0] += cabs2(o);
+            }
+            cl_sum<1>(acc, R);
+            if (threadIdx.x == 0) fin_k2_bicg(c, R.tot);
+            __syncthreads();
+            if (c->done) {  // half-step exit: x += α p
+                if (c->half) {
+                    for (int64_t i = g0; i < n; i += nt) {
+                        double2 xi = x[i];
+                        cfma(xi, al, p[i]);
+                        x[i] = xi;
+                    }
+                    if (threadIdx.x == 0) c->half = 0;
+                }
+                break;
+            }
+        }
+        {   // K3: t = A s ; ⟨t, s⟩, ‖t‖²   (s complete: the K2 reduction's cluster barrier)
+            double acc[3] = {0.0, 0.0, 0.0};
+            for (int64_t i = g0; i < n; i += nt) {
+                const double2 y = cl_row(A, s, i);
+                t[i] = y;
+                const double2 si = s[i];
+                acc[0] = fma(y.x, si.x, fma(y.y, si.y, acc[0]));
+                acc[1] = fma(y.x, si.y, fma(-y.y, si.x, acc[1]));
+                acc[2] += cabs2(y);
+            }
+            cl_sum<3>(acc, R);
+            if (threadIdx.x == 0) fin_k3_bicg(c, R.tot);
+            __syncthreads();
+            if (c->done) break;
+        }
+        {   // K4: x += α p + ω s ; r = s − ω t ; ‖r‖², ⟨r̂, r⟩
+            const double2 al = c->alpha, om = c->omega;
+            double acc[3] = {0.0, 0.0, 0.0};
+            for (int64_t i = g0; i < n; i += nt) {
+                const double2 si = s[i], ti = t[i];
+                double2 xi = x[i];
+                cfma(xi, al, p[i]);
+                cfma(xi, om, si);
+                x[i] = xi;
+                double2 rn = si;
+                rn.x = fma(-om.x, ti.x, fma(om.y, ti.y, rn.x));
+                rn.y = fma(-om.x, ti.y, fma(-om.y, ti.x, rn.y));
+                r[i] = rn;
+                const double2 q = rh[i];
+                acc[0] += cabs2(rn);
+                acc[1] = fma(q.x, rn.x, fma(q.y, rn.y, acc[1]));
+                acc[2] = fma(q.x, rn.y, fma(-q.y, rn.x, acc[2]));
+            }
+            cl_sum<3>(acc, R);
+            if (threadIdx.x == 0) fin_k4_bicg(c, R.tot);
+            __syncthreads();
+            if (c->done) break;
+        }
+        {   // K5: p = r + β (p − ω v), then a cluster barrier (p is gathered by K1)
+            const double2 be = c->beta, om = c->omega;
+            for (int64_t i = g0; i < n; i += nt) {
+                const double2 vi = v[i];
+                double2 d = p[i];
+                d.x = fma(-om.x, vi.x, fma(om.y, vi.y, d.x));
+                d.y = fma(-om.x, vi.y, fma(-om.y, vi.x, d.y));
+                double2 o = r[i];
+                cfma(o, be, d);
+                p[i] = o;
+            }
+            cl.sync();
+        }
+        bodies++;
+    }
+    if (cl.block_rank() == 0 && threadIdx.x == 0) {
+        cs.bodies = bodies;
+        *gctx = cs;
+    }
+    cl.sync();  // no CTA leaves while another may still read its reduction slots
+}
+
+// cluster size that can be launched on this device: 16 (non-portable), else 8, else 0
+static int cluster_size_available() {
+    static int cached = -1;  // per process
+    if (cached < 0) {
+        cached = 0;
+        cudaFuncSetAttribute((const void*)k_cluster_bicg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        for (int cs : {16, 8}) {
+            cudaLaunchConfig_t cfg;
+            memset(&cfg, 0, sizeof cfg);
+            cfg.gridDim = dim3(cs);
+            cfg.blockDim = dim3(kCBlock);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)k_cluster_bicg, &cfg) == cudaSuccess &&
+                nclusters >= 1) {
+                cached = cs;
+                break;
+            }
+            cudaGetLastError();
+        }
+    }
+    return cached;
+}
+// launch the cluster solver on one cluster; false when unavailable
+static bool cluster_launch(SolveCtx* dc, const CsrDev& av, cudaStream_t s, int* out_cs) {
+    const int cached = cluster_size_available();
+    if (cached == 0) return false;
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3(cached);
+    cfg.blockDim = dim3(kCBlock);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cached;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_cluster_bicg, dc, av) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    *out_cs = cached;
+    return true;
+}
+
 __global__ void k_set_ctx(SolveCtx* c, SolveCtx h) {
     *c = h;
     for (int i = 0; i < kTickets; i++) h.tickets[i] = 0u;  // workspace memory may be recycled
@@ -2070,12 +2337,16 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     //      persistent cooperative kernel.  Mode 4 measured SLOWER on every shape (C1 52 vs 39 µs per
     //      iteration, C3 514 vs 184: the fused phases need 128 registers → half the warps, and
     //      coherent gathers), so it is opt-in (ZK_LOOP_MODE=4) and parity-tested, not the default.
-    int mode = A->dist ? 3 : 1;
+    // default: the cluster solver (mode 5) for small BiCGStab systems, else the WHILE graph
+    int mode = A->dist ? 3 : (method == ZK_BICGSTAB && A->n_rows <= kClusterDefaultRows ? 5 : 1);
     if (const char* e = getenv("ZK_LOOP_MODE")) {
         int m = atoi(e);
-        if (m >= 1 && m <= 4) mode = m;
+        if (m >= 1 && m <= 5) mode = m;
     }
-    if (A->dist && (mode == 1 || mode == 4)) mode = 3;  // NCCL inside WHILE bodies / persistent kernels is not used
+    if (mode == 5 && (A->dist || method != ZK_BICGSTAB || A->n_rows > kClusterRows || A->n_rows == 0 ||
+                      cluster_size_available() == 0))
+        mode = A->dist ? 3 : 1;
+    if (A->dist && (mode == 1 || mode == 4 || mode == 5)) mode = 3;  // NCCL inside WHILE bodies / persistent kernels is not used
     int persist_grid = 0;
     const void* kp = nullptr;
     if (mode == 4 && (method == ZK_COCG || method == ZK_TFQMR || method == kBiCGStabL)) mode = 1;  // persistent: BiCGStab, CG
@@ -2203,6 +2474,9 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     } else if (mode == 4) {
         void* args[] = {&dc};
         ZK_CUDA(cudaLaunchCooperativeKernel(kp, dim3(persist_grid), dim3(kBlock), args, 0, s));
+    } else if (mode == 5) {
+        int csz = 0;
+        if (!cluster_launch(dc, hc.A, s, &csz)) return fail(ZK_ERR_CUDA, "cluster solver launch failed");
     } else {
         ZK_CUDA(cudaMallocHost(&hdone, sizeof(SolveCtx)));
         int launched = 0;
@@ -2269,7 +2543,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
                         : method == ZK_TFQMR ? 2 : method == kBiCGStabL ? 2 * ell - 1 : 0;
         const int fins = A->dist ? (method == ZK_BICGSTAB ? 4 : method == ZK_TFQMR ? 3 : 2) : 0;  // dist: 1-thread finish kernels
         const int pre = method == ZK_TFQMR ? (A->dist ? 2 : 1) : 0;                               // TFQMR: K0 (+ its finish)
-        info->gpu_launches = mode == 4 ? 4 : 3 + pre + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);
+        info->gpu_launches = (mode == 4 || mode == 5) ? 4 : 3 + pre + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);
         for (int i = 0; i < 4; i++) {
             info->kernel_ms[i] = out.tsum[i] * 1e-6;
             info->kernel_launches[i] = out.tcnt[i];

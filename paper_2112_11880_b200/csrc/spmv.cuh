@@ -232,6 +232,12 @@ __device__ __forceinline__ void spmv_body_b4(const CsrDev& A, const double2* __r
 #ifndef ZK_SELL_PIPE
 #define ZK_SELL_PIPE 0
 #endif
+#ifndef ZK_SELL_DEP
+#define ZK_SELL_DEP 0
+#endif
+#ifndef ZK_SELL_WSYNC
+#define ZK_SELL_WSYNC 0
+#endif
 #ifndef ZK_SELL_SMEM_ACC
 #define ZK_SELL_SMEM_ACC 0
 #endif
@@ -353,9 +359,21 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
                 }
             }
             if (PRE == 1 && k0 + U >= width && row < n) pre = epi.pre(row);
+#if ZK_SELL_WSYNC
+            __syncwarp();  // the batch's matrix loads stay ahead of its gathers in the schedule
+#endif
+#if ZK_SELL_DEP
+            // every gather address depends on the batch's LAST column load (an opaque 0), so the
+            // scheduler cannot start a gather — and stall on its column — before all U (value,
+            // column) loads of the batch are in flight
+            int dep;
+            asm("{.reg .pred q; setp.eq.s32 q, %1, 2147483647; selp.b32 %0, 1, 0, q;}" : "=r"(dep) : "r"(c[U - 1]));
+#else
+            const int dep = 0;
+#endif
             double2 xv[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather_ord(x + c[u]) : make_double2(0.0, 0.0);
+            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather_ord(x + (c[u] + dep)) : make_double2(0.0, 0.0);
 #pragma unroll
             for (int u = 0; u < U; u++)
                 if (c[u] >= 0) cfma(sum, v[u], xv[u]);

@@ -109,3 +109,21 @@ def test_random_csr_canonical():
     for i in range(500):
         c = col[rp[i]:rp[i + 1]]
         assert np.all(np.diff(c) > 0)
+
+
+def test_add_long_rows_stress_input():
+    """NEXT-4 irregular-row stress input: Twingo's max row length 39 (PAPER.md T1), canonical
+    CSR, every original entry kept, only the picked free rows grow."""
+    m = gen.make_matrix("C2")
+    s = gen.add_long_rows(m, frac=0.02, target_len=39)
+    lens0, lens1 = np.diff(m["row_ptr"]), np.diff(s["row_ptr"])
+    assert lens1.max() == 39 and np.all(lens1 >= lens0)
+    grown = np.flatnonzero(lens1 > lens0)
+    assert len(grown) == int(0.02 * m["free_mask"].sum()) and np.all(m["free_mask"][grown] == 1)
+    for i in grown[:50]:
+        c1 = s["col_idx"][s["row_ptr"][i]:s["row_ptr"][i + 1]]
+        assert np.all(np.diff(c1) > 0)
+        c0 = m["col_idx"][m["row_ptr"][i]:m["row_ptr"][i + 1]]
+        v0 = m["values"][m["row_ptr"][i]:m["row_ptr"][i + 1]]
+        v1 = s["values"][s["row_ptr"][i]:s["row_ptr"][i + 1]]
+        assert np.array_equal(v1[np.searchsorted(c1, c0)], v0)

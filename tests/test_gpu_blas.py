@@ -313,3 +313,17 @@ def test_sell_default_and_padding_fallback(monkeypatch):
         y = torch.empty(mat["n"], dtype=torch.complex128, device=DEV)
         zk.zcsrmv(M, 1, cuda(x), 0, y)
         assert np.all(np.abs(y.cpu().numpy() - oracle.zcsrmv(mat, x)) <= 1e-13 * row_scale(mat, x) + 1e-300)
+
+
+@pytest.mark.parametrize("mode", ["0", "3"])
+def test_zcsrmv_irregular_rows_stress(mode, monkeypatch):
+    """NEXT-4: Twingo-like irregular rows (2 % of the rows of the Twingo3D-0 shape grown to 39 entries)
+    through the CSR sub-warp kernel and the (heavily padded, forced) sliced-ELL kernel."""
+    monkeypatch.setenv("ZK_SPMV_MODE", mode)
+    m = gen.add_long_rows(gen.make_matrix("T0"))
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+    assert A.info["spmv_mode"] == int(mode) and A.info["max_row_len"] == 39
+    x = gen.rand_vector(m["n"], 8)
+    y = torch.empty(m["n"], dtype=torch.complex128, device=DEV)
+    zk.zcsrmv(A, 1, cuda(x), 0, y)
+    assert np.all(np.abs(y.cpu().numpy() - oracle.zcsrmv(m, x)) <= 1e-13 * row_scale(m, x) + 1e-300)

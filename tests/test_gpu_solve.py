@@ -44,6 +44,7 @@ def relerr(a, b):
 @pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
 def test_bicgstab_parity(cfg, spmv_mode, monkeypatch):
     monkeypatch.setenv("ZK_SPMV_MODE", spmv_mode)
+    monkeypatch.setenv("ZK_LOOP_MODE", "1")  # the WHILE-graph path with each SpMV mapping
     m = gen.make_matrix(cfg)
     b = gen.make_rhs(m)
     r = gpu_solve(m, b, tol=1e-8, maxit=1000, method="bicgstab")
@@ -367,6 +368,7 @@ def test_split_reductions_parity(method, monkeypatch):
         m = gen.make_matrix("C2")
         b = gen.make_rhs(m)
         ref = (oracle.bicgstab if method == "bicgstab" else oracle.cocg)(m, b, tol=1e-8)
+    monkeypatch.setenv("ZK_LOOP_MODE", "1")
     monkeypatch.setenv("ZK_SPLIT_RED", "1")
     r = gpu_solve(m, b, tol=1e-8, method=method)
     monkeypatch.setenv("ZK_SPLIT_RED", "0")
@@ -377,3 +379,63 @@ def test_split_reductions_parity(method, monkeypatch):
     assert np.max(np.abs(r["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-10
     assert relerr(r["x"], ref["x"]) <= 1e-6 and relerr(f["x"], ref["x"]) <= 1e-6
     assert r["gpu_launches"] > f["gpu_launches"]
+
+
+def test_bicgstab_irregular_rows_stress():
+    """NEXT-4 stress input (C2 with 2 % of its rows grown to 39 entries, Twingo's max): the
+    default mapping falls back to the CSR kernel (padding > 10 %) and BiCGStab matches the oracle."""
+    m = gen.add_long_rows(gen.make_matrix("C2"))
+    b = gen.make_rhs(m)
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+    assert A.info["spmv_mode"] == 0
+    r = zk.solve(A, cuda(b), tol=1e-8, method="bicgstab")
+    refs = [oracle.bicgstab(m, b, tol=1e-8, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    assert r["status"] == "CONVERGED" and 0.95 * min(its) <= r["iters"] <= 1.05 * max(its)
+    assert relerr(r["x"].cpu().numpy(), refs[0]["x"]) <= 1e-6
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "bicgstab_jacobi"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
+def test_cluster_solver_parity(cfg, method, monkeypatch):
+    """Loop mode 5 (the default for BiCGStab up to 4096 rows, selectable up to 65536): the whole
+    loop in one thread-block cluster, reductions over distributed shared memory, scalar steps
+    replicated per CTA."""
+    if cfg != "C1":
+        monkeypatch.setenv("ZK_LOOP_MODE", "5")
+    m = gen.make_matrix(cfg)
+    b = gen.make_rhs(m)
+    r = gpu_solve(m, b, tol=1e-8, method=method)
+    assert r["loop_mode"] == 5 and r["gpu_launches"] == 4
+    fn = oracle.bicgstab if method == "bicgstab" else oracle.bicgstab_jacobi
+    refs = [fn(m, b, tol=1e-8, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    assert r["status"] == "CONVERGED" and 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    k = min(12, r["iters"], refs[0]["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= 1e-10
+    assert relerr(r["x"], refs[0]["x"]) <= 1e-6 and r["true_relres"] <= 2e-8
+    r2 = gpu_solve(m, b, tol=1e-8, method=method)                  # deterministic
+    assert np.array_equal(r["x"], r2["x"]) and np.array_equal(r["hist"], r2["hist"])
+
+
+def test_cluster_solver_outcomes(monkeypatch):
+    """Mode 5 exits: MAXIT with the oracle's history, half-step exit (cI), breakdown."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "5")
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    r = gpu_solve(m, b, tol=1e-14, maxit=9)
+    ref = oracle.bicgstab(m, b, tol=1e-14, maxit=9)
+    assert r["loop_mode"] == 5 and r["status"] == ref["status"] == "MAXIT" and r["iters"] == 9
+    assert np.max(np.abs(r["hist"] - ref["hist"]) / ref["hist"]) <= 1e-10
+    assert relerr(r["x"], ref["x"]) <= 1e-10
+    n = 3000
+    c = 0.3 - 2j
+    d = dict(row_ptr=np.arange(n + 1, dtype=np.int64), col_idx=np.arange(n, dtype=np.int32),
+             values=np.full(n, c, np.complex128), n=n)
+    bb = gen.rand_vector(n, 1)
+    q = gpu_solve(d, bb, tol=1e-12)
+    assert q["loop_mode"] == 5 and q["status"] == "CONVERGED" and q["iters"] == 1
+    assert np.max(np.abs(q["x"] - bb / c)) <= 1e-15 * np.max(np.abs(bb / c))
+    sk = dict(row_ptr=np.array([0, 1, 2]), col_idx=np.array([1, 0], np.int32),
+              values=np.array([1, -1], np.complex128), n=2)
+    assert gpu_solve(sk, np.array([1, 0], np.complex128))["status"] == "BREAKDOWN_SIGMA"

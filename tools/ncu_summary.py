@@ -55,21 +55,26 @@ def launches(path):
     start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
     rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
     tot = collections.defaultdict(float)
+    dram = collections.defaultdict(float)
     cnt = collections.Counter()
+    tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+    bscale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for r in rows:
-        if r.get("Metric Name") != "gpu__time_duration.sum":
-            continue
+        k = r["Kernel Name"].split("(")[0]
+        name = r.get("Metric Name")
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "nsecond")
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0)
-        k = r["Kernel Name"].split("(")[0]
-        tot[k] += v
-        cnt[k] += 1
+        if name == "gpu__time_duration.sum":
+            tot[k] += v * tscale.get(unit, 1e-3)
+            cnt[k] += 1
+        elif name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            dram[k] += v * bscale.get(unit, 1.0)
     s = sum(tot.values())
     print(f"# ncu launch list: `{path}` ({sum(cnt.values())} launches, cold-cache serialised times)\n")
-    print("| kernel | launches | total µs | mean µs | share |\n|---|---|---|---|---|")
+    print("| kernel | launches | total µs | mean µs | share | DRAM GB per launch | GB/s |\n|---|---|---|---|---|---|---|")
     for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
-        print(f"| {k} | {cnt[k]} | {v:.1f} | {v / cnt[k]:.1f} | {v / s:.3f} |")
+        gb = dram[k] / cnt[k] / 1e9 if dram[k] else float("nan")
+        print(f"| {k} | {cnt[k]} | {v:.1f} | {v / cnt[k]:.1f} | {v / s:.3f} | {gb:.4f} | {gb / (v / cnt[k] * 1e-6):.0f} |")
 
 
 if __name__ == "__main__":
