@@ -426,11 +426,11 @@ struct EpiInit {  // r = b − A x0 ; x = x0 ; r̂ = p = r ; {‖b‖², ‖r‖
     __device__ Pre pre(int64_t i) const { return {ld_vec(b + i), x != x0 ? ld_gather_coh(x0 + i) : make_double2(0, 0)}; }
     __device__ void row(int64_t i, double2 y, const Pre& q, double (&acc)[4]) {
         const double2 rr = csub(q.b, y);
-        r[i] = rr;
-        p[i] = rr;
-        if (rh) rh[i] = rr;
-        if (x != x0) x[i] = q.x0;
-        if (d) d[i] = make_double2(0.0, 0.0);
+        st_vec(r + i, rr);
+        st_vec(p + i, rr);
+        if (rh) st_vec(rh + i, rr);
+        if (x != x0) st_vec(x + i, q.x0);
+        if (d) st_vec(d + i, make_double2(0.0, 0.0));
         acc[0] += cabs2(q.b);
         acc[1] += cabs2(rr);
         acc[2] = fma(rr.x, rr.x, fma(-rr.y, rr.y, acc[2]));  // rᵀr (COCG's ρ0)
@@ -459,7 +459,7 @@ struct EpiK1Bicg {  // v = A p ; {σ = ⟨r̂, v⟩, ‖v‖²}
     __device__ explicit EpiK1Bicg(SolveCtx* c_) : c(c_), v(c_->v), rh(c_->rh) {}
     __device__ Pre pre(int64_t i) const { return ld_vec(rh + i); }
     __device__ void row(int64_t i, double2 y, const Pre& r, double (&acc)[3]) {
-        v[i] = y;
+        st_vec(v + i, y);
         acc[0] = fma(r.x, y.x, fma(r.y, y.y, acc[0]));
         acc[1] = fma(r.x, y.y, fma(-r.y, y.x, acc[1]));
         acc[2] += cabs2(y);
@@ -476,7 +476,7 @@ struct EpiK3Bicg {  // t = A s ; {⟨t, s⟩, ⟨t, t⟩}
     __device__ explicit EpiK3Bicg(SolveCtx* c_) : c(c_), t(c_->t), s(c_->s) {}
     __device__ Pre pre(int64_t i) const { return ld_gather_coh(s + i); }
     __device__ void row(int64_t i, double2 y, const Pre& si, double (&acc)[3]) {
-        t[i] = y;
+        st_vec(t + i, y);
         acc[0] = fma(y.x, si.x, fma(y.y, si.y, acc[0]));
         acc[1] = fma(y.x, si.y, fma(-y.y, si.x, acc[1]));
         acc[2] += cabs2(y);
@@ -491,13 +491,17 @@ struct EpiK3Bicg {  // t = A s ; {⟨t, s⟩, ⟨t, t⟩}
 // two vectors ≈ 40 µs: BiCGStab 1.83 vs 1.90 ms per iteration.  Below kSplitRows the two extra
 // launches per iteration cost more than they save (latency-bound sizes), so the fused kernels stay.
 constexpr int64_t kSplitRows = 1 << 20;
+#ifndef ZK_STORE_ORD
+#define ZK_STORE_ORD 1
+#endif
 struct EpiStore {  // out = A x
     static constexpr int K = 0;
+    static constexpr bool kOrdered = ZK_STORE_ORD;  // all 9 column loads of a batch before its gathers (spmv.cuh)
     using Pre = double2;
     double2* __restrict__ out;
     __device__ explicit EpiStore(double2* o) : out(o) {}
     __device__ Pre pre(int64_t) const { return make_double2(0.0, 0.0); }
-    __device__ void row(int64_t i, double2 y, const Pre&, double (&)[1]) { out[i] = y; }
+    __device__ void row(int64_t i, double2 y, const Pre&, double (&)[1]) { st_vec(out + i, y); }
     __device__ void finish(double (&)[1]) {}
 };
 struct OpRed1Bicg {  // {⟨r̂, v⟩, ‖v‖²}
@@ -557,7 +561,7 @@ struct EpiK1Cg {  // q = A p ; {δ = ⟨p, q⟩}
     __device__ explicit EpiK1Cg(SolveCtx* c_) : c(c_), q(c_->q), p(c_->p) {}
     __device__ Pre pre(int64_t i) const { return ld_gather_coh(p + i); }
     __device__ void row(int64_t i, double2 y, const Pre& pi, double (&acc)[2]) {
-        q[i] = y;
+        st_vec(q + i, y);
         acc[0] = fma(pi.x, y.x, fma(pi.y, y.y, acc[0]));
         acc[1] = fma(pi.x, y.y, fma(-pi.y, y.x, acc[1]));
     }
@@ -578,11 +582,11 @@ struct OpInitZero {  // x0 = 0: x = 0 ; r = r̂ = p = b ; {‖b‖², ‖r‖²,
         : c(c_), b(c_->b), x(c_->x), r(c_->r), p(c_->p), rh(c_->rh), d(c_->d), kind(kind_) {}
     __device__ In load(int64_t i) const { return {ld_vec(b + i)}; }
     __device__ void apply(int64_t i, const In& v, double (&acc)[4]) const {
-        x[i] = make_double2(0.0, 0.0);
-        r[i] = v.b;
-        p[i] = v.b;
-        if (kind == 0 || kind >= 4) rh[i] = v.b;
-        if (kind >= 4) d[i] = make_double2(0.0, 0.0);
+        st_vec(x + i, make_double2(0.0, 0.0));
+        st_vec(r + i, v.b);
+        st_vec(p + i, v.b);
+        if (kind == 0 || kind >= 4) st_vec(rh + i, v.b);
+        if (kind >= 4) st_vec(d + i, make_double2(0.0, 0.0));
         const double bb = cabs2(v.b);
         acc[0] += bb;
         acc[1] += bb;
@@ -611,7 +615,7 @@ struct OpK2Bicg {  // s = r − α v ; {‖s‖²}
         double2 o = in.r;
         o.x = fma(-alpha.x, in.v.x, fma(alpha.y, in.v.y, o.x));
         o.y = fma(-alpha.x, in.v.y, fma(-alpha.y, in.v.x, o.y));
-        s[i] = o;
+        st_vec(s + i, o);
         acc[0] += cabs2(o);
     }
     __device__ void finish(double (&acc)[1]) const { reduce_finish<S_K2_BICG, 1>(c, acc); }
@@ -644,15 +648,15 @@ struct OpK4Bicg {  // x += αp + ωs ; r = s − ωt ; {‖r‖², ⟨r̂, r⟩}
         double2 xn = in.x;
         cfma(xn, alpha, in.p);
         if (half) {
-            x[i] = xn;
+            st_vec(x + i, xn);
             return;
         }
         cfma(xn, omega, in.s);
-        x[i] = xn;
+        st_vec(x + i, xn);
         double2 rn = in.s;
         rn.x = fma(-omega.x, in.t.x, fma(omega.y, in.t.y, rn.x));
         rn.y = fma(-omega.x, in.t.y, fma(-omega.y, in.t.x, rn.y));
-        r[i] = rn;
+        st_vec(r + i, rn);
         acc[0] += cabs2(rn);
         acc[1] = fma(in.rh.x, rn.x, fma(in.rh.y, rn.y, acc[1]));
         acc[2] = fma(in.rh.x, rn.y, fma(-in.rh.y, rn.x, acc[2]));
@@ -678,7 +682,7 @@ struct OpK5Bicg {  // p = r + β(p − ω v)
         d.y = fma(-omega.x, in.v.y, fma(-omega.y, in.v.x, d.y));
         double2 o = in.r;
         cfma(o, beta, d);
-        p[i] = o;
+        st_vec(p + i, o);
     }
     __device__ void finish(double (&)[1]) const {}
 };
@@ -696,9 +700,9 @@ struct OpK2Cg {  // x += α p ; r −= α q ; {‖r‖²}
         return {ld_vec(x + i), ld_vec(p + i), ld_vec(r + i), ld_vec(q + i)};
     }
     __device__ void apply(int64_t i, const In& in, double (&acc)[1]) const {
-        x[i] = make_double2(fma(alpha, in.p.x, in.x.x), fma(alpha, in.p.y, in.x.y));
+        st_vec(x + i, make_double2(fma(alpha, in.p.x, in.x.x), fma(alpha, in.p.y, in.x.y)));
         const double2 rn = make_double2(fma(-alpha, in.q.x, in.r.x), fma(-alpha, in.q.y, in.r.y));
-        r[i] = rn;
+        st_vec(r + i, rn);
         acc[0] += cabs2(rn);
     }
     __device__ void finish(double (&acc)[1]) const { reduce_finish<S_K2_CG, 1>(c, acc); }
@@ -713,7 +717,7 @@ struct OpK3Cg {  // p = r + β p
     __device__ explicit OpK3Cg(SolveCtx* c) : r(c->r), p(c->p), beta(c->beta_cg) {}
     __device__ In load(int64_t i) const { return {ld_vec(r + i), ld_vec(p + i)}; }
     __device__ void apply(int64_t i, const In& in, double (&)[1]) const {
-        p[i] = make_double2(fma(beta, in.p.x, in.r.x), fma(beta, in.p.y, in.r.y));
+        st_vec(p + i, make_double2(fma(beta, in.p.x, in.r.x), fma(beta, in.p.y, in.r.y)));
     }
     __device__ void finish(double (&)[1]) const {}
 };
@@ -727,7 +731,7 @@ struct EpiK1Cocg {  // q = A p ; {μ = pᵀ q} (unconjugated)
     __device__ explicit EpiK1Cocg(SolveCtx* c_) : c(c_), q(c_->q), p(c_->p) {}
     __device__ Pre pre(int64_t i) const { return ld_gather_coh(p + i); }
     __device__ void row(int64_t i, double2 y, const Pre& pi, double (&acc)[2]) {
-        q[i] = y;
+        st_vec(q + i, y);
         acc[0] = fma(pi.x, y.x, fma(-pi.y, y.y, acc[0]));
         acc[1] = fma(pi.x, y.y, fma(pi.y, y.x, acc[1]));
     }
@@ -747,11 +751,11 @@ struct OpK2Cocg {  // x += α p ; r −= α q ; {‖r‖², rᵀr}
     __device__ void apply(int64_t i, const In& in, double (&acc)[3]) const {
         double2 xn = in.x;
         cfma(xn, alpha, in.p);
-        x[i] = xn;
+        st_vec(x + i, xn);
         double2 rn = in.r;
         rn.x = fma(-alpha.x, in.q.x, fma(alpha.y, in.q.y, rn.x));
         rn.y = fma(-alpha.x, in.q.y, fma(-alpha.y, in.q.x, rn.y));
-        r[i] = rn;
+        st_vec(r + i, rn);
         acc[0] += cabs2(rn);
         acc[1] = fma(rn.x, rn.x, fma(-rn.y, rn.y, acc[1]));
         acc[2] = fma(2.0 * rn.x, rn.y, acc[2]);
@@ -770,7 +774,7 @@ struct OpK3Cocg {  // p = r + β p (complex β)
     __device__ void apply(int64_t i, const In& in, double (&)[1]) const {
         double2 o = in.r;
         cfma(o, beta, in.p);
-        p[i] = o;
+        st_vec(p + i, o);
     }
     __device__ void finish(double (&)[1]) const {}
 };
@@ -802,11 +806,11 @@ struct OpT1Tfqmr {  // y2 = y1 − α v ; w −= α u1 ; {‖w‖²}
         double2 o = in.y1;
         o.x = fma(-alpha.x, in.v.x, fma(alpha.y, in.v.y, o.x));
         o.y = fma(-alpha.x, in.v.y, fma(-alpha.y, in.v.x, o.y));
-        y2[i] = o;
+        st_vec(y2 + i, o);
         double2 wn = in.w;
         wn.x = fma(-alpha.x, in.u1.x, fma(alpha.y, in.u1.y, wn.x));
         wn.y = fma(-alpha.x, in.u1.y, fma(-alpha.y, in.u1.x, wn.y));
-        w[i] = wn;
+        st_vec(w + i, wn);
         acc[0] += cabs2(wn);
     }
     __device__ void finish(double (&acc)[1]) const { reduce_finish<S_T1_TFQMR, 1>(c, acc); }
@@ -824,11 +828,11 @@ struct EpiT2Tfqmr {  // u2 = A y2 ; w −= α u2 ; {‖w‖², ⟨r̃, w⟩}
     __device__ explicit EpiT2Tfqmr(SolveCtx* c_) : c(c_), u2(c_->u2), w(c_->w), rt(c_->rt), alpha(c_->alpha) {}
     __device__ Pre pre(int64_t i) const { return {ld_vec(w + i), ld_vec(rt + i)}; }
     __device__ void row(int64_t i, double2 y, const Pre& q, double (&acc)[3]) {
-        u2[i] = y;
+        st_vec(u2 + i, y);
         double2 wn = q.w;
         wn.x = fma(-alpha.x, y.x, fma(alpha.y, y.y, wn.x));
         wn.y = fma(-alpha.x, y.y, fma(-alpha.y, y.x, wn.y));
-        w[i] = wn;
+        st_vec(w + i, wn);
         acc[0] += cabs2(wn);
         acc[1] = fma(q.rt.x, wn.x, fma(q.rt.y, wn.y, acc[1]));
         acc[2] = fma(q.rt.x, wn.y, fma(-q.rt.y, wn.x, acc[2]));
@@ -865,12 +869,12 @@ struct OpT3Tfqmr {
         double2 xn = in.x;
         cfma(xn, eta1, d1);
         cfma(xn, eta2, d2);
-        x[i] = xn;
-        d[i] = d2;
+        st_vec(x + i, xn);
+        st_vec(d + i, d2);
         if (exit_only) return;
         double2 o = in.w;
         cfma(o, beta, in.y2);
-        y1[i] = o;
+        st_vec(y1 + i, o);
     }
     __device__ void finish(double (&)[1]) const {}
 };
@@ -890,7 +894,7 @@ struct OpT2bTfqmr {  // w −= α u2 ; {‖w‖², ⟨r̃, w⟩}
         double2 wn = in.w;
         wn.x = fma(-alpha.x, in.u2.x, fma(alpha.y, in.u2.y, wn.x));
         wn.y = fma(-alpha.x, in.u2.y, fma(-alpha.y, in.u2.x, wn.y));
-        w[i] = wn;
+        st_vec(w + i, wn);
         acc[0] += cabs2(wn);
         acc[1] = fma(in.rt.x, wn.x, fma(in.rt.y, wn.y, acc[1]));
         acc[2] = fma(in.rt.x, wn.y, fma(-in.rt.y, wn.x, acc[2]));
@@ -912,7 +916,7 @@ struct OpT4bTfqmr {  // v = u1 + β(u2 + β v) ; {σ = ⟨r̃, v⟩}
         cfma(t, beta, in.v);
         double2 vn = in.u1;
         cfma(vn, beta, t);
-        v[i] = vn;
+        st_vec(v + i, vn);
         acc[0] = fma(in.rt.x, vn.x, fma(in.rt.y, vn.y, acc[0]));
         acc[1] = fma(in.rt.x, vn.y, fma(-in.rt.y, vn.x, acc[1]));
     }
@@ -936,14 +940,14 @@ struct EpiT4Tfqmr {  // u1 = A y1 ; v = u1 + β(u2 + β v) (first: v = u1) ; {σ
         return {ld_vec(u2 + i), ld_vec(v + i), ld_vec(rt + i)};
     }
     __device__ void row(int64_t i, double2 y, const Pre& q, double (&acc)[2]) {
-        u1[i] = y;
+        st_vec(u1 + i, y);
         double2 vn = y;
         if (S != S_K0_TFQMR) {
             double2 t = q.u2;
             cfma(t, beta, q.v);
             cfma(vn, beta, t);
         }
-        v[i] = vn;
+        st_vec(v + i, vn);
         acc[0] = fma(q.rt.x, vn.x, fma(q.rt.y, vn.y, acc[0]));
         acc[1] = fma(q.rt.x, vn.y, fma(-q.rt.y, vn.x, acc[1]));
     }

@@ -246,14 +246,24 @@ __device__ __forceinline__ void spmv_body_b4(const CsrDev& A, const double2* __r
 #ifndef ZK_SELL_VGATHER
 #define ZK_SELL_VGATHER 0
 #endif
+// Per epilogue (Epi::kOrdered): the store-only epilogue of the split solver SpMVs needs it — left
+// to itself the compiler schedules that kernel at 64 registers with 3 matrix loads in flight per
+// gather batch instead of 9 (SASS; in-loop K1 708 µs vs 647 µs standalone at C4, ncu).
+template <class E>
+struct sell_ordered {
+    template <class T> static constexpr bool get(decltype(T::kOrdered)*) { return T::kOrdered; }
+    template <class T> static constexpr bool get(...) { return ZK_SELL_VGATHER != 0; }
+    static constexpr bool value = get<E>(nullptr);
+};
+template <bool ORD>
 __device__ __forceinline__ double2 ld_gather_ord(const double2* p) {
-#if ZK_SELL_VGATHER
-    double2 v;
-    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-    return v;
-#else
-    return ld_gather(p);
-#endif
+    if constexpr (ORD && ZK_GATHER_MODE == 0) {
+        double2 v;
+        asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+        return v;
+    } else {
+        return ld_gather(p);
+    }
 }
 template <class Epi, int LP = ZK_DEFAULT_LP>
 __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
@@ -264,6 +274,7 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
     // epilogue (Epi::kPrePlace): wide epilogues (TFQMR T2/T4: 2-3 operands) measured faster at 2,
     // the one-operand BiCGStab epilogues at 0 (profiles/r01_sell.md)
     constexpr int PRE = pre_place<Epi>::value;
+    constexpr bool ORD = sell_ordered<Epi>::value;
     constexpr bool AHEAD = PRE == 0 && pre_ahead<Epi>::value;
     const uint64_t pol = make_policy<LP>();
     double acc[KA];
@@ -334,7 +345,7 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
             }
             double2 xv[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather_ord(x + c[u]) : make_double2(0.0, 0.0);
+            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather_ord<ORD>(x + c[u]) : make_double2(0.0, 0.0);
 #pragma unroll
             for (int u = 0; u < U; u++)
                 if (c[u] >= 0) cfma(sum, v[u], xv[u]);
@@ -362,18 +373,23 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
 #if ZK_SELL_WSYNC
             __syncwarp();  // the batch's matrix loads stay ahead of its gathers in the schedule
 #endif
-#if ZK_SELL_DEP
             // every gather address depends on the batch's LAST column load (an opaque 0), so the
             // scheduler cannot start a gather — and stall on its column — before all U (value,
             // column) loads of the batch are in flight
-            int dep;
-            asm("{.reg .pred q; setp.eq.s32 q, %1, 2147483647; selp.b32 %0, 1, 0, q;}" : "=r"(dep) : "r"(c[U - 1]));
-#else
-            const int dep = 0;
-#endif
+            int dep = 0;
+            if constexpr (ORD) {
+                // ORD: every gather waits for ALL U column loads (an opaque 0 computed from their
+                // AND), so ptxas has to issue the whole batch before the first gather
+                int m = c[0];
+#pragma unroll
+                for (int u = 1; u < U; u++) m &= c[u];
+                asm("{.reg .pred q; setp.eq.s32 q, %1, 2147483647; selp.b32 %0, 1, 0, q;}" : "=r"(dep) : "r"(m));
+            } else if constexpr (ZK_SELL_DEP != 0) {
+                asm("{.reg .pred q; setp.eq.s32 q, %1, 2147483647; selp.b32 %0, 1, 0, q;}" : "=r"(dep) : "r"(c[U - 1]));
+            }
             double2 xv[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather_ord(x + (c[u] + dep)) : make_double2(0.0, 0.0);
+            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather_ord<ORD>(x + (c[u] + dep)) : make_double2(0.0, 0.0);
 #pragma unroll
             for (int u = 0; u < U; u++)
                 if (c[u] >= 0) cfma(sum, v[u], xv[u]);

@@ -95,13 +95,44 @@ __device__ __forceinline__ int ld_mat(const int* p, uint64_t pol) {
 #ifndef ZK_LD_CLOBBER
 #define ZK_LD_CLOBBER : "memory"
 #endif
+#ifndef ZK_LDV_POLICY
+#define ZK_LDV_POLICY 0
+#endif
 __device__ __forceinline__ double2 ld_stream_rw(const double2* p) {
     double2 v;
-    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) ZK_LD_CLOBBER);
+    if constexpr (ZK_LDV_POLICY == 1) {
+        uint64_t pol;
+        asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol) ZK_LD_CLOBBER);
+    } else {
+        asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) ZK_LD_CLOBBER);
+    }
     return v;
 }
 // Gather through the read-only path (L1 + L2 reuse of x across neighbouring rows).
-__device__ __forceinline__ double2 ld_gather(const double2* p) { return __ldg(p); }
+// Gather of x (ZK_GATHER_MODE): 2 (default) read-only path with an L2 evict_last policy; 0 plain
+// __ldg; 1 coherent ld.global.  In the solver loops x (p, s, y1, ...) was written by the previous
+// kernel and sits dirty in L2: with evict_normal gathers the matrix stream evicted x lines that
+// were gathered again later (C4 zk_zcsrmv after a rewrite of x: 811 µs at mode 0, 656 µs at
+// mode 2, 647 µs on a clean x either way; tools/inloop_probe.py).
+#ifndef ZK_GATHER_MODE
+#define ZK_GATHER_MODE 2
+#endif
+__device__ __forceinline__ double2 ld_gather(const double2* p) {
+    if constexpr (ZK_GATHER_MODE == 1) {
+        double2 v;
+        asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+        return v;
+    } else if constexpr (ZK_GATHER_MODE == 2) {
+        double2 v;
+        uint64_t pol;
+        asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+        return v;
+    } else {
+        return __ldg(p);
+    }
+}
 // Coherent loads for data written earlier in the SAME launch (the persistent solver phases,
 // separated by grid-wide barriers whose gpu-scope fences invalidate L1): never .nc.
 __device__ __forceinline__ double2 ld_gather_coh(const double2* p) {
@@ -110,6 +141,27 @@ __device__ __forceinline__ double2 ld_gather_coh(const double2* p) {
     return v;
 }
 __device__ __forceinline__ double2 ld_vec(const double2* p) { return ld_stream_rw(p); }
+// Vector stores of the solver kernels.  ZK_ST_POLICY: 0 plain write-back; 1 .cs (streaming,
+// evict-first); 2 L2::evict_first hint; 3 L2::evict_last hint.
+#ifndef ZK_ST_POLICY
+#define ZK_ST_POLICY 0
+#endif
+__device__ __forceinline__ void st_vec(double2* p, double2 v) {
+    if constexpr (ZK_ST_POLICY == 1) {
+        asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
+    } else if constexpr (ZK_ST_POLICY == 4) {
+        asm volatile("st.global.wt.v2.f64 [%0], {%1, %2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
+    } else if constexpr (ZK_ST_POLICY == 2 || ZK_ST_POLICY == 3) {
+        uint64_t pol;
+        if constexpr (ZK_ST_POLICY == 2)
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        else
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" :: "l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+    } else {
+        *p = v;
+    }
+}
 // Coherent L2 load (partials written by other blocks of the same launch).
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
