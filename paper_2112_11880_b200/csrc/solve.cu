@@ -490,7 +490,9 @@ struct EpiK3Bicg {  // t = A s ; {⟨t, s⟩, ⟨t, t⟩}
 // matrix loads gets interleaved with the gathers at the 80-register cap), the extra pass over
 // two vectors ≈ 40 µs: BiCGStab 1.83 vs 1.90 ms per iteration.  Below kSplitRows the two extra
 // launches per iteration cost more than they save (latency-bound sizes), so the fused kernels stay.
-constexpr int64_t kSplitRows = 1 << 20;
+// At the paper's largest shapes the split wins too: Audi3D-4 (C3, 648,849 rows) BiCGStab 169 vs
+// 176 µs per iteration, Twingo3D-2 (479,169 rows) 134 vs 137 µs (profiles/r01_c3_split.txt).
+constexpr int64_t kSplitRows = 1 << 18;
 #ifndef ZK_STORE_ORD
 #define ZK_STORE_ORD 1
 #endif
