@@ -341,6 +341,9 @@ extern "C" zk_status zk_csr_destroy(zk_csr A) {
         cudaFree(A->val);
     }
     if (A->cap_stream) cudaStreamDestroy(A->cap_stream);
+    if (A->pinned) cudaFreeHost(A->pinned);
+    for (auto& e : A->ev)
+        if (e) cudaEventDestroy(e);
     delete A;
     return ZK_OK;
 }

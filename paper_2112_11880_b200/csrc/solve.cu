@@ -25,6 +25,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <vector>
 
 #include <cooperative_groups.h>
 
@@ -1674,26 +1676,35 @@ __global__ void __launch_bounds__(kBlock, 2) k_persist_cg(SolveCtx* c) {
 }
 
 // ------------------------------------------------------------------ cluster solver (loop mode 5)
-// Small systems (the paper's Audi/Twingo shapes) are latency-bound: a WHILE-graph
-// iteration of 5 kernels costs ≈ 40 µs there, mostly dependent global-memory round trips of the
-// grid reductions and kernel boundaries.  Mode 5 runs the whole BiCGStab loop in ONE thread-block
-// cluster (up to 16 CTAs × 1024 threads on one GPC): each thread owns fixed rows/elements in every
-// phase (so own-row data needs no cross-CTA ordering), gathers of vectors written by other CTAs go
-// through L2 (ld.global.cg) after a cluster barrier, every reduction is a block reduction into a
-// shared-memory slot + one cluster barrier + a rank-ordered sum of the slots over distributed
-// shared memory, and every CTA runs the scalar step (the same fin_* functions) on its own
-// shared-memory copy of the context — identical totals in identical order give identical scalars,
-// so nothing is broadcast and the loop never touches global memory for control.
+// Small systems (the paper's Audi/Twingo shapes) are latency-bound: a WHILE-graph iteration of 5
+// kernels costs ≈ 34-36 µs there, mostly kernel boundaries and the dependent global-memory round
+// trips of the grid reductions.  Mode 5 runs the whole BiCGStab loop in ONE thread-block cluster
+// (16 CTAs × 512 threads, non-portable size; 8 if 16 cannot be scheduled):
+//  * rows are split into CS contiguous blocks, one per CTA; the CTA keeps its rows' entries of
+//    x, r, r̂, p, v, s, t in shared memory for the whole solve (only p and s, which other CTAs
+//    gather, are also written to global memory), and copies its block's column indices and row
+//    offsets — and its values too when they fit — into shared memory once at the start, so a
+//    SpMV chunk costs one L2 round trip (the gathers, with the values alongside) instead of two;
+//  * the SpMV phases give each row W lanes (W ∈ {8, 4, 2, 1}, chosen on the host to minimise
+//    passes × chunks per lane), each lane issuing all its loads of a chunk before using them;
+//    gathers read p / s (L1-cacheable weak loads) after the cluster barrier that published them;
+//  * every reduction is a block reduction into a shared-memory slot, one cluster barrier, and a
+//    fixed-order sum of the CS slots: lane r of warp 0 reads rank r's slot over distributed shared
+//    memory (one round trip instead of CS), then a fixed xor tree.  Every CTA runs the scalar step
+//    (the same fin_* functions) on its own shared-memory copy of the context — identical inputs in
+//    identical order give identical scalars, so nothing is broadcast and the loop never touches
+//    global memory for control.
 #ifndef ZK_CBLOCK
 #define ZK_CBLOCK 512
 #endif
 constexpr int kCBlock = ZK_CBLOCK;
 constexpr int kCWarps = kCBlock / 32;
-constexpr int64_t kClusterRows = 65536;   // mode 5 possible up to this size (ZK_LOOP_MODE=5)
-constexpr int64_t kClusterDefaultRows = 4096;  // and the default up to this size: measured per
-// iteration (incl. init/true-residual overhead) C1 33.7 vs 40.1 µs for the WHILE graph, but C2
-// 43.1 vs 39.3 and T0 36.4 vs 34.3 — the thread-per-row SpMV's dependent L2 round trips (7 chunks
-// of 4 entries per row) outweigh the saved kernel boundaries once rows exceed one round
+constexpr int kCVecs = 7;                        // x r r̂ p v s t: own rows in shared memory
+constexpr int kCSmemMax = 216 * 1024;            // dynamic shared memory: own rows + the block's matrix
+#ifndef ZK_CLUSTER_DEFAULT_ROWS
+#define ZK_CLUSTER_DEFAULT_ROWS 16384
+#endif
+constexpr int64_t kClusterDefaultRows = ZK_CLUSTER_DEFAULT_ROWS;  // default up to this size
 
 struct ClusterRed {
     double slot[2][kMaxRed];      // this CTA's partial sums, double-buffered across reductions
@@ -1702,7 +1713,7 @@ struct ClusterRed {
     int parity;
 };
 
-// cluster-wide sum of K doubles; result in R.tot (valid after return, all threads)
+// cluster-wide sum of K doubles; result in R.tot (valid after the caller's __syncthreads)
 template <int K>
 __device__ __forceinline__ void cl_sum(double (&v)[K], ClusterRed& R) {
     namespace cg = cooperative_groups;
@@ -1726,77 +1737,131 @@ __device__ __forceinline__ void cl_sum(double (&v)[K], ClusterRed& R) {
         }
     }
     cl.sync();  // release/acquire at cluster scope: slots (and this phase's global writes) visible
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
         const unsigned ncta = cl.num_blocks();
         double t[K];
+        if ((unsigned)lane < ncta) {
+            const double* rs = cl.map_shared_rank(&R.slot[par][0], lane);
 #pragma unroll
-        for (int k = 0; k < K; k++) t[k] = 0.0;
-        for (unsigned r = 0; r < ncta; r++) {  // fixed rank order
-            const double* rs = cl.map_shared_rank(&R.slot[par][0], r);
+            for (int k = 0; k < K; k++) t[k] = rs[k];
+        } else {
 #pragma unroll
-            for (int k = 0; k < K; k++) t[k] += rs[k];
+            for (int k = 0; k < K; k++) t[k] = 0.0;
         }
+        warp_sum<K>(t);  // fixed xor tree: every CTA forms lane 0's total in the same order
+        if (lane == 0) {
 #pragma unroll
-        for (int k = 0; k < K; k++) R.tot[k] = t[k];
-        R.parity = par ^ 1;
+            for (int k = 0; k < K; k++) R.tot[k] = t[k];
+            R.parity = par ^ 1;
+        }
     }
 }
 
-// y_i = Σ val·x[col] for row i (CSR, stored order, 4 entries in flight); x gathered through L2
-__device__ __forceinline__ double2 cl_row(const CsrDev& A, const double2* x, int64_t i) {
-    const int64_t rs = A.row_ptr[i], re = A.row_ptr[i + 1];
+// Gather of p / s inside the cluster solver: a weak load that may hit L1.  Correct because every
+// phase that reads them starts after a cluster barrier (acquire at cluster scope, which also
+// invalidates L1), and nothing writes them during the reading phase.  A CTA's rows gather from a
+// window near its own block (FE bandwidth), which fits L1 next to the shared-memory carve-out.
+__device__ __forceinline__ double2 ld_l1(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.ca.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
+// own row l of A·x on W lanes (sub = lane within the row's group): columns (and values when VS)
+// from the CTA's shared-memory copy, x gathered through L2.  valid == false: the lanes take part
+// in the shuffles only.
+template <int W, bool VS>
+__device__ __forceinline__ double2 cl_row(const double2* __restrict__ gval, const double2* sval, const int* scol,
+                                          const int* soff, const double2* x, int l, bool valid, int sub) {
+    constexpr int U = 4;  // 8 spills at the 128-register cap of 512-thread CTAs
     double2 sum = make_double2(0.0, 0.0);
-    for (int64_t p = rs; p < re; p += 4) {
-        double2 v[4];
-        int c[4];
+    if (valid) {
+        const int rs = soff[l], re = soff[l + 1];
+        for (int p0 = rs + sub; p0 < re; p0 += U * W) {
+            double2 v[U], xv[U];
+            int c[U];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            if (p + u < re) {
-                v[u] = __ldg(A.val + p + u);
-                c[u] = __ldg(A.col + p + u);
-            } else {
-                c[u] = -1;
+            for (int u = 0; u < U; u++) c[u] = p0 + u * W < re ? scol[p0 + u * W] : -1;
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (c[u] >= 0) {
+                    v[u] = VS ? sval[p0 + u * W] : __ldg(gval + p0 + u * W);
+                    xv[u] = ld_l1(x + c[u]);
+                }
             }
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (c[u] >= 0) cfma(sum, v[u], xv[u]);
         }
-        double2 xv[4];
+    }
 #pragma unroll
-        for (int u = 0; u < 4; u++) xv[u] = c[u] >= 0 ? __ldcg(x + c[u]) : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int u = 0; u < 4; u++)
-            if (c[u] >= 0) cfma(sum, v[u], xv[u]);
+    for (int o = W / 2; o > 0; o >>= 1) {
+        sum.x += __shfl_xor_sync(0xffffffffu, sum.x, o, W);
+        sum.y += __shfl_xor_sync(0xffffffffu, sum.y, o, W);
     }
     return sum;
 }
 
-__global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, const CsrDev A) {
+// dynamic shared memory: kCVecs × rpc vectors | [values nnz_max] | columns nnz_max | offsets rpc + 1
+template <int W, bool VS>
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, const CsrDev A, int nnz_max) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double2 own[];
     __shared__ SolveCtx cs;
     __shared__ ClusterRed R;
     if (threadIdx.x == 0) {
         cs = *gctx;
         R.parity = 0;
     }
+    const int n = (int)A.n_rows;
+    const int ncta = (int)cl.num_blocks();
+    const int rpc = (n + ncta - 1) / ncta;
+    const int row0 = (int)cl.block_rank() * rpc;
+    const int nr = max(0, min(rpc, n - row0));
+    double2 *X = own, *Rv = own + rpc, *RH = own + 2 * rpc, *P = own + 3 * rpc, *V = own + 4 * rpc,
+            *S = own + 5 * rpc, *T = own + 6 * rpc;
+    double2* sval = own + kCVecs * rpc;
+    int* scol = (int*)(sval + (VS ? nnz_max : 0));
+    int* soff = scol + nnz_max;
     __syncthreads();
     SolveCtx* c = &cs;
-    const int64_t n = A.n_rows;
-    const int64_t nt = (int64_t)cl.num_blocks() * kCBlock;
-    const int64_t g0 = (int64_t)cl.block_rank() * kCBlock + threadIdx.x;
-    double2 *x = cs.x, *r = cs.r, *p = cs.p, *v = cs.v, *s = cs.s, *t = cs.t;
-    const double2* rh = cs.rh;
+    double2 *xg = cs.x, *pg = cs.p, *sg = cs.s;
+    for (int l = threadIdx.x; l < nr; l += kCBlock) {  // r0, r̂, p, x0 from the init kernel
+        X[l] = xg[row0 + l];
+        Rv[l] = cs.r[row0 + l];
+        RH[l] = cs.rh[row0 + l];
+        P[l] = pg[row0 + l];
+    }
+    const int64_t nz0 = nr > 0 ? A.row_ptr[row0] : 0;
+    const int nnz_cta = nr > 0 ? (int)(A.row_ptr[row0 + nr] - nz0) : 0;
+    for (int l = threadIdx.x; l <= nr; l += kCBlock) soff[l] = nr > 0 ? (int)(A.row_ptr[row0 + l] - nz0) : 0;
+    for (int q = threadIdx.x; q < nnz_cta; q += kCBlock) {
+        scol[q] = A.col[nz0 + q];
+        if (VS) sval[q] = A.val[nz0 + q];
+    }
+    const double2* gval = A.val + nz0;
+    __syncthreads();
+    constexpr int RPP = kCBlock / W;  // rows per SpMV pass
+    const int sub = threadIdx.x & (W - 1);
+    const int grp = threadIdx.x / W;
     int bodies = 0;
     while (!c->done) {
         {   // K1: v = A p ; σ = ⟨r̂, v⟩, ‖v‖²
             double acc[3] = {0.0, 0.0, 0.0};
-            for (int64_t i = g0; i < n; i += nt) {
-                const double2 y = cl_row(A, p, i);
-                v[i] = y;
-                const double2 q = rh[i];
-                acc[0] = fma(q.x, y.x, fma(q.y, y.y, acc[0]));
-                acc[1] = fma(q.x, y.y, fma(-q.y, y.x, acc[1]));
-                acc[2] += cabs2(y);
+            for (int b = 0; b < nr; b += RPP) {
+                const int l = b + grp;
+                const double2 y = cl_row<W, VS>(gval, sval, scol, soff, pg, l, l < nr, sub);
+                if (sub == 0 && l < nr) {
+                    V[l] = y;
+                    const double2 q = RH[l];
+                    acc[0] = fma(q.x, y.x, fma(q.y, y.y, acc[0]));
+                    acc[1] = fma(q.x, y.y, fma(-q.y, y.x, acc[1]));
+                    acc[2] += cabs2(y);
+                }
             }
             cl_sum<3>(acc, R);
+            __syncthreads();
             if (threadIdx.x == 0) fin_k1_bicg(c, R.tot);
             __syncthreads();
             if (c->done) break;
@@ -1804,40 +1869,43 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
         {   // K2: s = r − α v ; ‖s‖²
             const double2 al = c->alpha;
             double acc[1] = {0.0};
-            for (int64_t i = g0; i < n; i += nt) {
-                const double2 vi = v[i];
-                double2 o = r[i];
+            for (int l = threadIdx.x; l < nr; l += kCBlock) {
+                const double2 vi = V[l];
+                double2 o = Rv[l];
                 o.x = fma(-al.x, vi.x, fma(al.y, vi.y, o.x));
                 o.y = fma(-al.x, vi.y, fma(-al.y, vi.x, o.y));
-                s[i] = o;
+                S[l] = o;
+                sg[row0 + l] = o;
                 acc[0] += cabs2(o);
             }
-            cl_sum<1>(acc, R);
+            cl_sum<1>(acc, R);  // its cluster barrier also publishes s for the K3 gathers
+            __syncthreads();
             if (threadIdx.x == 0) fin_k2_bicg(c, R.tot);
             __syncthreads();
             if (c->done) {  // half-step exit: x += α p
                 if (c->half) {
-                    for (int64_t i = g0; i < n; i += nt) {
-                        double2 xi = x[i];
-                        cfma(xi, al, p[i]);
-                        x[i] = xi;
-                    }
+                    for (int l = threadIdx.x; l < nr; l += kCBlock) cfma(X[l], al, P[l]);
+                    __syncthreads();
                     if (threadIdx.x == 0) c->half = 0;
                 }
                 break;
             }
         }
-        {   // K3: t = A s ; ⟨t, s⟩, ‖t‖²   (s complete: the K2 reduction's cluster barrier)
+        {   // K3: t = A s ; ⟨t, s⟩, ‖t‖²
             double acc[3] = {0.0, 0.0, 0.0};
-            for (int64_t i = g0; i < n; i += nt) {
-                const double2 y = cl_row(A, s, i);
-                t[i] = y;
-                const double2 si = s[i];
-                acc[0] = fma(y.x, si.x, fma(y.y, si.y, acc[0]));
-                acc[1] = fma(y.x, si.y, fma(-y.y, si.x, acc[1]));
-                acc[2] += cabs2(y);
+            for (int b = 0; b < nr; b += RPP) {
+                const int l = b + grp;
+                const double2 y = cl_row<W, VS>(gval, sval, scol, soff, sg, l, l < nr, sub);
+                if (sub == 0 && l < nr) {
+                    T[l] = y;
+                    const double2 si = S[l];
+                    acc[0] = fma(y.x, si.x, fma(y.y, si.y, acc[0]));
+                    acc[1] = fma(y.x, si.y, fma(-y.y, si.x, acc[1]));
+                    acc[2] += cabs2(y);
+                }
             }
             cl_sum<3>(acc, R);
+            __syncthreads();
             if (threadIdx.x == 0) fin_k3_bicg(c, R.tot);
             __syncthreads();
             if (c->done) break;
@@ -1845,41 +1913,44 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
         {   // K4: x += α p + ω s ; r = s − ω t ; ‖r‖², ⟨r̂, r⟩
             const double2 al = c->alpha, om = c->omega;
             double acc[3] = {0.0, 0.0, 0.0};
-            for (int64_t i = g0; i < n; i += nt) {
-                const double2 si = s[i], ti = t[i];
-                double2 xi = x[i];
-                cfma(xi, al, p[i]);
+            for (int l = threadIdx.x; l < nr; l += kCBlock) {
+                const double2 si = S[l], ti = T[l];
+                double2 xi = X[l];
+                cfma(xi, al, P[l]);
                 cfma(xi, om, si);
-                x[i] = xi;
+                X[l] = xi;
                 double2 rn = si;
                 rn.x = fma(-om.x, ti.x, fma(om.y, ti.y, rn.x));
                 rn.y = fma(-om.x, ti.y, fma(-om.y, ti.x, rn.y));
-                r[i] = rn;
-                const double2 q = rh[i];
+                Rv[l] = rn;
+                const double2 q = RH[l];
                 acc[0] += cabs2(rn);
                 acc[1] = fma(q.x, rn.x, fma(q.y, rn.y, acc[1]));
                 acc[2] = fma(q.x, rn.y, fma(-q.y, rn.x, acc[2]));
             }
             cl_sum<3>(acc, R);
+            __syncthreads();
             if (threadIdx.x == 0) fin_k4_bicg(c, R.tot);
             __syncthreads();
             if (c->done) break;
         }
         {   // K5: p = r + β (p − ω v), then a cluster barrier (p is gathered by K1)
             const double2 be = c->beta, om = c->omega;
-            for (int64_t i = g0; i < n; i += nt) {
-                const double2 vi = v[i];
-                double2 d = p[i];
+            for (int l = threadIdx.x; l < nr; l += kCBlock) {
+                const double2 vi = V[l];
+                double2 d = P[l];
                 d.x = fma(-om.x, vi.x, fma(om.y, vi.y, d.x));
                 d.y = fma(-om.x, vi.y, fma(-om.y, vi.x, d.y));
-                double2 o = r[i];
+                double2 o = Rv[l];
                 cfma(o, be, d);
-                p[i] = o;
+                P[l] = o;
+                pg[row0 + l] = o;
             }
             cl.sync();
         }
         bodies++;
     }
+    for (int l = threadIdx.x; l < nr; l += kCBlock) xg[row0 + l] = X[l];  // the solution leaves shared memory
     if (cl.block_rank() == 0 && threadIdx.x == 0) {
         cs.bodies = bodies;
         *gctx = cs;
@@ -1887,17 +1958,50 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
     cl.sync();  // no CTA leaves while another may still read its reduction slots
 }
 
+// lanes per row of the cluster SpMV: minimise passes × chunks per lane (ties: more lanes)
+static int cluster_w(int64_t n, int cs, int max_len) {
+    const int64_t rpc = (n + cs - 1) / cs;
+    int best = 8;
+    int64_t best_cost = INT64_MAX;
+    for (int w : {8, 4, 2, 1}) {
+        const int64_t passes = (rpc + kCBlock / w - 1) / (kCBlock / w);
+        const int64_t chunks = ((max_len + w - 1) / w + 3) / 4;  // cl_row: U = 4 entries per lane per chunk
+        const int64_t cost = passes * (chunks < 1 ? 1 : chunks);
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = w;
+        }
+    }
+    return best;
+}
+template <int W>
+static const void* cluster_kernel(bool vs) {
+    return vs ? (const void*)k_cluster_bicg<W, true> : (const void*)k_cluster_bicg<W, false>;
+}
+static const void* cluster_kernel(int w, bool vs) {
+    return w == 8 ? cluster_kernel<8>(vs) : w == 4 ? cluster_kernel<4>(vs) : w == 2 ? cluster_kernel<2>(vs) : cluster_kernel<1>(vs);
+}
+static size_t cluster_smem(int64_t n, int cs, int64_t nnz_max, bool vs) {
+    const int64_t rpc = (n + cs - 1) / cs;
+    return (size_t)(kCVecs * 16 * rpc + (vs ? 16 : 0) * nnz_max + 4 * nnz_max + 4 * (rpc + 1));
+}
+
 // cluster size that can be launched on this device: 16 (non-portable), else 8, else 0
 static int cluster_size_available() {
     static int cached = -1;  // per process
     if (cached < 0) {
         cached = 0;
-        cudaFuncSetAttribute((const void*)k_cluster_bicg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        for (int w : {1, 2, 4, 8})
+            for (bool vs : {false, true}) {
+                cudaFuncSetAttribute(cluster_kernel(w, vs), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                cudaFuncSetAttribute(cluster_kernel(w, vs), cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmemMax);
+            }
         for (int cs : {16, 8}) {
             cudaLaunchConfig_t cfg;
             memset(&cfg, 0, sizeof cfg);
             cfg.gridDim = dim3(cs);
             cfg.blockDim = dim3(kCBlock);
+            cfg.dynamicSmemBytes = kCSmemMax;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
             at[0].val.clusterDim.x = cs;
@@ -1906,7 +2010,7 @@ static int cluster_size_available() {
             cfg.attrs = at;
             cfg.numAttrs = 1;
             int nclusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)k_cluster_bicg, &cfg) == cudaSuccess &&
+            if (cudaOccupancyMaxActiveClusters(&nclusters, cluster_kernel(1, false), &cfg) == cudaSuccess &&
                 nclusters >= 1) {
                 cached = cs;
                 break;
@@ -1916,27 +2020,61 @@ static int cluster_size_available() {
     }
     return cached;
 }
-// launch the cluster solver on one cluster; false when unavailable
-static bool cluster_launch(SolveCtx* dc, const CsrDev& av, cudaStream_t s, int* out_cs) {
-    const int cached = cluster_size_available();
-    if (cached == 0) return false;
+
+// most nonzeros in one CTA's row block (one-off: CS + 1 row-pointer reads, cached in the handle)
+static int64_t cluster_nnz_max(zk_csr_s* A, int cs, cudaStream_t s) {
+    if (A->cl_cs == cs && A->cl_nnz_max >= 0) return A->cl_nnz_max;
+    const int64_t n = A->n_rows, rpc = (n + cs - 1) / cs;
+    std::vector<int64_t> rp(cs + 1, 0);
+    for (int k = 0; k <= cs; k++) {
+        const int64_t i = std::min<int64_t>((int64_t)k * rpc, n);
+        if (cudaMemcpyAsync(&rp[k], A->row_ptr + i, sizeof(int64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess) return -1;
+    }
+    if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+    int64_t mx = 0;
+    for (int k = 0; k < cs; k++) mx = std::max(mx, rp[k + 1] - rp[k]);
+    A->cl_cs = cs;
+    A->cl_nnz_max = mx;
+    return mx;
+}
+// can the cluster solver hold this system (own rows + the block's columns in shared memory)?
+static bool cluster_fits(zk_csr_s* A, cudaStream_t s) {
+    const int cs = cluster_size_available();
+    if (cs == 0 || A->n_rows == 0 || A->n_rows > (int64_t)cs * (kCSmemMax / (kCVecs * 16))) return false;
+    const int64_t nz = cluster_nnz_max(A, cs, s);
+    return nz >= 0 && cluster_smem(A->n_rows, cs, nz, false) <= (size_t)kCSmemMax;
+}
+
+// launch the cluster solver on one cluster (A or A·M⁻¹ in av); false when unavailable
+static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStream_t s, int* out_cs) {
+    const int cs = cluster_size_available();
+    if (cs == 0) return false;
+    const int64_t nz = cluster_nnz_max(A, cs, s);
+    if (nz < 0) return false;
+    const bool vs = cluster_smem(av.n_rows, cs, nz, true) <= (size_t)kCSmemMax;
+    const int w = cluster_w(av.n_rows, cs, A->max_len);
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof cfg);
-    cfg.gridDim = dim3(cached);
+    cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(kCBlock);
+    cfg.dynamicSmemBytes = cluster_smem(av.n_rows, cs, nz, vs);
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cached;
+    at[0].val.clusterDim.x = cs;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, k_cluster_bicg, dc, av) != cudaSuccess) {
+    void* args[] = {(void*)&dc, (void*)&av, (void*)&nz};
+    int nzi = (int)nz;
+    args[2] = &nzi;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, cluster_kernel(w, vs), args);
+    if (e != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
-    *out_cs = cached;
+    *out_cs = cs;
     return true;
 }
 
@@ -2349,8 +2487,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         int m = atoi(e);
         if (m >= 1 && m <= 5) mode = m;
     }
-    if (mode == 5 && (A->dist || method != ZK_BICGSTAB || A->n_rows > kClusterRows || A->n_rows == 0 ||
-                      cluster_size_available() == 0))
+    if (mode == 5 && (A->dist || method != ZK_BICGSTAB || !cluster_fits(A, (cudaStream_t)stream)))
         mode = A->dist ? 3 : 1;
     if (A->dist && (mode == 1 || mode == 4 || mode == 5)) mode = 3;  // NCCL inside WHILE bodies / persistent kernels is not used
     int persist_grid = 0;
@@ -2402,9 +2539,17 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     hc.use_cond = mode == 1 ? 1 : 0;
     hc.cond = mode == 1 ? gc.cond : 0ull;
 
-    cudaEvent_t ev0, ev1;
-    ZK_CUDA(cudaEventCreate(&ev0));
-    ZK_CUDA(cudaEventCreate(&ev1));
+    for (auto& e : A->ev)
+        if (!e) ZK_CUDA(cudaEventCreate(&e));
+    cudaEvent_t ev0 = A->ev[0], ev1 = A->ev[1];
+    const size_t rb_bytes = sizeof(SolveCtx) + sizeof(double) * ((size_t)maxit + 1);
+    if (A->pinned_bytes < rb_bytes) {  // pinned readback staging, grown on demand
+        if (A->pinned) cudaFreeHost(A->pinned);
+        A->pinned = nullptr;
+        A->pinned_bytes = 0;
+        ZK_CUDA(cudaMallocHost(&A->pinned, rb_bytes));
+        A->pinned_bytes = rb_bytes;
+    }
     ZK_CUDA(cudaEventRecord(ev0, s));
     int64_t n_spmv = 0;
 
@@ -2482,7 +2627,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         ZK_CUDA(cudaLaunchCooperativeKernel(kp, dim3(persist_grid), dim3(kBlock), args, 0, s));
     } else if (mode == 5) {
         int csz = 0;
-        if (!cluster_launch(dc, hc.A, s, &csz)) return fail(ZK_ERR_CUDA, "cluster solver launch failed");
+        if (!cluster_launch(A, dc, hc.A, s, &csz)) return fail(ZK_ERR_CUDA, "cluster solver launch failed");
     } else {
         ZK_CUDA(cudaMallocHost(&hdone, sizeof(SolveCtx)));
         int launched = 0;
@@ -2523,15 +2668,16 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     ZK_CUDA(cudaEventRecord(ev1, s));
 
     SolveCtx out;
-    ZK_CUDA(cudaMemcpyAsync(&out, dc, sizeof(SolveCtx), cudaMemcpyDeviceToHost, s));
-    ZK_CUDA(cudaMemcpyAsync(resid_hist, hc.hist, sizeof(double) * ((size_t)maxit + 1), cudaMemcpyDeviceToHost, s));
+    double* hist_pinned = (double*)((char*)A->pinned + sizeof(SolveCtx));
+    ZK_CUDA(cudaMemcpyAsync(A->pinned, dc, sizeof(SolveCtx), cudaMemcpyDeviceToHost, s));
+    ZK_CUDA(cudaMemcpyAsync(hist_pinned, hc.hist, sizeof(double) * ((size_t)maxit + 1), cudaMemcpyDeviceToHost, s));
     cudaError_t e = cudaStreamSynchronize(s);
     if (hdone) cudaFreeHost(hdone);
     if (e != cudaSuccess) return cuda_fail(e, "zk_solve", __FILE__, __LINE__);
+    memcpy(&out, A->pinned, sizeof(SolveCtx));
+    memcpy(resid_hist, hist_pinned, sizeof(double) * ((size_t)maxit + 1));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ev0, ev1);
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
 
     *iters = out.iters;
     const int passes = out.iters;

@@ -71,6 +71,14 @@ struct zk_csr_s {
     int max_len = 0;
     double mean_len = 0.0;
     zk::DeviceInfo dev;
+    // cluster solver (loop mode 5): the most nonzeros of one CTA's row block at cluster size cl_cs
+    int cl_cs = 0;
+    int64_t cl_nnz_max = -1;
+    // zk_solve readback: pinned host staging for the context + residual history (one stream sync,
+    // no pageable copies) and the two timing events, kept across solves
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaStream_t cap_stream = nullptr;  // private stream used for graph capture
     zk::GraphCache graph[8];            // per solver method code (ZK_BICGSTAB .. ZK_TFQMR)
     zk_comm_s* comm = nullptr;
