@@ -326,6 +326,36 @@ def main():
                            "gbs": step_bytes(ms_["n"], ms_["nnz"], rs_["iters"]) / (t_ms * 1e-3) / 1e9}
             As.close()
 
+    # PAPER.md T9/T10 context: the paper's three solvers (P-BiCGSTAB → Jacobi-BiCGStab, P-TFQMR →
+    # TFQMR, P-BiCGSTAB(8) → BiCGStab(8)) at the paper's tol 1e-9, x0 = 0 (reading L10) on
+    # the T1 shapes; iteration counts are not comparable (synthetic matrices, L8), per-iteration times
+    # are shown beside the paper's derived K20c ms/iteration
+    table9 = None
+    if world == 1 and not a.no_shapes:
+        table9 = {}
+        k20c = {"C1": 1.43, "C2": 2.00, "T0": 1.79, "C3": 50.3, "C3T": 37.7}  # P-BiCGSTAB ms/iter (T9/T10, derived)
+        for cfg in ("C1", "T0", "C2", "C3", "C3T"):
+            ms_ = gen.make_matrix(cfg)
+            As = zk.csr_create(ms_["row_ptr"], ms_["col_idx"], ms_["values"], ms_["n"])
+            bs = torch.from_numpy(gen.make_rhs(ms_)).to(dev)
+            row = {"n": ms_["n"], "nnz": ms_["nnz"], "k20c_p_bicgstab_ms_per_iter": k20c[cfg]}
+            for meth, ell, key in (("bicgstab_jacobi", 8, "p_bicgstab"), ("tfqmr", 8, "tfqmr"),
+                                   ("bicgstab_l", 8, "bicgstab8")):
+                wss = zk.alloc_workspace(As, meth, 1000, dev, ell)
+                rs_ = zk.solve(As, bs, None, 1e-9, 1000, meth, workspace=wss, stream=stream, ell=ell)
+                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                g0.record(stream)
+                for _ in range(3):
+                    rs_ = zk.solve(As, bs, None, 1e-9, 1000, meth, workspace=wss, stream=stream, ell=ell)
+                g1.record(stream)
+                torch.cuda.synchronize()
+                t_ms = g0.elapsed_time(g1) / 3
+                row[key] = {"iters": rs_["iters"], "status": rs_["status"], "time_to_tol_ms": t_ms,
+                            "ms_per_iteration": t_ms / max(rs_["iters"], 1), "loop_mode": rs_["loop_mode"]}
+                del wss
+            table9[cfg] = row
+            As.close()
+
     # the other solvers of the path on the same C4 system, after the timed
     # region: per-iteration time and counted GB/s of their fused kernels (one warm-up + 2 timed solves)
     methods = None
@@ -417,6 +447,7 @@ def main():
                          "vector_kernels_ms_per_iter": vec_ms / a.steps / iters},
             "spmv": spmv,
             "paper_shapes_bicgstab": shapes,
+            "paper_table9_solvers_tol1e-9": table9,
             "methods_c4": methods,
             "roofline": roofline,
             "cpu_baseline": cpu,

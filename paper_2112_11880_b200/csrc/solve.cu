@@ -1699,7 +1699,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_persist_cg(SolveCtx* c) {
 #endif
 constexpr int kCBlock = ZK_CBLOCK;
 constexpr int kCWarps = kCBlock / 32;
-constexpr int kCVecs = 7;                        // x r r̂ p v s t: own rows in shared memory
+constexpr int kCVecs = 7;                        // BiCGStab: x r r̂ p v s t own rows in shared memory
+constexpr int kCVecsTfqmr = 9;                   // TFQMR: x w y1 y2 u1 u2 v d r̃
 constexpr int kCSmemMax = 216 * 1024;            // dynamic shared memory: own rows + the block's matrix
 #ifndef ZK_CLUSTER_DEFAULT_ROWS
 #define ZK_CLUSTER_DEFAULT_ROWS 16384
@@ -1802,6 +1803,21 @@ __device__ __forceinline__ double2 cl_row(const double2* __restrict__ gval, cons
     return sum;
 }
 
+// The CTA's block of the matrix into shared memory (columns, row offsets relative to the block,
+// values when VS); returns the block's first value in global memory (used when !VS).
+template <bool VS>
+__device__ __forceinline__ const double2* cl_stage(const CsrDev& A, int row0, int nr, double2* sval, int* scol,
+                                                   int* soff) {
+    const int64_t nz0 = nr > 0 ? A.row_ptr[row0] : 0;
+    const int nnz_cta = nr > 0 ? (int)(A.row_ptr[row0 + nr] - nz0) : 0;
+    for (int l = threadIdx.x; l <= nr; l += kCBlock) soff[l] = nr > 0 ? (int)(A.row_ptr[row0 + l] - nz0) : 0;
+    for (int q = threadIdx.x; q < nnz_cta; q += kCBlock) {
+        scol[q] = A.col[nz0 + q];
+        if (VS) sval[q] = A.val[nz0 + q];
+    }
+    return A.val + nz0;
+}
+
 // dynamic shared memory: kCVecs × rpc vectors | [values nnz_max] | columns nnz_max | offsets rpc + 1
 template <int W, bool VS>
 __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, const CsrDev A, int nnz_max) {
@@ -1833,14 +1849,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
         RH[l] = cs.rh[row0 + l];
         P[l] = pg[row0 + l];
     }
-    const int64_t nz0 = nr > 0 ? A.row_ptr[row0] : 0;
-    const int nnz_cta = nr > 0 ? (int)(A.row_ptr[row0 + nr] - nz0) : 0;
-    for (int l = threadIdx.x; l <= nr; l += kCBlock) soff[l] = nr > 0 ? (int)(A.row_ptr[row0 + l] - nz0) : 0;
-    for (int q = threadIdx.x; q < nnz_cta; q += kCBlock) {
-        scol[q] = A.col[nz0 + q];
-        if (VS) sval[q] = A.val[nz0 + q];
-    }
-    const double2* gval = A.val + nz0;
+    const double2* gval = cl_stage<VS>(A, row0, nr, sval, scol, soff);
     __syncthreads();
     constexpr int RPP = kCBlock / W;  // rows per SpMV pass
     const int sub = threadIdx.x & (W - 1);
@@ -1958,6 +1967,168 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
     cl.sync();  // no CTA leaves while another may still read its reduction slots
 }
 
+// TFQMR (NEXT-2) in one cluster: the per-row arithmetic of OpT1/EpiT2/OpT3/EpiT4 and the same
+// scalar steps (fin_t1 / fin_t2 / fin_sigma), including the exits inside an iteration (half = 1:
+// only x += η1·d1 remains; half = 2: T3's d and x updates without y1).  y1 and y2 are gathered by
+// the SpMVs, so they are also written to global memory.
+template <int W, bool VS>
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, const CsrDev A, int nnz_max) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double2 own[];
+    __shared__ SolveCtx cs;
+    __shared__ ClusterRed R;
+    if (threadIdx.x == 0) {
+        cs = *gctx;
+        R.parity = 0;
+    }
+    const int n = (int)A.n_rows;
+    const int ncta = (int)cl.num_blocks();
+    const int rpc = (n + ncta - 1) / ncta;
+    const int row0 = (int)cl.block_rank() * rpc;
+    const int nr = max(0, min(rpc, n - row0));
+    double2 *X = own, *Wv = own + rpc, *Y1 = own + 2 * rpc, *Y2 = own + 3 * rpc, *U1 = own + 4 * rpc,
+            *U2 = own + 5 * rpc, *V = own + 6 * rpc, *D = own + 7 * rpc, *RT = own + 8 * rpc;
+    double2* sval = own + kCVecsTfqmr * rpc;
+    int* scol = (int*)(sval + (VS ? nnz_max : 0));
+    int* soff = scol + nnz_max;
+    __syncthreads();
+    SolveCtx* c = &cs;
+    double2 *xg = cs.x, *y1g = cs.y1, *y2g = cs.y2;
+    for (int l = threadIdx.x; l < nr; l += kCBlock) {  // state after the init kernel and K0
+        const int i = row0 + l;
+        X[l] = xg[i];
+        Wv[l] = cs.w[i];
+        Y1[l] = y1g[i];
+        U1[l] = cs.u1[i];
+        V[l] = cs.v[i];
+        D[l] = cs.d[i];
+        RT[l] = cs.rt[i];
+        U2[l] = make_double2(0.0, 0.0);
+        Y2[l] = make_double2(0.0, 0.0);
+    }
+    const double2* gval = cl_stage<VS>(A, row0, nr, sval, scol, soff);
+    __syncthreads();
+    constexpr int RPP = kCBlock / W;
+    const int sub = threadIdx.x & (W - 1);
+    const int grp = threadIdx.x / W;
+    int bodies = 0;
+    while (!c->done) {
+        {   // T1: y2 = y1 − α v ; w −= α u1 ; ‖w‖²
+            const double2 al = c->alpha;
+            double acc[1] = {0.0};
+            for (int l = threadIdx.x; l < nr; l += kCBlock) {
+                const double2 vv = V[l], uu = U1[l];
+                double2 o = Y1[l];
+                o.x = fma(-al.x, vv.x, fma(al.y, vv.y, o.x));
+                o.y = fma(-al.x, vv.y, fma(-al.y, vv.x, o.y));
+                Y2[l] = o;
+                y2g[row0 + l] = o;
+                double2 wn = Wv[l];
+                wn.x = fma(-al.x, uu.x, fma(al.y, uu.y, wn.x));
+                wn.y = fma(-al.x, uu.y, fma(-al.y, uu.x, wn.y));
+                Wv[l] = wn;
+                acc[0] += cabs2(wn);
+            }
+            cl_sum<1>(acc, R);  // also publishes y2 for the T2 gathers
+            __syncthreads();
+            if (threadIdx.x == 0) fin_t1_tfqmr(c, R.tot);
+            __syncthreads();
+            if (c->done) {
+                if (c->half == 1) {  // the first half step ended the loop: x += η1·d1, d1 = y1 + c1·d
+                    const double2 eta = c->eta1, coef = c->coef1;
+                    for (int l = threadIdx.x; l < nr; l += kCBlock) {
+                        double2 d1 = Y1[l];
+                        cfma(d1, coef, D[l]);
+                        cfma(X[l], eta, d1);
+                    }
+                }
+                break;
+            }
+        }
+        {   // T2: u2 = A y2 ; w −= α u2 ; ‖w‖², ⟨r̃, w⟩
+            const double2 al = c->alpha;
+            double acc[3] = {0.0, 0.0, 0.0};
+            for (int b = 0; b < nr; b += RPP) {
+                const int l = b + grp;
+                const double2 y = cl_row<W, VS>(gval, sval, scol, soff, y2g, l, l < nr, sub);
+                if (sub == 0 && l < nr) {
+                    U2[l] = y;
+                    double2 wn = Wv[l];
+                    wn.x = fma(-al.x, y.x, fma(al.y, y.y, wn.x));
+                    wn.y = fma(-al.x, y.y, fma(-al.y, y.x, wn.y));
+                    Wv[l] = wn;
+                    const double2 q = RT[l];
+                    acc[0] += cabs2(wn);
+                    acc[1] = fma(q.x, wn.x, fma(q.y, wn.y, acc[1]));
+                    acc[2] = fma(q.x, wn.y, fma(-q.y, wn.x, acc[2]));
+                }
+            }
+            cl_sum<3>(acc, R);
+            __syncthreads();
+            if (threadIdx.x == 0) fin_t2_tfqmr(c, R.tot);
+            __syncthreads();
+        }
+        {   // T3: d1 = y1 + c1·d ; d = y2 + c2·d1 ; x += η1·d1 + η2·d ; y1 = w + β y2 (not on exit)
+            const bool done = c->done != 0;
+            if (done && c->half != 2) break;
+            const double2 coef1 = c->coef1, coef2 = c->coef2, eta1 = c->eta1, eta2 = c->eta, be = c->beta;
+            for (int l = threadIdx.x; l < nr; l += kCBlock) {
+                double2 d1 = Y1[l];
+                cfma(d1, coef1, D[l]);
+                const double2 y2 = Y2[l];
+                double2 d2 = y2;
+                cfma(d2, coef2, d1);
+                double2 xn = X[l];
+                cfma(xn, eta1, d1);
+                cfma(xn, eta2, d2);
+                X[l] = xn;
+                D[l] = d2;
+                if (!done) {
+                    double2 o = Wv[l];
+                    cfma(o, be, y2);
+                    Y1[l] = o;
+                    y1g[row0 + l] = o;
+                }
+            }
+            if (done) break;
+            cl.sync();  // y1 complete for the T4 gathers
+        }
+        {   // T4: u1 = A y1 ; v = u1 + β(u2 + β v) ; σ = ⟨r̃, v⟩
+            const double2 be = c->beta;
+            double acc[2] = {0.0, 0.0};
+            for (int b = 0; b < nr; b += RPP) {
+                const int l = b + grp;
+                const double2 y = cl_row<W, VS>(gval, sval, scol, soff, y1g, l, l < nr, sub);
+                if (sub == 0 && l < nr) {
+                    U1[l] = y;
+                    double2 t = U2[l];
+                    cfma(t, be, V[l]);
+                    double2 vn = y;
+                    cfma(vn, be, t);
+                    V[l] = vn;
+                    const double2 q = RT[l];
+                    acc[0] = fma(q.x, vn.x, fma(q.y, vn.y, acc[0]));
+                    acc[1] = fma(q.x, vn.y, fma(-q.y, vn.x, acc[1]));
+                }
+            }
+            cl_sum<2>(acc, R);
+            __syncthreads();
+            if (threadIdx.x == 0) fin_sigma_tfqmr(c, R.tot);
+            __syncthreads();
+        }
+        bodies++;
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < nr; l += kCBlock) xg[row0 + l] = X[l];
+    if (cl.block_rank() == 0 && threadIdx.x == 0) {
+        cs.half = 0;
+        cs.bodies = bodies;
+        *gctx = cs;
+    }
+    cl.sync();
+}
+
 // lanes per row of the cluster SpMV: minimise passes × chunks per lane (ties: more lanes)
 static int cluster_w(int64_t n, int cs, int max_len) {
     const int64_t rpc = (n + cs - 1) / cs;
@@ -1975,15 +2146,18 @@ static int cluster_w(int64_t n, int cs, int max_len) {
     return best;
 }
 template <int W>
-static const void* cluster_kernel(bool vs) {
+static const void* cluster_kernel(bool vs, bool tfqmr) {
+    if (tfqmr) return vs ? (const void*)k_cluster_tfqmr<W, true> : (const void*)k_cluster_tfqmr<W, false>;
     return vs ? (const void*)k_cluster_bicg<W, true> : (const void*)k_cluster_bicg<W, false>;
 }
-static const void* cluster_kernel(int w, bool vs) {
-    return w == 8 ? cluster_kernel<8>(vs) : w == 4 ? cluster_kernel<4>(vs) : w == 2 ? cluster_kernel<2>(vs) : cluster_kernel<1>(vs);
+static const void* cluster_kernel(int w, bool vs, bool tfqmr = false) {
+    return w == 8 ? cluster_kernel<8>(vs, tfqmr) : w == 4 ? cluster_kernel<4>(vs, tfqmr)
+         : w == 2 ? cluster_kernel<2>(vs, tfqmr) : cluster_kernel<1>(vs, tfqmr);
 }
-static size_t cluster_smem(int64_t n, int cs, int64_t nnz_max, bool vs) {
+static int cluster_nvec(bool tfqmr) { return tfqmr ? kCVecsTfqmr : kCVecs; }
+static size_t cluster_smem(int64_t n, int cs, int64_t nnz_max, bool vs, bool tfqmr = false) {
     const int64_t rpc = (n + cs - 1) / cs;
-    return (size_t)(kCVecs * 16 * rpc + (vs ? 16 : 0) * nnz_max + 4 * nnz_max + 4 * (rpc + 1));
+    return (size_t)(cluster_nvec(tfqmr) * 16 * rpc + (vs ? 16 : 0) * nnz_max + 4 * nnz_max + 4 * (rpc + 1));
 }
 
 // cluster size that can be launched on this device: 16 (non-portable), else 8, else 0
@@ -1992,10 +2166,11 @@ static int cluster_size_available() {
     if (cached < 0) {
         cached = 0;
         for (int w : {1, 2, 4, 8})
-            for (bool vs : {false, true}) {
-                cudaFuncSetAttribute(cluster_kernel(w, vs), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-                cudaFuncSetAttribute(cluster_kernel(w, vs), cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmemMax);
-            }
+            for (bool vs : {false, true})
+                for (bool tf : {false, true}) {
+                    cudaFuncSetAttribute(cluster_kernel(w, vs, tf), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                    cudaFuncSetAttribute(cluster_kernel(w, vs, tf), cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmemMax);
+                }
         for (int cs : {16, 8}) {
             cudaLaunchConfig_t cfg;
             memset(&cfg, 0, sizeof cfg);
@@ -2038,26 +2213,32 @@ static int64_t cluster_nnz_max(zk_csr_s* A, int cs, cudaStream_t s) {
     return mx;
 }
 // can the cluster solver hold this system (own rows + the block's columns in shared memory)?
-static bool cluster_fits(zk_csr_s* A, cudaStream_t s) {
+static bool cluster_fits(zk_csr_s* A, cudaStream_t s, bool tfqmr) {
     const int cs = cluster_size_available();
-    if (cs == 0 || A->n_rows == 0 || A->n_rows > (int64_t)cs * (kCSmemMax / (kCVecs * 16))) return false;
+    if (cs == 0 || A->n_rows == 0 || A->n_rows > (int64_t)cs * (kCSmemMax / (cluster_nvec(tfqmr) * 16))) return false;
     const int64_t nz = cluster_nnz_max(A, cs, s);
-    return nz >= 0 && cluster_smem(A->n_rows, cs, nz, false) <= (size_t)kCSmemMax;
+    return nz >= 0 && cluster_smem(A->n_rows, cs, nz, false, tfqmr) <= (size_t)kCSmemMax;
 }
 
 // launch the cluster solver on one cluster (A or A·M⁻¹ in av); false when unavailable
-static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStream_t s, int* out_cs) {
+static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStream_t s, int* out_cs, bool tfqmr) {
     const int cs = cluster_size_available();
     if (cs == 0) return false;
     const int64_t nz = cluster_nnz_max(A, cs, s);
     if (nz < 0) return false;
-    const bool vs = cluster_smem(av.n_rows, cs, nz, true) <= (size_t)kCSmemMax;
-    const int w = cluster_w(av.n_rows, cs, A->max_len);
+    bool vs = cluster_smem(av.n_rows, cs, nz, true, tfqmr) <= (size_t)kCSmemMax;
+    int w = cluster_w(av.n_rows, cs, A->max_len);
+    if (const char* e = getenv("ZK_CLUSTER_W")) {  // tests: force a lane count (1, 2, 4, 8)
+        const int f = atoi(e);
+        if (f == 1 || f == 2 || f == 4 || f == 8) w = f;
+    }
+    if (const char* e = getenv("ZK_CLUSTER_VS"))  // tests: 0 keeps the values in global memory
+        vs = vs && atoi(e) != 0;
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof cfg);
     cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(kCBlock);
-    cfg.dynamicSmemBytes = cluster_smem(av.n_rows, cs, nz, vs);
+    cfg.dynamicSmemBytes = cluster_smem(av.n_rows, cs, nz, vs, tfqmr);
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -2069,7 +2250,7 @@ static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStre
     void* args[] = {(void*)&dc, (void*)&av, (void*)&nz};
     int nzi = (int)nz;
     args[2] = &nzi;
-    cudaError_t e = cudaLaunchKernelExC(&cfg, cluster_kernel(w, vs), args);
+    cudaError_t e = cudaLaunchKernelExC(&cfg, cluster_kernel(w, vs, tfqmr), args);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return false;
@@ -2482,12 +2663,13 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     //      iteration, C3 514 vs 184: the fused phases need 128 registers → half the warps, and
     //      coherent gathers), so it is opt-in (ZK_LOOP_MODE=4) and parity-tested, not the default.
     // default: the cluster solver (mode 5) for small BiCGStab systems, else the WHILE graph
-    int mode = A->dist ? 3 : (method == ZK_BICGSTAB && A->n_rows <= kClusterDefaultRows ? 5 : 1);
+    int mode = A->dist ? 3 : ((method == ZK_BICGSTAB || method == ZK_TFQMR) && A->n_rows <= kClusterDefaultRows ? 5 : 1);
     if (const char* e = getenv("ZK_LOOP_MODE")) {
         int m = atoi(e);
         if (m >= 1 && m <= 5) mode = m;
     }
-    if (mode == 5 && (A->dist || method != ZK_BICGSTAB || !cluster_fits(A, (cudaStream_t)stream)))
+    if (mode == 5 && (A->dist || (method != ZK_BICGSTAB && method != ZK_TFQMR) ||
+                      !cluster_fits(A, (cudaStream_t)stream, method == ZK_TFQMR)))
         mode = A->dist ? 3 : 1;
     if (A->dist && (mode == 1 || mode == 4 || mode == 5)) mode = 3;  // NCCL inside WHILE bodies / persistent kernels is not used
     int persist_grid = 0;
@@ -2627,7 +2809,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         ZK_CUDA(cudaLaunchCooperativeKernel(kp, dim3(persist_grid), dim3(kBlock), args, 0, s));
     } else if (mode == 5) {
         int csz = 0;
-        if (!cluster_launch(A, dc, hc.A, s, &csz)) return fail(ZK_ERR_CUDA, "cluster solver launch failed");
+        if (!cluster_launch(A, dc, hc.A, s, &csz, method == ZK_TFQMR)) return fail(ZK_ERR_CUDA, "cluster solver launch failed");
     } else {
         ZK_CUDA(cudaMallocHost(&hdone, sizeof(SolveCtx)));
         int launched = 0;

@@ -439,3 +439,24 @@ def test_cluster_solver_outcomes(monkeypatch):
     sk = dict(row_ptr=np.array([0, 1, 2]), col_idx=np.array([1, 0], np.int32),
               values=np.array([1, -1], np.complex128), n=2)
     assert gpu_solve(sk, np.array([1, 0], np.complex128))["status"] == "BREAKDOWN_SIGMA"
+
+
+@pytest.mark.parametrize("w", ["1", "2", "4", "8"])
+@pytest.mark.parametrize("vs", ["0", "1"])
+@pytest.mark.parametrize("cfg", ["C1", "T0"])
+def test_cluster_solver_lane_variants(cfg, w, vs, monkeypatch):
+    """Every instantiation of the cluster solver (W lanes per row, values in shared memory or in
+    global memory) against the oracle: same parity bar as test_cluster_solver_parity."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "5")
+    monkeypatch.setenv("ZK_CLUSTER_W", w)
+    monkeypatch.setenv("ZK_CLUSTER_VS", vs)
+    m = gen.make_matrix(cfg)
+    b = gen.make_rhs(m)
+    r = gpu_solve(m, b, tol=1e-8)
+    assert r["loop_mode"] == 5
+    refs = [oracle.bicgstab(m, b, tol=1e-8, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    assert r["status"] == "CONVERGED" and 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    k = min(12, r["iters"], refs[0]["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= 1e-10
+    assert relerr(r["x"], refs[0]["x"]) <= 1e-6 and r["true_relres"] <= 2e-8

@@ -49,6 +49,7 @@ def diag(n, c):
 @pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
 def test_tfqmr_parity(cfg, spmv_mode, monkeypatch):
     monkeypatch.setenv("ZK_SPMV_MODE", spmv_mode)
+    monkeypatch.setenv("ZK_LOOP_MODE", "1")  # the WHILE-graph kernels with each SpMV mapping
     m = gen.make_matrix(cfg)
     b = gen.make_rhs(m)
     r = gpu_solve(m, b, tol=1e-8, maxit=1000)
@@ -203,3 +204,48 @@ def test_tfqmr_split_schedule(split, monkeypatch):
         q = gpu_solve(m, b, tol=1e-14, maxit=kk)
         ref = oracle.tfqmr(m, b, tol=1e-14, maxit=kk)
         assert q["status"] == "MAXIT" and relerr(q["x"], ref["x"]) <= 1e-11
+
+
+@pytest.mark.parametrize("variant", ["auto", "w1", "w2", "w4", "w8", "gval"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
+def test_tfqmr_cluster_parity(cfg, variant, monkeypatch):
+    """Loop mode 5 for TFQMR (the default up to 16384 rows): the whole loop in one thread-block
+    cluster, own rows in shared memory; every lane-count instantiation and the values-in-global
+    variant, against the oracle with the bars of test_tfqmr_parity; deterministic."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "5")
+    if variant.startswith("w"):
+        monkeypatch.setenv("ZK_CLUSTER_W", variant[1:])
+    if variant == "gval":
+        monkeypatch.setenv("ZK_CLUSTER_VS", "0")
+    m = gen.make_matrix(cfg)
+    b = gen.make_rhs(m)
+    r = gpu_solve(m, b, tol=1e-8, maxit=1000)
+    assert r["loop_mode"] == 5 and r["gpu_launches"] == 4
+    refs = [oracle.tfqmr(m, b, tol=1e-8, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    assert r["status"] == "CONVERGED" and 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    k = min(12, r["iters"], refs[0]["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= 1e-10
+    assert relerr(r["x"], refs[0]["x"]) <= 1e-6
+    assert r["hist"][-1] <= 1e-8 and r["true_relres"] <= 10 * 1e-8
+    r2 = gpu_solve(m, b, tol=1e-8, maxit=1000)
+    assert np.array_equal(r["x"], r2["x"]) and np.array_equal(r["hist"], r2["hist"])
+
+
+def test_tfqmr_cluster_exits(monkeypatch):
+    """Mode 5 exits inside an iteration: MAXIT after each of the first 6 iterations (x equal to the
+    oracle's, including the pending half-step updates), and convergence at either half step."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "5")
+    m = gen.make_matrix("T0")
+    b = gen.make_rhs(m)
+    for k in range(1, 7):
+        r = gpu_solve(m, b, tol=1e-14, maxit=k)
+        ref = oracle.tfqmr(m, b, tol=1e-14, maxit=k)
+        assert r["loop_mode"] == 5 and r["status"] == ref["status"] == "MAXIT" and r["iters"] == k
+        assert relerr(r["x"], ref["x"]) <= 1e-11, k
+        assert np.max(np.abs(r["hist"] - ref["hist"]) / ref["hist"]) <= 1e-10
+    for tol in (3e-3, 1e-3, 3e-4, 1e-4):  # stops land on both half steps
+        r = gpu_solve(m, b, tol=tol)
+        ref = oracle.tfqmr(m, b, tol=tol)
+        assert r["status"] == ref["status"] == "CONVERGED" and r["iters"] == ref["iters"]
+        assert relerr(r["x"], ref["x"]) <= 1e-9
