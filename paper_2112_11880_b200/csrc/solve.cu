@@ -1701,6 +1701,7 @@ constexpr int kCBlock = ZK_CBLOCK;
 constexpr int kCWarps = kCBlock / 32;
 constexpr int kCVecs = 7;                        // BiCGStab: x r r̂ p v s t own rows in shared memory
 constexpr int kCVecsTfqmr = 9;                   // TFQMR: x w y1 y2 u1 u2 v d r̃
+constexpr int kCVecsCg = 4;                      // CG / COCG: x r p q
 constexpr int kCSmemMax = 216 * 1024;            // dynamic shared memory: own rows + the block's matrix
 #ifndef ZK_CLUSTER_DEFAULT_ROWS
 #define ZK_CLUSTER_DEFAULT_ROWS 16384
@@ -2129,6 +2130,134 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, co
     cl.sync();
 }
 
+// CG (conjugated products, real α/β) and COCG (NEXT-4: unconjugated, complex α/β) in one cluster:
+// the per-row arithmetic of EpiK1Cg/OpK2Cg/OpK3Cg and EpiK1Cocg/OpK2Cocg/OpK3Cocg, the same
+// scalar steps.  p is gathered by the SpMV, so it is also written to global memory.
+template <int W, bool VS, bool COCG>
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const CsrDev A, int nnz_max) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double2 own[];
+    __shared__ SolveCtx cs;
+    __shared__ ClusterRed R;
+    if (threadIdx.x == 0) {
+        cs = *gctx;
+        R.parity = 0;
+    }
+    const int n = (int)A.n_rows;
+    const int ncta = (int)cl.num_blocks();
+    const int rpc = (n + ncta - 1) / ncta;
+    const int row0 = (int)cl.block_rank() * rpc;
+    const int nr = max(0, min(rpc, n - row0));
+    double2 *X = own, *Rv = own + rpc, *P = own + 2 * rpc, *Q = own + 3 * rpc;
+    double2* sval = own + kCVecsCg * rpc;
+    int* scol = (int*)(sval + (VS ? nnz_max : 0));
+    int* soff = scol + nnz_max;
+    __syncthreads();
+    SolveCtx* c = &cs;
+    double2 *xg = cs.x, *pg = cs.p;
+    for (int l = threadIdx.x; l < nr; l += kCBlock) {
+        X[l] = xg[row0 + l];
+        Rv[l] = cs.r[row0 + l];
+        P[l] = pg[row0 + l];
+    }
+    const double2* gval = cl_stage<VS>(A, row0, nr, sval, scol, soff);
+    __syncthreads();
+    constexpr int RPP = kCBlock / W;
+    const int sub = threadIdx.x & (W - 1);
+    const int grp = threadIdx.x / W;
+    int bodies = 0;
+    while (!c->done) {
+        {   // K1: q = A p ; CG δ = ⟨p, q⟩ / COCG μ = pᵀq
+            double acc[2] = {0.0, 0.0};
+            for (int b = 0; b < nr; b += RPP) {
+                const int l = b + grp;
+                const double2 y = cl_row<W, VS>(gval, sval, scol, soff, pg, l, l < nr, sub);
+                if (sub == 0 && l < nr) {
+                    Q[l] = y;
+                    const double2 pi = P[l];
+                    if (COCG) {
+                        acc[0] = fma(pi.x, y.x, fma(-pi.y, y.y, acc[0]));
+                        acc[1] = fma(pi.x, y.y, fma(pi.y, y.x, acc[1]));
+                    } else {
+                        acc[0] = fma(pi.x, y.x, fma(pi.y, y.y, acc[0]));
+                        acc[1] = fma(pi.x, y.y, fma(-pi.y, y.x, acc[1]));
+                    }
+                }
+            }
+            cl_sum<2>(acc, R);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                if (COCG) fin_k1_cocg(c, R.tot);
+                else fin_k1_cg(c, R.tot);
+            }
+            __syncthreads();
+            if (c->done) break;
+        }
+        {   // K2: x += α p ; r −= α q ; ‖r‖² (COCG: and rᵀr)
+            constexpr int K2 = COCG ? 3 : 1;
+            double acc[K2];
+#pragma unroll
+            for (int k = 0; k < K2; k++) acc[k] = 0.0;
+            for (int l = threadIdx.x; l < nr; l += kCBlock) {
+                const double2 pi = P[l], qi = Q[l];
+                if (COCG) {
+                    const double2 al = c->alpha;
+                    double2 xn = X[l];
+                    cfma(xn, al, pi);
+                    X[l] = xn;
+                    double2 rn = Rv[l];
+                    rn.x = fma(-al.x, qi.x, fma(al.y, qi.y, rn.x));
+                    rn.y = fma(-al.x, qi.y, fma(-al.y, qi.x, rn.y));
+                    Rv[l] = rn;
+                    acc[0] += cabs2(rn);
+                    acc[K2 > 1 ? 1 : 0] = fma(rn.x, rn.x, fma(-rn.y, rn.y, acc[K2 > 1 ? 1 : 0]));
+                    acc[K2 > 2 ? 2 : 0] = fma(2.0 * rn.x, rn.y, acc[K2 > 2 ? 2 : 0]);
+                } else {
+                    const double al = c->alpha_cg;
+                    const double2 xi = X[l], ri = Rv[l];
+                    X[l] = make_double2(fma(al, pi.x, xi.x), fma(al, pi.y, xi.y));
+                    const double2 rn = make_double2(fma(-al, qi.x, ri.x), fma(-al, qi.y, ri.y));
+                    Rv[l] = rn;
+                    acc[0] += cabs2(rn);
+                }
+            }
+            cl_sum<K2>(acc, R);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                if (COCG) fin_k2_cocg(c, R.tot);
+                else fin_k2_cg(c, R.tot);
+            }
+            __syncthreads();
+            if (c->done) break;
+        }
+        {   // K3: p = r + β p, then a cluster barrier (p is gathered by K1)
+            for (int l = threadIdx.x; l < nr; l += kCBlock) {
+                double2 o;
+                if (COCG) {
+                    o = Rv[l];
+                    cfma(o, c->beta, P[l]);
+                } else {
+                    const double be = c->beta_cg;
+                    const double2 pi = P[l], ri = Rv[l];
+                    o = make_double2(fma(be, pi.x, ri.x), fma(be, pi.y, ri.y));
+                }
+                P[l] = o;
+                pg[row0 + l] = o;
+            }
+            cl.sync();
+        }
+        bodies++;
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < nr; l += kCBlock) xg[row0 + l] = X[l];
+    if (cl.block_rank() == 0 && threadIdx.x == 0) {
+        cs.bodies = bodies;
+        *gctx = cs;
+    }
+    cl.sync();
+}
+
 // lanes per row of the cluster SpMV: minimise passes × chunks per lane (ties: more lanes)
 static int cluster_w(int64_t n, int cs, int max_len) {
     const int64_t rpc = (n + cs - 1) / cs;
@@ -2145,19 +2274,27 @@ static int cluster_w(int64_t n, int cs, int max_len) {
     }
     return best;
 }
+// cluster solver kinds: 0 BiCGStab (and Jacobi-BiCGStab), 1 TFQMR, 2 CG, 3 COCG
+static int cluster_kind(int method) {
+    return method == ZK_BICGSTAB ? 0 : method == ZK_TFQMR ? 1 : method == ZK_CG ? 2 : method == ZK_COCG ? 3 : -1;
+}
 template <int W>
-static const void* cluster_kernel(bool vs, bool tfqmr) {
-    if (tfqmr) return vs ? (const void*)k_cluster_tfqmr<W, true> : (const void*)k_cluster_tfqmr<W, false>;
-    return vs ? (const void*)k_cluster_bicg<W, true> : (const void*)k_cluster_bicg<W, false>;
+static const void* cluster_kernel(bool vs, int kind) {
+    switch (kind) {
+        case 1: return vs ? (const void*)k_cluster_tfqmr<W, true> : (const void*)k_cluster_tfqmr<W, false>;
+        case 2: return vs ? (const void*)k_cluster_cg<W, true, false> : (const void*)k_cluster_cg<W, false, false>;
+        case 3: return vs ? (const void*)k_cluster_cg<W, true, true> : (const void*)k_cluster_cg<W, false, true>;
+        default: return vs ? (const void*)k_cluster_bicg<W, true> : (const void*)k_cluster_bicg<W, false>;
+    }
 }
-static const void* cluster_kernel(int w, bool vs, bool tfqmr = false) {
-    return w == 8 ? cluster_kernel<8>(vs, tfqmr) : w == 4 ? cluster_kernel<4>(vs, tfqmr)
-         : w == 2 ? cluster_kernel<2>(vs, tfqmr) : cluster_kernel<1>(vs, tfqmr);
+static const void* cluster_kernel(int w, bool vs, int kind = 0) {
+    return w == 8 ? cluster_kernel<8>(vs, kind) : w == 4 ? cluster_kernel<4>(vs, kind)
+         : w == 2 ? cluster_kernel<2>(vs, kind) : cluster_kernel<1>(vs, kind);
 }
-static int cluster_nvec(bool tfqmr) { return tfqmr ? kCVecsTfqmr : kCVecs; }
-static size_t cluster_smem(int64_t n, int cs, int64_t nnz_max, bool vs, bool tfqmr = false) {
+static int cluster_nvec(int kind) { return kind == 1 ? kCVecsTfqmr : kind >= 2 ? kCVecsCg : kCVecs; }
+static size_t cluster_smem(int64_t n, int cs, int64_t nnz_max, bool vs, int kind = 0) {
     const int64_t rpc = (n + cs - 1) / cs;
-    return (size_t)(cluster_nvec(tfqmr) * 16 * rpc + (vs ? 16 : 0) * nnz_max + 4 * nnz_max + 4 * (rpc + 1));
+    return (size_t)(cluster_nvec(kind) * 16 * rpc + (vs ? 16 : 0) * nnz_max + 4 * nnz_max + 4 * (rpc + 1));
 }
 
 // cluster size that can be launched on this device: 16 (non-portable), else 8, else 0
@@ -2167,9 +2304,9 @@ static int cluster_size_available() {
         cached = 0;
         for (int w : {1, 2, 4, 8})
             for (bool vs : {false, true})
-                for (bool tf : {false, true}) {
-                    cudaFuncSetAttribute(cluster_kernel(w, vs, tf), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-                    cudaFuncSetAttribute(cluster_kernel(w, vs, tf), cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmemMax);
+                for (int kind = 0; kind < 4; kind++) {
+                    cudaFuncSetAttribute(cluster_kernel(w, vs, kind), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                    cudaFuncSetAttribute(cluster_kernel(w, vs, kind), cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmemMax);
                 }
         for (int cs : {16, 8}) {
             cudaLaunchConfig_t cfg;
@@ -2213,20 +2350,21 @@ static int64_t cluster_nnz_max(zk_csr_s* A, int cs, cudaStream_t s) {
     return mx;
 }
 // can the cluster solver hold this system (own rows + the block's columns in shared memory)?
-static bool cluster_fits(zk_csr_s* A, cudaStream_t s, bool tfqmr) {
+static bool cluster_fits(zk_csr_s* A, cudaStream_t s, int kind) {
     const int cs = cluster_size_available();
-    if (cs == 0 || A->n_rows == 0 || A->n_rows > (int64_t)cs * (kCSmemMax / (cluster_nvec(tfqmr) * 16))) return false;
+    if (kind < 0 || cs == 0 || A->n_rows == 0 || A->n_rows > (int64_t)cs * (kCSmemMax / (cluster_nvec(kind) * 16)))
+        return false;
     const int64_t nz = cluster_nnz_max(A, cs, s);
-    return nz >= 0 && cluster_smem(A->n_rows, cs, nz, false, tfqmr) <= (size_t)kCSmemMax;
+    return nz >= 0 && cluster_smem(A->n_rows, cs, nz, false, kind) <= (size_t)kCSmemMax;
 }
 
 // launch the cluster solver on one cluster (A or A·M⁻¹ in av); false when unavailable
-static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStream_t s, int* out_cs, bool tfqmr) {
+static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStream_t s, int* out_cs, int kind) {
     const int cs = cluster_size_available();
     if (cs == 0) return false;
     const int64_t nz = cluster_nnz_max(A, cs, s);
     if (nz < 0) return false;
-    bool vs = cluster_smem(av.n_rows, cs, nz, true, tfqmr) <= (size_t)kCSmemMax;
+    bool vs = cluster_smem(av.n_rows, cs, nz, true, kind) <= (size_t)kCSmemMax;
     int w = cluster_w(av.n_rows, cs, A->max_len);
     if (const char* e = getenv("ZK_CLUSTER_W")) {  // tests: force a lane count (1, 2, 4, 8)
         const int f = atoi(e);
@@ -2238,7 +2376,7 @@ static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStre
     memset(&cfg, 0, sizeof cfg);
     cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(kCBlock);
-    cfg.dynamicSmemBytes = cluster_smem(av.n_rows, cs, nz, vs, tfqmr);
+    cfg.dynamicSmemBytes = cluster_smem(av.n_rows, cs, nz, vs, kind);
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -2250,7 +2388,7 @@ static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStre
     void* args[] = {(void*)&dc, (void*)&av, (void*)&nz};
     int nzi = (int)nz;
     args[2] = &nzi;
-    cudaError_t e = cudaLaunchKernelExC(&cfg, cluster_kernel(w, vs, tfqmr), args);
+    cudaError_t e = cudaLaunchKernelExC(&cfg, cluster_kernel(w, vs, kind), args);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return false;
@@ -2663,13 +2801,12 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     //      iteration, C3 514 vs 184: the fused phases need 128 registers → half the warps, and
     //      coherent gathers), so it is opt-in (ZK_LOOP_MODE=4) and parity-tested, not the default.
     // default: the cluster solver (mode 5) for small BiCGStab systems, else the WHILE graph
-    int mode = A->dist ? 3 : ((method == ZK_BICGSTAB || method == ZK_TFQMR) && A->n_rows <= kClusterDefaultRows ? 5 : 1);
+    int mode = A->dist ? 3 : (cluster_kind(method) >= 0 && A->n_rows <= kClusterDefaultRows ? 5 : 1);
     if (const char* e = getenv("ZK_LOOP_MODE")) {
         int m = atoi(e);
         if (m >= 1 && m <= 5) mode = m;
     }
-    if (mode == 5 && (A->dist || (method != ZK_BICGSTAB && method != ZK_TFQMR) ||
-                      !cluster_fits(A, (cudaStream_t)stream, method == ZK_TFQMR)))
+    if (mode == 5 && (A->dist || !cluster_fits(A, (cudaStream_t)stream, cluster_kind(method))))
         mode = A->dist ? 3 : 1;
     if (A->dist && (mode == 1 || mode == 4 || mode == 5)) mode = 3;  // NCCL inside WHILE bodies / persistent kernels is not used
     int persist_grid = 0;
@@ -2809,7 +2946,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         ZK_CUDA(cudaLaunchCooperativeKernel(kp, dim3(persist_grid), dim3(kBlock), args, 0, s));
     } else if (mode == 5) {
         int csz = 0;
-        if (!cluster_launch(A, dc, hc.A, s, &csz, method == ZK_TFQMR)) return fail(ZK_ERR_CUDA, "cluster solver launch failed");
+        if (!cluster_launch(A, dc, hc.A, s, &csz, cluster_kind(method))) return fail(ZK_ERR_CUDA, "cluster solver launch failed");
     } else {
         ZK_CUDA(cudaMallocHost(&hdone, sizeof(SolveCtx)));
         int launched = 0;

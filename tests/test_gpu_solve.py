@@ -63,6 +63,7 @@ def test_bicgstab_parity(cfg, spmv_mode, monkeypatch):
 @pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
 def test_cg_parity_twisted_hpd(cfg, spmv_mode, monkeypatch):
     monkeypatch.setenv("ZK_SPMV_MODE", spmv_mode)
+    monkeypatch.setenv("ZK_LOOP_MODE", "1")  # the WHILE-graph kernels with each SpMV mapping
     mg = gen.make_matrix(cfg, eta=0.0, twist_seed=gen.SEED_TWIST)
     b = np.exp(1j * mg["phase"]) * gen.make_rhs(mg)
     r = gpu_solve(mg, b, tol=1e-8, method="cg")
@@ -460,3 +461,52 @@ def test_cluster_solver_lane_variants(cfg, w, vs, monkeypatch):
     k = min(12, r["iters"], refs[0]["iters"]) + 1
     assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= 1e-10
     assert relerr(r["x"], refs[0]["x"]) <= 1e-6 and r["true_relres"] <= 2e-8
+
+
+@pytest.mark.parametrize("variant", ["auto", "w1", "w2", "w4", "w8", "gval"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
+@pytest.mark.parametrize("method", ["cg", "cocg"])
+def test_cg_cocg_cluster_parity(method, cfg, variant, monkeypatch):
+    """Loop mode 5 for CG (gauge-twisted HPD variant, L9) and COCG (the absorbing complex-symmetric
+    matrices): every lane-count instantiation and the values-in-global variant against the oracle
+    (±5 % iterations, hist prefix 1e-10, solution 1e-6); deterministic."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "5")
+    if variant.startswith("w"):
+        monkeypatch.setenv("ZK_CLUSTER_W", variant[1:])
+    if variant == "gval":
+        monkeypatch.setenv("ZK_CLUSTER_VS", "0")
+    if method == "cg":
+        m = gen.make_matrix(cfg, eta=0.0, twist_seed=gen.SEED_TWIST)
+        b = np.exp(1j * m["phase"]) * gen.make_rhs(m)
+        ref = oracle.cg(m, b, tol=1e-8)
+    else:
+        m = gen.make_matrix(cfg)
+        b = gen.make_rhs(m)
+        ref = oracle.cocg(m, b, tol=1e-8)
+    r = gpu_solve(m, b, tol=1e-8, method=method)
+    assert r["loop_mode"] == 5 and r["gpu_launches"] == 4
+    assert r["status"] == ref["status"] == "CONVERGED"
+    assert abs(r["iters"] - ref["iters"]) <= 0.05 * ref["iters"], (r["iters"], ref["iters"])
+    k = min(12, r["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]) <= 1e-10
+    assert relerr(r["x"], ref["x"]) <= 1e-6 and r["true_relres"] <= 2e-8
+    r2 = gpu_solve(m, b, tol=1e-8, method=method)
+    assert np.array_equal(r["x"], r2["x"]) and np.array_equal(r["hist"], r2["hist"])
+
+
+def test_cg_cluster_outcomes(monkeypatch):
+    """Mode 5 CG exits: MAXIT with the oracle's history and x, NOT_HPD on an indefinite matrix."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "5")
+    m = gen.make_matrix("T0", eta=0.0, twist_seed=gen.SEED_TWIST)
+    b = np.exp(1j * m["phase"]) * gen.make_rhs(m)
+    r = gpu_solve(m, b, tol=1e-14, maxit=9, method="cg")
+    ref = oracle.cg(m, b, tol=1e-14, maxit=9)
+    assert r["loop_mode"] == 5 and r["status"] == ref["status"] == "MAXIT" and r["iters"] == 9
+    assert np.max(np.abs(r["hist"] - ref["hist"]) / ref["hist"]) <= 1e-10
+    assert relerr(r["x"], ref["x"]) <= 1e-10
+    n = 500
+    vals = np.where(np.arange(n) % 2 == 0, 1.0, -1.0).astype(np.complex128)
+    d = dict(row_ptr=np.arange(n + 1, dtype=np.int64), col_idx=np.arange(n, dtype=np.int32), values=vals, n=n)
+    bb = np.ones(n, np.complex128)
+    q = gpu_solve(d, bb, tol=1e-10, method="cg")
+    assert q["loop_mode"] == 5 and q["status"] == oracle.cg(d, bb, tol=1e-10)["status"] == "NOT_HPD"
