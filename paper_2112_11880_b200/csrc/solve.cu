@@ -1819,9 +1819,33 @@ __device__ __forceinline__ const double2* cl_stage(const CsrDev& A, int row0, in
     return A.val + nz0;
 }
 
+// The solve's exit check ‖b − A x‖/‖b‖ inside the cluster kernel (EpiTrue + fin_true; the host
+// k_true launch is skipped).  The caller has written its rows of x to xg; the cluster barrier here
+// publishes them for the gathers.
+template <int W, bool VS>
+__device__ __forceinline__ void cl_true(SolveCtx* c, ClusterRed& R, const double2* gval, const double2* sval,
+                                        const int* scol, const int* soff, const double2* xg, int row0, int nr) {
+    namespace cg = cooperative_groups;
+    cg::this_cluster().sync();
+    if (c->status == ST_ZERO_RHS) return;  // replicated state: the same branch in every CTA
+    constexpr int RPP = kCBlock / W;
+    const int sub = threadIdx.x & (W - 1), grp = threadIdx.x / W;
+    const double2* bg = c->b;
+    double acc[1] = {0.0};
+    for (int b = 0; b < nr; b += RPP) {
+        const int l = b + grp;
+        const double2 y = cl_row<W, VS>(gval, sval, scol, soff, xg, l, l < nr, sub);
+        if (sub == 0 && l < nr) acc[0] += cabs2(csub(bg[row0 + l], y));
+    }
+    cl_sum<1>(acc, R);
+    __syncthreads();
+    if (threadIdx.x == 0) fin_true(c, R.tot);
+    __syncthreads();
+}
+
 // dynamic shared memory: kCVecs × rpc vectors | [values nnz_max] | columns nnz_max | offsets rpc + 1
 template <int W, bool VS>
-__global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, const CsrDev A, int nnz_max) {
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, const CsrDev A, int nnz_max, int do_true) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ double2 own[];
@@ -1961,6 +1985,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
         bodies++;
     }
     for (int l = threadIdx.x; l < nr; l += kCBlock) xg[row0 + l] = X[l];  // the solution leaves shared memory
+    if (do_true) cl_true<W, VS>(c, R, gval, sval, scol, soff, xg, row0, nr);
     if (cl.block_rank() == 0 && threadIdx.x == 0) {
         cs.bodies = bodies;
         *gctx = cs;
@@ -1973,7 +1998,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
 // only x += η1·d1 remains; half = 2: T3's d and x updates without y1).  y1 and y2 are gathered by
 // the SpMVs, so they are also written to global memory.
 template <int W, bool VS>
-__global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, const CsrDev A, int nnz_max) {
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, const CsrDev A, int nnz_max, int do_true) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ double2 own[];
@@ -2122,6 +2147,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, co
     }
     __syncthreads();
     for (int l = threadIdx.x; l < nr; l += kCBlock) xg[row0 + l] = X[l];
+    if (do_true) cl_true<W, VS>(c, R, gval, sval, scol, soff, xg, row0, nr);
     if (cl.block_rank() == 0 && threadIdx.x == 0) {
         cs.half = 0;
         cs.bodies = bodies;
@@ -2134,7 +2160,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, co
 // the per-row arithmetic of EpiK1Cg/OpK2Cg/OpK3Cg and EpiK1Cocg/OpK2Cocg/OpK3Cocg, the same
 // scalar steps.  p is gathered by the SpMV, so it is also written to global memory.
 template <int W, bool VS, bool COCG>
-__global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const CsrDev A, int nnz_max) {
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const CsrDev A, int nnz_max, int do_true) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ double2 own[];
@@ -2251,6 +2277,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const
     }
     __syncthreads();
     for (int l = threadIdx.x; l < nr; l += kCBlock) xg[row0 + l] = X[l];
+    if (do_true) cl_true<W, VS>(c, R, gval, sval, scol, soff, xg, row0, nr);
     if (cl.block_rank() == 0 && threadIdx.x == 0) {
         cs.bodies = bodies;
         *gctx = cs;
@@ -2359,7 +2386,8 @@ static bool cluster_fits(zk_csr_s* A, cudaStream_t s, int kind) {
 }
 
 // launch the cluster solver on one cluster (A or A·M⁻¹ in av); false when unavailable
-static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStream_t s, int* out_cs, int kind) {
+static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStream_t s, int* out_cs, int kind,
+                           bool do_true) {
     const int cs = cluster_size_available();
     if (cs == 0) return false;
     const int64_t nz = cluster_nnz_max(A, cs, s);
@@ -2385,9 +2413,9 @@ static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStre
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    void* args[] = {(void*)&dc, (void*)&av, (void*)&nz};
     int nzi = (int)nz;
-    args[2] = &nzi;
+    int dt = do_true ? 1 : 0;
+    void* args[] = {(void*)&dc, (void*)&av, (void*)&nzi, (void*)&dt};
     cudaError_t e = cudaLaunchKernelExC(&cfg, cluster_kernel(w, vs, kind), args);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -2946,7 +2974,8 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         ZK_CUDA(cudaLaunchCooperativeKernel(kp, dim3(persist_grid), dim3(kBlock), args, 0, s));
     } else if (mode == 5) {
         int csz = 0;
-        if (!cluster_launch(A, dc, hc.A, s, &csz, cluster_kind(method))) return fail(ZK_ERR_CUDA, "cluster solver launch failed");
+        if (!cluster_launch(A, dc, hc.A, s, &csz, cluster_kind(method), !jacobi))  // the kernel also forms the true residual
+            return fail(ZK_ERR_CUDA, "cluster solver launch failed");
     } else {
         ZK_CUDA(cudaMallocHost(&hdone, sizeof(SolveCtx)));
         int launched = 0;
@@ -2977,12 +3006,13 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         ZK_TRY(dist_halo(A, xg, s));
         gx = xg;
     }
-    ZK_TRY(with_spmv(A, [&](auto wc, auto mc) -> zk_status {
-        constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
-        { auto kf = k_true<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); kf<<<L.grid, kBlock, L.smem, s>>>(dc, gx, csr_dev(A)); }
-        ZK_CUDA(cudaGetLastError());
-        return ZK_OK;
-    }));
+    if (!(mode == 5 && !jacobi))  // mode 5 formed it inside the cluster kernel (Jacobi: on the original A here)
+        ZK_TRY(with_spmv(A, [&](auto wc, auto mc) -> zk_status {
+            constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
+            { auto kf = k_true<W, MODE>; const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE); kf<<<L.grid, kBlock, L.smem, s>>>(dc, gx, csr_dev(A)); }
+            ZK_CUDA(cudaGetLastError());
+            return ZK_OK;
+        }));
     if (A->dist) ZK_TRY(dist_finish<S_TRUE>(A, dc, 1, s));
     ZK_CUDA(cudaEventRecord(ev1, s));
 
@@ -3014,7 +3044,9 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
                         : method == ZK_TFQMR ? 2 : method == kBiCGStabL ? 2 * ell - 1 : 0;
         const int fins = A->dist ? (method == ZK_BICGSTAB ? 4 : method == ZK_TFQMR ? 3 : 2) : 0;  // dist: 1-thread finish kernels
         const int pre = method == ZK_TFQMR ? (A->dist ? 2 : 1) : 0;                               // TFQMR: K0 (+ its finish)
-        info->gpu_launches = (mode == 4 || mode == 5) ? 4 : 3 + pre + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);
+        // mode 5: set_ctx + init (+ TFQMR's K0) + the cluster kernel (+ Jacobi: x = M⁻¹u and k_true)
+        info->gpu_launches = mode == 4 ? 4 : mode == 5 ? 3 + pre + (jacobi ? 2 : 0)
+                                                       : 3 + pre + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);
         for (int i = 0; i < 4; i++) {
             info->kernel_ms[i] = out.tsum[i] * 1e-6;
             info->kernel_launches[i] = out.tcnt[i];
