@@ -2710,14 +2710,14 @@ int64_t dist_gather_len(const zk_csr_s* A);  // dist.cu: n_rows + halo slots
 static WsLayout ws_layout(const zk_csr_s* A, int method, int32_t maxit, int ell = 0) {
     WsLayout L;
     size_t off = 0;
-    L.ctx = off;
-    off += up256(sizeof(SolveCtx));
+    L.ctx = off;  // ctx and hist adjacent: the exit readback is one copy
+    off += sizeof(SolveCtx);
+    L.hist = off;
+    off += up256(sizeof(SolveCtx) + sizeof(double) * ((size_t)(maxit > 0 ? maxit : 0) + 1)) - sizeof(SolveCtx);
     L.partials = off;
     off += up256(sizeof(double) * kMaxRed * kMaxGrid);
     L.tickets = off;
-    off += sizeof(unsigned int) * kTickets;
-    L.hist = off;
-    off += up256(sizeof(double) * ((size_t)(maxit > 0 ? maxit : 0) + 1));
+    off += up256(sizeof(unsigned int) * kTickets);
     L.vec0 = off;
     const int64_t len = A->dist ? dist_gather_len(A) : A->n_rows;
     L.vec_bytes = up256(sizeof(double2) * (size_t)(len > 0 ? len : 1));
@@ -2977,23 +2977,23 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         if (!cluster_launch(A, dc, hc.A, s, &csz, cluster_kind(method), !jacobi))  // the kernel also forms the true residual
             return fail(ZK_ERR_CUDA, "cluster solver launch failed");
     } else {
-        ZK_CUDA(cudaMallocHost(&hdone, sizeof(SolveCtx)));
+        hdone = (SolveCtx*)A->pinned;  // the handle's pinned staging (no per-solve cudaMallocHost)
         int launched = 0;
         const int chunk = mode == 2 ? kChunk : 4;
         for (;;) {
             if (mode == 2) {
                 cudaError_t e = cudaGraphLaunch(gc.exec, s);
-                if (e != cudaSuccess) { cudaFreeHost(hdone); return cuda_fail(e, "cudaGraphLaunch", __FILE__, __LINE__); }
+                if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch", __FILE__, __LINE__);
             } else {
                 for (int i = 0; i < chunk; i++) {
                     zk_status st = enqueue_iteration(A, dc, hc, method, s);
-                    if (st != ZK_OK) { cudaFreeHost(hdone); return st; }
+                    if (st != ZK_OK) return st;
                 }
             }
             launched += chunk;
             cudaError_t e = cudaMemcpyAsync(hdone, dc, sizeof(SolveCtx), cudaMemcpyDeviceToHost, s);
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-            if (e != cudaSuccess) { cudaFreeHost(hdone); return cuda_fail(e, "loop poll", __FILE__, __LINE__); }
+            if (e != cudaSuccess) return cuda_fail(e, "loop poll", __FILE__, __LINE__);
             if (hdone->done || launched > maxit + 1) break;
         }
     }
@@ -3018,10 +3018,9 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
 
     SolveCtx out;
     double* hist_pinned = (double*)((char*)A->pinned + sizeof(SolveCtx));
-    ZK_CUDA(cudaMemcpyAsync(A->pinned, dc, sizeof(SolveCtx), cudaMemcpyDeviceToHost, s));
-    ZK_CUDA(cudaMemcpyAsync(hist_pinned, hc.hist, sizeof(double) * ((size_t)maxit + 1), cudaMemcpyDeviceToHost, s));
+    static_assert(sizeof(SolveCtx) % sizeof(double) == 0, "hist follows the ctx");
+    ZK_CUDA(cudaMemcpyAsync(A->pinned, dc, rb_bytes, cudaMemcpyDeviceToHost, s));  // ctx + hist
     cudaError_t e = cudaStreamSynchronize(s);
-    if (hdone) cudaFreeHost(hdone);
     if (e != cudaSuccess) return cuda_fail(e, "zk_solve", __FILE__, __LINE__);
     memcpy(&out, A->pinned, sizeof(SolveCtx));
     memcpy(resid_hist, hist_pinned, sizeof(double) * ((size_t)maxit + 1));
