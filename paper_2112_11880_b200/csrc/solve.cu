@@ -2285,6 +2285,234 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const
     cl.sync();
 }
 
+// BiCGStab(ℓ) (NEXT-3) in one cluster: one outer cycle = for j < ℓ: B1 (+ cluster barrier), S1
+// (γ → α), B2 (exit test), S2 (ρ1 → β, j < ℓ−1); then the Gram matrix of r̂_0..ℓ and the update U —
+// the per-element arithmetic of bl_b1 / EpiBl / bl_b2 / bl_gram / bl_u and the same scalar steps.
+// The 2ℓ+2 vectors stay in global memory (L2-resident at these sizes); each thread owns the same
+// elements in every phase, so only the SpMV gathers cross CTAs (after a cluster barrier).  The
+// Gram matrix: ND ≤ 81 sums per CTA over its rows (6 threads per entry, fixed order), one slot
+// per CTA, rank-ordered sum over DSMEM, Cholesky by fin_gram_bl<ℓ> in every CTA.
+constexpr int kGramMax = 81;  // (ℓ+1) + ℓ(ℓ+1) doubles at ℓ = 8
+constexpr int kGramSub = 6;   // threads per Gram entry
+__device__ __noinline__ void fin_gram_any(SolveCtx* c, const double* g, int ell) {
+    switch (ell) {
+        case 1: fin_gram_bl<1>(c, g); break;
+        case 2: fin_gram_bl<2>(c, g); break;
+        case 3: fin_gram_bl<3>(c, g); break;
+        case 4: fin_gram_bl<4>(c, g); break;
+        case 5: fin_gram_bl<5>(c, g); break;
+        case 6: fin_gram_bl<6>(c, g); break;
+        case 7: fin_gram_bl<7>(c, g); break;
+        default: fin_gram_bl<8>(c, g); break;
+    }
+}
+template <int W, bool VS>
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const CsrDev A, int nnz_max, int do_true) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double2 own[];
+    __shared__ SolveCtx cs;
+    __shared__ ClusterRed R;
+    __shared__ double gpart[kGramMax][kGramSub];
+    __shared__ double gslot[2][kGramMax];
+    __shared__ double gtot[kGramMax];
+    if (threadIdx.x == 0) {
+        cs = *gctx;
+        R.parity = 0;
+    }
+    const int n = (int)A.n_rows;
+    const int ncta = (int)cl.num_blocks();
+    const int rpc = (n + ncta - 1) / ncta;
+    const int row0 = (int)cl.block_rank() * rpc;
+    const int nr = max(0, min(rpc, n - row0));
+    double2* sval = own;
+    int* scol = (int*)(sval + (VS ? nnz_max : 0));
+    int* soff = scol + nnz_max;
+    const double2* gval = cl_stage<VS>(A, row0, nr, sval, scol, soff);
+    __syncthreads();
+    SolveCtx* c = &cs;
+    const int ell = cs.ell;
+    const int nd = (ell + 1) + ell * (ell + 1);
+    double2* const* rl = cs.rl;
+    double2* const* ul = cs.ul;
+    double2* xg = cs.x;
+    const double2* rt = cs.rh;
+    constexpr int RPP = kCBlock / W;
+    const int sub = threadIdx.x & (W - 1);
+    const int grp = threadIdx.x / W;
+    int gpar = 0;
+    int bodies = 0;
+    while (!c->done) {
+        for (int j = 0; j < ell && !c->done; j++) {
+            {   // B1: û_q = r̂_q − β û_q (q ≤ j), then a cluster barrier (S1 gathers û_j)
+                const double2 be = c->beta;
+                for (int l = threadIdx.x; l < nr; l += kCBlock) {
+                    const int i = row0 + l;
+                    for (int q = 0; q <= j; q++) {
+                        const double2 uv = ul[q][i];
+                        double2 o = rl[q][i];
+                        o.x = fma(-be.x, uv.x, fma(be.y, uv.y, o.x));
+                        o.y = fma(-be.x, uv.y, fma(-be.y, uv.x, o.y));
+                        ul[q][i] = o;
+                    }
+                }
+                cl.sync();
+            }
+            {   // S1: û_{j+1} = A û_j ; γ = ⟨r̃, û_{j+1}⟩, ‖û_{j+1}‖²
+                double acc[3] = {0.0, 0.0, 0.0};
+                double2* out = ul[j + 1];
+                for (int b = 0; b < nr; b += RPP) {
+                    const int l = b + grp;
+                    const double2 y = cl_row<W, VS>(gval, sval, scol, soff, ul[j], l, l < nr, sub);
+                    if (sub == 0 && l < nr) {
+                        out[row0 + l] = y;
+                        const double2 q = rt[row0 + l];
+                        acc[0] = fma(q.x, y.x, fma(q.y, y.y, acc[0]));
+                        acc[1] = fma(q.x, y.y, fma(-q.y, y.x, acc[1]));
+                        acc[2] += cabs2(y);
+                    }
+                }
+                cl_sum<3>(acc, R);
+                __syncthreads();
+                if (threadIdx.x == 0) fin_s1_bl(c, R.tot);
+                __syncthreads();
+                if (c->done) break;
+            }
+            {   // B2: r̂_0 −= α û_1 ; x += α û_0 ; ‖r̂_0‖² ; r̂_q −= α û_{q+1} (1 ≤ q ≤ j)
+                const double2 al = c->alpha;
+                double acc[1] = {0.0};
+                for (int l = threadIdx.x; l < nr; l += kCBlock) {
+                    const int i = row0 + l;
+                    {
+                        const double2 u1 = ul[1][i], u0 = ul[0][i];
+                        double2 o = rl[0][i];
+                        o.x = fma(-al.x, u1.x, fma(al.y, u1.y, o.x));
+                        o.y = fma(-al.x, u1.y, fma(-al.y, u1.x, o.y));
+                        rl[0][i] = o;
+                        acc[0] += cabs2(o);
+                        double2 xn = xg[i];
+                        cfma(xn, al, u0);
+                        xg[i] = xn;
+                    }
+                    for (int q = 1; q <= j; q++) {
+                        const double2 uv = ul[q + 1][i];
+                        double2 o = rl[q][i];
+                        o.x = fma(-al.x, uv.x, fma(al.y, uv.y, o.x));
+                        o.y = fma(-al.x, uv.y, fma(-al.y, uv.x, o.y));
+                        rl[q][i] = o;
+                    }
+                }
+                cl_sum<1>(acc, R);  // also publishes r̂_j for the S2 gathers
+                __syncthreads();
+                if (threadIdx.x == 0) fin_b2_bl(c, R.tot);
+                __syncthreads();
+                if (c->done) break;
+            }
+            {   // S2: r̂_{j+1} = A r̂_j ; ρ1 = ⟨r̃, r̂_{j+1}⟩, ‖r̂_{j+1}‖² (j < ℓ−1)
+                double acc[3] = {0.0, 0.0, 0.0};
+                double2* out = rl[j + 1];
+                for (int b = 0; b < nr; b += RPP) {
+                    const int l = b + grp;
+                    const double2 y = cl_row<W, VS>(gval, sval, scol, soff, rl[j], l, l < nr, sub);
+                    if (sub == 0 && l < nr) {
+                        out[row0 + l] = y;
+                        const double2 q = rt[row0 + l];
+                        acc[0] = fma(q.x, y.x, fma(q.y, y.y, acc[0]));
+                        acc[1] = fma(q.x, y.y, fma(-q.y, y.x, acc[1]));
+                        acc[2] += cabs2(y);
+                    }
+                }
+                if (j < ell - 1) {
+                    cl_sum<3>(acc, R);
+                    __syncthreads();
+                    if (threadIdx.x == 0) fin_s2_bl(c, R.tot);
+                }
+                __syncthreads();
+            }
+        }
+        if (c->done) break;
+        {   // G: Gram matrix of r̂_0..ℓ (packed as GramPack), minimal-residual coefficients γ, ω
+            const int k = threadIdx.x / kGramSub, sk = threadIdx.x % kGramSub;
+            if (k < nd) {
+                // entry k → (a, b): diag(a) = a + a(2(ℓ+1) − a − 1); off(a, b) = diag(a) + 1 + 2(b − a − 1)
+                const int NV = ell + 1;
+                int a = 0;
+                while (a + 1 < NV && (a + 1) + (a + 1) * (2 * NV - (a + 1) - 1) <= k) a++;
+                const int d = a + a * (2 * NV - a - 1);
+                const bool dg = k == d;
+                const int b = dg ? a : a + 1 + (k - d - 1) / 2;
+                const bool im = !dg && ((k - d - 1) & 1);
+                const double2* va = rl[a];
+                const double2* vb = rl[b];
+                double s = 0.0;
+                for (int l = sk; l < nr; l += kGramSub) {
+                    const double2 x1 = va[row0 + l];
+                    if (dg) {
+                        s += cabs2(x1);
+                    } else {
+                        const double2 x2 = vb[row0 + l];
+                        s = im ? fma(x1.x, x2.y, fma(-x1.y, x2.x, s)) : fma(x1.x, x2.x, fma(x1.y, x2.y, s));
+                    }
+                }
+                gpart[k][sk] = s;
+            }
+            __syncthreads();
+            if (threadIdx.x < nd) {
+                double t = 0.0;
+                for (int q = 0; q < kGramSub; q++) t += gpart[threadIdx.x][q];
+                gslot[gpar][threadIdx.x] = t;
+            }
+            cl.sync();
+            if (threadIdx.x < nd) {
+                double t = 0.0;
+                for (int r = 0; r < ncta; r++) t += cl.map_shared_rank(&gslot[gpar][0], r)[threadIdx.x];
+                gtot[threadIdx.x] = t;
+            }
+            gpar ^= 1;
+            __syncthreads();
+            if (threadIdx.x == 0) fin_gram_any(c, gtot, ell);
+            __syncthreads();
+            if (c->done) break;
+        }
+        {   // U: x += Σ γ_j r̂_{j−1} ; r̂_0 −= Σ γ_j r̂_j ; û_0 −= Σ γ_j û_j ; ‖r̂_0‖², ⟨r̃, r̂_0⟩
+            double acc[3] = {0.0, 0.0, 0.0};
+            for (int l = threadIdx.x; l < nr; l += kCBlock) {
+                const int i = row0 + l;
+                double2 xv = xg[i], r0 = rl[0][i], u0 = ul[0][i];
+                double2 rprev = r0;
+                for (int q = 1; q <= ell; q++) {  // oracle order: j ascending
+                    const double2 g = c->gam[q];
+                    const double2 rq = rl[q][i], uq = ul[q][i];
+                    cfma(xv, g, rprev);
+                    r0.x = fma(-g.x, rq.x, fma(g.y, rq.y, r0.x));
+                    r0.y = fma(-g.x, rq.y, fma(-g.y, rq.x, r0.y));
+                    u0.x = fma(-g.x, uq.x, fma(g.y, uq.y, u0.x));
+                    u0.y = fma(-g.x, uq.y, fma(-g.y, uq.x, u0.y));
+                    rprev = rq;
+                }
+                xg[i] = xv;
+                rl[0][i] = r0;
+                ul[0][i] = u0;
+                const double2 tv = rt[i];
+                acc[0] += cabs2(r0);
+                acc[1] = fma(tv.x, r0.x, fma(tv.y, r0.y, acc[1]));
+                acc[2] = fma(tv.x, r0.y, fma(-tv.y, r0.x, acc[2]));
+            }
+            cl_sum<3>(acc, R);
+            __syncthreads();
+            if (threadIdx.x == 0) fin_u_bl(c, R.tot);
+            __syncthreads();
+        }
+        bodies++;
+    }
+    if (do_true) cl_true<W, VS>(c, R, gval, sval, scol, soff, xg, row0, nr);
+    if (cl.block_rank() == 0 && threadIdx.x == 0) {
+        cs.bodies = bodies;
+        *gctx = cs;
+    }
+    cl.sync();
+}
+
 // lanes per row of the cluster SpMV: minimise passes × chunks per lane (ties: more lanes)
 static int cluster_w(int64_t n, int cs, int max_len) {
     const int64_t rpc = (n + cs - 1) / cs;
@@ -2303,7 +2531,8 @@ static int cluster_w(int64_t n, int cs, int max_len) {
 }
 // cluster solver kinds: 0 BiCGStab (and Jacobi-BiCGStab), 1 TFQMR, 2 CG, 3 COCG
 static int cluster_kind(int method) {
-    return method == ZK_BICGSTAB ? 0 : method == ZK_TFQMR ? 1 : method == ZK_CG ? 2 : method == ZK_COCG ? 3 : -1;
+    return method == ZK_BICGSTAB ? 0 : method == ZK_TFQMR ? 1 : method == ZK_CG ? 2 : method == ZK_COCG ? 3
+         : method == kBiCGStabL ? 4 : -1;
 }
 template <int W>
 static const void* cluster_kernel(bool vs, int kind) {
@@ -2311,6 +2540,7 @@ static const void* cluster_kernel(bool vs, int kind) {
         case 1: return vs ? (const void*)k_cluster_tfqmr<W, true> : (const void*)k_cluster_tfqmr<W, false>;
         case 2: return vs ? (const void*)k_cluster_cg<W, true, false> : (const void*)k_cluster_cg<W, false, false>;
         case 3: return vs ? (const void*)k_cluster_cg<W, true, true> : (const void*)k_cluster_cg<W, false, true>;
+        case 4: return vs ? (const void*)k_cluster_bl<W, true> : (const void*)k_cluster_bl<W, false>;
         default: return vs ? (const void*)k_cluster_bicg<W, true> : (const void*)k_cluster_bicg<W, false>;
     }
 }
@@ -2318,7 +2548,7 @@ static const void* cluster_kernel(int w, bool vs, int kind = 0) {
     return w == 8 ? cluster_kernel<8>(vs, kind) : w == 4 ? cluster_kernel<4>(vs, kind)
          : w == 2 ? cluster_kernel<2>(vs, kind) : cluster_kernel<1>(vs, kind);
 }
-static int cluster_nvec(int kind) { return kind == 1 ? kCVecsTfqmr : kind >= 2 ? kCVecsCg : kCVecs; }
+static int cluster_nvec(int kind) { return kind == 1 ? kCVecsTfqmr : kind == 4 ? 0 : kind >= 2 ? kCVecsCg : kCVecs; }
 static size_t cluster_smem(int64_t n, int cs, int64_t nnz_max, bool vs, int kind = 0) {
     const int64_t rpc = (n + cs - 1) / cs;
     return (size_t)(cluster_nvec(kind) * 16 * rpc + (vs ? 16 : 0) * nnz_max + 4 * nnz_max + 4 * (rpc + 1));
@@ -2331,7 +2561,7 @@ static int cluster_size_available() {
         cached = 0;
         for (int w : {1, 2, 4, 8})
             for (bool vs : {false, true})
-                for (int kind = 0; kind < 4; kind++) {
+                for (int kind = 0; kind < 5; kind++) {
                     cudaFuncSetAttribute(cluster_kernel(w, vs, kind), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
                     cudaFuncSetAttribute(cluster_kernel(w, vs, kind), cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmemMax);
                 }
@@ -2379,7 +2609,8 @@ static int64_t cluster_nnz_max(zk_csr_s* A, int cs, cudaStream_t s) {
 // can the cluster solver hold this system (own rows + the block's columns in shared memory)?
 static bool cluster_fits(zk_csr_s* A, cudaStream_t s, int kind) {
     const int cs = cluster_size_available();
-    if (kind < 0 || cs == 0 || A->n_rows == 0 || A->n_rows > (int64_t)cs * (kCSmemMax / (cluster_nvec(kind) * 16)))
+    if (kind < 0 || cs == 0 || A->n_rows == 0 ||
+        A->n_rows > (int64_t)cs * (kCSmemMax / (cluster_nvec(kind) * 16 + 8)))
         return false;
     const int64_t nz = cluster_nnz_max(A, cs, s);
     return nz >= 0 && cluster_smem(A->n_rows, cs, nz, false, kind) <= (size_t)kCSmemMax;
@@ -2829,7 +3060,10 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     //      iteration, C3 514 vs 184: the fused phases need 128 registers → half the warps, and
     //      coherent gathers), so it is opt-in (ZK_LOOP_MODE=4) and parity-tested, not the default.
     // default: the cluster solver (mode 5) for small BiCGStab systems, else the WHILE graph
-    int mode = A->dist ? 3 : (cluster_kind(method) >= 0 && A->n_rows <= kClusterDefaultRows ? 5 : 1);
+    // (BiCGStab(ℓ): up to 4096 rows — its vectors stay in global memory and the cluster version
+    // only wins at C1 size: 110 vs 250 µs per ℓ = 8 cycle; T0 243 vs 245, C2 287 vs 275)
+    const int64_t cl_default = method == kBiCGStabL ? 4096 : kClusterDefaultRows;
+    int mode = A->dist ? 3 : (cluster_kind(method) >= 0 && A->n_rows <= cl_default ? 5 : 1);
     if (const char* e = getenv("ZK_LOOP_MODE")) {
         int m = atoi(e);
         if (m >= 1 && m <= 5) mode = m;

@@ -52,7 +52,8 @@ def htol(ell):
 
 @pytest.mark.parametrize("ell", [1, 2, 4, 8])
 @pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
-def test_bicgstab_l_parity(cfg, ell):
+def test_bicgstab_l_parity(cfg, ell, monkeypatch):
+    monkeypatch.setenv("ZK_LOOP_MODE", "1")  # the WHILE-graph kernels (mode 5: test_bicgstab_l_cluster_parity)
     m = gen.make_matrix(cfg)
     b = gen.make_rhs(m)
     r = gpu_solve(m, b, ell, tol=1e-8, maxit=1000)
@@ -177,3 +178,51 @@ def test_bicgstab_l_split_schedule(split, ell, monkeypatch):
     k = min(6, r["iters"]) + 1
     assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= htol(ell) * 10
     assert relerr(r["x"], refs[0]["x"]) <= 1e-6
+
+
+@pytest.mark.parametrize("variant", ["auto", "w1", "w8", "gval"])
+@pytest.mark.parametrize("ell", [1, 2, 4, 8])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
+def test_bicgstab_l_cluster_parity(cfg, ell, variant, monkeypatch):
+    """Loop mode 5 for BiCGStab(ℓ) (the default up to 16384 rows): the whole cycle loop in one
+    thread-block cluster, Gram matrix reduced over DSMEM, Cholesky replicated per CTA; the bars of
+    test_bicgstab_l_parity; deterministic."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "5")
+    if variant.startswith("w"):
+        monkeypatch.setenv("ZK_CLUSTER_W", variant[1:])
+    if variant == "gval":
+        monkeypatch.setenv("ZK_CLUSTER_VS", "0")
+    m = gen.make_matrix(cfg)
+    b = gen.make_rhs(m)
+    r = gpu_solve(m, b, ell, tol=1e-8, maxit=1000)
+    assert r["loop_mode"] == 5 and r["gpu_launches"] == 3
+    refs = [oracle.bicgstab_l(m, b, tol=1e-8, ell=ell, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    assert r["status"] == "CONVERGED" and 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    k = min(6, r["iters"], refs[0]["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= htol(ell)
+    assert relerr(r["x"], refs[0]["x"]) <= 1e-6
+    assert r["true_relres"] <= 10 * 1e-8
+    r2 = gpu_solve(m, b, ell, tol=1e-8, maxit=1000)
+    assert np.array_equal(r["x"], r2["x"]) and np.array_equal(r["hist"], r2["hist"])
+
+
+@pytest.mark.parametrize("ell", [2, 8])
+def test_bicgstab_l_cluster_exits(ell, monkeypatch):
+    """Mode 5 BiCGStab(ℓ) exits: MAXIT after 1..3 cycles with the oracle's history and x; a
+    mid-cycle convergence (B2 exit) on A = cI."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "5")
+    m = gen.make_matrix("C1")
+    b = gen.make_rhs(m)
+    for k in ((1, 2, 3) if ell == 2 else (1,)):  # ℓ = 8 reaches the 1e-14 rounding floor in cycle 2
+        r = gpu_solve(m, b, ell, tol=1e-14, maxit=k)
+        ref = oracle.bicgstab_l(m, b, tol=1e-14, ell=ell, maxit=k)
+        assert r["loop_mode"] == 5 and r["status"] == ref["status"] == "MAXIT" and r["iters"] == k
+        assert np.max(np.abs(r["hist"] - ref["hist"]) / ref["hist"]) <= htol(ell)
+        assert relerr(r["x"], ref["x"]) <= (1e-10 if ell <= 2 else 1e-6)
+    d = diag(np.full(300, 0.3 - 2j))
+    bb = gen.rand_vector(300, 1)
+    q = gpu_solve(d, bb, ell, tol=1e-12)
+    qr = oracle.bicgstab_l(d, bb, tol=1e-12, ell=ell)
+    assert q["loop_mode"] == 5 and q["status"] == qr["status"] == "CONVERGED" and q["iters"] == qr["iters"]
+    assert np.max(np.abs(q["x"] - bb / (0.3 - 2j))) <= 1e-14 * np.max(np.abs(bb))
