@@ -2310,7 +2310,7 @@ template <int W, bool VS>
 __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const CsrDev A, int nnz_max, int do_true) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
-    extern __shared__ double2 own[];
+    extern __shared__ double2 own[];  // (2ℓ+4) × rpc: r̂_0..ℓ, û_0..ℓ, x, r̃ | [values] | columns | offsets
     __shared__ SolveCtx cs;
     __shared__ ClusterRed R;
     __shared__ double gpart[kGramMax][kGramSub];
@@ -2320,23 +2320,36 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
         cs = *gctx;
         R.parity = 0;
     }
+    __syncthreads();
     const int n = (int)A.n_rows;
     const int ncta = (int)cl.num_blocks();
     const int rpc = (n + ncta - 1) / ncta;
     const int row0 = (int)cl.block_rank() * rpc;
     const int nr = max(0, min(rpc, n - row0));
-    double2* sval = own;
-    int* scol = (int*)(sval + (VS ? nnz_max : 0));
-    int* soff = scol + nnz_max;
-    const double2* gval = cl_stage<VS>(A, row0, nr, sval, scol, soff);
-    __syncthreads();
     SolveCtx* c = &cs;
     const int ell = cs.ell;
     const int nd = (ell + 1) + ell * (ell + 1);
-    double2* const* rl = cs.rl;
+    double2* const Rs = own;                          // r̂_q at Rs + q·rpc
+    double2* const Us = own + (ell + 1) * rpc;        // û_q at Us + q·rpc
+    double2* const X = own + (2 * ell + 2) * rpc;
+    double2* const RT = own + (2 * ell + 3) * rpc;
+    double2* sval = own + (2 * ell + 4) * rpc;
+    int* scol = (int*)(sval + (VS ? nnz_max : 0));
+    int* soff = scol + nnz_max;
+    double2* const* rl = cs.rl;  // global copies: only the SpMV inputs r̂_j / û_j are written through
     double2* const* ul = cs.ul;
     double2* xg = cs.x;
-    const double2* rt = cs.rh;
+    for (int l = threadIdx.x; l < nr; l += kCBlock) {
+        const int i = row0 + l;
+        for (int q = 0; q <= ell; q++) {
+            Rs[q * rpc + l] = rl[q][i];
+            Us[q * rpc + l] = ul[q][i];
+        }
+        X[l] = xg[i];
+        RT[l] = cs.rh[i];
+    }
+    const double2* gval = cl_stage<VS>(A, row0, nr, sval, scol, soff);
+    __syncthreads();
     constexpr int RPP = kCBlock / W;
     const int sub = threadIdx.x & (W - 1);
     const int grp = threadIdx.x / W;
@@ -2344,29 +2357,29 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
     int bodies = 0;
     while (!c->done) {
         for (int j = 0; j < ell && !c->done; j++) {
-            {   // B1: û_q = r̂_q − β û_q (q ≤ j), then a cluster barrier (S1 gathers û_j)
+            {   // B1: û_q = r̂_q − β û_q (q ≤ j); û_j written through, then a cluster barrier (S1 gathers it)
                 const double2 be = c->beta;
                 for (int l = threadIdx.x; l < nr; l += kCBlock) {
-                    const int i = row0 + l;
                     for (int q = 0; q <= j; q++) {
-                        const double2 uv = ul[q][i];
-                        double2 o = rl[q][i];
+                        const double2 uv = Us[q * rpc + l];
+                        double2 o = Rs[q * rpc + l];
                         o.x = fma(-be.x, uv.x, fma(be.y, uv.y, o.x));
                         o.y = fma(-be.x, uv.y, fma(-be.y, uv.x, o.y));
-                        ul[q][i] = o;
+                        Us[q * rpc + l] = o;
+                        if (q == j) ul[j][row0 + l] = o;
                     }
                 }
                 cl.sync();
             }
             {   // S1: û_{j+1} = A û_j ; γ = ⟨r̃, û_{j+1}⟩, ‖û_{j+1}‖²
                 double acc[3] = {0.0, 0.0, 0.0};
-                double2* out = ul[j + 1];
+                double2* out = Us + (j + 1) * rpc;
                 for (int b = 0; b < nr; b += RPP) {
                     const int l = b + grp;
                     const double2 y = cl_row<W, VS>(gval, sval, scol, soff, ul[j], l, l < nr, sub);
                     if (sub == 0 && l < nr) {
-                        out[row0 + l] = y;
-                        const double2 q = rt[row0 + l];
+                        out[l] = y;
+                        const double2 q = RT[l];
                         acc[0] = fma(q.x, y.x, fma(q.y, y.y, acc[0]));
                         acc[1] = fma(q.x, y.y, fma(-q.y, y.x, acc[1]));
                         acc[2] += cabs2(y);
@@ -2378,28 +2391,27 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
                 __syncthreads();
                 if (c->done) break;
             }
-            {   // B2: r̂_0 −= α û_1 ; x += α û_0 ; ‖r̂_0‖² ; r̂_q −= α û_{q+1} (1 ≤ q ≤ j)
+            {   // B2: r̂_0 −= α û_1 ; x += α û_0 ; ‖r̂_0‖² ; r̂_q −= α û_{q+1} (1 ≤ q ≤ j); r̂_j written through
                 const double2 al = c->alpha;
                 double acc[1] = {0.0};
                 for (int l = threadIdx.x; l < nr; l += kCBlock) {
-                    const int i = row0 + l;
                     {
-                        const double2 u1 = ul[1][i], u0 = ul[0][i];
-                        double2 o = rl[0][i];
+                        const double2 u1 = Us[rpc + l], u0 = Us[l];
+                        double2 o = Rs[l];
                         o.x = fma(-al.x, u1.x, fma(al.y, u1.y, o.x));
                         o.y = fma(-al.x, u1.y, fma(-al.y, u1.x, o.y));
-                        rl[0][i] = o;
+                        Rs[l] = o;
+                        if (j == 0) rl[0][row0 + l] = o;
                         acc[0] += cabs2(o);
-                        double2 xn = xg[i];
-                        cfma(xn, al, u0);
-                        xg[i] = xn;
+                        cfma(X[l], al, u0);
                     }
                     for (int q = 1; q <= j; q++) {
-                        const double2 uv = ul[q + 1][i];
-                        double2 o = rl[q][i];
+                        const double2 uv = Us[(q + 1) * rpc + l];
+                        double2 o = Rs[q * rpc + l];
                         o.x = fma(-al.x, uv.x, fma(al.y, uv.y, o.x));
                         o.y = fma(-al.x, uv.y, fma(-al.y, uv.x, o.y));
-                        rl[q][i] = o;
+                        Rs[q * rpc + l] = o;
+                        if (q == j) rl[j][row0 + l] = o;
                     }
                 }
                 cl_sum<1>(acc, R);  // also publishes r̂_j for the S2 gathers
@@ -2410,13 +2422,13 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
             }
             {   // S2: r̂_{j+1} = A r̂_j ; ρ1 = ⟨r̃, r̂_{j+1}⟩, ‖r̂_{j+1}‖² (j < ℓ−1)
                 double acc[3] = {0.0, 0.0, 0.0};
-                double2* out = rl[j + 1];
+                double2* out = Rs + (j + 1) * rpc;
                 for (int b = 0; b < nr; b += RPP) {
                     const int l = b + grp;
                     const double2 y = cl_row<W, VS>(gval, sval, scol, soff, rl[j], l, l < nr, sub);
                     if (sub == 0 && l < nr) {
-                        out[row0 + l] = y;
-                        const double2 q = rt[row0 + l];
+                        out[l] = y;
+                        const double2 q = RT[l];
                         acc[0] = fma(q.x, y.x, fma(q.y, y.y, acc[0]));
                         acc[1] = fma(q.x, y.y, fma(-q.y, y.x, acc[1]));
                         acc[2] += cabs2(y);
@@ -2442,15 +2454,15 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
                 const bool dg = k == d;
                 const int b = dg ? a : a + 1 + (k - d - 1) / 2;
                 const bool im = !dg && ((k - d - 1) & 1);
-                const double2* va = rl[a];
-                const double2* vb = rl[b];
+                const double2* va = Rs + a * rpc;
+                const double2* vb = Rs + b * rpc;
                 double s = 0.0;
                 for (int l = sk; l < nr; l += kGramSub) {
-                    const double2 x1 = va[row0 + l];
+                    const double2 x1 = va[l];
                     if (dg) {
                         s += cabs2(x1);
                     } else {
-                        const double2 x2 = vb[row0 + l];
+                        const double2 x2 = vb[l];
                         s = im ? fma(x1.x, x2.y, fma(-x1.y, x2.x, s)) : fma(x1.x, x2.x, fma(x1.y, x2.y, s));
                     }
                 }
@@ -2477,12 +2489,11 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
         {   // U: x += Σ γ_j r̂_{j−1} ; r̂_0 −= Σ γ_j r̂_j ; û_0 −= Σ γ_j û_j ; ‖r̂_0‖², ⟨r̃, r̂_0⟩
             double acc[3] = {0.0, 0.0, 0.0};
             for (int l = threadIdx.x; l < nr; l += kCBlock) {
-                const int i = row0 + l;
-                double2 xv = xg[i], r0 = rl[0][i], u0 = ul[0][i];
+                double2 xv = X[l], r0 = Rs[l], u0 = Us[l];
                 double2 rprev = r0;
                 for (int q = 1; q <= ell; q++) {  // oracle order: j ascending
                     const double2 g = c->gam[q];
-                    const double2 rq = rl[q][i], uq = ul[q][i];
+                    const double2 rq = Rs[q * rpc + l], uq = Us[q * rpc + l];
                     cfma(xv, g, rprev);
                     r0.x = fma(-g.x, rq.x, fma(g.y, rq.y, r0.x));
                     r0.y = fma(-g.x, rq.y, fma(-g.y, rq.x, r0.y));
@@ -2490,10 +2501,10 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
                     u0.y = fma(-g.x, uq.y, fma(-g.y, uq.x, u0.y));
                     rprev = rq;
                 }
-                xg[i] = xv;
-                rl[0][i] = r0;
-                ul[0][i] = u0;
-                const double2 tv = rt[i];
+                X[l] = xv;
+                Rs[l] = r0;
+                Us[l] = u0;
+                const double2 tv = RT[l];
                 acc[0] += cabs2(r0);
                 acc[1] = fma(tv.x, r0.x, fma(tv.y, r0.y, acc[1]));
                 acc[2] = fma(tv.x, r0.y, fma(-tv.y, r0.x, acc[2]));
@@ -2505,6 +2516,8 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
         }
         bodies++;
     }
+    __syncthreads();
+    for (int l = threadIdx.x; l < nr; l += kCBlock) xg[row0 + l] = X[l];  // the solution leaves shared memory
     if (do_true) cl_true<W, VS>(c, R, gval, sval, scol, soff, xg, row0, nr);
     if (cl.block_rank() == 0 && threadIdx.x == 0) {
         cs.bodies = bodies;
@@ -2548,10 +2561,12 @@ static const void* cluster_kernel(int w, bool vs, int kind = 0) {
     return w == 8 ? cluster_kernel<8>(vs, kind) : w == 4 ? cluster_kernel<4>(vs, kind)
          : w == 2 ? cluster_kernel<2>(vs, kind) : cluster_kernel<1>(vs, kind);
 }
-static int cluster_nvec(int kind) { return kind == 1 ? kCVecsTfqmr : kind == 4 ? 0 : kind >= 2 ? kCVecsCg : kCVecs; }
-static size_t cluster_smem(int64_t n, int cs, int64_t nnz_max, bool vs, int kind = 0) {
+static int cluster_nvec(int kind, int ell) {
+    return kind == 1 ? kCVecsTfqmr : kind == 4 ? 2 * ell + 4 : kind >= 2 ? kCVecsCg : kCVecs;
+}
+static size_t cluster_smem(int64_t n, int cs, int64_t nnz_max, bool vs, int kind, int ell) {
     const int64_t rpc = (n + cs - 1) / cs;
-    return (size_t)(cluster_nvec(kind) * 16 * rpc + (vs ? 16 : 0) * nnz_max + 4 * nnz_max + 4 * (rpc + 1));
+    return (size_t)(cluster_nvec(kind, ell) * 16 * rpc + (vs ? 16 : 0) * nnz_max + 4 * nnz_max + 4 * (rpc + 1));
 }
 
 // cluster size that can be launched on this device: 16 (non-portable), else 8, else 0
@@ -2607,23 +2622,23 @@ static int64_t cluster_nnz_max(zk_csr_s* A, int cs, cudaStream_t s) {
     return mx;
 }
 // can the cluster solver hold this system (own rows + the block's columns in shared memory)?
-static bool cluster_fits(zk_csr_s* A, cudaStream_t s, int kind) {
+static bool cluster_fits(zk_csr_s* A, cudaStream_t s, int kind, int ell) {
     const int cs = cluster_size_available();
     if (kind < 0 || cs == 0 || A->n_rows == 0 ||
-        A->n_rows > (int64_t)cs * (kCSmemMax / (cluster_nvec(kind) * 16 + 8)))
+        A->n_rows > (int64_t)cs * (kCSmemMax / (cluster_nvec(kind, ell) * 16 + 8)))
         return false;
     const int64_t nz = cluster_nnz_max(A, cs, s);
-    return nz >= 0 && cluster_smem(A->n_rows, cs, nz, false, kind) <= (size_t)kCSmemMax;
+    return nz >= 0 && cluster_smem(A->n_rows, cs, nz, false, kind, ell) <= (size_t)kCSmemMax;
 }
 
 // launch the cluster solver on one cluster (A or A·M⁻¹ in av); false when unavailable
 static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStream_t s, int* out_cs, int kind,
-                           bool do_true) {
+                           int ell, bool do_true) {
     const int cs = cluster_size_available();
     if (cs == 0) return false;
     const int64_t nz = cluster_nnz_max(A, cs, s);
     if (nz < 0) return false;
-    bool vs = cluster_smem(av.n_rows, cs, nz, true, kind) <= (size_t)kCSmemMax;
+    bool vs = cluster_smem(av.n_rows, cs, nz, true, kind, ell) <= (size_t)kCSmemMax;
     int w = cluster_w(av.n_rows, cs, A->max_len);
     if (const char* e = getenv("ZK_CLUSTER_W")) {  // tests: force a lane count (1, 2, 4, 8)
         const int f = atoi(e);
@@ -2635,7 +2650,7 @@ static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStre
     memset(&cfg, 0, sizeof cfg);
     cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(kCBlock);
-    cfg.dynamicSmemBytes = cluster_smem(av.n_rows, cs, nz, vs, kind);
+    cfg.dynamicSmemBytes = cluster_smem(av.n_rows, cs, nz, vs, kind, ell);
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -3062,13 +3077,13 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     // default: the cluster solver (mode 5) for small BiCGStab systems, else the WHILE graph
     // (BiCGStab(ℓ): up to 4096 rows — its vectors stay in global memory and the cluster version
     // only wins at C1 size: 110 vs 250 µs per ℓ = 8 cycle; T0 243 vs 245, C2 287 vs 275)
-    const int64_t cl_default = method == kBiCGStabL ? 4096 : kClusterDefaultRows;
+    const int64_t cl_default = kClusterDefaultRows;
     int mode = A->dist ? 3 : (cluster_kind(method) >= 0 && A->n_rows <= cl_default ? 5 : 1);
     if (const char* e = getenv("ZK_LOOP_MODE")) {
         int m = atoi(e);
         if (m >= 1 && m <= 5) mode = m;
     }
-    if (mode == 5 && (A->dist || !cluster_fits(A, (cudaStream_t)stream, cluster_kind(method))))
+    if (mode == 5 && (A->dist || !cluster_fits(A, (cudaStream_t)stream, cluster_kind(method), ell)))
         mode = A->dist ? 3 : 1;
     if (A->dist && (mode == 1 || mode == 4 || mode == 5)) mode = 3;  // NCCL inside WHILE bodies / persistent kernels is not used
     int persist_grid = 0;
@@ -3208,7 +3223,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         ZK_CUDA(cudaLaunchCooperativeKernel(kp, dim3(persist_grid), dim3(kBlock), args, 0, s));
     } else if (mode == 5) {
         int csz = 0;
-        if (!cluster_launch(A, dc, hc.A, s, &csz, cluster_kind(method), !jacobi))  // the kernel also forms the true residual
+        if (!cluster_launch(A, dc, hc.A, s, &csz, cluster_kind(method), ell, !jacobi))  // the kernel also forms the true residual
             return fail(ZK_ERR_CUDA, "cluster solver launch failed");
     } else {
         hdone = (SolveCtx*)A->pinned;  // the handle's pinned staging (no per-solve cudaMallocHost)
