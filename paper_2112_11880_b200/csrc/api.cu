@@ -263,9 +263,9 @@ extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, 
         A->owned = false;
     } else {
         A->owned = true;
-        cudaError_t e = cudaMalloc(&A->row_ptr, sizeof(int64_t) * (n_rows + 1));
-        if (e == cudaSuccess) e = cudaMalloc(&A->col, sizeof(int) * (nnz > 0 ? nnz : 1));
-        if (e == cudaSuccess) e = cudaMalloc(&A->val, sizeof(double2) * (nnz > 0 ? nnz : 1));
+        cudaError_t e = dev_alloc(&A->row_ptr, sizeof(int64_t) * (n_rows + 1), s);
+        if (e == cudaSuccess) e = dev_alloc(&A->col, sizeof(int) * (nnz > 0 ? nnz : 1), s);
+        if (e == cudaSuccess) e = dev_alloc(&A->val, sizeof(double2) * (nnz > 0 ? nnz : 1), s);
         if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(csr)", __FILE__, __LINE__));
         const cudaMemcpyKind kind = where == ZK_PTRS_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
         e = cudaMemcpyAsync(A->row_ptr, row_ptr, sizeof(int64_t) * (n_rows + 1), kind, s);
@@ -322,6 +322,11 @@ extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, 
             choose_mapping(A, 0);
         }
     }
+    // the arrays may have come from the stream-ordered pool: usable from any stream after this
+    {
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cleanup(cuda_fail(e, "zk_csr_create", __FILE__, __LINE__));
+    }
     *out = A;
     return ZK_OK;
 }
@@ -336,9 +341,9 @@ extern "C" zk_status zk_csr_destroy(zk_csr A) {
     jacobi_destroy(A);
     sell_destroy(A);
     if (A->owned) {
-        cudaFree(A->row_ptr);
-        cudaFree(A->col);
-        cudaFree(A->val);
+        dev_free(A->row_ptr);
+        dev_free(A->col);
+        dev_free(A->val);
     }
     if (A->cap_stream) cudaStreamDestroy(A->cap_stream);
     if (A->pinned) cudaFreeHost(A->pinned);

@@ -49,9 +49,9 @@ zk_status jacobi_prepare(zk_csr_s* A, cudaStream_t s) {
     const int64_t n = A->n_rows, nnz = A->nnz;
     double2 *val = nullptr, *diag = nullptr, *dinv = nullptr;
     unsigned long long* bad = nullptr;
-    cudaError_t e = cudaMalloc(&val, sizeof(double2) * (nnz > 0 ? nnz : 1));
-    if (e == cudaSuccess) e = cudaMalloc(&diag, sizeof(double2) * (n > 0 ? n : 1));
-    if (e == cudaSuccess) e = cudaMalloc(&dinv, sizeof(double2) * (n > 0 ? n : 1));
+    cudaError_t e = dev_alloc(&val, sizeof(double2) * (nnz > 0 ? nnz : 1), s);
+    if (e == cudaSuccess) e = dev_alloc(&diag, sizeof(double2) * (n > 0 ? n : 1), s);
+    if (e == cudaSuccess) e = dev_alloc(&dinv, sizeof(double2) * (n > 0 ? n : 1), s);
     if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s);
     if (e == cudaSuccess && n > 0) {
@@ -69,9 +69,9 @@ zk_status jacobi_prepare(zk_csr_s* A, cudaStream_t s) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     cudaFree(bad);
     if (e != cudaSuccess || hbad != ~0ull) {
-        cudaFree(val);
-        cudaFree(diag);
-        cudaFree(dinv);
+        dev_free(val);
+        dev_free(diag);
+        dev_free(dinv);
         if (e != cudaSuccess) return cuda_fail(e, "jacobi_prepare", __FILE__, __LINE__);
         char buf[160];
         snprintf(buf, sizeof buf, "row %lld has no nonzero stored diagonal (Jacobi preconditioner)",
@@ -79,21 +79,23 @@ zk_status jacobi_prepare(zk_csr_s* A, cudaStream_t s) {
         return fail(ZK_ERR_INVALID_CSR, buf);
     }
     if (A->sl_val) {  // the same scaling of the sliced-ELL copy (SpMV mode 3)
-        e = cudaMalloc(&A->jac_sl_val, sizeof(double2) * (size_t)(A->sl_nnz > 0 ? A->sl_nnz : 1));
+        e = dev_alloc(&A->jac_sl_val, sizeof(double2) * (size_t)(A->sl_nnz > 0 ? A->sl_nnz : 1), s);
         if (e == cudaSuccess && A->sl_nnz > 0) {
             jacobi_scale_kernel<<<grid_for(A->sl_nnz, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(
                 A->sl_col, A->sl_val, dinv, A->sl_nnz, A->jac_sl_val);
             e = cudaGetLastError();
         }
         if (e != cudaSuccess) {
-            cudaFree(val);
-            cudaFree(diag);
-            cudaFree(dinv);
-            cudaFree(A->jac_sl_val);
+            dev_free(val);
+            dev_free(diag);
+            dev_free(dinv);
+            dev_free(A->jac_sl_val);
             A->jac_sl_val = nullptr;
             return cuda_fail(e, "jacobi_prepare (sliced ELL)", __FILE__, __LINE__);
         }
     }
+    e = cudaStreamSynchronize(s);  // pool memory: usable from any stream afterwards
+    if (e != cudaSuccess) return cuda_fail(e, "jacobi_prepare", __FILE__, __LINE__);
     A->jac_val = val;
     A->jac_diag = diag;
     A->jac_dinv = dinv;
@@ -108,9 +110,9 @@ zk_status cscale(const zk_csr_s* A, const double2* d, const double2* in, double2
 }
 
 void jacobi_destroy(zk_csr_s* A) {
-    cudaFree(A->jac_val);
-    cudaFree(A->jac_diag);
-    cudaFree(A->jac_dinv);
+    dev_free(A->jac_val);
+    dev_free(A->jac_diag);
+    dev_free(A->jac_dinv);
     A->jac_val = A->jac_diag = A->jac_dinv = nullptr;
 }
 

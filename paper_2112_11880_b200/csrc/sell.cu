@@ -51,10 +51,10 @@ __global__ void sell_fill_kernel(const int64_t* __restrict__ row_ptr, const int*
 }
 
 void sell_destroy(zk_csr_s* A) {
-    cudaFree(A->sl_ptr);
-    cudaFree(A->sl_col);
-    cudaFree(A->sl_val);
-    cudaFree(A->jac_sl_val);
+    dev_free(A->sl_ptr);
+    dev_free(A->sl_col);
+    dev_free(A->sl_val);
+    dev_free(A->jac_sl_val);
     A->sl_ptr = nullptr;
     A->sl_col = nullptr;
     A->sl_val = nullptr;
@@ -69,7 +69,7 @@ zk_status sell_build(zk_csr_s* A, cudaStream_t s) {
     const int64_t n_sl = (n + 31) / 32;
     A->n_slices = n_sl;
     int* w = nullptr;
-    cudaError_t e = cudaMalloc(&A->sl_ptr, sizeof(int64_t) * (size_t)(n_sl + 1));
+    cudaError_t e = dev_alloc(&A->sl_ptr, sizeof(int64_t) * (size_t)(n_sl + 1), s);
     if (e == cudaSuccess) e = cudaMalloc(&w, sizeof(int) * (size_t)(n_sl > 0 ? n_sl : 1));
     if (e != cudaSuccess) {
         cudaFree(w);
@@ -91,8 +91,8 @@ zk_status sell_build(zk_csr_s* A, cudaStream_t s) {
     for (int64_t i = 0; i < n_sl; i++) hp[(size_t)i + 1] = hp[(size_t)i] + 32 * (int64_t)hw[(size_t)i];
     A->sl_nnz = hp[(size_t)n_sl];
     e = cudaMemcpyAsync(A->sl_ptr, hp.data(), sizeof(int64_t) * (size_t)(n_sl + 1), cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMalloc(&A->sl_col, sizeof(int) * (size_t)(A->sl_nnz > 0 ? A->sl_nnz : 1));
-    if (e == cudaSuccess) e = cudaMalloc(&A->sl_val, sizeof(double2) * (size_t)(A->sl_nnz > 0 ? A->sl_nnz : 1));
+    if (e == cudaSuccess) e = dev_alloc(&A->sl_col, sizeof(int) * (size_t)(A->sl_nnz > 0 ? A->sl_nnz : 1), s);
+    if (e == cudaSuccess) e = dev_alloc(&A->sl_val, sizeof(double2) * (size_t)(A->sl_nnz > 0 ? A->sl_nnz : 1), s);
     if (e == cudaSuccess && n_sl > 0) {
         sell_fill_kernel<<<grid_for(n_sl * 32, kBlock, grid), kBlock, 0, s>>>(A->row_ptr, A->col, A->val, n, n_sl,
                                                                            A->sl_ptr, A->sl_col, A->sl_val);

@@ -61,3 +61,51 @@ def create_borrow_close():
 
 
 print("h2d + csr_create(borrow)+close:", ev(create_borrow_close))
+
+b = torch.from_numpy(gen.make_rhs(m)).pin_memory()
+x_h = torch.empty(n, dtype=torch.complex128).pin_memory()
+A0 = zk.csr_create(rp, ci, va, n)
+ws = zk.alloc_workspace(A0, "bicgstab", 1000)
+for step in range(3):
+    t0 = time.perf_counter()
+    A = zk.csr_create(rp, ci, va, n)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    bd = b.to("cuda", non_blocking=True)
+    r = zk.solve(A, bd, None, 1e-8, 1000, "bicgstab", workspace=ws)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    x_h.copy_(r["x"], non_blocking=True)
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    A.close()
+    torch.cuda.synchronize()
+    t4 = time.perf_counter()
+    print(f"step {step}: create {1e3*(t1-t0):.1f} ms, solve {1e3*(t2-t1):.1f} ms (device {r['solve_ms']:.1f}, "
+          f"iters {r['iters']}, mode {r['loop_mode']}), x D2H {1e3*(t3-t2):.1f}, close {1e3*(t4-t3):.1f}", flush=True)
+
+# the bench's e2e loop verbatim (non-default stream, no host syncs between steps)
+stream = torch.cuda.Stream()
+with torch.cuda.stream(stream):
+    for reps in (2, 2):
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t = time.perf_counter()
+        f0.record(stream)
+        for _ in range(reps):
+            h0 = time.perf_counter()
+            Ah = zk.csr_create(rp, ci, va, n, stream=stream)
+            h1 = time.perf_counter()
+            bd = b.to("cuda", non_blocking=True)
+            re = zk.solve(Ah, bd, None, 1e-8, 1000, "bicgstab", workspace=ws, stream=stream)
+            h2 = time.perf_counter()
+            x_h.copy_(re["x"], non_blocking=True)
+            Ah.close()
+            h3 = time.perf_counter()
+            print(f"  host: create {1e3*(h1-h0):.1f} solve {1e3*(h2-h1):.1f} (device {re['solve_ms']:.1f}) "
+                  f"copy+close {1e3*(h3-h2):.1f} ms", flush=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        print(f"bench-style e2e: {f0.elapsed_time(f1) / reps:.1f} ms/step (events), "
+              f"{(time.perf_counter() - t) * 1e3 / reps:.1f} ms/step (wall), last solve: mode {re['loop_mode']} "
+              f"iters {re['iters']} device {re['solve_ms']:.1f} ms", flush=True)
