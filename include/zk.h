@@ -150,7 +150,10 @@ zk_status zk_comm_destroy(zk_comm c);
  * s          stream for the copies / validation; the call synchronises s before returning.
  * Errors: ZK_ERR_INVALID_CSR (message names the first bad row), ZK_ERR_NONFINITE,
  *         ZK_ERR_INVALID_VALUE, ZK_ERR_OOM, ZK_ERR_CUDA, ZK_ERR_NCCL.
- * The library owns its device copies (not borrowed arrays) and its scratch; zk_csr_destroy frees them. */
+ * The library owns its device copies (not borrowed arrays) and its scratch; zk_csr_destroy frees them.
+ * The large copies come from the device's stream-ordered memory pool, whose release threshold the
+ * library raises: memory freed by zk_csr_destroy stays reserved for the next zk_csr_create instead of
+ * returning to the driver (environment ZK_POOL=0: plain cudaMalloc/cudaFree). */
 zk_status zk_csr_create(zk_csr* A, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
                         const int32_t* col_idx, const zk_z* values, uint32_t flags, zk_comm comm,
                         int64_t row_begin, zk_stream s);
