@@ -327,3 +327,42 @@ def test_zcsrmv_irregular_rows_stress(mode, monkeypatch):
     y = torch.empty(m["n"], dtype=torch.complex128, device=DEV)
     zk.zcsrmv(A, 1, cuda(x), 0, y)
     assert np.all(np.abs(y.cpu().numpy() - oracle.zcsrmv(m, x)) <= 1e-13 * row_scale(m, x) + 1e-300)
+
+
+def test_handle_memory_reused_across_create_destroy():
+    """Per-handle device arrays come from the stream-ordered pool (zk_host.h dev_alloc): creating
+    and destroying the same-size handle repeatedly must not grow device memory use."""
+    m = gen.make_matrix("C2")
+    torch.cuda.synchronize()
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+    A.close()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(20):
+        A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+        A.close()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 <= 64 << 20, (free0, free1)
+
+
+def test_plain_cudamalloc_path_subprocess():
+    """ZK_POOL=0 (plain cudaMalloc/cudaFree) in a fresh process: create, SpMV against the oracle,
+    a solve, destroy."""
+    import subprocess
+    import sys
+    import os
+    code = (
+        "import numpy as np, torch, gen, oracle\n"
+        "from paper_2112_11880_b200 import zk\n"
+        "m = gen.make_matrix('C1'); x = gen.rand_vector(m['n'], 1)\n"
+        "A = zk.csr_create(m['row_ptr'], m['col_idx'], m['values'], m['n'])\n"
+        "y = torch.empty(m['n'], dtype=torch.complex128, device='cuda')\n"
+        "zk.zcsrmv(A, 1.0, torch.from_numpy(x).cuda(), 0.0, y)\n"
+        "ref = oracle.zcsrmv(m, x)\n"
+        "assert np.max(np.abs(y.cpu().numpy() - ref)) <= 1e-13 * np.abs(ref).max()\n"
+        "r = zk.solve(A, torch.from_numpy(gen.make_rhs(m)).cuda(), tol=1e-8)\n"
+        "assert r['status'] == 'CONVERGED'\n"
+        "A.close(); print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ZK_POOL="0", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
