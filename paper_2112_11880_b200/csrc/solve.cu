@@ -3074,11 +3074,9 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     //      persistent cooperative kernel.  Mode 4 measured SLOWER on every shape (C1 52 vs 39 µs per
     //      iteration, C3 514 vs 184: the fused phases need 128 registers → half the warps, and
     //      coherent gathers), so it is opt-in (ZK_LOOP_MODE=4) and parity-tested, not the default.
-    // default: the cluster solver (mode 5) for small BiCGStab systems, else the WHILE graph
-    // (BiCGStab(ℓ): up to 4096 rows — its vectors stay in global memory and the cluster version
-    // only wins at C1 size: 110 vs 250 µs per ℓ = 8 cycle; T0 243 vs 245, C2 287 vs 275)
-    const int64_t cl_default = kClusterDefaultRows;
-    int mode = A->dist ? 3 : (cluster_kind(method) >= 0 && A->n_rows <= cl_default ? 5 : 1);
+    // default: the cluster solver (mode 5) for small systems, else the WHILE graph
+    // (every solver when its own rows fit the cluster's shared memory, see cluster_fits)
+    int mode = A->dist ? 3 : (cluster_kind(method) >= 0 && A->n_rows <= kClusterDefaultRows ? 5 : 1);
     if (const char* e = getenv("ZK_LOOP_MODE")) {
         int m = atoi(e);
         if (m >= 1 && m <= 5) mode = m;

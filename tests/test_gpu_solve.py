@@ -399,7 +399,7 @@ def test_bicgstab_irregular_rows_stress():
 @pytest.mark.parametrize("method", ["bicgstab", "bicgstab_jacobi"])
 @pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
 def test_cluster_solver_parity(cfg, method, monkeypatch):
-    """Loop mode 5 (the default for BiCGStab up to 4096 rows, selectable up to 65536): the whole
+    """Loop mode 5 (the default up to 16384 rows when the rows fit the cluster's shared memory): the whole
     loop in one thread-block cluster, reductions over distributed shared memory, scalar steps
     replicated per CTA."""
     if cfg != "C1":
