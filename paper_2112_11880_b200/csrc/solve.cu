@@ -1838,7 +1838,6 @@ __device__ __forceinline__ void cl_true(SolveCtx* c, ClusterRed& R, const double
         if (sub == 0 && l < nr) acc[0] += cabs2(csub(bg[row0 + l], y));
     }
     cl_sum<1>(acc, R);
-    __syncthreads();
     if (threadIdx.x == 0) fin_true(c, R.tot);
     __syncthreads();
 }
@@ -1895,7 +1894,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
                 }
             }
             cl_sum<3>(acc, R);
-            __syncthreads();
             if (threadIdx.x == 0) fin_k1_bicg(c, R.tot);
             __syncthreads();
             if (c->done) break;
@@ -1913,7 +1911,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
                 acc[0] += cabs2(o);
             }
             cl_sum<1>(acc, R);  // its cluster barrier also publishes s for the K3 gathers
-            __syncthreads();
             if (threadIdx.x == 0) fin_k2_bicg(c, R.tot);
             __syncthreads();
             if (c->done) {  // half-step exit: x += α p
@@ -1939,7 +1936,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
                 }
             }
             cl_sum<3>(acc, R);
-            __syncthreads();
             if (threadIdx.x == 0) fin_k3_bicg(c, R.tot);
             __syncthreads();
             if (c->done) break;
@@ -1963,7 +1959,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
                 acc[2] = fma(q.x, rn.y, fma(-q.y, rn.x, acc[2]));
             }
             cl_sum<3>(acc, R);
-            __syncthreads();
             if (threadIdx.x == 0) fin_k4_bicg(c, R.tot);
             __syncthreads();
             if (c->done) break;
@@ -2057,7 +2052,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, co
                 acc[0] += cabs2(wn);
             }
             cl_sum<1>(acc, R);  // also publishes y2 for the T2 gathers
-            __syncthreads();
             if (threadIdx.x == 0) fin_t1_tfqmr(c, R.tot);
             __syncthreads();
             if (c->done) {
@@ -2091,7 +2085,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, co
                 }
             }
             cl_sum<3>(acc, R);
-            __syncthreads();
             if (threadIdx.x == 0) fin_t2_tfqmr(c, R.tot);
             __syncthreads();
         }
@@ -2139,7 +2132,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, co
                 }
             }
             cl_sum<2>(acc, R);
-            __syncthreads();
             if (threadIdx.x == 0) fin_sigma_tfqmr(c, R.tot);
             __syncthreads();
         }
@@ -2212,7 +2204,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const
                 }
             }
             cl_sum<2>(acc, R);
-            __syncthreads();
             if (threadIdx.x == 0) {
                 if (COCG) fin_k1_cocg(c, R.tot);
                 else fin_k1_cg(c, R.tot);
@@ -2249,7 +2240,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const
                 }
             }
             cl_sum<K2>(acc, R);
-            __syncthreads();
             if (threadIdx.x == 0) {
                 if (COCG) fin_k2_cocg(c, R.tot);
                 else fin_k2_cg(c, R.tot);
@@ -2386,7 +2376,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
                     }
                 }
                 cl_sum<3>(acc, R);
-                __syncthreads();
                 if (threadIdx.x == 0) fin_s1_bl(c, R.tot);
                 __syncthreads();
                 if (c->done) break;
@@ -2415,7 +2404,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
                     }
                 }
                 cl_sum<1>(acc, R);  // also publishes r̂_j for the S2 gathers
-                __syncthreads();
                 if (threadIdx.x == 0) fin_b2_bl(c, R.tot);
                 __syncthreads();
                 if (c->done) break;
@@ -2436,7 +2424,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
                 }
                 if (j < ell - 1) {
                     cl_sum<3>(acc, R);
-                    __syncthreads();
                     if (threadIdx.x == 0) fin_s2_bl(c, R.tot);
                 }
                 __syncthreads();
@@ -2510,7 +2497,6 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
                 acc[2] = fma(tv.x, r0.y, fma(-tv.y, r0.x, acc[2]));
             }
             cl_sum<3>(acc, R);
-            __syncthreads();
             if (threadIdx.x == 0) fin_u_bl(c, R.tot);
             __syncthreads();
         }
