@@ -2512,23 +2512,14 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
     cl.sync();
 }
 
-// lanes per row of the cluster SpMV: minimise passes × chunks per lane (ties: more lanes)
-static int cluster_w(int64_t n, int cs, int max_len) {
+// lanes per row of the cluster SpMV: 8 when one pass of 512 threads covers the CTA's rows, else 4.
+// Measured per BiCGStab iteration (µs, W = 1 / 2 / 4 / 8): Twingo3D-0 31.8 / 24.2 / 19.8 / 20.9,
+// Audi3D-2 35.8 / 25.3 / 24.2 / 24.9; Audi3D-1 (108 rows per CTA) 10.5 at W = 8.
+static int cluster_w(int64_t n, int cs, int /*max_len*/) {
     const int64_t rpc = (n + cs - 1) / cs;
-    int best = 8;
-    int64_t best_cost = INT64_MAX;
-    for (int w : {8, 4, 2, 1}) {
-        const int64_t passes = (rpc + kCBlock / w - 1) / (kCBlock / w);
-        const int64_t chunks = ((max_len + w - 1) / w + 3) / 4;  // cl_row: U = 4 entries per lane per chunk
-        const int64_t cost = passes * (chunks < 1 ? 1 : chunks);
-        if (cost < best_cost) {
-            best_cost = cost;
-            best = w;
-        }
-    }
-    return best;
+    return rpc * 8 <= kCBlock ? 8 : 4;
 }
-// cluster solver kinds: 0 BiCGStab (and Jacobi-BiCGStab), 1 TFQMR, 2 CG, 3 COCG
+// cluster solver kinds: 0 BiCGStab (and Jacobi-BiCGStab), 1 TFQMR, 2 CG, 3 COCG, 4 BiCGStab(ℓ)
 static int cluster_kind(int method) {
     return method == ZK_BICGSTAB ? 0 : method == ZK_TFQMR ? 1 : method == ZK_CG ? 2 : method == ZK_COCG ? 3
          : method == kBiCGStabL ? 4 : -1;
