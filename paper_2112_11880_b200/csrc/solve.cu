@@ -1329,6 +1329,7 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) bl_b2(SolveCtx* c, VecSet
 template <int S, bool RED>
 struct EpiBl {  // out = A v ; {⟨r̃, out⟩, ‖out‖²} when RED
     static constexpr int K = RED ? 3 : 0;
+    static constexpr bool kOrdered = !RED;  // store-only (split schedule): as EpiStore (spmv.cuh)
     static constexpr int KA = K > 0 ? K : 1;
     using Pre = double2;
     SolveCtx* c;
