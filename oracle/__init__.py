@@ -19,6 +19,7 @@ import numpy as np
 _DIR = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_DIR, "zk_oracle.c")
 _SO = os.path.join(_DIR, "liboracle.so")
+_SO_OMP = os.path.join(_DIR, "liboracle_omp.so")  # timing-only all-core build (ROWWISE loops, see zk_oracle.c)
 
 ORD_SEQ, ORD_REV, ORD_BLOCK256, ORD_NEUMAIER = 0, 1, 2, 3
 
@@ -26,44 +27,62 @@ STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN_RHO", 3: "BREAKDOWN_SIGMA",
           4: "BREAKDOWN_OMEGA", 5: "NOT_HPD", 6: "NONFINITE", 7: "ZERO_RHS"}
 
 
-def build(force: bool = False) -> str:
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
-                               "-fPIC", "-shared", "-o", _SO, _SRC, "-lm"])
-    return _SO
+def build(force: bool = False, omp: bool = False) -> str:
+    so = _SO_OMP if omp else _SO
+    if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
+                              + (["-fopenmp"] if omp else []) + ["-o", so, _SRC, "-lm"])
+    return so
 
 
 _h = None
+_h_omp = None
+
+
+def use_all_cores(on: bool = True):
+    """Route every call through the OpenMP build (bench.py timing only).  Same bits: only the
+    independent per-row / per-element loops (ROWWISE in zk_oracle.c) are split over threads."""
+    global _h, _h_omp
+    if on:
+        if _h_omp is None:
+            _h_omp = _load(build(omp=True))
+        _h = _h_omp
+    else:
+        _h = _load(build())
 
 
 def _lib():
     global _h
     if _h is None:
-        lib = ctypes.CDLL(build())
-        P, I64, D, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
-        lib.oracle_zdotc.argtypes = [I64, P, P, I, P]
-        lib.oracle_zdotc.restype = None
-        lib.oracle_sumsq.argtypes = [I64, P, I]
-        lib.oracle_sumsq.restype = D
-        lib.oracle_dznrm2.argtypes = [I64, P, I]
-        lib.oracle_dznrm2.restype = D
-        lib.oracle_zaxpy.argtypes = [I64, D, D, P, P]
-        lib.oracle_zaxpy.restype = None
-        lib.oracle_zscal.argtypes = [I64, D, D, P]
-        lib.oracle_zscal.restype = None
-        lib.oracle_zcsrmv.argtypes = [I64, P, P, P, D, D, P, D, D, P, I]
-        lib.oracle_zcsrmv.restype = None
-        lib.oracle_zassign.argtypes = [I64, D, D, P]
-        lib.oracle_zassign.restype = None
-        lib.oracle_zaxmy.argtypes = [I64, P, P]
-        lib.oracle_zaxmy.restype = None
-        for f in (lib.oracle_bicgstab, lib.oracle_cg, lib.oracle_bicgstab_jacobi, lib.oracle_cocg, lib.oracle_tfqmr):
-            f.argtypes = [I64, P, P, P, P, P, D, ctypes.c_int32, I, P, P, P, P]
-            f.restype = I
-        lib.oracle_bicgstab_l.argtypes = [I64, P, P, P, P, P, D, ctypes.c_int32, I, I, P, P, P, P]
-        lib.oracle_bicgstab_l.restype = I
-        _h = lib
+        _h = _load(build())
     return _h
+
+
+def _load(path):
+    lib = ctypes.CDLL(path)
+    P, I64, D, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+    lib.oracle_zdotc.argtypes = [I64, P, P, I, P]
+    lib.oracle_zdotc.restype = None
+    lib.oracle_sumsq.argtypes = [I64, P, I]
+    lib.oracle_sumsq.restype = D
+    lib.oracle_dznrm2.argtypes = [I64, P, I]
+    lib.oracle_dznrm2.restype = D
+    lib.oracle_zaxpy.argtypes = [I64, D, D, P, P]
+    lib.oracle_zaxpy.restype = None
+    lib.oracle_zscal.argtypes = [I64, D, D, P]
+    lib.oracle_zscal.restype = None
+    lib.oracle_zcsrmv.argtypes = [I64, P, P, P, D, D, P, D, D, P, I]
+    lib.oracle_zcsrmv.restype = None
+    lib.oracle_zassign.argtypes = [I64, D, D, P]
+    lib.oracle_zassign.restype = None
+    lib.oracle_zaxmy.argtypes = [I64, P, P]
+    lib.oracle_zaxmy.restype = None
+    for f in (lib.oracle_bicgstab, lib.oracle_cg, lib.oracle_bicgstab_jacobi, lib.oracle_cocg, lib.oracle_tfqmr):
+        f.argtypes = [I64, P, P, P, P, P, D, ctypes.c_int32, I, P, P, P, P]
+        f.restype = I
+    lib.oracle_bicgstab_l.argtypes = [I64, P, P, P, P, P, D, ctypes.c_int32, I, I, P, P, P, P]
+    lib.oracle_bicgstab_l.restype = I
+    return lib
 
 
 def _c128(a) -> np.ndarray:

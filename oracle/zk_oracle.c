@@ -39,6 +39,17 @@ enum {
 #define RE(v, i) ((v)[2 * (i)])
 #define IM(v, i) ((v)[2 * (i) + 1])
 
+/* Timing-only OpenMP build (liboracle_omp.so, bench.py's all-core cpu_baseline row, SURVEY.md
+ * §8(d) "CPU oracle timing"): ROWWISE marks loops whose iterations are independent (one output
+ * row / element each, computed exactly as in the serial loop), so splitting them over threads
+ * changes no bit of any result.  Sums over i (dot, norm) stay sequential.  The default build has
+ * no -fopenmp and ROWWISE expands to nothing. */
+#ifdef _OPENMP
+#define ROWWISE _Pragma("omp parallel for schedule(static)")
+#else
+#define ROWWISE
+#endif
+
 /* ------------------------------------------------------------------------ */
 /* summation helper: adds term[i] for i in [0,n) in the requested order     */
 /* ------------------------------------------------------------------------ */
@@ -133,6 +144,7 @@ void oracle_zscal(int64_t n, double ar, double ai, double* x) {
 void oracle_zcsrmv(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, const double* val,
                    double ar, double ai, const double* x, double br, double bi, double* y,
                    int order) {
+    ROWWISE
     for (int64_t i = 0; i < n_rows; i++) {
         double sr = 0.0, si = 0.0;
         if (order == ORD_REV) {
@@ -252,6 +264,7 @@ int oracle_bicgstab(int64_t n, const int64_t* row_ptr, const int32_t* col, const
             memcpy(p, r, bytes);                               /* p = r */
         } else {
             cplx beta = cmul(cdiv(rho, rho_prev), cdiv(alpha, omega));  /* β = (ρ/ρ_prev)(α/ω) */
+            ROWWISE
             for (int64_t i = 0; i < n; i++) {                  /* p = r + β(p − ω v) */
                 cplx pv = {RE(p, i), IM(p, i)}, vv = {RE(v, i), IM(v, i)};
                 cplx wv = cmul(omega, vv);
@@ -267,6 +280,7 @@ int oracle_bicgstab(int64_t n, const int64_t* row_ptr, const int32_t* col, const
         if (!cfinite(sigma)) { status = ST_NONFINITE; break; }
         if (cabs_(sigma) <= 1e-30 * nrh * vnorm) { status = ST_BREAKDOWN_SIGMA; break; }
         alpha = cdiv(rho, sigma);                              /* α = ρ/σ */
+        ROWWISE
         for (int64_t i = 0; i < n; i++) {                      /* s = r − α v */
             cplx vv = {RE(v, i), IM(v, i)};
             cplx av = cmul(alpha, vv);
@@ -294,6 +308,7 @@ int oracle_bicgstab(int64_t n, const int64_t* row_ptr, const int32_t* col, const
         cplx ts = dotc(&A, t, s);                              /* ω = ⟨t, s⟩/τ */
         omega.re = ts.re / tau;
         omega.im = ts.im / tau;
+        ROWWISE
         for (int64_t i = 0; i < n; i++) {                      /* x += αp + ωs ; r = s − ωt */
             cplx pv = {RE(p, i), IM(p, i)}, sv = {RE(s, i), IM(s, i)}, tv = {RE(t, i), IM(t, i)};
             cplx ap = cmul(alpha, pv), ws = cmul(omega, sv), wt = cmul(omega, tv);

@@ -434,3 +434,39 @@ def test_bicgstab_l_outcomes():
     bn = bc.copy()
     bn[0] = np.nan
     assert oracle.bicgstab_l(mc, bn, ell=2)["status"] == "NONFINITE"
+
+
+@pytest.mark.parametrize("ell", [1, 2, 3, 4, 8])
+def test_bicgstab_l_order_spread_within_gpu_bar(ell):
+    """The GPU history bars of tests/test_gpu_bicgstab_l.py (HTOL) are derived from the oracle's
+    own summation-order spread over the first 6 cycles: recompute the spread
+    on C1/C2/T0 and require it to be at least 5× inside the bar, and the bar to be no looser than
+    100× the spread (or 1e-10, the BiCGStab bar), so a bar cannot silently drift loose."""
+    from tests.test_gpu_bicgstab_l import HTOL
+    orders = (oracle.ORD_SEQ, oracle.ORD_REV, oracle.ORD_BLOCK256)
+    worst = 0.0
+    for cfg in ("C1", "C2", "T0"):
+        m = gen.make_matrix(cfg)
+        b = gen.make_rhs(m)
+        refs = [oracle.bicgstab_l(m, b, tol=1e-8, ell=ell, order=o) for o in orders]
+        k = min(6, min(r["iters"] for r in refs)) + 1
+        h0 = refs[0]["hist"][:k]
+        worst = max(worst, max(np.max(np.abs(r["hist"][:k] - h0) / h0) for r in refs[1:]))
+    assert worst * 5 <= HTOL[ell], (ell, worst)
+    assert HTOL[ell] <= max(100 * worst, 1e-10), (ell, worst)
+
+
+def test_oracle_openmp_build_is_bitwise_identical():
+    """bench.py's all-core cpu_baseline row uses liboracle_omp.so (ROWWISE loops split over
+    threads): it must compute exactly the bits of the plain build (SpMV and a full BiCGStab)."""
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    x = gen.rand_vector(m["n"], 3)
+    y1, r1 = oracle.zcsrmv(m, x), oracle.bicgstab(m, b)
+    oracle.use_all_cores(True)
+    try:
+        y2, r2 = oracle.zcsrmv(m, x), oracle.bicgstab(m, b)
+    finally:
+        oracle.use_all_cores(False)
+    assert np.array_equal(y1, y2)
+    assert r1["iters"] == r2["iters"] and np.array_equal(r1["x"], r2["x"]) and np.array_equal(r1["hist"], r2["hist"])
