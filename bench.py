@@ -50,8 +50,60 @@ def args_():
     p.add_argument("--spmv-reps", type=int, default=100)
     p.add_argument("--no-shapes", action="store_true", help="skip the PAPER.md T1-shape latency runs")
     p.add_argument("--no-methods", action="store_true",
-                   help="skip the per-method C4 solves (Jacobi-BiCGStab, COCG, TFQMR, BiCGStab(2), BiCGStab(8))")
+                   help="skip the per-method C4 solves (CG, Jacobi-BiCGStab, COCG, TFQMR, BiCGStab(2), BiCGStab(8))")
+    p.add_argument("--no-blas1", action="store_true", help="skip the BLAS-1 GB/s sweep")
+    p.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                   help="N > 1: strong = the fixed C5 system (400^3, 64M rows; BASELINE.json configs[4]) "
+                        "split into z-slabs; weak = a 200x200x(200N) box, 8M rows per GPU")
     return p.parse_args()
+
+
+# ---------------------------------------------------------------- BLAS-1 sweep (north star: dot-product GB/s)
+BLAS1_SIZES = (648_849, 2_000_000, 9_000_000, 14_000_000, 1 << 26, 1 << 28)  # PAPER.md T2-T7 h + B200 sizes
+
+
+def blas1_sweep(zk, torch, dev, stream, peak, read_gbs, reps=10):
+    """zdotc, dznrm2, zaxpy, zscal, zassign, zaxmy GB/s (algorithmic bytes, metrics.blas1_bytes) at
+    the paper's vector lengths (T2-T7: 648,849 / 2M / 9M / 14M) and at 64M / 256M elements.  Each
+    rep: a 512 MB L2 flush (outside the timed pair), then CUDA events around the one call on its
+    stream; the median rep is reported."""
+    from paper_2112_11880_b200 import metrics as M
+    flush = torch.empty(1 << 29, dtype=torch.uint8, device=dev)
+    out = {}
+    res_c = torch.empty(1, dtype=torch.complex128, device=dev)
+    res_d = torch.empty(1, dtype=torch.float64, device=dev)
+    for n in BLAS1_SIZES:
+        x = torch.full((n,), 0.5 - 0.25j, dtype=torch.complex128, device=dev)
+        y = torch.full((n,), 0.125 + 1j, dtype=torch.complex128, device=dev)
+        ops = {"zdotc": lambda: zk.zdotc(x, y, res_c, stream=stream),
+               "dznrm2": lambda: zk.dznrm2(x, res_d, stream=stream),
+               "zaxpy": lambda: zk.zaxpy(1e-3, x, y, stream=stream),
+               "zscal": lambda: zk.zscal(1.0 + 0j, y, stream=stream),
+               "zassign": lambda: zk.zassign(0.5 - 0.25j, y, stream=stream),
+               "zaxmy": lambda: zk.zaxmy(x, y, stream=stream)}
+        row = {}
+        for name, f in ops.items():
+            f()
+            ts = []
+            for _ in range(reps):
+                with torch.cuda.stream(stream):
+                    flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                f()
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ms = sorted(ts)[len(ts) // 2]
+            gbs = M.blas1_bytes(name, n) / (ms * 1e-3) / 1e9
+            row[name] = {"us": round(1e3 * ms, 2), "gbs": round(gbs, 1), "frac_of_copy_peak": round(gbs / peak, 3),
+                         "frac_of_read_stream": round(gbs / read_gbs, 3), "frac_of_8tbs_spec": round(gbs / 8000.0, 3),
+                         "gflops": round(M.FLOPS_PER_ELEM[name] * n / (ms * 1e-3) / 1e9, 1)}
+        out[str(n)] = row
+        del x, y
+    del flush
+    return {"sizes": out, "l2": "512 MB flush before every timed call", "reps": reps, "stat": "median",
+            "headline_zdotc_gbs_256M": out[str(1 << 28)]["zdotc"]["gbs"]}
 
 
 def workload_name(cfg: str, spec) -> str:
@@ -177,19 +229,34 @@ def main():
     zk.lib()
 
     comm = None
+    scaling = "weak"
     if world > 1:
-        # row-partitioned weak scaling: a 200 x 200 x (200*N) box at the C4 spacing, rank r owns
-        # the z-slab of rows [r*8M, (r+1)*8M) (exactly C4 at N = 1); NCCL halo + allreduce
-        base = gen.CONFIGS[a.config]
-        spec = gen.BoxSpec(base.nx, base.ny, base.nz * world, base.h, base.lam, base.shell, 0)
         uid = [zk.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = zk.Comm(uid[0], world, rank, local)
-        plane = spec.nx * spec.ny
-        row_range = (rank * base.nz * plane, (rank + 1) * base.nz * plane)
+        if a.scaling == "strong":
+            # BASELINE.json configs[4]: the fixed C5 system (unit-cube interior 400^3, 64M rows) split
+            # into N contiguous z-slabs (rank r: planes [r*400/N, (r+1)*400/N)); NCCL halo + allreduce
+            a.config = "C5" if a.config == "C4" else a.config
+            spec = gen.CONFIGS[a.config]
+            plane = spec.nx * spec.ny
+            z0, z1 = rank * spec.nz // world, (rank + 1) * spec.nz // world
+            row_range = (z0 * plane, z1 * plane)
+            scaling = "strong"
+        else:
+            # weak scaling: a 200 x 200 x (200*N) box at the C4 spacing, rank r owns the z-slab of
+            # rows [r*8M, (r+1)*8M) (exactly C4 at N = 1)
+            base = gen.CONFIGS[a.config]
+            spec = gen.BoxSpec(base.nx, base.ny, base.nz * world, base.h, base.lam, base.shell, 0)
+            plane = spec.nx * spec.ny
+            row_range = (rank * base.nz * plane, (rank + 1) * base.nz * plane)
     else:
         spec = gen.CONFIGS[a.config]
         row_range = None
+    if a.config == "C5" and world == 1:
+        # 64M rows on one GPU: CSR 34.9 GB + its SELL copy + workspace ≈ 78 GB; a second handle
+        # (e2e upload, the CG matrix of methods_c4) would not fit beside it
+        a.no_e2e = a.no_methods = True
     t_gen = time.perf_counter()
     mat = gen.make_matrix(spec, row_range=row_range)
     b_h = gen.make_rhs(mat)
@@ -303,6 +370,10 @@ def main():
                         3: "sliced ELL (SELL-32 device copy)"}[A.info["spmv_mode"]],
             "stored_entries": A.info["sell_entries"] or nnz}
 
+    blas1 = None
+    if world == 1 and not a.no_blas1:
+        blas1 = blas1_sweep(zk, torch, dev, stream, peak, read_gbs)
+
     # the paper's own matrix shapes (PAPER.md T1; latency-bound on B200): BiCGStab per iteration
     shapes = None
     if world == 1 and not a.no_shapes:
@@ -361,6 +432,30 @@ def main():
     methods = None
     if world == 1 and not a.no_methods:
         methods = {}
+        # CG (A7) needs Hermitian positive definite A: the gauge-twisted eta = 0 version of the same
+        # box (reading L9), same n / nnz / pattern
+        mg = gen.make_matrix(spec, eta=0.0, twist_seed=gen.SEED_TWIST)
+        bg = torch.from_numpy(np.exp(1j * mg["phase"]) * gen.make_rhs(mg)).to(dev)
+        Ag = zk.csr_create(torch.from_numpy(mg["row_ptr"]).to(dev), torch.from_numpy(mg["col_idx"]).to(dev),
+                           torch.from_numpy(mg["values"]).to(dev), n, stream=stream)
+        del mg
+        wsg = zk.alloc_workspace(Ag, "cg", a.maxit, dev)
+        rm = zk.solve(Ag, bg, None, a.tol, a.maxit, "cg", workspace=wsg, stream=stream)
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for _ in range(2):
+            rm = zk.solve(Ag, bg, None, a.tol, a.maxit, "cg", workspace=wsg, stream=stream)
+        h1.record(stream)
+        torch.cuda.synchronize()
+        t_ms = h0.elapsed_time(h1) / 2
+        its = max(rm["iters"], 1)
+        gbs = M.cg_iter_bytes(n, nnz) * its / (t_ms * 1e-3) / 1e9
+        methods["cg_twisted_hpd"] = {"status": rm["status"], "iters": rm["iters"], "time_to_tol_ms": t_ms,
+                                     "ms_per_iteration": t_ms / its, "bytes_per_iteration": M.cg_iter_bytes(n, nnz),
+                                     "iter_gbs": gbs, "frac_of_peak": gbs / peak, "true_relres": rm["true_relres"],
+                                     "spmv_launch_us": 1e3 * rm["kernel_ms"][0] / max(rm["kernel_launches"][0], 1)}
+        Ag.close()
+        del wsg, bg
         runs = [("bicgstab_jacobi", 0, M.bicgstab_iter_bytes(n, nnz)), ("cocg", 0, M.cocg_iter_bytes(n, nnz)),
                 ("tfqmr", 0, M.tfqmr_iter_bytes(n, nnz)),
                 ("bicgstab_l", 2, M.bicgstab_l_cycle_bytes(n, nnz, 2)),
@@ -423,25 +518,41 @@ def main():
             e2e["ms_per_step"] = float(t.item())
             e2e["value"] = bytes_step_all / (e2e["ms_per_step"] * 1e-3) / 1e9
 
-    cpu = None
+    cpu = cpu_all = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         rr, dt = oracle_sample(mat, b_h, 3)
         cb = step_bytes(n, nnz, rr["iters"])
         cpu = {"value": cb / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
                "sample": f"oracle BiCGStab on {a.config} capped at 3 iterations (+ init and true-residual SpMV), "
                          f"single thread, {dt:.1f} s", "ms_per_iteration": 1e3 * dt / max(rr["iters"], 1)}
+        # all host cores (SURVEY.md §8(d) "CPU oracle timing" (ii)): the same oracle source built with
+        # -fopenmp, its per-row / per-element loops split over the affinity set (same bits)
+        import oracle
+        cores = len(os.sched_getaffinity(0))
+        os.environ["OMP_NUM_THREADS"] = str(cores)
+        oracle.use_all_cores(True)
+        try:
+            rr, dt = oracle_sample(mat, b_h, 10)
+        finally:
+            oracle.use_all_cores(False)
+        cb = step_bytes(n, nnz, rr["iters"])
+        cpu_all = {"value": cb / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle (OpenMP build)",
+                   "sample": f"oracle BiCGStab on {a.config} capped at 10 iterations, liboracle_omp.so "
+                             f"(SpMV rows and vector updates over {cores} threads, dots sequential), {dt:.1f} s",
+                   "ms_per_iteration": 1e3 * dt / max(rr["iters"], 1)}
 
     if rank == 0:
         r = results[-1]
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
-            "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic",
             "config": {"workload": workload_name(a.config, spec) if world == 1 else
-                       f"{a.config} per rank: 27-point Q1-hex complex Helmholtz box {spec.nx}x{spec.ny}x{spec.nz} "
-                       f"(n={n_glob:,}), z-slab row blocks of {n:,} rows per GPU",
+                       f"{a.config}: 27-point Q1-hex complex Helmholtz box {spec.nx}x{spec.ny}x{spec.nz} "
+                       f"(n={n_glob:,}), {scaling} scaling, z-slab row blocks of {n:,} rows on rank 0",
                        "n": n_glob, "nnz_rank0": nnz, "method": "bicgstab",
-                       "tol": a.tol, "x0": "zero", "l2": "inputs larger than L2 (matrix 4.3 GB per GPU)",
+                       "tol": a.tol, "x0": "zero",
+                       "l2": f"inputs larger than L2 (matrix {M.csr_bytes(n, nnz) / 1e9:.1f} GB per GPU)",
                        "parallelism": "1 GPU" if world == 1 else
                        f"row-partitioned x{world}: NCCL halo exchange per SpMV + allreduce per reduction point"},
             "bicgstab": {"iters": iters, "status": r["status"], "ms_per_iteration": ms_step / iters,
@@ -456,6 +567,8 @@ def main():
             "methods_c4": methods,
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "cpu_baseline_all_cores": cpu_all,
+            "blas1": blas1,
             "e2e": e2e,
             "clocks": ck,
             "gpu_launches": sum(q["gpu_launches"] for q in results) + 0,

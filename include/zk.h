@@ -103,6 +103,10 @@ typedef struct {
     int32_t tma_stages;    /* TMA mode: pipeline depth */
     int64_t sell_entries;  /* mode 3: stored entries incl. padding (slices of 32 rows, each padded to
                               its longest row); 0 otherwise */
+    int64_t interior_rows; /* distributed: rows whose SpMV runs while the halo exchange is in flight
+                              (the longest run of 32-row slices referencing no halo column; the
+                              boundary rows follow the exchange); 0 on one GPU or with
+                              ZK_DIST_OVERLAP=0 (blocking exchange, then the whole SpMV) */
 } zk_csr_info_t;
 
 typedef struct {
@@ -134,6 +138,25 @@ int32_t zk_version(void);                   /* 100*major + minor */
 zk_status zk_comm_get_unique_id(void* id128);
 zk_status zk_comm_create(zk_comm* out, const void* id128, int32_t nranks, int32_t rank, int32_t device);
 zk_status zk_comm_destroy(zk_comm c);
+
+/* ---- in-process communicator (LOCAL transport): the ranks are host threads of one process ----
+ * Same row-partitioned semantics as the NCCL communicator (halo exchange before each SpMV, sums of
+ * the reduction partials in RANK ORDER, bitwise identical on every rank), with the data moved by
+ * stream-ordered device copies and a rank-order sum kernel, ordered with CUDA events; no device
+ * spinning, so several ranks may share ONE GPU (NCCL refuses that): this is how the multi-rank path
+ * runs with real halos on a single B200, and how one process can drive several GPUs.
+ * zk_local_group_create: a group of nranks (1..16) ranks; the caller owns one reference.
+ * zk_comm_create_local: called by EVERY rank concurrently (one host thread each; it rendezvouses
+ *   with the other ranks before returning), `device` = the rank's GPU.  Every later collective
+ *   call (zk_csr_create/zk_zcsrmv/zk_zdotc/zk_dznrm2/zk_solve with this comm) must likewise be made
+ *   by all ranks, each on its own stream; a rank that does not arrive within ZK_LOCAL_TIMEOUT_S
+ *   seconds (default 120) makes the others fail with ZK_ERR_NCCL.
+ * zk_local_group_destroy drops the caller's reference (the group lives until its comms are gone).
+ * Errors: ZK_ERR_INVALID_VALUE (bad rank / count, rank joined twice), ZK_ERR_CUDA, ZK_ERR_NCCL. */
+typedef struct zk_local_group_s* zk_local_group;
+zk_status zk_local_group_create(zk_local_group* out, int32_t nranks);
+zk_status zk_local_group_destroy(zk_local_group g);
+zk_status zk_comm_create_local(zk_comm* out, zk_local_group g, int32_t rank, int32_t device);
 
 /* ---- CSR create / upload ("Compressed Sparse Row (CSR)";
  *      upload once before the iterations; invariants S:38-44) ----

@@ -172,6 +172,17 @@ zk_status zcsrmv_local(const zk_csr_s* A, double2 alpha, const double2* x, doubl
     });
 }
 
+// one part (a slice set, CsrDev) of a SELL SpMV: the interior / boundary launches of dist.cu
+zk_status zcsrmv_part(const zk_csr_s* A, double2 alpha, const double2* x, double2 beta, double2* y,
+                      cudaStream_t s, const CsrDev& part) {
+    const void* k = (const void*)zcsrmv_kernel<32, 3>;
+    const LaunchCfg L = spmv_cfg_part(A, k, part);
+    EpiAxpby e{alpha, beta, y, beta.x == 0.0 && beta.y == 0.0};
+    zcsrmv_kernel<32, 3><<<L.grid, kBlock, 0, s>>>(part, A->tma, x, e);
+    ZK_CUDA(cudaGetLastError());
+    return ZK_OK;
+}
+
 // SpMV mapping from the row statistics (env ZK_SPMV_MODE / ZK_SPMV_W override, for sweeps):
 //  sub-warp kernel by default (measured faster than the TMA-staged variant on C4), lanes per row
 //  ≈ mean/8; the TMA-staged mode is available for rows ≤ 128 long (W ∈ {4, 8, 16}).
@@ -221,15 +232,17 @@ void jacobi_destroy(zk_csr_s* A);                                               
 zk_status sell_build(zk_csr_s* A, cudaStream_t s);                                               // sell.cu
 void sell_destroy(zk_csr_s* A);                                                                  // sell.cu
 int dist_nranks(const zk_csr_s* A);                                                              // dist.cu
+zk_status dist_agree_failed(zk_comm_s* c, bool failed, cudaStream_t s, int* any_failed);         // dist.cu
+int64_t dist_interior_rows(const zk_csr_s* A);                                                   // dist.cu
 }  // namespace zk
 
 using namespace zk;
 
-extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, int64_t nnz,
-                                   const int64_t* row_ptr, const int32_t* col_idx, const zk_z* values,
-                                   uint32_t flags, zk_comm comm, int64_t row_begin, zk_stream stream) {
-    if (!out) return fail(ZK_ERR_INVALID_VALUE, "out is NULL");
-    *out = nullptr;
+// everything of zk_csr_create that one rank does alone: argument checks, device arrays, validation,
+// row statistics, SpMV mapping.  *outA is set as soon as a handle exists (the caller frees it on error).
+static zk_status csr_create_local(zk_csr_s** outA, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                  const int64_t* row_ptr, const int32_t* col_idx, const zk_z* values,
+                                  uint32_t flags, zk_comm comm, int64_t row_begin, cudaStream_t s) {
     if (n_rows < 0 || n_cols < 0 || nnz < 0) return fail(ZK_ERR_INVALID_VALUE, "negative size");
     if (n_cols > INT32_MAX) return fail(ZK_ERR_INVALID_VALUE, "n_cols exceeds int32 column ids");
     if (n_rows >= INT32_MAX) return fail(ZK_ERR_INVALID_VALUE, "n_rows must be < 2^31 per matrix (rank)");
@@ -239,13 +252,9 @@ extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, 
     if (where == 3u) return fail(ZK_ERR_INVALID_VALUE, "bad flags");
     if (comm && where == ZK_PTRS_DEVICE_BORROW)
         return fail(ZK_ERR_INVALID_VALUE, "distributed matrices are renumbered: use ZK_PTRS_HOST or ZK_PTRS_DEVICE");
-    cudaStream_t s = (cudaStream_t)stream;
-
     zk_csr_s* A = new zk_csr_s();
-    auto cleanup = [&](zk_status st) {
-        zk_csr_destroy(A);
-        return st;
-    };
+    *outA = A;
+    auto cleanup = [&](zk_status st) { return st; };
     zk_status st = current_device(&A->dev);
     if (st != ZK_OK) return cleanup(st);
     A->n_rows = n_rows;
@@ -308,10 +317,37 @@ extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, 
     choose_mapping(A);
     if (cudaStreamCreateWithFlags(&A->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
         return cleanup(fail(ZK_ERR_CUDA, "cudaStreamCreate"));
+    return ZK_OK;
+}
 
+extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                   const int64_t* row_ptr, const int32_t* col_idx, const zk_z* values,
+                                   uint32_t flags, zk_comm comm, int64_t row_begin, zk_stream stream) {
+    if (!out) return fail(ZK_ERR_INVALID_VALUE, "out is NULL");
+    *out = nullptr;
+    cudaStream_t s = (cudaStream_t)stream;
+    zk_csr_s* A = nullptr;
+    auto cleanup = [&](zk_status st) {
+        zk_csr_destroy(A);
+        return st;
+    };
+    zk_status st = csr_create_local(&A, n_rows, n_cols, nnz, row_ptr, col_idx, values, flags, comm, row_begin, s);
     if (comm) {
+        // every rank learns whether any rank failed before the setup collectives (a rank that
+        // returned early would leave its peers blocked in the halo-plan allgather)
+        const std::string mine = zk_last_error();
+        int any = 0;
+        const zk_status ast = dist_agree_failed(comm, st != ZK_OK, s, &any);
+        if (ast != ZK_OK) return cleanup(ast);
+        if (st != ZK_OK) {
+            set_error(mine);
+            return cleanup(st);
+        }
+        if (any) return cleanup(fail(ZK_ERR_INVALID_VALUE, "zk_csr_create failed on another rank"));
         st = dist_setup(A, nullptr, nullptr, s);
         if (st != ZK_OK) return cleanup(st);
+    } else if (st != ZK_OK) {
+        return cleanup(st);
     }
     if (A->spmv_mode == 3) {  // after the halo renumbering: the copy holds the final column ids
         st = sell_build(A, s);
@@ -370,6 +406,7 @@ extern "C" zk_status zk_csr_info(zk_csr A, zk_csr_info_t* info) {
     info->rows_per_tile = A->spmv_mode == 1 ? A->tma.R : 0;
     info->tma_stages = A->spmv_mode == 1 ? A->tma.S : 0;
     info->sell_entries = A->spmv_mode == 3 ? A->sl_nnz : 0;
+    info->interior_rows = A->dist ? dist_interior_rows(A) : 0;
     return ZK_OK;
 }
 

@@ -1,14 +1,47 @@
 // blas1.cu — zaxpy, zscal (T3/T4), zdotc (T6), dznrm2 (T7).
 // SURVEY.md §8(a) A3-A5.  Grid-stride double2 streams with 4 elements in flight per thread;
 // the reductions are single-pass with a deterministic last-block finish (zk_internal.cuh).
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "spmv.cuh"
 #include "zk_host.h"
 
 namespace zk {
 
-// per-device scratch of the standalone reductions (self-cleaning tickets; one user at a time)
-__device__ double g_partials[kMaxRed * kMaxGrid];
-__device__ unsigned int g_ticket[4];
+// Scratch of the standalone reductions (block partials + self-cleaning ticket), one per
+// (device, stream): calls on different streams — or from different host threads / ranks of a
+// local group, each on its own stream — never share partials or tickets.  Calls on
+// ONE stream are serialised by the stream.  Allocated on the first call on a stream and kept.
+struct RedScratch {
+    double* partials;      // [kMaxRed][kMaxGrid]
+    unsigned int* ticket;  // [1]
+};
+static zk_status red_scratch(cudaStream_t s, RedScratch* out) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, RedScratch> cache;
+    int dev = 0;
+    ZK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({dev, s});
+    if (it != cache.end()) {
+        *out = it->second;
+        return ZK_OK;
+    }
+    char* p = nullptr;
+    const size_t pb = sizeof(double) * kMaxRed * kMaxGrid;
+    ZK_CUDA(cudaMalloc(&p, pb + 256));
+    cudaError_t e = cudaMemsetAsync(p + pb, 0, 256, s);  // stream-ordered before the first use on s
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return cuda_fail(e, "cudaMemset(ticket)", __FILE__, __LINE__);
+    }
+    RedScratch r{(double*)p, (unsigned int*)(p + pb)};
+    cache[{dev, s}] = r;
+    *out = r;
+    return ZK_OK;
+}
 
 struct OpAxpy {
     static constexpr int K = 0;
@@ -61,6 +94,7 @@ struct OpDotc {
     const double2* __restrict__ x;
     const double2* __restrict__ y;
     double2* out;
+    RedScratch sc;
     __device__ In load(int64_t i) const { return {ld_stream(x + i), ld_stream(y + i)}; }
     __device__ void apply(int64_t, const In& v, double (&acc)[2]) const {
         // conj(x)·y: re += xr·yr + xi·yi, im += xr·yi − xi·yr
@@ -71,7 +105,7 @@ struct OpDotc {
     }
     __device__ void finish(double (&acc)[2]) const {
         double tot[2];
-        if (grid_sum<2>(acc, g_partials, &g_ticket[0], tot) && threadIdx.x == 0) *out = make_double2(tot[0], tot[1]);
+        if (grid_sum<2>(acc, sc.partials, sc.ticket, tot) && threadIdx.x == 0) *out = make_double2(tot[0], tot[1]);
     }
 };
 
@@ -81,6 +115,7 @@ struct OpNrm2 {
     const double2* __restrict__ x;
     double* out;
     bool squared;
+    RedScratch sc;
     __device__ In load(int64_t i) const { return {ld_stream(x + i)}; }
     __device__ void apply(int64_t, const In& v, double (&acc)[1]) const {
         acc[0] = fma(v.x.x, v.x.x, acc[0]);
@@ -88,7 +123,7 @@ struct OpNrm2 {
     }
     __device__ void finish(double (&acc)[1]) const {
         double tot[1];
-        if (grid_sum<1>(acc, g_partials, &g_ticket[1], tot) && threadIdx.x == 0) *out = squared ? tot[0] : sqrt(tot[0]);
+        if (grid_sum<1>(acc, sc.partials, sc.ticket, tot) && threadIdx.x == 0) *out = squared ? tot[0] : sqrt(tot[0]);
     }
 };
 
@@ -112,10 +147,14 @@ static zk_status launch_vec(int64_t n, const Op& op, cudaStream_t s) {
 
 // used by dist.cu: local partial of a distributed reduction
 zk_status dotc_local(int64_t n, const double2* x, const double2* y, double2* out, cudaStream_t s) {
-    return launch_vec(n, OpDotc{x, y, out}, s);
+    RedScratch sc;
+    ZK_TRY(red_scratch(s, &sc));
+    return launch_vec(n, OpDotc{x, y, out, sc}, s);
 }
-zk_status sumsq_local(int64_t n, const double2* x, double* out, cudaStream_t s) {
-    return launch_vec(n, OpNrm2{x, out, true}, s);
+zk_status sumsq_local(int64_t n, const double2* x, double* out, cudaStream_t s, bool squared = true) {
+    RedScratch sc;
+    ZK_TRY(red_scratch(s, &sc));
+    return launch_vec(n, OpNrm2{x, out, squared, sc}, s);
 }
 __global__ void sqrt_kernel(double* v) { *v = sqrt(*v); }
 zk_status sqrt_inplace(double* v, cudaStream_t s) {
@@ -165,7 +204,7 @@ extern "C" zk_status zk_dznrm2(int64_t n, const zk_z* x, double* result, zk_comm
         ZK_CUDA(cudaMemsetAsync(result, 0, sizeof(double), st));
         return ZK_OK;
     }
-    if (!comm) return launch_vec(n, OpNrm2{(const double2*)x, result, false}, st);
+    if (!comm) return sumsq_local(n, (const double2*)x, result, st, false);
     ZK_TRY(sumsq_local(n, (const double2*)x, result, st));
     ZK_TRY(comm_allreduce_sum(comm, result, 1, st));
     return sqrt_inplace(result, st);

@@ -5,6 +5,7 @@
 // peers (NVLink through NVSwitch); each reduction point ends with an ncclAllReduce of the
 // block partials' sums (≤ 4 doubles), identical on every rank, so all ranks take the same branch.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -14,8 +15,8 @@
 
 namespace zk {
 zk_status comm_allreduce_sum(zk_comm_s* c, double* buf, int count, cudaStream_t s);
-zk_status comm_group_start();
-zk_status comm_group_end();
+zk_status comm_group_start(zk_comm_s* c);
+zk_status comm_group_end(zk_comm_s* c, cudaStream_t s);
 zk_status comm_send(zk_comm_s* c, const void* buf, size_t bytes, int peer, cudaStream_t s);
 zk_status comm_recv(zk_comm_s* c, void* buf, size_t bytes, int peer, cudaStream_t s);
 zk_status comm_allgather(zk_comm_s* c, const void* send, void* recv, size_t bytes, cudaStream_t s);
@@ -23,6 +24,8 @@ int comm_rank(const zk_comm_s* c);
 int comm_size(const zk_comm_s* c);
 zk_status zcsrmv_local(const zk_csr_s* A, double2 alpha, const double2* x, double2 beta, double2* y,
                        cudaStream_t s);
+zk_status zcsrmv_part(const zk_csr_s* A, double2 alpha, const double2* x, double2 beta, double2* y,
+                      cudaStream_t s, const CsrDev& part);
 
 struct DistPlan {
     int nranks = 1, rank = 0;
@@ -34,6 +37,11 @@ struct DistPlan {
     int* d_send_idx = nullptr;                 // local rows to pack, concatenated per peer
     double2* d_sendbuf = nullptr;
     double2* d_xg = nullptr;                   // gather scratch of zk_zcsrmv: [x | halo]
+    // interior / boundary split (SURVEY.md §8(e) "Halo" row): the longest run of 32-row slices
+    // whose rows reference no halo column, [ov_lo, ov_hi); their SpMV overlaps the exchange
+    int ov_lo = 0, ov_hi = 0, n_slices = 0;
+    cudaStream_t cs = nullptr;                 // exchange stream
+    cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
 };
 
 static DistPlan* plan(const zk_csr_s* A) { return (DistPlan*)A->dist; }
@@ -50,8 +58,28 @@ void dist_destroy(zk_csr_s* A) {
     cudaFree(P->d_send_idx);
     cudaFree(P->d_sendbuf);
     cudaFree(P->d_xg);
+    if (P->cs) cudaStreamDestroy(P->cs);
+    if (P->ev_pack) cudaEventDestroy(P->ev_pack);
+    if (P->ev_halo) cudaEventDestroy(P->ev_halo);
     delete P;
     A->dist = nullptr;
+}
+
+// *any_failed = 1 if `failed` on any rank (one allreduce of a double; every rank calls it)
+zk_status dist_agree_failed(zk_comm_s* c, bool failed, cudaStream_t s, int* any_failed) {
+    double* d = nullptr;
+    double h = failed ? 1.0 : 0.0;
+    ZK_CUDA(cudaMalloc(&d, sizeof(double)));
+    cudaError_t e = cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, s);
+    zk_status st = e == cudaSuccess ? comm_allreduce_sum(c, d, 1, s) : cuda_fail(e, "agree", __FILE__, __LINE__);
+    if (st == ZK_OK) {
+        e = cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = cuda_fail(e, "agree", __FILE__, __LINE__);
+    }
+    cudaFree(d);
+    *any_failed = h > 0.0 ? 1 : 0;
+    return st;
 }
 
 int64_t dist_gather_len(const zk_csr_s* A) { return A->n_rows + (plan(A) ? plan(A)->n_ext : 0); }
@@ -113,13 +141,13 @@ zk_status dist_setup(zk_csr_s* A, const int64_t*, const int*, cudaStream_t s) {
     ZK_CUDA(cudaMalloc(&d_req_out, sizeof(int) * (n_ext > 0 ? n_ext : 1)));
     ZK_CUDA(cudaMalloc(&d_req_in, sizeof(int) * (P->n_send > 0 ? P->n_send : 1)));
     if (n_ext) ZK_CUDA(cudaMemcpyAsync(d_req_out, ext.data(), sizeof(int) * n_ext, cudaMemcpyHostToDevice, s));
-    ZK_TRY(comm_group_start());
+    ZK_TRY(comm_group_start(c));
     for (int q = 0; q < np; q++) {
         if (q == me) continue;
         if (P->recv_cnt[q]) ZK_TRY(comm_send(c, d_req_out + P->recv_off[q], sizeof(int) * P->recv_cnt[q], q, s));
         if (P->send_cnt[q]) ZK_TRY(comm_recv(c, d_req_in + P->send_off[q], sizeof(int) * P->send_cnt[q], q, s));
     }
-    ZK_TRY(comm_group_end());
+    ZK_TRY(comm_group_end(c, s));
     std::vector<int> req(P->n_send > 0 ? P->n_send : 1);
     if (P->n_send) ZK_CUDA(cudaMemcpyAsync(req.data(), d_req_in, sizeof(int) * P->n_send, cudaMemcpyDeviceToHost, s));
     ZK_CUDA(cudaStreamSynchronize(s));
@@ -139,18 +167,72 @@ zk_status dist_setup(zk_csr_s* A, const int64_t*, const int*, cudaStream_t s) {
     // ---- 5. renumber columns to [local | halo] in the library's own copy
     ZK_TRY(zk_halo_renumber(A->nnz, col.data(), A->row_begin, A->n_rows, n_ext, ext.data(), col.data()));
     if (A->nnz) ZK_CUDA(cudaMemcpyAsync(A->col, col.data(), sizeof(int) * A->nnz, cudaMemcpyHostToDevice, s));
+    // ---- 6. interior slices: the longest run of 32-row slices with no halo column
+    std::vector<int64_t> rp(A->n_rows + 1);
+    ZK_CUDA(cudaMemcpyAsync(rp.data(), A->row_ptr, sizeof(int64_t) * (A->n_rows + 1), cudaMemcpyDeviceToHost, s));
     ZK_CUDA(cudaStreamSynchronize(s));
+    const int64_t ns = (A->n_rows + 31) / 32;
+    P->n_slices = (int)ns;
+    int64_t best_lo = 0, best_len = 0, run_lo = 0;
+    for (int64_t sl = 0; sl <= ns; sl++) {
+        bool interior = sl < ns;
+        if (interior) {
+            const int64_t r0 = sl * 32, r1 = std::min<int64_t>(r0 + 32, A->n_rows);
+            for (int64_t p = rp[r0]; p < rp[r1] && interior; p++) interior = col[p] < A->n_rows;
+        }
+        if (!interior) {
+            if (sl - run_lo > best_len) {
+                best_len = sl - run_lo;
+                best_lo = run_lo;
+            }
+            run_lo = sl + 1;
+        }
+    }
+    P->ov_lo = (int)best_lo;
+    P->ov_hi = (int)(best_lo + best_len);
+    ZK_CUDA(cudaStreamCreateWithFlags(&P->cs, cudaStreamNonBlocking));
+    ZK_CUDA(cudaEventCreateWithFlags(&P->ev_pack, cudaEventDisableTiming));
+    ZK_CUDA(cudaEventCreateWithFlags(&P->ev_halo, cudaEventDisableTiming));
     return ZK_OK;
 }
 
-zk_status dist_halo(const zk_csr_s* A, double2* xg, cudaStream_t s) {
+// halo exchange with the interior slices overlapped: is it available for this matrix?
+// (SELL mapping, a non-empty interior run; ZK_DIST_OVERLAP=0 turns it off)
+bool dist_overlap(const zk_csr_s* A) {
+    const int on = getenv("ZK_DIST_OVERLAP") ? atoi(getenv("ZK_DIST_OVERLAP")) : 1;
+    const DistPlan* P = plan(A);
+    return on && P && A->spmv_mode == 3 && P->ov_hi > P->ov_lo && P->n_slices == (int)A->n_slices;
+}
+// the interior run and the boundary rest (prefix + suffix) of the slice set of `a`
+void dist_split(const zk_csr_s* A, const CsrDev& a, CsrDev* in, CsrDev* bd) {
+    const DistPlan* P = plan(A);
+    *in = a;
+    in->sl_lo = P->ov_lo;
+    in->sl_cnt = P->ov_hi - P->ov_lo;
+    in->sl_gap_at = in->sl_cnt;
+    in->sl_gap = 0;
+    in->main_part = 1;
+    *bd = a;
+    bd->sl_lo = 0;
+    bd->sl_cnt = P->ov_lo + (P->n_slices - P->ov_hi);
+    bd->sl_gap_at = P->ov_lo;
+    bd->sl_gap = P->ov_hi - P->ov_lo;
+    bd->main_part = 0;
+}
+
+static zk_status halo_pack(const zk_csr_s* A, const double2* xg, cudaStream_t s) {
     const DistPlan* P = plan(A);
     if (P->n_send) {
         const int G = grid_for(P->n_send, kBlock, A->dev.num_sms * 4);
         pack_kernel<<<G, kBlock, 0, s>>>(xg, P->d_send_idx, P->n_send, P->d_sendbuf);
         ZK_CUDA(cudaGetLastError());
     }
-    ZK_TRY(comm_group_start());
+    return ZK_OK;
+}
+// grouped send/recv of the packed entries into xg's halo slots, on stream s
+static zk_status halo_exchange(const zk_csr_s* A, double2* xg, cudaStream_t s) {
+    const DistPlan* P = plan(A);
+    ZK_TRY(comm_group_start(A->comm));
     for (int q = 0; q < P->nranks; q++) {
         if (q == P->rank) continue;
         if (P->send_cnt[q])
@@ -158,7 +240,28 @@ zk_status dist_halo(const zk_csr_s* A, double2* xg, cudaStream_t s) {
         if (P->recv_cnt[q])
             ZK_TRY(comm_recv(A->comm, xg + A->n_rows + P->recv_off[q], sizeof(double2) * P->recv_cnt[q], q, s));
     }
-    return comm_group_end();
+    return comm_group_end(A->comm, s);
+}
+
+// blocking halo: xg's halo slots are filled in stream order on s
+zk_status dist_halo(const zk_csr_s* A, double2* xg, cudaStream_t s) {
+    ZK_TRY(halo_pack(A, xg, s));
+    return halo_exchange(A, xg, s);
+}
+
+// overlapped halo: pack on s, exchange on the plan's own stream; dist_halo_end makes s wait for it
+zk_status dist_halo_begin(const zk_csr_s* A, double2* xg, cudaStream_t s) {
+    const DistPlan* P = plan(A);
+    ZK_TRY(halo_pack(A, xg, s));
+    ZK_CUDA(cudaEventRecord(P->ev_pack, s));
+    ZK_CUDA(cudaStreamWaitEvent(P->cs, P->ev_pack, 0));
+    ZK_TRY(halo_exchange(A, xg, P->cs));
+    ZK_CUDA(cudaEventRecord(P->ev_halo, P->cs));
+    return ZK_OK;
+}
+zk_status dist_halo_end(const zk_csr_s* A, cudaStream_t s) {
+    ZK_CUDA(cudaStreamWaitEvent(s, plan(A)->ev_halo, 0));
+    return ZK_OK;
 }
 
 zk_status dist_allreduce_ctx(const zk_csr_s* A, double* red, int count, cudaStream_t s) {
@@ -169,8 +272,31 @@ zk_status dist_zcsrmv(const zk_csr_s* A, double2 alpha, const double2* x, double
                       cudaStream_t s) {
     const DistPlan* P = plan(A);
     ZK_CUDA(cudaMemcpyAsync(P->d_xg, x, sizeof(double2) * A->n_rows, cudaMemcpyDeviceToDevice, s));
-    ZK_TRY(dist_halo(A, P->d_xg, s));
-    return zcsrmv_local(A, alpha, P->d_xg, beta, y, s);
+    if (!dist_overlap(A)) {
+        ZK_TRY(dist_halo(A, P->d_xg, s));
+        return zcsrmv_local(A, alpha, P->d_xg, beta, y, s);
+    }
+    CsrDev in, bd;
+    dist_split(A, csr_dev(A), &in, &bd);
+    ZK_TRY(dist_halo_begin(A, P->d_xg, s));
+    ZK_TRY(zcsrmv_part(A, alpha, P->d_xg, beta, y, s, in));  // interior rows: local x only
+    ZK_TRY(dist_halo_end(A, s));
+    return bd.sl_cnt > 0 ? zcsrmv_part(A, alpha, P->d_xg, beta, y, s, bd) : ZK_OK;
+}
+
+bool comm_is_local(const zk_comm_s* c);
+// libzk kernels a distributed SpMV / allreduce launches beyond the SpMV / finish kernel itself
+void dist_launch_extra(const zk_csr_s* A, int* per_spmv, int* per_allreduce) {
+    const DistPlan* P = plan(A);
+    *per_spmv = (P && P->n_send ? 1 : 0) + (dist_overlap(A) ? 1 : 0);
+    *per_allreduce = comm_is_local(A->comm) ? 1 : 0;
+}
+int64_t dist_n_send(const zk_csr_s* A) { return plan(A) ? plan(A)->n_send : 0; }
+// rows of the interior slice run whose SpMV overlaps the halo exchange (0 without an overlap)
+int64_t dist_interior_rows(const zk_csr_s* A) {
+    if (!dist_overlap(A)) return 0;
+    const DistPlan* P = plan(A);
+    return std::min<int64_t>((int64_t)P->ov_hi * 32, A->n_rows) - (int64_t)P->ov_lo * 32;
 }
 
 int64_t dist_n_halo(const zk_csr_s* A) { return plan(A) ? plan(A)->n_ext : 0; }

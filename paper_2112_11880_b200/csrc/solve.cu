@@ -556,6 +556,26 @@ struct OpRed3Bicg {  // {⟨t, s⟩, ‖t‖²}
     __device__ void finish(double (&acc)[3]) const { reduce_finish<S_K3_BICG, 3>(c, acc); }
 };
 
+// Split schedule with a TAIL reduction (SPLIT = 2, SELL mapping on one GPU): the SpMV stores
+// out = A x like EpiStore, then each warp runs Op (the r1/r3/rq/T2b/T4b pass) over the rows it
+// just produced (spmv.cuh sell_tail) and the kernel's last block finishes the stage — the
+// separate reduction launch, its ramp and tail disappear; the loop keeps the store-only schedule.
+template <class Op>
+struct EpiStoreTail {
+    static constexpr int K = Op::K;
+    static constexpr bool kOrdered = ZK_STORE_ORD;
+    static constexpr bool kTail = true;
+    using Pre = double2;
+    using TailOp = Op;
+    double2* __restrict__ out;
+    SolveCtx* c;  // the Op (its pointers and scalars) is built only after the loop: nothing of it is live there
+    __device__ EpiStoreTail(double2* o, SolveCtx* c_) : out(o), c(c_) {}
+    __device__ Pre pre(int64_t) const { return make_double2(0.0, 0.0); }
+    __device__ void row(int64_t i, double2 y, const Pre&, double (&)[K]) { st_vec(out + i, y); }
+    __device__ Op tail_op() const { return Op(c); }
+    __device__ void finish(double (&)[K]) {}  // the tail's Op finishes the stage
+};
+
 struct EpiK1Cg {  // q = A p ; {δ = ⟨p, q⟩}
     static constexpr int K = 2;
     using Pre = double2;
@@ -987,15 +1007,18 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_true(SolveCtx
     EpiTrue e(c);
     spmv_any<W, MODE>(A, T, xg, e);
 }
-template <int W, int MODE, bool SP>
+// SPLIT: 0 fused epilogue; 1 products only (r1_bicg reduces); 2 products + tail reduction (SELL)
+template <int W, int MODE, int SPLIT>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_bicg(SolveCtx* c, const CsrDev A) {
-    constexpr bool SPLIT = SP;  // products only; r1_bicg reduces
     pdl_enter();
     if (c->done) return;
     stamp_start<S_K1_BICG>(c);
     const TmaPlan T = c->T;
     const double2* p = c->p;
-    if constexpr (SPLIT) {
+    if constexpr (SPLIT == 2) {
+        EpiStoreTail<OpRed1Bicg> e(c->v, c);
+        spmv_any<W, MODE>(A, T, p, e);
+    } else if constexpr (SPLIT == 1) {
         EpiStore e(c->v);
         spmv_any<W, MODE>(A, T, p, e);
     } else {
@@ -1022,14 +1045,17 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_bicg(SolveCtx* c) {
     OpK2Bicg op(c);
     vec_body(c->A.n_rows, op);
 }
-template <int W, int MODE, bool SPLIT>
+template <int W, int MODE, int SPLIT>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k3_bicg(SolveCtx* c, const CsrDev A) {
     pdl_enter();
     if (c->done) return;
     stamp_start<S_K3_BICG>(c);
     const TmaPlan T = c->T;
     const double2* s = c->s;
-    if constexpr (SPLIT) {
+    if constexpr (SPLIT == 2) {
+        EpiStoreTail<OpRed3Bicg> e(c->t, c);
+        spmv_any<W, MODE>(A, T, s, e);
+    } else if constexpr (SPLIT == 1) {
         EpiStore e(c->t);
         spmv_any<W, MODE>(A, T, s, e);
     } else {
@@ -1055,14 +1081,17 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k5_bicg(SolveCtx* c) {
     }
     set_cond(c);  // after the stream loop: the device-runtime call does not pressure its registers
 }
-template <int W, int MODE, bool SPLIT>
+template <int W, int MODE, int SPLIT>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cocg(SolveCtx* c, const CsrDev A) {
     pdl_enter();
     if (c->done) return;
     stamp_start<S_K1_COCG>(c);
     const TmaPlan T = c->T;
     const double2* p = c->p;
-    if constexpr (SPLIT) {
+    if constexpr (SPLIT == 2) {
+        EpiStoreTail<OpRedPq<false, S_K1_COCG>> e(c->q, c);
+        spmv_any<W, MODE>(A, T, p, e);
+    } else if constexpr (SPLIT == 1) {
         EpiStore e(c->q);
         spmv_any<W, MODE>(A, T, p, e);
     } else {
@@ -1085,14 +1114,17 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k3_cocg(SolveCtx* c) {
     }
     set_cond(c);
 }
-template <int W, int MODE, bool SPLIT>
+template <int W, int MODE, int SPLIT>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cg(SolveCtx* c, const CsrDev A) {
     pdl_enter();
     if (c->done) return;
     stamp_start<S_K1_CG>(c);
     const TmaPlan T = c->T;
     const double2* p = c->p;
-    if constexpr (SPLIT) {
+    if constexpr (SPLIT == 2) {
+        EpiStoreTail<OpRedPq<true, S_K1_CG>> e(c->q, c);
+        spmv_any<W, MODE>(A, T, p, e);
+    } else if constexpr (SPLIT == 1) {
         EpiStore e(c->q);
         spmv_any<W, MODE>(A, T, p, e);
     } else {
@@ -1138,11 +1170,11 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t1_tfqmr(SolveCtx* c) {
     OpT1Tfqmr op(c);
     vec_body(c->A.n_rows, op);
 }
-template <int W, int MODE, bool SPLIT>
+template <int W, int MODE, int SPLIT>
 __global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t2_tfqmr(SolveCtx* c, const CsrDev A) {
     pdl_enter();
     if (c->done) {
-        if (c->half != 1) return;
+        if (c->half != 1 || !A.main_part) return;  // once per SpMV (distributed: 2 partial launches)
         // the first half step ended the loop: only its x += η1·d1, d1 = y1 + c1·d, remains
         double2* __restrict__ x = c->x;
         const double2* __restrict__ d = c->d;
@@ -1161,7 +1193,10 @@ __global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t2_tfqmr(SolveCtx* c, cons
     stamp_start<S_T2_TFQMR>(c);
     const TmaPlan T = c->T;
     const double2* y2 = c->y2;
-    if constexpr (SPLIT) {
+    if constexpr (SPLIT == 2) {
+        EpiStoreTail<OpT2bTfqmr> e(c->u2, c);
+        spmv_any<W, MODE>(A, T, y2, e);
+    } else if constexpr (SPLIT == 1) {
         EpiStore e(c->u2);
         spmv_any<W, MODE>(A, T, y2, e);
     } else {
@@ -1192,16 +1227,20 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t3_tfqmr(SolveCtx* c) {
     OpT3Tfqmr op(c, done);
     vec_body(c->A.n_rows, op);
 }
-template <int W, int MODE, bool SPLIT>
+template <int W, int MODE, int SPLIT>
 __global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t4_tfqmr(SolveCtx* c, const CsrDev A) {
     pdl_enter();
     if (c->done) {
-        if (!SPLIT && c->half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;  // T2/T3 applied the last x update
+        // T2/T3 applied the last x update (split: t4b_tfqmr clears it)
+        if (SPLIT != 1 && c->half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;
     } else {
         stamp_start<S_T4_TFQMR>(c);
         const TmaPlan T = c->T;
         const double2* y1 = c->y1;
-        if constexpr (SPLIT) {
+        if constexpr (SPLIT == 2) {
+            EpiStoreTail<OpT4bTfqmr> e(c->u1, c);
+            spmv_any<W, MODE>(A, T, y1, e);
+        } else if constexpr (SPLIT == 1) {
             EpiStore e(c->u1);
             spmv_any<W, MODE>(A, T, y1, e);
         } else {
@@ -1209,7 +1248,7 @@ __global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t4_tfqmr(SolveCtx* c, cons
             spmv_any<W, MODE>(A, T, y1, e);
         }
     }
-    if (!SPLIT) set_cond(c);  // split: t4b_tfqmr is the body's last kernel
+    if (SPLIT != 1) set_cond(c);  // split: t4b_tfqmr is the body's last kernel
 }
 // ------------------------------------------------------------------ BiCGStab(ℓ) kernels (NEXT-3)
 // One outer cycle (oracle_bicgstab_l): for j = 0..ℓ−1 the BiCG step runs as
@@ -2677,9 +2716,47 @@ static zk_status dist_finish(const zk_csr_s* A, SolveCtx* c, int count, cudaStre
     return ZK_OK;
 }
 
+// Split schedule (store-only SpMVs + a reduction pass): from kSplitRows rows, and always on a
+// distributed matrix, whose SpMVs are split into interior / boundary launches around the halo
+// exchange (a fused epilogue reduction cannot span two launches)
 static bool split_reductions(const zk_csr_s* A) {
+    if (A->dist) return true;
     if (const char* e = getenv("ZK_SPLIT_RED")) return atoi(e) != 0;
     return A->n_rows >= kSplitRows;
+}
+
+// Split schedule with the reduction as the SpMV kernel's tail (EpiStoreTail) instead of a separate
+// pass: SELL mapping, one GPU (a distributed SpMV is two launches).  ZK_SPLIT_TAIL=0/1 forces it.
+static bool split_tail(const zk_csr_s* A) {
+    if (A->dist || A->spmv_mode != 3 || !split_reductions(A)) return false;
+    if (const char* e = getenv("ZK_SPLIT_TAIL")) return atoi(e) != 0;
+    return false;
+}
+
+bool dist_overlap(const zk_csr_s* A);                                            // dist.cu
+void dist_launch_extra(const zk_csr_s* A, int* per_spmv, int* per_allreduce);    // dist.cu
+int64_t dist_n_send(const zk_csr_s* A);                                           // dist.cu
+void dist_split(const zk_csr_s* A, const CsrDev& a, CsrDev* in, CsrDev* bd);     // dist.cu
+zk_status dist_halo_begin(const zk_csr_s* A, double2* xg, cudaStream_t s);       // dist.cu
+zk_status dist_halo_end(const zk_csr_s* A, cudaStream_t s);                       // dist.cu
+
+// One store-only loop SpMV y = A·xg.  One GPU: launch(A's view, false).  Distributed: the halo
+// exchange of xg runs on the plan's stream while the interior slices (no halo column) compute,
+// then the boundary slices (SURVEY.md §8(e) "Halo": pack → send/recv ‖ interior SpMV → boundary
+// SpMV); without an interior run (or with ZK_DIST_OVERLAP=0) a blocking exchange first.
+template <class L>
+static zk_status loop_spmv(const zk_csr_s* A, const CsrDev& av, double2* xg, cudaStream_t s, L&& launch) {
+    if (!A->dist) return launch(av, false);
+    if (!dist_overlap(A)) {
+        ZK_TRY(dist_halo(A, xg, s));
+        return launch(av, false);
+    }
+    CsrDev in, bd;
+    dist_split(A, av, &in, &bd);
+    ZK_TRY(dist_halo_begin(A, xg, s));
+    ZK_TRY(launch(in, true));
+    ZK_TRY(dist_halo_end(A, s));
+    return bd.sl_cnt > 0 ? launch(bd, true) : ZK_OK;
 }
 
 // enqueue one iteration of `method`
@@ -2706,31 +2783,37 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
     const bool dist = A->dist != nullptr;
     if (dist) pdl = false;
     const bool split = split_reductions(A);
+    const bool tail = split_tail(A);
     return with_spmv(A, [&](auto wc, auto mc) -> zk_status {
         constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
+        // a split-schedule SpMV kernel over the slice set `a` (the whole matrix, or one part)
+        auto part = [&](auto kf) {
+            return [&, kf](const CsrDev& a, bool is_part) -> zk_status {
+                const LaunchCfg L = is_part ? spmv_cfg_part(A, (const void*)kf, a) : spmv_cfg(A, (const void*)kf, W, MODE);
+                return launch_loop(pdl, kf, L.grid, L.smem, s, dc, a);
+            };
+        };
         if (method == ZK_BICGSTAB) {
-            if (dist) ZK_TRY(dist_halo(A, hc.p, s));
-            if (split) {
-                auto kf = k1_bicg<W, MODE, true>;
-                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
-                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+            if (tail) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_bicg<W, MODE, 2>)));
+            } else if (split) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_bicg<W, MODE, 1>)));
                 ZK_TRY(launch_loop(pdl, r1_bicg, vec_grid(A, (const void*)r1_bicg), 0, s, dc));
             } else {
-                auto kf = k1_bicg<W, MODE, false>;
+                auto kf = k1_bicg<W, MODE, 0>;
                 const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
                 ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
             }
             if (dist) ZK_TRY((dist_finish<S_K1_BICG>(A, dc, 3, s)));
             ZK_TRY(launch_loop(pdl, k2_bicg, vec_grid(A, (const void*)k2_bicg), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_K2_BICG>(A, dc, 1, s)));
-            if (dist) ZK_TRY(dist_halo(A, hc.s, s));
-            if (split) {
-                auto kf = k3_bicg<W, MODE, true>;
-                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
-                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+            if (tail) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.s, s, part(k3_bicg<W, MODE, 2>)));
+            } else if (split) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.s, s, part(k3_bicg<W, MODE, 1>)));
                 ZK_TRY(launch_loop(pdl, r3_bicg, vec_grid(A, (const void*)r3_bicg), 0, s, dc));
             } else {
-                auto kf = k3_bicg<W, MODE, false>;
+                auto kf = k3_bicg<W, MODE, 0>;
                 const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
                 ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
             }
@@ -2783,41 +2866,38 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
         } else if (method == ZK_TFQMR) {
             ZK_TRY(launch_loop(pdl, t1_tfqmr, vec_grid(A, (const void*)t1_tfqmr), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_T1_TFQMR>(A, dc, 1, s)));
-            if (dist) ZK_TRY(dist_halo(A, hc.y2, s));
-            if (split) {
-                auto kf = t2_tfqmr<W, MODE, true>;
-                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
-                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+            if (tail) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.y2, s, part(t2_tfqmr<W, MODE, 2>)));
+            } else if (split) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.y2, s, part(t2_tfqmr<W, MODE, 1>)));
                 ZK_TRY(launch_loop(pdl, t2b_tfqmr, vec_grid(A, (const void*)t2b_tfqmr), 0, s, dc));
             } else {
-                auto kf = t2_tfqmr<W, MODE, false>;
+                auto kf = t2_tfqmr<W, MODE, 0>;
                 const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
                 ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
             }
             if (dist) ZK_TRY((dist_finish<S_T2_TFQMR>(A, dc, 3, s)));
             ZK_TRY(launch_loop(pdl, t3_tfqmr, vec_grid(A, (const void*)t3_tfqmr), 0, s, dc));
-            if (dist) ZK_TRY(dist_halo(A, hc.y1, s));
-            if (split) {
-                auto kf = t4_tfqmr<W, MODE, true>;
-                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
-                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+            if (tail) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.y1, s, part(t4_tfqmr<W, MODE, 2>)));
+            } else if (split) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.y1, s, part(t4_tfqmr<W, MODE, 1>)));
                 ZK_TRY(launch_loop(pdl, t4b_tfqmr, vec_grid(A, (const void*)t4b_tfqmr), 0, s, dc));
             } else {
-                auto kf = t4_tfqmr<W, MODE, false>;
+                auto kf = t4_tfqmr<W, MODE, 0>;
                 const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
                 ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
             }
             if (dist) ZK_TRY((dist_finish<S_T4_TFQMR>(A, dc, 2, s)));
         } else if (method == ZK_COCG) {
-            if (dist) ZK_TRY(dist_halo(A, hc.p, s));
-            if (split) {
-                auto kf = k1_cocg<W, MODE, true>;
-                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
-                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+            if (tail) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cocg<W, MODE, 2>)));
+            } else if (split) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cocg<W, MODE, 1>)));
                 auto kr = rq_kernel<false, S_K1_COCG>;
                 ZK_TRY(launch_loop(pdl, kr, vec_grid(A, (const void*)kr), 0, s, dc));
             } else {
-                auto kf = k1_cocg<W, MODE, false>;
+                auto kf = k1_cocg<W, MODE, 0>;
                 const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
                 ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
             }
@@ -2826,15 +2906,14 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             if (dist) ZK_TRY((dist_finish<S_K2_COCG>(A, dc, 3, s)));
             ZK_TRY(launch_loop(pdl, k3_cocg, vec_grid(A, (const void*)k3_cocg), 0, s, dc));
         } else {
-            if (dist) ZK_TRY(dist_halo(A, hc.p, s));
-            if (split) {
-                auto kf = k1_cg<W, MODE, true>;
-                const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
-                ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
+            if (tail) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cg<W, MODE, 2>)));
+            } else if (split) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cg<W, MODE, 1>)));
                 auto kr = rq_kernel<true, S_K1_CG>;
                 ZK_TRY(launch_loop(pdl, kr, vec_grid(A, (const void*)kr), 0, s, dc));
             } else {
-                auto kf = k1_cg<W, MODE, false>;
+                auto kf = k1_cg<W, MODE, 0>;
                 const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
                 ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A));
             }
@@ -3085,8 +3164,10 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     GraphCache& gc = A->graph[method];
     // one graph per (method, ℓ, Jacobi): the SpMV kernels take the CSR view (A or A·M⁻¹) as a
     // launch parameter baked into the graph
-    const int gkey = (method * 16 + ell) * 2 + (jacobi ? 1 : 0);
-    if (mode <= 2 && (gc.ws != workspace || gc.mode != mode || gc.method != gkey || !gc.exec)) {
+    const int gkey = ((method * 16 + ell) * 2 + (jacobi ? 1 : 0)) * 2 + (split_tail(A) ? 1 : 0);
+    // key: workspace pointer, loop mode, method/ℓ/Jacobi and maxit (ws_layout places the partials,
+    // tickets and vectors after hist[maxit+1]; BiCGStab(ℓ) bakes its vector pointers into the graph)
+    if (mode <= 2 && (gc.ws != workspace || gc.mode != mode || gc.method != gkey || gc.maxit != maxit || !gc.exec)) {
         drop_graph(gc);
         const bool pdl = !(getenv("ZK_PDL") && atoi(getenv("ZK_PDL")) == 0);
         zk_status st = mode == 1 ? build_while_graph(A, dc, hc, method, gc, pdl) : build_chunk_graph(A, dc, hc, method, gc);
@@ -3106,6 +3187,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
             gc.ws = workspace;
             gc.mode = mode;
             gc.method = gkey;
+            gc.maxit = maxit;
         }
     }
     hc.use_cond = mode == 1 ? 1 : 0;
@@ -3263,7 +3345,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         info->solve_ms = ms;
         info->loop_mode = mode;
         int per_body = method == ZK_BICGSTAB ? 5 : method == ZK_TFQMR ? 4 : method == kBiCGStabL ? 4 * ell + 2 : 3;
-        if (split_reductions(A) && mode != 4)  // the separate reduction / update passes
+        if (split_reductions(A) && !split_tail(A) && mode != 4)  // the separate reduction / update passes
             per_body += method == ZK_BICGSTAB ? 2 : (method == ZK_CG || method == ZK_COCG) ? 1
                         : method == ZK_TFQMR ? 2 : method == kBiCGStabL ? 2 * ell - 1 : 0;
         const int fins = A->dist ? (method == ZK_BICGSTAB ? 4 : method == ZK_TFQMR ? 3 : 2) : 0;  // dist: 1-thread finish kernels
@@ -3271,6 +3353,16 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         // mode 5: set_ctx + init (+ TFQMR's K0) + the cluster kernel (+ Jacobi: x = M⁻¹u and k_true)
         info->gpu_launches = mode == 4 ? 4 : mode == 5 ? 3 + pre + (jacobi ? 2 : 0)
                                                        : 3 + pre + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);
+        if (A->dist) {  // + per SpMV: pack kernel, second (boundary) launch; + per allreduce: LOCAL sum kernel
+            int per_spmv = 0, per_red = 0;
+            dist_launch_extra(A, &per_spmv, &per_red);
+            const int spmv_it = (method == ZK_BICGSTAB || method == ZK_TFQMR) ? 2 : 1;
+            const int red_it = fins;
+            const int init_spmv = (x0 ? 1 : 0) + (method == ZK_TFQMR ? 1 : 0) + 1;  // + final true residual
+            const int init_red = 2 + (method == ZK_TFQMR ? 1 : 0);
+            info->gpu_launches += out.bodies * (spmv_it * per_spmv + red_it * per_red) + init_red * per_red +
+                                  init_spmv * (per_spmv > 0 && dist_n_send(A) ? 1 : 0);
+        }
         for (int i = 0; i < 4; i++) {
             info->kernel_ms[i] = out.tsum[i] * 1e-6;
             info->kernel_launches[i] = out.tcnt[i];

@@ -249,6 +249,23 @@ __device__ __forceinline__ void spmv_body_b4(const CsrDev& A, const double2* __r
 // Per epilogue (Epi::kOrdered): the store-only epilogue of the split solver SpMVs needs it — left
 // to itself the compiler schedules that kernel at 64 registers with 3 matrix loads in flight per
 // gather batch instead of 9 (SASS; in-loop K1 708 µs vs 647 µs standalone at C4, ncu).
+// Per epilogue (Epi::kTail): after its slice loop the warp walks ITS slices once more and calls
+// epi.tail_load / epi.tail_apply on its rows — a fused reduction pass over vectors the loop just
+// wrote (each lane re-reads only what it stored itself), with no register pressure on the loop
+// (the running sums are not live there) and no extra launch.  SELL kernel only.
+// elements in flight per thread of a vector Op (Op::U, default 4)
+template <class Op>
+struct vec_unroll {
+    template <class T> static constexpr int get(decltype(T::U)*) { return T::U; }
+    template <class T> static constexpr int get(...) { return 4; }
+    static constexpr int value = get<Op>(nullptr);
+};
+template <class E>
+struct sell_tail {
+    template <class T> static constexpr bool get(decltype(T::kTail)*) { return T::kTail; }
+    template <class T> static constexpr bool get(...) { return false; }
+    static constexpr bool value = get<E>(nullptr);
+};
 template <class E>
 struct sell_ordered {
     template <class T> static constexpr bool get(decltype(T::kOrdered)*) { return T::kOrdered; }
@@ -289,25 +306,30 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
 #endif
     const int lane = threadIdx.x & 31;
     const int n = (int)A.n_rows;
-    const int n_sl = (n + 31) >> 5;
+    // logical slices t ∈ [0, sl_cnt) → physical slice phys(t) (the whole matrix, or one part of a
+    // distributed SpMV split into interior / boundary slices, CsrDev)
+    const int n_sl = A.sl_cnt;
+    auto phys = [&](int t) { return A.sl_lo + t + (t >= A.sl_gap_at ? A.sl_gap : 0); };
     const int nw = gridDim.x * kWarps;
-    int s = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    int t = blockIdx.x * kWarps + (threadIdx.x >> 5);
     int64_t base = 0;
     int width = 0;
     typename Epi::Pre pre{};
-    if (s < n_sl) {
+    if (t < n_sl) {
+        const int s = phys(t);
         base = __ldg(A.sl_ptr + s);
         width = (int)((__ldg(A.sl_ptr + s + 1) - base) >> 5);
         if (AHEAD && s * 32 + lane < n) pre = epi.pre(s * 32 + lane);
     }
-    for (; s < n_sl; s += nw) {
-        const int row = s * 32 + lane;
-        const int ns = s + nw;  // next slice: bounds and epilogue operands one step ahead
+    for (; t < n_sl; t += nw) {
+        const int row = phys(t) * 32 + lane;
+        const int nt = t + nw;  // next slice: bounds and epilogue operands one step ahead
         int64_t nbase = 0;
         int nwidth = 0;
         typename Epi::Pre npre{};
         if (PRE == 0 && !AHEAD && row < n) pre = epi.pre(row);
-        if (ns < n_sl) {
+        if (nt < n_sl) {
+            const int ns = phys(nt);
             nbase = __ldg(A.sl_ptr + ns);
             nwidth = (int)((__ldg(A.sl_ptr + ns + 1) - nbase) >> 5);
             if (AHEAD && ns * 32 + lane < n) npre = epi.pre(ns * 32 + lane);
@@ -417,17 +439,31 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
 #pragma unroll
     for (int k = 0; k < KA; k++) acc[k] = sacc[k][threadIdx.x];
 #endif
-    epi.finish(acc);
+    if constexpr (sell_tail<Epi>::value) {
+        constexpr int TU = vec_unroll<typename Epi::TailOp>::value;  // slices in flight per step
+        const auto op = epi.tail_op();
+        const int t0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
+        for (int tb = t0; tb < n_sl; tb += TU * nw) {
+            typename Epi::TailOp::In in[TU] = {};
+            int rows[TU];
+#pragma unroll
+            for (int u = 0; u < TU; u++) {
+                const int tt = tb + u * nw;
+                rows[u] = tt < n_sl ? phys(tt) * 32 + lane : n;
+                if (rows[u] < n) in[u] = op.load(rows[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < TU; u++)
+                if (rows[u] < n) op.apply(rows[u], in[u], acc);
+        }
+        op.finish(acc);
+    } else {
+        epi.finish(acc);
+    }
 }
 
 // Grid-stride elementwise body with U elements in flight per thread.
 //   Op::K, Op::In, In load(int64_t i), void apply(int64_t i, const In&, double (&acc)[K]), finish(acc)
-template <class Op>
-struct vec_unroll {
-    template <class T> static constexpr int get(decltype(T::U)*) { return T::U; }
-    template <class T> static constexpr int get(...) { return 4; }
-    static constexpr int value = get<Op>(nullptr);
-};
 
 template <class Op>
 __device__ __forceinline__ void vec_body(int64_t n, Op& op) {

@@ -247,7 +247,9 @@ namespace zk {
 // SpMV body selected at compile time: MODE 1 = TMA-staged tiles, MODE 0 = sub-warp kernel
 template <int W, int MODE, class Epi>
 __device__ __forceinline__ void spmv_any(const CsrDev& A, const TmaPlan& T, const double2* __restrict__ x, Epi& epi) {
-    if constexpr (MODE == 1) {
+    if constexpr (sell_tail<Epi>::value && MODE != 3) {
+        __trap();  // tail epilogues exist only in the SELL body (the host never launches this)
+    } else if constexpr (MODE == 1) {
         spmv_tma_body<W>(A, T, x, epi);
     } else if constexpr (MODE == 2) {
         spmv_body_b4<W>(A, x, epi);

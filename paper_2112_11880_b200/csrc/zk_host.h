@@ -40,6 +40,7 @@ struct GraphCache {
     const void* ws = nullptr;
     int method = -1;
     int mode = 0;
+    int maxit = -1;  // the workspace layout (hist, partials, vectors) depends on maxit
     cudaGraphExec_t exec = nullptr;
     cudaGraph_t graph = nullptr;
     unsigned long long cond = 0;  // cudaGraphConditionalHandle
@@ -164,7 +165,8 @@ zk_status with_spmv(const zk_csr_s* A, F&& f) {
 }
 
 inline CsrDev csr_dev(const zk_csr_s* A) {
-    return CsrDev{A->row_ptr, A->col, A->val, A->n_rows, A->nnz, A->sl_ptr, A->sl_col, A->sl_val};
+    const int ns = (int)A->n_slices;
+    return CsrDev{A->row_ptr, A->col, A->val, A->n_rows, A->nnz, A->sl_ptr, A->sl_col, A->sl_val, 0, ns, ns, 0, 1};
 }
 
 struct LaunchCfg {
@@ -184,5 +186,11 @@ inline LaunchCfg spmv_cfg(const zk_csr_s* A, const void* kernel, int W, int mode
     if (cap > kMaxGrid) cap = kMaxGrid;
     if (mode == 3) return {grid_for(A->n_slices, kWarps, cap), 0};  // one warp per 32-row slice
     return {grid_for(A->n_rows, kBlock / W, cap), 0};
+}
+// SELL launch over the slice set of `a` (a partial range of a distributed SpMV)
+inline LaunchCfg spmv_cfg_part(const zk_csr_s* A, const void* kernel, const CsrDev& a) {
+    int cap = A->dev.num_sms * blocks_per_sm(kernel, 0);
+    if (cap > kMaxGrid) cap = kMaxGrid;
+    return {grid_for(a.sl_cnt > 0 ? a.sl_cnt : 1, kWarps, cap), 0};
 }
 }  // namespace zk

@@ -178,6 +178,7 @@ __device__ __forceinline__ void warp_sum(double (&v)[K]) {
 // Block-wide sum of K doubles (fixed order). Result valid in thread 0. Uses `sm` (kWarps*K doubles).
 template <int K>
 __device__ __forceinline__ void block_sum(double (&v)[K], double* sm) {
+    __syncwarp();  // reconverge the warp (row loops of different trip counts) before the shuffles/barrier
     warp_sum<K>(v);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) {
@@ -242,6 +243,13 @@ struct CsrDev {
     const int64_t* sl_ptr;
     const int* sl_col;
     const double2* sl_val;
+    // slice set walked by the SELL kernel (distributed interior/boundary split, dist.cu): logical
+    // slices t ∈ [0, sl_cnt) map to physical slices sl_lo + t (+ sl_gap for t ≥ sl_gap_at), i.e.
+    // one contiguous run, or a prefix and a suffix around a skipped run.  The whole matrix:
+    // sl_lo = 0, sl_cnt = n_slices, sl_gap_at = sl_cnt.  main_part = 0 on the second partial
+    // launch of one SpMV (work that must happen once per SpMV is skipped there).
+    int sl_lo, sl_cnt, sl_gap_at, sl_gap;
+    int main_part;
 };
 
 }  // namespace zk

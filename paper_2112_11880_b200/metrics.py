@@ -24,7 +24,9 @@ def spmv_bytes(n: int, nnz: int, beta_nonzero: bool = False) -> int:
 
 
 def blas1_bytes(op: str, n: int) -> int:
-    return {"zdotc": 2 * Z * n, "dznrm2": Z * n, "zaxpy": 3 * Z * n, "zscal": 2 * Z * n}[op]
+    """Algorithmic bytes of one BLAS-1 call: read x (and y), write the output vector."""
+    return {"zdotc": 2 * Z * n, "dznrm2": Z * n, "zaxpy": 3 * Z * n, "zscal": 2 * Z * n,
+            "zassign": Z * n, "zaxmy": 3 * Z * n}[op]
 
 
 def bicgstab_iter_bytes(n: int, nnz: int) -> int:

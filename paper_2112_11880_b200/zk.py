@@ -52,7 +52,8 @@ class zk_csr_info_t(ctypes.Structure):
                 ("max_row_len", ctypes.c_int32), ("lanes_per_row", ctypes.c_int32),
                 ("mean_row_len", ctypes.c_double), ("n_halo", ctypes.c_int64),
                 ("borrowed", ctypes.c_int32), ("nranks", ctypes.c_int32), ("spmv_mode", ctypes.c_int32),
-                ("rows_per_tile", ctypes.c_int32), ("tma_stages", ctypes.c_int32), ("sell_entries", ctypes.c_int64)]
+                ("rows_per_tile", ctypes.c_int32), ("tma_stages", ctypes.c_int32), ("sell_entries", ctypes.c_int64),
+                ("interior_rows", ctypes.c_int64)]
 
 
 class zk_solve_info(ctypes.Structure):
@@ -71,6 +72,9 @@ SIGNATURES = {
     "zk_comm_get_unique_id": (I32, [P]),
     "zk_comm_create": (I32, [ctypes.POINTER(P), P, I32, I32, I32]),
     "zk_comm_destroy": (I32, [P]),
+    "zk_local_group_create": (I32, [ctypes.POINTER(P), I32]),
+    "zk_local_group_destroy": (I32, [P]),
+    "zk_comm_create_local": (I32, [ctypes.POINTER(P), P, I32, I32]),
     "zk_csr_create": (I32, [ctypes.POINTER(P), I64, I64, I64, P, P, P, U32, P, I64, P]),
     "zk_csr_destroy": (I32, [P]),
     "zk_csr_info": (I32, [P, ctypes.POINTER(zk_csr_info_t)]),
@@ -135,13 +139,24 @@ def _dev_c128(t: torch.Tensor, name: str) -> int:
 
 
 class Comm:
-    """NCCL communicator owned by libzk (one per rank)."""
+    """Communicator owned by libzk (one per rank): NCCL (one process per GPU, zk_comm_create) or
+    LOCAL (ranks are threads of this process, zk_comm_create_local; see Comm.local)."""
 
     def __init__(self, id_bytes: bytes, nranks: int, rank: int, device: int):
         h = P()
         buf = ctypes.create_string_buffer(bytes(id_bytes), 128)
         _check(lib().zk_comm_create(ctypes.byref(h), buf, nranks, rank, device))
         self.handle, self.nranks, self.rank = h, nranks, rank
+
+    @classmethod
+    def local(cls, group: "LocalGroup", rank: int, device: int) -> "Comm":
+        """zk_comm_create_local: every rank calls this concurrently from its own thread."""
+        self = cls.__new__(cls)
+        h = P()
+        _check(lib().zk_comm_create_local(ctypes.byref(h), group.handle, int(rank), int(device)))
+        self.handle, self.nranks, self.rank = h, group.nranks, int(rank)
+        self.group = group
+        return self
 
     @staticmethod
     def unique_id() -> bytes:
@@ -152,6 +167,26 @@ class Comm:
     def close(self):
         if self.handle:
             lib().zk_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class LocalGroup:
+    """zk_local_group_create: a group of `nranks` in-process ranks (threads), see include/zk.h."""
+
+    def __init__(self, nranks: int):
+        h = P()
+        _check(lib().zk_local_group_create(ctypes.byref(h), int(nranks)))
+        self.handle, self.nranks = h, int(nranks)
+
+    def close(self):
+        if self.handle:
+            lib().zk_local_group_destroy(self.handle)
             self.handle = None
 
     def __del__(self):

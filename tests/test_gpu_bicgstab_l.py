@@ -4,9 +4,10 @@ oracle.bicgstab_l.
 Bars (iterations are outer cycles of 2ℓ SpMVs):
   * cycle count within [0.95·min, 1.05·max] of the oracle's counts under its summation orders
     (seq, rev, block-256), as for BiCGStab (SURVEY.md §8(c) L11);
-  * residual histories: ℓ ≤ 2 to 1e-10 relative over the first 6 cycles; ℓ = 8 to 1e-3 — the
-    ℓ = 8 minimal-residual step solves a Gram system of A^j r̂ (j ≤ 8) whose conditioning
-    amplifies rounding: the oracle's own summation orders already differ by up to 9e-5 there;
+  * residual histories over the first 6 cycles to HTOL[ℓ] (1e-10 for ℓ ≤ 2, 1e-9 / 1e-8 / 1e-3
+    for ℓ = 3 / 4 / 8): ≈ 10× the oracle's own summation-order spread at that ℓ — the
+    minimal-residual step solves a Gram system of A^j r̂ (j ≤ ℓ) whose conditioning amplifies
+    rounding (the orders already differ by 9e-5 at ℓ = 8);
   * solutions to 1e-6 relative (C1/C2/T0); true residual ≤ 10·tol (S:388);
   * C4 (bench shape, ℓ = 8): DST-I closed form within 2κ·tol, first cycle's residual vs the oracle;
   * outcomes match the oracle's; loop modes bitwise identical; a comm handle → ZK_ERR_UNSUPPORTED."""
@@ -46,8 +47,17 @@ def diag(d):
                 values=np.asarray(d, np.complex128), n=n)
 
 
+# History bar per ℓ, derived from the ORACLE'S OWN summation-order spread over the first 6 cycles
+# on C1/C2/T0 (max over rev / block-256 vs seq; tests/test_oracle_solvers.py::
+# test_bicgstab_l_order_spread_within_gpu_bar recomputes it and requires spread ≤ bar/5):
+#   ℓ = 1: 1.6e-14, ℓ = 2: 1.5e-12, ℓ = 3: 1.0e-11, ℓ = 4: 6.9e-10, ℓ = 8: 9.2e-5
+# — the ℓ×ℓ normal equations of the Gram matrix square its conditioning (DESIGN R18), so the
+# rounding of any summation order grows with ℓ.  The bar is ≈ 10× the spread, rounded up.
+HTOL = {1: 1e-10, 2: 1e-10, 3: 1e-9, 4: 1e-8, 8: 1e-3}
+
+
 def htol(ell):
-    return 1e-10 if ell <= 2 else 1e-3
+    return HTOL[ell]
 
 
 @pytest.mark.parametrize("ell", [1, 2, 4, 8])
@@ -176,7 +186,7 @@ def test_bicgstab_l_split_schedule(split, ell, monkeypatch):
     its = [q["iters"] for q in refs]
     assert r["status"] == "CONVERGED" and 0.95 * min(its) <= r["iters"] <= 1.05 * max(its)
     k = min(6, r["iters"]) + 1
-    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= htol(ell) * 10
+    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= htol(ell)
     assert relerr(r["x"], refs[0]["x"]) <= 1e-6
 
 

@@ -160,6 +160,7 @@ def test_tfqmr_distributed_path_single_rank_comm(monkeypatch):
     m = gen.make_matrix("C2")
     b = gen.make_rhs(m)
     monkeypatch.setenv("ZK_LOOP_MODE", "3")
+    monkeypatch.setenv("ZK_SPLIT_RED", "1")  # a distributed solve always runs the split schedule
     base = gpu_solve(m, b, tol=1e-8)
     monkeypatch.delenv("ZK_LOOP_MODE")
     comm = zk.Comm(zk.Comm.unique_id(), 1, 0, 0)
@@ -186,11 +187,14 @@ def test_tfqmr_c4_full_size():
     assert np.max(np.abs(r["hist"][:4] - ref["hist"][:4]) / ref["hist"][:4]) <= 1e-10
 
 
-@pytest.mark.parametrize("split", ["0", "1"])
+@pytest.mark.parametrize("split", ["0", "1", "tail"])
 def test_tfqmr_split_schedule(split, monkeypatch):
-    """Both TFQMR schedules (fused epilogues; split: T2/T4 store A·y and vector passes finish —
-    the default from 2^20 rows) against the oracle on C2, and their MAXIT exits."""
-    monkeypatch.setenv("ZK_SPLIT_RED", split)
+    """The TFQMR schedules (fused epilogues; split: T2/T4 store A·y and vector passes finish; tail:
+    T2/T4 run those passes as their own tails — the default from 2^18 rows) against the oracle on
+    C2 in the WHILE-graph loop, and their MAXIT exits."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "1")
+    monkeypatch.setenv("ZK_SPLIT_RED", "0" if split == "0" else "1")
+    monkeypatch.setenv("ZK_SPLIT_TAIL", "1" if split == "tail" else "0")
     m = gen.make_matrix("C2")
     b = gen.make_rhs(m)
     r = gpu_solve(m, b, tol=1e-8)
