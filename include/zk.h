@@ -96,11 +96,9 @@ typedef struct {
     int64_t n_halo;        /* off-rank x entries received per SpMV (0 on one GPU) */
     int32_t borrowed;      /* 1 if the arrays are borrowed (ZK_PTRS_DEVICE_BORROW) */
     int32_t nranks;
-    int32_t spmv_mode;     /* 0 = sub-warp rows, 1 = TMA bulk-copy staged row tiles, 2 = aligned 4-blocks,
-                              3 = sliced ELL (SELL-32 copy of the matrix, the default unless its padding
-                              exceeds 10 % of nnz; a library-owned copy, also for borrowed arrays) */
-    int32_t rows_per_tile; /* TMA mode: rows per staged tile */
-    int32_t tma_stages;    /* TMA mode: pipeline depth */
+    int32_t spmv_mode;     /* 0 = CSR, a sub-warp of lanes_per_row lanes per row; 3 = sliced ELL (SELL-32
+                              copy of the matrix, the default unless its padding exceeds 10 % of nnz; a
+                              library-owned copy, also for borrowed arrays) */
     int64_t sell_entries;  /* mode 3: stored entries incl. padding (slices of 32 rows, each padded to
                               its longest row); 0 otherwise */
     int64_t interior_rows; /* distributed: rows whose SpMV runs while the halo exchange is in flight
@@ -115,8 +113,9 @@ typedef struct {
     double true_relres;    /* ||b - A x|| / ||b|| recomputed at exit */
     int64_t n_spmv;        /* SpMV applications performed (incl. initial residual and final check) */
     double solve_ms;       /* device time of the solve (CUDA events, entry to final check) */
-    int32_t loop_mode;     /* 1 = CUDA graph WHILE node, 2 = chunked graph launches, 3 = per-iteration launches,
-                              4 = one persistent cooperative kernel (opt-in: env ZK_LOOP_MODE=4) */
+    int32_t loop_mode;     /* 1 = CUDA graph WHILE node, 2 = chunked graph launches, 3 = per-iteration launches
+                              (distributed matrices), 5 = the whole loop in one thread-block cluster (small
+                              systems); env ZK_LOOP_MODE forces 1, 2, 3 or 5 */
     int32_t gpu_launches;  /* libzk kernels launched by this solve */
     /* in-loop kernel timing from the device global timer (first block start -> last block end),
      * summed over launches: [0] SpMV kernels (BiCGStab K1+K3 / CG K1), [1] fused vector kernels
@@ -174,13 +173,29 @@ zk_status zk_comm_create_local(zk_comm* out, zk_local_group g, int32_t rank, int
  * Errors: ZK_ERR_INVALID_CSR (message names the first bad row), ZK_ERR_NONFINITE,
  *         ZK_ERR_INVALID_VALUE, ZK_ERR_OOM, ZK_ERR_CUDA, ZK_ERR_NCCL.
  * The library owns its device copies (not borrowed arrays) and its scratch; zk_csr_destroy frees them.
- * The large copies come from the device's stream-ordered memory pool, whose release threshold the
- * library raises: memory freed by zk_csr_destroy stays reserved for the next zk_csr_create instead of
- * returning to the driver (environment ZK_POOL=0: plain cudaMalloc/cudaFree). */
+ * The large copies come from libzk's own stream-ordered memory pool on the device (not the device's
+ * default pool): memory freed by zk_csr_destroy stays reserved for the next zk_csr_create while any
+ * handle lives, and the pool is trimmed back to the driver when the last handle is destroyed
+ * (environment ZK_POOL=0: plain cudaMalloc/cudaFree).
+ * Borrowed arrays (ZK_PTRS_DEVICE_BORROW): the SpMV reads the library's sliced-ELL copy of the values
+ * (and ZK_BICGSTAB_JACOBI its cached A·M⁻¹), both built from the borrowed arrays; after changing the
+ * values in place call zk_csr_update_values, or the handle keeps using the old values. */
 zk_status zk_csr_create(zk_csr* A, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
                         const int32_t* col_idx, const zk_z* values, uint32_t flags, zk_comm comm,
                         int64_t row_begin, zk_stream s);
 zk_status zk_csr_destroy(zk_csr A);
+/* New values, same sparsity pattern (e.g. a Helmholtz frequency sweep on one mesh: A = K − k²M for
+ * several k, §2):
+ *   owned handle (ZK_PTRS_HOST / ZK_PTRS_DEVICE at create): `values` = zk_z[nnz] in the original
+ *     CSR order (this rank's rows on >1 GPU), host or device per `flags`, copied into the library;
+ *   borrowed handle: update the borrowed values array in place, then call with values = NULL (or
+ *     the borrowed pointer itself).
+ * The sliced-ELL copy is refilled and the cached Jacobi A·M⁻¹ dropped (rebuilt by the next
+ * ZK_BICGSTAB_JACOBI solve).  Values are checked for finiteness unless flags has ZK_SKIP_VALIDATE.
+ * Errors: ZK_ERR_NONFINITE (names the first bad entry; the handle then holds the rejected values —
+ * call again with finite ones before the next SpMV or solve), ZK_ERR_INVALID_VALUE, ZK_ERR_CUDA.
+ * Synchronises s. */
+zk_status zk_csr_update_values(zk_csr A, const zk_z* values, uint32_t flags, zk_stream s);
 zk_status zk_csr_info(zk_csr A, zk_csr_info_t* info);
 
 /* ---- ZSpMV: y <- alpha*A*x + beta*y (§3, Table 8 "SpMV CSR") ----

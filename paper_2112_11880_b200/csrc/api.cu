@@ -1,4 +1,5 @@
 // api.cu — libzk diagnostics, CSR create/upload/validate and ZSpMV (A2).
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -29,6 +30,38 @@ zk_status current_device(DeviceInfo* out) {
     ZK_CUDA(cudaGetDevice(&out->device));
     ZK_CUDA(cudaDeviceGetAttribute(&out->num_sms, cudaDevAttrMultiProcessorCount, out->device));
     return ZK_OK;
+}
+
+static std::mutex g_pool_mu;
+static std::unordered_map<int, cudaMemPool_t> g_pools;
+static int g_handles = 0;
+
+cudaMemPool_t dev_pool(int device) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_pools.find(device);
+    if (it != g_pools.end()) return it->second;
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+        cudaGetLastError();
+        pool = nullptr;  // no pool support: cudaMalloc
+    } else {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    g_pools[device] = pool;
+    return pool;
+}
+
+void handle_count(int delta) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_handles += delta;
+    if (g_handles == 0)
+        for (auto& kv : g_pools)
+            if (kv.second) cudaMemPoolTrimTo(kv.second, 0);  // no live handle: give the memory back
 }
 
 int blocks_per_sm(const void* kernel, int smem) {
@@ -108,6 +141,16 @@ __global__ void __launch_bounds__(kBlock) validate_kernel(const int64_t* __restr
     atomicMax(&out->max_len, my_max);
 }
 
+// first non-finite entry of a value array (zk_csr_update_values)
+__global__ void __launch_bounds__(kBlock) nonfinite_kernel(const double2* __restrict__ val, int64_t nnz,
+                                                          unsigned long long* first) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += stride) {
+        const double2 v = val[p];
+        if (!isfinite(v.x) || !isfinite(v.y)) atomicMin(first, (unsigned long long)p);
+    }
+}
+
 // ------------------------------------------------------------------ ZSpMV kernel (zk_zcsrmv)
 struct EpiAxpby {
     static constexpr int K = 0;
@@ -125,48 +168,20 @@ struct EpiAxpby {
 };
 
 template <int W, int MODE>
-__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) zcsrmv_kernel(CsrDev A, TmaPlan T, const double2* __restrict__ x,
-                                                       EpiAxpby epi) {
-    spmv_any<W, MODE>(A, T, x, epi);
-}
-// load-policy sweep variants of the sub-warp kernel (tools/microbench.py; env ZK_SPMV_LP)
-template <int W, int LP, int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) zcsrmv_lp_kernel(CsrDev A, const double2* __restrict__ x,
-                                                                EpiAxpby epi) {
-    spmv_body<W, EpiAxpby, LP>(A, x, epi);
-}
-template <int LP, int MINB>
-static zk_status launch_lp(const zk_csr_s* A, const double2* x, EpiAxpby e, cudaStream_t s) {
-    const void* k = (const void*)zcsrmv_lp_kernel<8, LP, MINB>;
-    const int G = grid_for(A->n_rows, kBlock / 8, A->dev.num_sms * blocks_per_sm(k, 0));
-    zcsrmv_lp_kernel<8, LP, MINB><<<G, kBlock, 0, s>>>(csr_dev(A), x, e);
-    ZK_CUDA(cudaGetLastError());
-    return ZK_OK;
+__global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) zcsrmv_kernel(CsrDev A, const double2* __restrict__ x,
+                                                                              EpiAxpby epi) {
+    spmv_any<W, MODE>(A, x, epi);
 }
 
 zk_status zcsrmv_local(const zk_csr_s* A, double2 alpha, const double2* x, double2 beta, double2* y,
                        cudaStream_t s) {
-    const int lp = getenv("ZK_SPMV_LP") ? atoi(getenv("ZK_SPMV_LP")) : -1;
-    if (lp >= 0 && A->spmv_mode == 0) {
-        EpiAxpby e{alpha, beta, y, beta.x == 0.0 && beta.y == 0.0};
-        switch (lp) {  // 10·minBlocksPerSM + policy
-            case 0: return launch_lp<0, 1>(A, x, e, s);
-            case 1: return launch_lp<1, 1>(A, x, e, s);
-            case 2: return launch_lp<2, 1>(A, x, e, s);
-            case 3: return launch_lp<3, 1>(A, x, e, s);
-            case 41: return launch_lp<1, 4>(A, x, e, s);
-            case 51: return launch_lp<1, 5>(A, x, e, s);
-            case 61: return launch_lp<1, 6>(A, x, e, s);
-            default: return launch_lp<1, 8>(A, x, e, s);
-        }
-    }
     return with_spmv(A, [&](auto wc, auto mc) -> zk_status {
         constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
         const void* k = (const void*)zcsrmv_kernel<W, MODE>;
         const LaunchCfg L = spmv_cfg(A, k, W, MODE);
         const CsrDev d = csr_dev(A);
         EpiAxpby e{alpha, beta, y, beta.x == 0.0 && beta.y == 0.0};
-        zcsrmv_kernel<W, MODE><<<L.grid, kBlock, L.smem, s>>>(d, A->tma, x, e);
+        zcsrmv_kernel<W, MODE><<<L.grid, kBlock, L.smem, s>>>(d, x, e);
         ZK_CUDA(cudaGetLastError());
         return ZK_OK;
     });
@@ -178,48 +193,32 @@ zk_status zcsrmv_part(const zk_csr_s* A, double2 alpha, const double2* x, double
     const void* k = (const void*)zcsrmv_kernel<32, 3>;
     const LaunchCfg L = spmv_cfg_part(A, k, part);
     EpiAxpby e{alpha, beta, y, beta.x == 0.0 && beta.y == 0.0};
-    zcsrmv_kernel<32, 3><<<L.grid, kBlock, 0, s>>>(part, A->tma, x, e);
+    zcsrmv_kernel<32, 3><<<L.grid, kBlock, 0, s>>>(part, x, e);
     ZK_CUDA(cudaGetLastError());
     return ZK_OK;
 }
 
-// SpMV mapping from the row statistics (env ZK_SPMV_MODE / ZK_SPMV_W override, for sweeps):
-//  sub-warp kernel by default (measured faster than the TMA-staged variant on C4), lanes per row
-//  ≈ mean/8; the TMA-staged mode is available for rows ≤ 128 long (W ∈ {4, 8, 16}).
 // SpMV mapping.  Default: the sliced-ELL copy (mode 3) — on C4 zk_zcsrmv 647 µs vs 812 µs for the
 // best CSR mapping (profiles/r01_sell.md) — unless its padding exceeds kSellMaxPad of the nonzeros
-// (checked after the build; then the sub-warp CSR kernel).  ZK_SPMV_MODE forces a mapping.
+// (checked after the build; then the CSR sub-warp kernel, mode 0, with W ≈ mean row length / 8
+// lanes per row).  ZK_SPMV_MODE=0/3 forces a mapping, ZK_SPMV_W the lanes of mode 0.  (Round 1's
+// TMA-staged and blocked-4 CSR mappings measured slower on every shape and were removed.)
 constexpr double kSellMaxPad = 0.10;
 static void choose_mapping(zk_csr_s* A, int force_mode = -1) {
-    int mode = -1, w = -1;
-    if (const char* e = getenv("ZK_SPMV_MODE")) mode = atoi(e);
-    else mode = 3;
+    int mode = 3, w = -1;
+    if (const char* e = getenv("ZK_SPMV_MODE")) mode = atoi(e) == 0 ? 0 : 3;
     if (force_mode >= 0) mode = force_mode;
     if (const char* e = getenv("ZK_SPMV_W")) w = atoi(e);
-    int stages = 4, stage_nnz = 756;
-    if (const char* e = getenv("ZK_TMA_STAGES")) stages = atoi(e) < 2 ? 2 : (atoi(e) > 8 ? 8 : atoi(e));
-    if (const char* e = getenv("ZK_TMA_NNZ")) stage_nnz = atoi(e) < 256 ? 256 : atoi(e);
-    const bool tma_ok = make_tma_plan(A->n_rows, A->nnz, A->max_len, &A->tma, stages, stage_nnz);
-    const bool aligned = ((uintptr_t)A->val % 32 == 0) && ((uintptr_t)A->col % 16 == 0);
-    if (mode < 0 || mode > 3) mode = 0;  // measured: sub-warp W=4 beats blocked-4 (1000-1360 µs) and TMA
-    if (mode == 1 && !tma_ok) mode = 0;
-    if (mode == 2 && !aligned) mode = 0;
     A->spmv_mode = mode;
-    const bool forced = (w == 2 || w == 4 || w == 8 || w == 16 || w == 32);
-    if (mode == 2) {
-        // lanes ≈ aligned 4-blocks per row (a 27-nonzero row spans ≤ 8): one round of loads
-        if (!forced) {
-            w = 4;
-            while (w < 16 && 4.0 * w < A->mean_len + 4.0) w *= 2;
-        }
-        w = w <= 4 ? 4 : (w >= 16 ? 16 : 8);
-    } else if (!forced) {
+    if (mode == 3) {
+        A->W = 32;  // a warp per 32-row slice (sell.cu)
+        return;
+    }
+    if (!(w == 2 || w == 4 || w == 8 || w == 16 || w == 32)) {
         // ≈ 8 nonzeros per lane (two chunks of U = 4): W = 4 for the 27-point rows
         w = 2;
         while (w < 32 && 8.0 * w < A->mean_len) w *= 2;
     }
-    if (mode == 1) w = w <= 4 ? 4 : (w >= 16 ? 16 : 8);
-    if (mode == 3) w = 32;  // a warp per 32-row slice (sell.cu)
     A->W = w;
 }
 
@@ -228,9 +227,7 @@ void dist_destroy(zk_csr_s* A);                                                 
 zk_status dist_zcsrmv(const zk_csr_s* A, double2 alpha, const double2* x, double2 beta, double2* y,
                       cudaStream_t s);                                                           // dist.cu
 int64_t dist_n_halo(const zk_csr_s* A);                                                          // dist.cu
-void jacobi_destroy(zk_csr_s* A);                                                                // jacobi.cu
 zk_status sell_build(zk_csr_s* A, cudaStream_t s);                                               // sell.cu
-void sell_destroy(zk_csr_s* A);                                                                  // sell.cu
 int dist_nranks(const zk_csr_s* A);                                                              // dist.cu
 zk_status dist_agree_failed(zk_comm_s* c, bool failed, cudaStream_t s, int* any_failed);         // dist.cu
 int64_t dist_interior_rows(const zk_csr_s* A);                                                   // dist.cu
@@ -363,29 +360,89 @@ extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, 
         cudaError_t e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) return cleanup(cuda_fail(e, "zk_csr_create", __FILE__, __LINE__));
     }
+    handle_count(+1);
+    A->counted = true;
     *out = A;
     return ZK_OK;
 }
 
 extern "C" zk_status zk_csr_destroy(zk_csr A) {
     if (!A) return ZK_OK;
+    const bool trace = getenv("ZK_TRACE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = now();
+    cudaDeviceSynchronize();  // once: no array may be in use by pending work when it is freed
+    const auto t1 = now();
     for (auto& g : A->graph) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
         if (g.graph) cudaGraphDestroy(g.graph);
     }
+    const auto t2 = now();
     if (A->dist) dist_destroy(A);
-    jacobi_destroy(A);
-    sell_destroy(A);
+    jacobi_destroy(A, true);
+    sell_destroy(A, true);
     if (A->owned) {
-        dev_free(A->row_ptr);
-        dev_free(A->col);
-        dev_free(A->val);
+        dev_free(A->row_ptr, true);
+        dev_free(A->col, true);
+        dev_free(A->val, true);
     }
+    const auto t3 = now();
     if (A->cap_stream) cudaStreamDestroy(A->cap_stream);
     if (A->pinned) cudaFreeHost(A->pinned);
     for (auto& e : A->ev)
         if (e) cudaEventDestroy(e);
+    if (A->counted) handle_count(-1);
     delete A;
+    if (trace)
+        fprintf(stderr, "zk_csr_destroy: sync %.2f ms, graphs %.2f ms, frees %.2f ms, rest %.2f ms\n", ms(t0, t1),
+                ms(t1, t2), ms(t2, t3), ms(t3, now()));
+    return ZK_OK;
+}
+
+namespace zk {
+zk_status sell_refill(zk_csr_s* A, cudaStream_t s);  // sell.cu
+}
+
+extern "C" zk_status zk_csr_update_values(zk_csr A, const zk_z* values, uint32_t flags, zk_stream stream) {
+    if (!A) return fail(ZK_ERR_INVALID_VALUE, "NULL handle");
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t where = flags & 3u;
+    if (A->owned) {
+        if (!values && A->nnz > 0) return fail(ZK_ERR_INVALID_VALUE, "NULL values");
+        if (where != ZK_PTRS_HOST && where != ZK_PTRS_DEVICE) return fail(ZK_ERR_INVALID_VALUE, "bad flags");
+        if (A->nnz > 0)
+            ZK_CUDA(cudaMemcpyAsync(A->val, values, sizeof(double2) * A->nnz,
+                                    where == ZK_PTRS_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    } else if (values && (const void*)values != (const void*)A->val) {
+        return fail(ZK_ERR_INVALID_VALUE, "borrowed handle: update the borrowed array in place, pass it or NULL");
+    }
+    if (!(flags & ZK_SKIP_VALIDATE) && A->nnz > 0) {  // finite values (the pattern is unchanged)
+        unsigned long long h = ~0ull, *d = nullptr;
+        ZK_CUDA(cudaMalloc(&d, sizeof h));
+        cudaError_t e = cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) {
+            nonfinite_kernel<<<grid_for(A->nnz, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(A->val, A->nnz, d);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(d);
+        if (e != cudaSuccess) return cuda_fail(e, "zk_csr_update_values", __FILE__, __LINE__);
+        if (h != ~0ull) {
+            char buf[128];
+            snprintf(buf, sizeof buf, "value %llu (CSR order) is not finite", h);
+            return fail(ZK_ERR_NONFINITE, buf);
+        }
+    }
+    if (A->spmv_mode == 3) ZK_TRY(sell_refill(A, s));
+    ZK_CUDA(cudaStreamSynchronize(s));
+    for (auto& g : A->graph) {  // graphs bake the Jacobi values' address: rebuilt on the next solve
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph) cudaGraphDestroy(g.graph);
+        g = GraphCache{};
+    }
+    jacobi_destroy(A, true);   // A·M⁻¹ is rebuilt from the new values on the next Jacobi solve
     return ZK_OK;
 }
 
@@ -403,8 +460,6 @@ extern "C" zk_status zk_csr_info(zk_csr A, zk_csr_info_t* info) {
     info->borrowed = A->owned ? 0 : 1;
     info->nranks = dist_nranks(A);
     info->spmv_mode = A->spmv_mode;
-    info->rows_per_tile = A->spmv_mode == 1 ? A->tma.R : 0;
-    info->tma_stages = A->spmv_mode == 1 ? A->tma.S : 0;
     info->sell_entries = A->spmv_mode == 3 ? A->sl_nnz : 0;
     info->interior_rows = A->dist ? dist_interior_rows(A) : 0;
     return ZK_OK;

@@ -109,10 +109,10 @@ zk_status cscale(const zk_csr_s* A, const double2* d, const double2* in, double2
     return ZK_OK;
 }
 
-void jacobi_destroy(zk_csr_s* A) {
-    dev_free(A->jac_val);
-    dev_free(A->jac_diag);
-    dev_free(A->jac_dinv);
+void jacobi_destroy(zk_csr_s* A, bool synced) {
+    dev_free(A->jac_val, synced);
+    dev_free(A->jac_diag, synced);
+    dev_free(A->jac_dinv, synced);
     A->jac_val = A->jac_diag = A->jac_dinv = nullptr;
 }
 

@@ -50,11 +50,11 @@ __global__ void sell_fill_kernel(const int64_t* __restrict__ row_ptr, const int*
     }
 }
 
-void sell_destroy(zk_csr_s* A) {
-    dev_free(A->sl_ptr);
-    dev_free(A->sl_col);
-    dev_free(A->sl_val);
-    dev_free(A->jac_sl_val);
+void sell_destroy(zk_csr_s* A, bool synced) {
+    dev_free(A->sl_ptr, synced);
+    dev_free(A->sl_col, synced);
+    dev_free(A->sl_val, synced);
+    dev_free(A->jac_sl_val, synced);
     A->sl_ptr = nullptr;
     A->sl_col = nullptr;
     A->sl_val = nullptr;
@@ -102,6 +102,18 @@ zk_status sell_build(zk_csr_s* A, cudaStream_t s) {
     if (e != cudaSuccess) {
         sell_destroy(A);
         return cuda_fail(e, "sell_build", __FILE__, __LINE__);
+    }
+    return ZK_OK;
+}
+
+// Re-fill the SELL values (and columns) from the CSR arrays after zk_csr_update_values: same
+// pattern, so the slice layout (sl_ptr) is unchanged.
+zk_status sell_refill(zk_csr_s* A, cudaStream_t s) {
+    const int64_t n_sl = A->n_slices;
+    if (n_sl > 0) {
+        sell_fill_kernel<<<grid_for(n_sl * 32, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(
+            A->row_ptr, A->col, A->val, A->n_rows, n_sl, A->sl_ptr, A->sl_col, A->sl_val);
+        ZK_CUDA(cudaGetLastError());
     }
     return ZK_OK;
 }

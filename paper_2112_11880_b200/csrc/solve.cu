@@ -51,7 +51,6 @@ struct SolveCtx {
     double* partials;       // [kMaxRed][kMaxGrid]
     unsigned int* tickets;  // [kTickets], one per reduction stage (self-resetting; cleared at solve start)
     CsrDev A;
-    TmaPlan T;
     // scalars
     double2 rho, alpha, omega, beta;
     double nb, nrh, rnorm, gamma, alpha_cg, beta_cg;
@@ -982,15 +981,14 @@ struct EpiT4Tfqmr {  // u1 = A y1 ; v = u1 + β(u2 + β v) (first: v = u1) ; {σ
 #ifndef ZK_VEC_MINB
 #define ZK_VEC_MINB 4  // fused vector kernels: ≤ 64 registers, 4 CTAs / 32 warps per SM
 #endif
-// The CSR view and TMA plan are copied into registers/locals once (not re-read from the ctx).
+// The CSR view is copied into registers/locals once (not re-read from the ctx).
 template <int W, int MODE, int S>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_init_x0(SolveCtx* c, const double2* __restrict__ xg,
                                                                           int bicg) {
     stamp_start<S>(c);
     const CsrDev A = c->A;
-    const TmaPlan T = c->T;
     EpiInit<S> e(c, xg, bicg == 1);
-    spmv_any<W, MODE>(A, T, xg, e);
+    spmv_any<W, MODE>(A, xg, e);
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k_init_zero(SolveCtx* c, int kind) {
     stamp_start<S_INIT_BICG>(c);
@@ -1003,9 +1001,8 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k_true(SolveCtx
     // A: the ORIGINAL operator (the Jacobi path iterates on A·M⁻¹ but checks ‖b − A x‖)
     if (c->status == ST_ZERO_RHS) return;
     stamp_start<S_TRUE>(c);
-    const TmaPlan T = c->T;
     EpiTrue e(c);
-    spmv_any<W, MODE>(A, T, xg, e);
+    spmv_any<W, MODE>(A, xg, e);
 }
 // SPLIT: 0 fused epilogue; 1 products only (r1_bicg reduces); 2 products + tail reduction (SELL)
 template <int W, int MODE, int SPLIT>
@@ -1013,17 +1010,16 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_bicg(SolveCt
     pdl_enter();
     if (c->done) return;
     stamp_start<S_K1_BICG>(c);
-    const TmaPlan T = c->T;
     const double2* p = c->p;
     if constexpr (SPLIT == 2) {
         EpiStoreTail<OpRed1Bicg> e(c->v, c);
-        spmv_any<W, MODE>(A, T, p, e);
+        spmv_any<W, MODE>(A, p, e);
     } else if constexpr (SPLIT == 1) {
         EpiStore e(c->v);
-        spmv_any<W, MODE>(A, T, p, e);
+        spmv_any<W, MODE>(A, p, e);
     } else {
         EpiK1Bicg e(c);
-        spmv_any<W, MODE>(A, T, p, e);
+        spmv_any<W, MODE>(A, p, e);
     }
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) r1_bicg(SolveCtx* c) {
@@ -1050,17 +1046,16 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k3_bicg(SolveCt
     pdl_enter();
     if (c->done) return;
     stamp_start<S_K3_BICG>(c);
-    const TmaPlan T = c->T;
     const double2* s = c->s;
     if constexpr (SPLIT == 2) {
         EpiStoreTail<OpRed3Bicg> e(c->t, c);
-        spmv_any<W, MODE>(A, T, s, e);
+        spmv_any<W, MODE>(A, s, e);
     } else if constexpr (SPLIT == 1) {
         EpiStore e(c->t);
-        spmv_any<W, MODE>(A, T, s, e);
+        spmv_any<W, MODE>(A, s, e);
     } else {
         EpiK3Bicg e(c);
-        spmv_any<W, MODE>(A, T, s, e);
+        spmv_any<W, MODE>(A, s, e);
     }
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k4_bicg(SolveCtx* c) {
@@ -1086,17 +1081,16 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cocg(SolveCt
     pdl_enter();
     if (c->done) return;
     stamp_start<S_K1_COCG>(c);
-    const TmaPlan T = c->T;
     const double2* p = c->p;
     if constexpr (SPLIT == 2) {
         EpiStoreTail<OpRedPq<false, S_K1_COCG>> e(c->q, c);
-        spmv_any<W, MODE>(A, T, p, e);
+        spmv_any<W, MODE>(A, p, e);
     } else if constexpr (SPLIT == 1) {
         EpiStore e(c->q);
-        spmv_any<W, MODE>(A, T, p, e);
+        spmv_any<W, MODE>(A, p, e);
     } else {
         EpiK1Cocg e(c);
-        spmv_any<W, MODE>(A, T, p, e);
+        spmv_any<W, MODE>(A, p, e);
     }
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_cocg(SolveCtx* c) {
@@ -1119,17 +1113,16 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cg(SolveCtx*
     pdl_enter();
     if (c->done) return;
     stamp_start<S_K1_CG>(c);
-    const TmaPlan T = c->T;
     const double2* p = c->p;
     if constexpr (SPLIT == 2) {
         EpiStoreTail<OpRedPq<true, S_K1_CG>> e(c->q, c);
-        spmv_any<W, MODE>(A, T, p, e);
+        spmv_any<W, MODE>(A, p, e);
     } else if constexpr (SPLIT == 1) {
         EpiStore e(c->q);
-        spmv_any<W, MODE>(A, T, p, e);
+        spmv_any<W, MODE>(A, p, e);
     } else {
         EpiK1Cg e(c);
-        spmv_any<W, MODE>(A, T, p, e);
+        spmv_any<W, MODE>(A, p, e);
     }
 }
 template <bool CONJ, int S>
@@ -1158,10 +1151,9 @@ template <int W, int MODE>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k0_tfqmr(SolveCtx* c, const CsrDev A) {  // u1 = v = A y1, σ
     if (c->done) return;
     stamp_start<S_K0_TFQMR>(c);
-    const TmaPlan T = c->T;
     const double2* y1 = c->y1;
     EpiT4Tfqmr<S_K0_TFQMR> e(c);
-    spmv_any<W, MODE>(A, T, y1, e);
+    spmv_any<W, MODE>(A, y1, e);
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t1_tfqmr(SolveCtx* c) {
     pdl_enter();
@@ -1191,17 +1183,16 @@ __global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t2_tfqmr(SolveCtx* c, cons
         return;
     }
     stamp_start<S_T2_TFQMR>(c);
-    const TmaPlan T = c->T;
     const double2* y2 = c->y2;
     if constexpr (SPLIT == 2) {
         EpiStoreTail<OpT2bTfqmr> e(c->u2, c);
-        spmv_any<W, MODE>(A, T, y2, e);
+        spmv_any<W, MODE>(A, y2, e);
     } else if constexpr (SPLIT == 1) {
         EpiStore e(c->u2);
-        spmv_any<W, MODE>(A, T, y2, e);
+        spmv_any<W, MODE>(A, y2, e);
     } else {
         EpiT2Tfqmr e(c);
-        spmv_any<W, MODE>(A, T, y2, e);
+        spmv_any<W, MODE>(A, y2, e);
     }
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t2b_tfqmr(SolveCtx* c) {
@@ -1235,17 +1226,16 @@ __global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t4_tfqmr(SolveCtx* c, cons
         if (SPLIT != 1 && c->half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;
     } else {
         stamp_start<S_T4_TFQMR>(c);
-        const TmaPlan T = c->T;
         const double2* y1 = c->y1;
         if constexpr (SPLIT == 2) {
             EpiStoreTail<OpT4bTfqmr> e(c->u1, c);
-            spmv_any<W, MODE>(A, T, y1, e);
+            spmv_any<W, MODE>(A, y1, e);
         } else if constexpr (SPLIT == 1) {
             EpiStore e(c->u1);
-            spmv_any<W, MODE>(A, T, y1, e);
+            spmv_any<W, MODE>(A, y1, e);
         } else {
             EpiT4Tfqmr<S_T4_TFQMR> e(c);
-            spmv_any<W, MODE>(A, T, y1, e);
+            spmv_any<W, MODE>(A, y1, e);
         }
     }
     if (SPLIT != 1) set_cond(c);  // split: t4b_tfqmr is the body's last kernel
@@ -1397,9 +1387,8 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) bl_s1(SolveCtx*
     pdl_enter();
     if (c->done) return;
     stamp_start<S_S1_BL>(c);  // RED = false (split): bl_r<S_S1_BL> reduces and closes the timer
-    const TmaPlan T = c->T;
     EpiBl<S_S1_BL, RED> e(c, P.u[j + 1]);
-    spmv_any<W, MODE>(A, T, P.u[j], e);
+    spmv_any<W, MODE>(A, P.u[j], e);
 }
 template <int W, int MODE, bool RED>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) bl_s2(SolveCtx* c, const CsrDev A, VecSet P, int j,
@@ -1407,9 +1396,8 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) bl_s2(SolveCtx*
     pdl_enter();
     if (c->done) return;
     if (stamp) stamp_start<S_S2_BL>(c);
-    const TmaPlan T = c->T;
     EpiBl<S_S2_BL, RED> e(c, P.r[j + 1]);
-    spmv_any<W, MODE>(A, T, P.r[j], e);
+    spmv_any<W, MODE>(A, P.r[j], e);
 }
 
 template <int S>
@@ -1618,102 +1606,6 @@ static BlKernel bl_u_of(int L) {
     }
 }
 static int bl_nd(int L) { return (L + 1) + (L + 1) * L; }
-
-// ------------------------------------------------------------------ persistent solver (loop mode 4)
-// The whole iteration loop as ONE cooperative launch for latency-bound systems (the paper's
-// Audi3D/Twingo shapes: a WHILE-graph body of 5 launches costs ~40 µs per iteration there).  The
-// phases are the same fused bodies as the per-launch kernels, separated by grid-wide barriers
-// instead of kernel boundaries; the last-block scalar steps run unchanged.  Data written in one
-// phase and read in a later one is loaded coherently (ld_vec / ld_gather_coh; the barrier's
-// gpu-scope fences order it), never through the non-coherent read-only path.
-__device__ __forceinline__ int vol_int(const int* p) { return *(const volatile int*)p; }
-
-// The phases inline into one body, which needs ~128 registers without spilling (at the 64-register
-// cap of the per-launch kernels it spilled ~1.4 KB per thread): the persistent kernel runs 2 CTAs
-// per SM, which is plenty for the latency-bound sizes it is selected for.
-template <int W>
-__device__ __forceinline__ void ph_k1_bicg(SolveCtx* c) {
-    stamp_start<S_K1_BICG>(c);
-    const CsrDev A = c->A;
-    EpiK1Bicg e(c);
-    spmv_body<W, EpiK1Bicg, ZK_DEFAULT_LP, true>(A, c->p, e);
-}
-__device__ __forceinline__ void ph_k2_bicg(SolveCtx* c) {
-    stamp_start<S_K2_BICG>(c);
-    OpK2Bicg op(c);
-    vec_body(c->A.n_rows, op);
-}
-template <int W>
-__device__ __forceinline__ void ph_k3_bicg(SolveCtx* c) {
-    stamp_start<S_K3_BICG>(c);
-    const CsrDev A = c->A;
-    EpiK3Bicg e(c);
-    spmv_body<W, EpiK3Bicg, ZK_DEFAULT_LP, true>(A, c->s, e);
-}
-__device__ __forceinline__ void ph_k4_bicg(SolveCtx* c, bool half) {
-    if (!half) stamp_start<S_K4_BICG>(c);
-    OpK4Bicg op(c, half);
-    vec_body(c->A.n_rows, op);
-}
-__device__ __forceinline__ void ph_k5_bicg(SolveCtx* c) {
-    OpK5Bicg op(c);
-    vec_body(c->A.n_rows, op);
-}
-template <int W>
-__device__ __forceinline__ void ph_k1_cg(SolveCtx* c) {
-    stamp_start<S_K1_CG>(c);
-    const CsrDev A = c->A;
-    EpiK1Cg e(c);
-    spmv_body<W, EpiK1Cg, ZK_DEFAULT_LP, true>(A, c->p, e);
-}
-__device__ __forceinline__ void ph_k2_cg(SolveCtx* c) {
-    stamp_start<S_K2_CG>(c);
-    OpK2Cg op(c);
-    vec_body(c->A.n_rows, op);
-}
-__device__ __forceinline__ void ph_k3_cg(SolveCtx* c) {
-    OpK3Cg op(c);
-    vec_body(c->A.n_rows, op);
-}
-
-template <int W>
-__global__ void __launch_bounds__(kBlock, 2) k_persist_bicg(SolveCtx* c) {
-    namespace cg = cooperative_groups;
-    cg::grid_group g = cg::this_grid();
-    while (!vol_int(&c->done)) {
-        ph_k1_bicg<W>(c);
-        g.sync();
-        if (!vol_int(&c->done)) ph_k2_bicg(c);
-        g.sync();
-        if (!vol_int(&c->done)) ph_k3_bicg<W>(c);
-        g.sync();
-        const bool half = vol_int(&c->half) != 0;
-        if (!vol_int(&c->done) || half) ph_k4_bicg(c, half);
-        g.sync();
-        if (vol_int(&c->done)) {
-            if (half && blockIdx.x == 0 && threadIdx.x == 0) c->half = 0;
-        } else {
-            ph_k5_bicg(c);
-        }
-        if (blockIdx.x == 0 && threadIdx.x == 0) c->bodies += 1;
-        g.sync();
-    }
-}
-
-template <int W>
-__global__ void __launch_bounds__(kBlock, 2) k_persist_cg(SolveCtx* c) {
-    namespace cg = cooperative_groups;
-    cg::grid_group g = cg::this_grid();
-    while (!vol_int(&c->done)) {
-        ph_k1_cg<W>(c);
-        g.sync();
-        if (!vol_int(&c->done)) ph_k2_cg(c);
-        g.sync();
-        if (!vol_int(&c->done)) ph_k3_cg(c);
-        if (blockIdx.x == 0 && threadIdx.x == 0) c->bodies += 1;
-        g.sync();
-    }
-}
 
 // ------------------------------------------------------------------ cluster solver (loop mode 5)
 // Small systems (the paper's Audi/Twingo shapes) are latency-bound: a WHILE-graph iteration of 5
@@ -2726,11 +2618,15 @@ static bool split_reductions(const zk_csr_s* A) {
 }
 
 // Split schedule with the reduction as the SpMV kernel's tail (EpiStoreTail) instead of a separate
-// pass: SELL mapping, one GPU (a distributed SpMV is two launches).  ZK_SPLIT_TAIL=0/1 forces it.
+// pass: SELL mapping, one GPU (a distributed SpMV is two launches).  Default; ZK_SPLIT_TAIL=0 keeps
+// the separate pass.  Measured (tools/ab_split.py, WHILE graph, µs per iteration, pass → tail):
+// Audi3D-4 (C3) BiCGStab 168.0 → 162.2, CG 86.3 → 82.8, TFQMR 173.7 → 165.5; Twingo3D-2 (C3T)
+// 133.3 → 128.0, 69.0 → 64.8, 138.0 → 129.7; C4 1707 → 1694, 901 → 908, 1808 → 1797
+// (profiles/r02_split_tail.txt).
 static bool split_tail(const zk_csr_s* A) {
     if (A->dist || A->spmv_mode != 3 || !split_reductions(A)) return false;
     if (const char* e = getenv("ZK_SPLIT_TAIL")) return atoi(e) != 0;
-    return false;
+    return true;
 }
 
 bool dist_overlap(const zk_csr_s* A);                                            // dist.cu
@@ -3119,7 +3015,6 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         hc.A.val = A->jac_val;
         hc.A.sl_val = A->jac_sl_val;
     }
-    hc.T = A->tma;
     hc.tol = tol;
     hc.maxit = maxit;
     hc.status = ZK_MAXIT;
@@ -3127,39 +3022,19 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     hc.dist = A->dist ? 1 : 0;
     for (int i = 0; i < 4; i++) hc.t0[i] = ~0ull;
 
-    // ---- loop mode: 1 = WHILE graph (default), 2 = chunked graphs, 3 = direct launches, 4 = one
-    //      persistent cooperative kernel.  Mode 4 measured SLOWER on every shape (C1 52 vs 39 µs per
-    //      iteration, C3 514 vs 184: the fused phases need 128 registers → half the warps, and
-    //      coherent gathers), so it is opt-in (ZK_LOOP_MODE=4) and parity-tested, not the default.
-    // default: the cluster solver (mode 5) for small systems, else the WHILE graph
-    // (every solver when its own rows fit the cluster's shared memory, see cluster_fits)
+    // ---- loop mode: 1 = WHILE graph (default), 2 = chunked graphs, 3 = direct launches,
+    //      5 = the whole loop in one thread-block cluster (default for small systems whose own rows
+    //      fit the cluster's shared memory, see cluster_fits).  (A round-1 mode 4, one persistent
+    //      cooperative kernel with grid barriers, measured slower on every shape — C1 52 vs 39 µs
+    //      per iteration, C3 514 vs 184 — and was removed.)
     int mode = A->dist ? 3 : (cluster_kind(method) >= 0 && A->n_rows <= kClusterDefaultRows ? 5 : 1);
     if (const char* e = getenv("ZK_LOOP_MODE")) {
         int m = atoi(e);
-        if (m >= 1 && m <= 5) mode = m;
+        if (m >= 1 && m <= 5 && m != 4) mode = m;
     }
     if (mode == 5 && (A->dist || !cluster_fits(A, (cudaStream_t)stream, cluster_kind(method), ell)))
         mode = A->dist ? 3 : 1;
-    if (A->dist && (mode == 1 || mode == 4 || mode == 5)) mode = 3;  // NCCL inside WHILE bodies / persistent kernels is not used
-    int persist_grid = 0;
-    const void* kp = nullptr;
-    if (mode == 4 && (method == ZK_COCG || method == ZK_TFQMR || method == kBiCGStabL)) mode = 1;  // persistent: BiCGStab, CG
-    if (mode == 4) {
-        int dev_coop = 0;
-        cudaDeviceGetAttribute(&dev_coop, cudaDevAttrCooperativeLaunch, A->dev.device);
-        const int W = A->W == 2 || A->W == 4 || A->W == 8 ? A->W : 4;
-        kp = method == ZK_BICGSTAB
-                 ? (W == 2 ? (const void*)k_persist_bicg<2>
-                           : W == 8 ? (const void*)k_persist_bicg<8> : (const void*)k_persist_bicg<4>)
-                 : (W == 2 ? (const void*)k_persist_cg<2>
-                           : W == 8 ? (const void*)k_persist_cg<8> : (const void*)k_persist_cg<4>);
-        const int cap = A->dev.num_sms * blocks_per_sm(kp, 0);
-        // one row tile per block in the SpMV phases (a smaller grid serialises dependent load
-        // chains across tiles), capped at the co-resident limit
-        int64_t g = (A->n_rows + kBlock / W - 1) / (kBlock / W);
-        persist_grid = (int)(g < 1 ? 1 : (g > cap ? cap : g));
-        if (!dev_coop || cap < 1) mode = 1;
-    }
+    if (A->dist && (mode == 1 || mode == 5)) mode = 3;  // collectives inside WHILE bodies / clusters are not used
     static_assert(kBiCGStabL < (int)(sizeof(((zk_csr_s*)nullptr)->graph) / sizeof(GraphCache)), "graph slot per method");
     GraphCache& gc = A->graph[method];
     // one graph per (method, ℓ, Jacobi): the SpMV kernels take the CSR view (A or A·M⁻¹) as a
@@ -3276,9 +3151,6 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     SolveCtx* hdone = nullptr;  // pinned copy of the ctx for the chunked modes
     if (mode == 1) {
         ZK_CUDA(cudaGraphLaunch(gc.exec, s));
-    } else if (mode == 4) {
-        void* args[] = {&dc};
-        ZK_CUDA(cudaLaunchCooperativeKernel(kp, dim3(persist_grid), dim3(kBlock), args, 0, s));
     } else if (mode == 5) {
         int csz = 0;
         if (!cluster_launch(A, dc, hc.A, s, &csz, cluster_kind(method), ell, !jacobi))  // the kernel also forms the true residual
@@ -3345,13 +3217,13 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         info->solve_ms = ms;
         info->loop_mode = mode;
         int per_body = method == ZK_BICGSTAB ? 5 : method == ZK_TFQMR ? 4 : method == kBiCGStabL ? 4 * ell + 2 : 3;
-        if (split_reductions(A) && !split_tail(A) && mode != 4)  // the separate reduction / update passes
+        if (split_reductions(A) && !split_tail(A))  // the separate reduction / update passes
             per_body += method == ZK_BICGSTAB ? 2 : (method == ZK_CG || method == ZK_COCG) ? 1
                         : method == ZK_TFQMR ? 2 : method == kBiCGStabL ? 2 * ell - 1 : 0;
         const int fins = A->dist ? (method == ZK_BICGSTAB ? 4 : method == ZK_TFQMR ? 3 : 2) : 0;  // dist: 1-thread finish kernels
         const int pre = method == ZK_TFQMR ? (A->dist ? 2 : 1) : 0;                               // TFQMR: K0 (+ its finish)
         // mode 5: set_ctx + init (+ TFQMR's K0) + the cluster kernel (+ Jacobi: x = M⁻¹u and k_true)
-        info->gpu_launches = mode == 4 ? 4 : mode == 5 ? 3 + pre + (jacobi ? 2 : 0)
+        info->gpu_launches = mode == 5 ? 3 + pre + (jacobi ? 2 : 0)
                                                        : 3 + pre + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);
         if (A->dist) {  // + per SpMV: pack kernel, second (boundary) launch; + per allreduce: LOCAL sum kernel
             int per_spmv = 0, per_red = 0;

@@ -126,100 +126,6 @@ __device__ __forceinline__ void spmv_body(const CsrDev& A, const double2* __rest
 }
 
 // ---------------------------------------------------------------------------------------------
-// Blocked mapping (MODE 2, the default for rows of ≥ 8 nonzeros): a row's range [rs, re) is
-// covered by the 16-B aligned blocks of 4 nonzeros that intersect it; lane `sub` of the row's W
-// lanes takes blocks sub, sub+W, ...  One block = one 128-bit column load + two 256-bit value
-// loads (LDG.E.256, L2 evict_normal), so a warp instruction covers whole aligned sectors: the
-// per-lane strided mapping above requested ~7 sectors of column indices and ~20 of values per
-// 8-row instruction group (ncu: L2 at 73 % of peak, column sectors 3x their payload).  Entries of
-// the block outside [rs, re) belong to the neighbouring rows and are masked.  Requires 32-B aligned
-// values, 16-B aligned columns (checked at create); the final block of the array (nnz % 4 != 0)
-// is read element-wise.
-__device__ __forceinline__ void ld_val_pair(const double2* p, double2& a, double2& b) {
-    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_normal.v4.b64 {%0, %1, %2, %3}, [%4];"
-                 : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
-}
-__device__ __forceinline__ int4 ld_col4(const int* p, uint64_t pol) {
-    int4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
-    return v;
-}
-
-template <int W, class Epi>
-__device__ __forceinline__ void spmv_body_b4(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
-    static_assert(W >= 2 && W <= 32 && (W & (W - 1)) == 0, "W must be a power of two");
-    constexpr int RPB = kBlock / W;
-    constexpr int KA = Epi::K > 0 ? Epi::K : 1;
-    const uint64_t pol = make_policy<1>();
-    double acc[KA];
-#pragma unroll
-    for (int k = 0; k < KA; k++) acc[k] = 0.0;
-    const int sub = threadIdx.x & (W - 1);
-    const int grp = threadIdx.x / W;
-    const int n = (int)A.n_rows;
-    const int64_t nnz_full = A.nnz & ~(int64_t)3;  // blocks below this are complete
-    const int G = gridDim.x;
-    int row = blockIdx.x * RPB + grp;
-    int64_t rs = 0, re = 0;
-    typename Epi::Pre pre{};
-    if (row < n) {
-        rs = __ldg(A.row_ptr + row);
-        re = __ldg(A.row_ptr + row + 1);
-        if (sub == 0) pre = epi.pre(row);
-    }
-    for (int tile = blockIdx.x; tile * RPB < n; tile += G) {
-        const int nrow = row + G * RPB;
-        int64_t nrs = 0, nre = 0;
-        typename Epi::Pre npre{};
-        if (nrow < n) {
-            nrs = __ldg(A.row_ptr + nrow);
-            nre = __ldg(A.row_ptr + nrow + 1);
-            if (sub == 0) npre = epi.pre(nrow);
-        }
-        double2 sum = make_double2(0.0, 0.0);
-        const int64_t b0 = rs & ~(int64_t)3;
-        for (int64_t p0 = b0 + 4 * sub; p0 < re; p0 += 4 * W) {
-            double2 v[4];
-            int c[4];
-            if (p0 < nnz_full) {
-                const int4 c4 = ld_col4(A.col + p0, pol);
-                ld_val_pair(A.val + p0, v[0], v[1]);
-                ld_val_pair(A.val + p0 + 2, v[2], v[3]);
-                c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
-            } else {  // the array's final partial block
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const bool in = p0 + u < A.nnz;
-                    c[u] = in ? __ldg(A.col + p0 + u) : 0;
-                    v[u] = in ? __ldg(A.val + p0 + u) : make_double2(0.0, 0.0);
-                }
-            }
-            double2 xv[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const bool in = p0 + u >= rs && p0 + u < re;
-                xv[u] = in ? ld_gather(x + c[u]) : make_double2(0.0, 0.0);
-                if (!in) v[u] = make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) cfma(sum, v[u], xv[u]);
-        }
-#pragma unroll
-        for (int o = W / 2; o > 0; o >>= 1) {
-            sum.x += __shfl_xor_sync(0xffffffffu, sum.x, o, W);
-            sum.y += __shfl_xor_sync(0xffffffffu, sum.y, o, W);
-        }
-        if (sub == 0 && row < n) epi.row(row, sum, pre, acc);
-        row = nrow;
-        rs = nrs;
-        re = nre;
-        pre = npre;
-    }
-    epi.finish(acc);
-}
-
-// ---------------------------------------------------------------------------------------------
 // Sliced-ELL mapping (MODE 3, built at create by sell.cu): one warp per slice of 32 consecutive
 // rows, lane = row.  The slice's entries are stored column-major (entry k of the slice's rows at
 // k·32 + lane), so every value / column load instruction of a warp reads 512 / 128 contiguous
@@ -229,30 +135,15 @@ __device__ __forceinline__ void spmv_body_b4(const CsrDev& A, const double2* __r
 #ifndef ZK_SELL_U
 #define ZK_SELL_U 9
 #endif
-#ifndef ZK_SELL_PIPE
-#define ZK_SELL_PIPE 0
+// Matrix-stream L2 policy of the SELL kernel: evict_first (LP 4).  Every SELL load instruction
+// consumes whole sectors (nothing is re-requested), and the matrix stream no longer pushes the
+// solver vectors out of L2: measured (tools/ab_lib.py, µs per iteration, evict_normal →
+// evict_first) Audi3D-4 (C3) BiCGStab 164.3 → 150.2, CG 86.1 → 75.3, TFQMR 168.3 → 155.5;
+// Twingo3D-2 130.1 → 117.3, 67.4 → 58.5, 131.4 → 118.7; C4 unchanged (1732 either way)
+// (profiles/r02_sell_lp.txt).
+#ifndef ZK_SELL_LP
+#define ZK_SELL_LP 4
 #endif
-#ifndef ZK_SELL_DEP
-#define ZK_SELL_DEP 0
-#endif
-#ifndef ZK_SELL_WSYNC
-#define ZK_SELL_WSYNC 0
-#endif
-#ifndef ZK_SELL_SMEM_ACC
-#define ZK_SELL_SMEM_ACC 0
-#endif
-// ZK_SELL_VGATHER: gathers as volatile asm, so they stay behind ALL the batch's matrix loads in
-// program order (the compiler otherwise interleaves load column → wait → gather per entry)
-#ifndef ZK_SELL_VGATHER
-#define ZK_SELL_VGATHER 0
-#endif
-// Per epilogue (Epi::kOrdered): the store-only epilogue of the split solver SpMVs needs it — left
-// to itself the compiler schedules that kernel at 64 registers with 3 matrix loads in flight per
-// gather batch instead of 9 (SASS; in-loop K1 708 µs vs 647 µs standalone at C4, ncu).
-// Per epilogue (Epi::kTail): after its slice loop the warp walks ITS slices once more and calls
-// epi.tail_load / epi.tail_apply on its rows — a fused reduction pass over vectors the loop just
-// wrote (each lane re-reads only what it stored itself), with no register pressure on the loop
-// (the running sums are not live there) and no extra launch.  SELL kernel only.
 // elements in flight per thread of a vector Op (Op::U, default 4)
 template <class Op>
 struct vec_unroll {
@@ -260,29 +151,26 @@ struct vec_unroll {
     template <class T> static constexpr int get(...) { return 4; }
     static constexpr int value = get<Op>(nullptr);
 };
+// Per epilogue (Epi::kTail): after its slice loop the warp walks ITS slices once more and runs
+// Epi::TailOp (built by epi.tail_op()) on its rows — a fused reduction pass over vectors the loop
+// just wrote (each lane re-reads only what it stored itself), with no register pressure on the
+// loop (neither the running sums nor the Op's operands are live there) and no extra launch.
 template <class E>
 struct sell_tail {
     template <class T> static constexpr bool get(decltype(T::kTail)*) { return T::kTail; }
     template <class T> static constexpr bool get(...) { return false; }
     static constexpr bool value = get<E>(nullptr);
 };
+// Per epilogue (Epi::kOrdered): the store-only epilogue of the split solver SpMVs needs it — left
+// to itself the compiler schedules that kernel at 64 registers with 3 matrix loads in flight per
+// gather batch instead of 9 (SASS; in-loop K1 708 µs vs 647 µs standalone at C4, ncu).
 template <class E>
 struct sell_ordered {
     template <class T> static constexpr bool get(decltype(T::kOrdered)*) { return T::kOrdered; }
-    template <class T> static constexpr bool get(...) { return ZK_SELL_VGATHER != 0; }
+    template <class T> static constexpr bool get(...) { return false; }
     static constexpr bool value = get<E>(nullptr);
 };
-template <bool ORD>
-__device__ __forceinline__ double2 ld_gather_ord(const double2* p) {
-    if constexpr (ORD && ZK_GATHER_MODE == 0) {
-        double2 v;
-        asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-        return v;
-    } else {
-        return ld_gather(p);
-    }
-}
-template <class Epi, int LP = ZK_DEFAULT_LP>
+template <class Epi, int LP = ZK_SELL_LP>
 __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
     constexpr int U = ZK_SELL_U;
     constexpr int KA = Epi::K > 0 ? Epi::K : 1;
@@ -297,13 +185,6 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
     double acc[KA];
 #pragma unroll
     for (int k = 0; k < KA; k++) acc[k] = 0.0;
-#if ZK_SELL_SMEM_ACC
-    // the epilogue's running sums live in per-thread shared-memory slots, not in registers held
-    // across the whole kernel (the row loop runs at the 80-register cap)
-    __shared__ double sacc[KA][kBlock];
-#pragma unroll
-    for (int k = 0; k < KA; k++) sacc[k][threadIdx.x] = 0.0;
-#endif
     const int lane = threadIdx.x & 31;
     const int n = (int)A.n_rows;
     // logical slices t ∈ [0, sl_cnt) → physical slice phys(t) (the whole matrix, or one part of a
@@ -337,47 +218,6 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
         const double2* vr = A.sl_val + base + lane;
         const int* cr = A.sl_col + base + lane;
         double2 sum = make_double2(0.0, 0.0);
-#if ZK_SELL_PIPE
-        // one batch of lookahead: the (value, column) loads of batch k0 + U are issued before the
-        // gathers of batch k0 wait, so the matrix stream's DRAM latency hides behind the gathers'
-        double2 v[U];
-        int c[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            if (u < width) {
-                v[u] = ld_mat<LP>(vr + u * 32, pol);
-                c[u] = ld_mat<LP>(cr + u * 32, pol);
-            } else {
-                v[u] = make_double2(0.0, 0.0);
-                c[u] = -1;
-            }
-        }
-        for (int k0 = 0; k0 < width; k0 += U) {
-            double2 nv[U];
-            int nc[U];
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                if (k0 + U + u < width) {
-                    nv[u] = ld_mat<LP>(vr + (k0 + U + u) * 32, pol);
-                    nc[u] = ld_mat<LP>(cr + (k0 + U + u) * 32, pol);
-                } else {
-                    nv[u] = make_double2(0.0, 0.0);
-                    nc[u] = -1;
-                }
-            }
-            double2 xv[U];
-#pragma unroll
-            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather_ord<ORD>(x + c[u]) : make_double2(0.0, 0.0);
-#pragma unroll
-            for (int u = 0; u < U; u++)
-                if (c[u] >= 0) cfma(sum, v[u], xv[u]);
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                v[u] = nv[u];
-                c[u] = nc[u];
-            }
-        }
-#else
         for (int k0 = 0; k0 < width; k0 += U) {
             double2 v[U];
             int c[U];
@@ -392,53 +232,30 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
                 }
             }
             if (PRE == 1 && k0 + U >= width && row < n) pre = epi.pre(row);
-#if ZK_SELL_WSYNC
-            __syncwarp();  // the batch's matrix loads stay ahead of its gathers in the schedule
-#endif
-            // every gather address depends on the batch's LAST column load (an opaque 0), so the
-            // scheduler cannot start a gather — and stall on its column — before all U (value,
-            // column) loads of the batch are in flight
+            // ORD: every gather address depends on ALL U column loads of the batch (an opaque 0
+            // computed from their AND), so ptxas has to issue the whole batch of (value, column)
+            // loads before the first gather — and cannot stall on one column at a time
             int dep = 0;
             if constexpr (ORD) {
-                // ORD: every gather waits for ALL U column loads (an opaque 0 computed from their
-                // AND), so ptxas has to issue the whole batch before the first gather
                 int m = c[0];
 #pragma unroll
                 for (int u = 1; u < U; u++) m &= c[u];
                 asm("{.reg .pred q; setp.eq.s32 q, %1, 2147483647; selp.b32 %0, 1, 0, q;}" : "=r"(dep) : "r"(m));
-            } else if constexpr (ZK_SELL_DEP != 0) {
-                asm("{.reg .pred q; setp.eq.s32 q, %1, 2147483647; selp.b32 %0, 1, 0, q;}" : "=r"(dep) : "r"(c[U - 1]));
             }
             double2 xv[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather_ord<ORD>(x + (c[u] + dep)) : make_double2(0.0, 0.0);
+            for (int u = 0; u < U; u++) xv[u] = c[u] >= 0 ? ld_gather(x + (c[u] + dep)) : make_double2(0.0, 0.0);
 #pragma unroll
             for (int u = 0; u < U; u++)
                 if (c[u] >= 0) cfma(sum, v[u], xv[u]);
         }
-#endif
         if (PRE == 1 && width == 0 && row < n) pre = epi.pre(row);
         if (PRE == 2 && row < n) pre = epi.pre(row);
-#if ZK_SELL_SMEM_ACC
-        if (row < n) {
-            double racc[KA];
-#pragma unroll
-            for (int k = 0; k < KA; k++) racc[k] = sacc[k][threadIdx.x];
-            epi.row(row, sum, pre, racc);
-#pragma unroll
-            for (int k = 0; k < KA; k++) sacc[k][threadIdx.x] = racc[k];
-        }
-#else
         if (row < n) epi.row(row, sum, pre, acc);
-#endif
         base = nbase;
         width = nwidth;
         if (AHEAD) pre = npre;
     }
-#if ZK_SELL_SMEM_ACC
-#pragma unroll
-    for (int k = 0; k < KA; k++) acc[k] = sacc[k][threadIdx.x];
-#endif
     if constexpr (sell_tail<Epi>::value) {
         constexpr int TU = vec_unroll<typename Epi::TailOp>::value;  // slices in flight per step
         const auto op = epi.tail_op();
@@ -461,6 +278,23 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
         epi.finish(acc);
     }
 }
+
+// The SpMV body of a mapping: MODE 3 sliced ELL (the default), MODE 0 CSR sub-warp rows
+// (matrices whose SELL padding would exceed 10 %).
+template <int W, int MODE, class Epi>
+__device__ __forceinline__ void spmv_any(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
+    static_assert(MODE == 0 || MODE == 3, "SpMV mappings: 0 (CSR sub-warp) and 3 (SELL-32)");
+    if constexpr (sell_tail<Epi>::value && MODE != 3) {
+        __trap();  // tail epilogues exist only in the SELL body (the host never launches this)
+    } else if constexpr (MODE == 3) {
+        spmv_body_sell(A, x, epi);
+    } else {
+        spmv_body<W>(A, x, epi);
+    }
+}
+// minimum resident CTAs per SM of an SpMV kernel (__launch_bounds__): 3 for SELL (80 registers,
+// 9 entries in flight per lane), 4 for the CSR sub-warp kernel (64 registers)
+__host__ __device__ constexpr int spmv_min_blocks(int mode) { return mode == 3 ? 3 : 4; }
 
 // Grid-stride elementwise body with U elements in flight per thread.
 //   Op::K, Op::In, In load(int64_t i), void apply(int64_t i, const In&, double (&acc)[K]), finish(acc)

@@ -6,7 +6,7 @@
 #include <string>
 
 #include "../../include/zk.h"
-#include "spmv_tma.cuh"
+#include "spmv.cuh"
 
 namespace zk {
 
@@ -56,9 +56,9 @@ struct zk_csr_s {
     int* col = nullptr;          // device (local column ids after the halo renumbering on >1 GPU)
     double2* val = nullptr;      // device
     bool owned = false;
+    bool counted = false;        // included in the live-handle count (pool trim at zero)
     int W = 8;                   // SpMV lanes per row
-    int spmv_mode = 0;           // 0 sub-warp CSR (spmv.cuh), 1 TMA-staged tiles, 2 blocked-4, 3 sliced ELL (sell.cu)
-    zk::TmaPlan tma{};
+    int spmv_mode = 0;           // 0 sub-warp CSR (spmv.cuh), 3 sliced ELL (sell.cu)
     // Jacobi right preconditioning (jacobi.cu), built on the first ZK_BICGSTAB_JACOBI solve
     double2* jac_val = nullptr;   // a_ij / a_jj
     double2* jac_diag = nullptr;  // a_ii
@@ -92,12 +92,14 @@ struct zk_csr_s {
 #include <type_traits>
 
 namespace zk {
-// Big per-handle device arrays (CSR copy, SELL copy, Jacobi values) come from the device's
-// stream-ordered memory pool with the release threshold raised, so memory freed by one handle is
-// reused by the next create instead of being unmapped and re-mapped (and re-cleared) by the driver:
-// measured C4 (8.6 GB per handle), back-to-back create/destroy — zk_csr_create 88-772 ms and
-// zk_csr_destroy 8-192 ms with cudaMalloc/cudaFree.  ZK_POOL=0 restores cudaMalloc/cudaFree.
-// The pool keeps the memory reserved for libzk after a handle is destroyed.
+// Big per-handle device arrays (CSR copy, SELL copy, Jacobi values) come from a PRIVATE
+// stream-ordered memory pool per device (cudaMemPoolCreate; release threshold raised), so memory
+// freed by one handle is reused by the next create instead of being unmapped and re-mapped (and
+// re-cleared) by the driver: measured C4 (8.6 GB per handle), back-to-back create/destroy —
+// zk_csr_create 88-772 ms and zk_csr_destroy 8-192 ms with cudaMalloc/cudaFree.  The pool is
+// libzk's own (the device's default pool, which PyTorch and other libraries may use, keeps its
+// settings), and it is trimmed back to the driver when the last handle is destroyed.
+// ZK_POOL=0 restores cudaMalloc/cudaFree.
 inline bool pool_enabled() {
     static int on = -1;
     if (on < 0) {
@@ -106,55 +108,42 @@ inline bool pool_enabled() {
     }
     return on == 1;
 }
+cudaMemPool_t dev_pool(int device);  // api.cu: libzk's pool on `device` (created on first use)
+void handle_count(int delta);         // api.cu: live zk_csr handles; 0 → trim every pool
 inline cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t s) {
     if (!pool_enabled()) return cudaMalloc(p, bytes);
-    static int dev_done = -1;  // per process, first device used (multi-device processes: per create)
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev_done != dev) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        dev_done = dev;
-    }
-    return cudaMallocAsync(p, bytes, s);
+    cudaMemPool_t pool = dev_pool(dev);
+    if (!pool) return cudaMallocAsync(p, bytes, s);  // no private pool: the default pool
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 template <class T>
 inline cudaError_t dev_alloc(T** p, size_t bytes, cudaStream_t s) {
     return dev_alloc(reinterpret_cast<void**>(p), bytes, s);
 }
-// p must not be in use by pending work (the device is synchronised first, as cudaFree would)
-inline void dev_free(void* p) {
+// p must not be in use by pending work: the device is synchronised first, as cudaFree would,
+// unless the caller already did (synced = true: zk_csr_destroy syncs once for all its arrays).
+// (cudaFreeAsync returns a pool allocation to its own pool; a cudaMalloc'd one — ZK_POOL=0 or no
+// pool support — is freed by cudaFree.)
+inline void dev_free(void* p, bool synced = false) {
     if (!p) return;
     if (!pool_enabled()) {
         cudaFree(p);
         return;
     }
-    cudaDeviceSynchronize();
+    if (!synced) cudaDeviceSynchronize();
     cudaFreeAsync(p, 0);
 }
+void sell_destroy(zk_csr_s* A, bool synced = false);    // sell.cu  (synced: the device is already idle)
+void jacobi_destroy(zk_csr_s* A, bool synced = false);  // jacobi.cu
+
 // Call f(std::integral_constant<int, W>, std::integral_constant<int, MODE>) for the matrix's SpMV
-// mapping (instantiated combinations: sub-warp W ∈ {2,4,8,16,32}, TMA W ∈ {4,8,16}).
+// mapping (instantiated: SELL-32 (W = 32, MODE 3) and the CSR sub-warp kernel, W ∈ {2,4,8,16,32}).
 template <class F>
 zk_status with_spmv(const zk_csr_s* A, F&& f) {
     using std::integral_constant;
     if (A->spmv_mode == 3) return f(integral_constant<int, 32>{}, integral_constant<int, 3>{});
-    if (A->spmv_mode == 2) {
-        switch (A->W) {
-            case 4: return f(integral_constant<int, 4>{}, integral_constant<int, 2>{});
-            case 16: return f(integral_constant<int, 16>{}, integral_constant<int, 2>{});
-            default: return f(integral_constant<int, 8>{}, integral_constant<int, 2>{});
-        }
-    }
-    if (A->spmv_mode == 1) {
-        switch (A->W) {
-            case 4: return f(integral_constant<int, 4>{}, integral_constant<int, 1>{});
-            case 16: return f(integral_constant<int, 16>{}, integral_constant<int, 1>{});
-            default: return f(integral_constant<int, 8>{}, integral_constant<int, 1>{});
-        }
-    }
     switch (A->W) {
         case 2: return f(integral_constant<int, 2>{}, integral_constant<int, 0>{});
         case 4: return f(integral_constant<int, 4>{}, integral_constant<int, 0>{});
@@ -173,15 +162,8 @@ struct LaunchCfg {
     int grid;
     int smem;
 };
-// grid and dynamic smem for an SpMV kernel of A (TMA: one CTA per resident slot, ≤ n_tiles)
+// grid (and dynamic smem: none) of an SpMV kernel of A: at most one wave of resident CTAs
 inline LaunchCfg spmv_cfg(const zk_csr_s* A, const void* kernel, int W, int mode) {
-    if (mode == 1) {
-        const int smem = A->tma.smem_bytes;
-        int cap = A->dev.num_sms * blocks_per_sm(kernel, smem);
-        if (cap > kMaxGrid) cap = kMaxGrid;
-        int64_t g = A->tma.n_tiles < cap ? A->tma.n_tiles : cap;
-        return {(int)(g < 1 ? 1 : g), smem};
-    }
     int cap = A->dev.num_sms * blocks_per_sm(kernel, 0);
     if (cap > kMaxGrid) cap = kMaxGrid;
     if (mode == 3) return {grid_for(A->n_slices, kWarps, cap), 0};  // one warp per 32-row slice

@@ -59,11 +59,14 @@ __device__ __forceinline__ int ld_stream(const int* p) {
 // LP 0: .L1::no_allocate alone (L2 treats it as evict-first: partially consumed sectors can be
 // evicted before the neighbouring row asks for them, ncu showed 1.25x DRAM reads);
 // LP 1: no L1 allocation, L2 evict_normal; LP 2: L2 evict_last; LP 3: plain read-only path.
+// LP 4: no L1 allocation, explicit L2 evict_first (SELL: every load instruction consumes whole
+// sectors, so nothing is re-fetched; the solver vectors keep their L2 lines)
 template <int LP>
 __device__ __forceinline__ uint64_t make_policy() {
     uint64_t pol = 0;
     if (LP == 1) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
     if (LP == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    if (LP == 4) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 template <int LP>

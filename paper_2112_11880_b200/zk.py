@@ -52,7 +52,7 @@ class zk_csr_info_t(ctypes.Structure):
                 ("max_row_len", ctypes.c_int32), ("lanes_per_row", ctypes.c_int32),
                 ("mean_row_len", ctypes.c_double), ("n_halo", ctypes.c_int64),
                 ("borrowed", ctypes.c_int32), ("nranks", ctypes.c_int32), ("spmv_mode", ctypes.c_int32),
-                ("rows_per_tile", ctypes.c_int32), ("tma_stages", ctypes.c_int32), ("sell_entries", ctypes.c_int64),
+                ("sell_entries", ctypes.c_int64),
                 ("interior_rows", ctypes.c_int64)]
 
 
@@ -77,6 +77,7 @@ SIGNATURES = {
     "zk_comm_create_local": (I32, [ctypes.POINTER(P), P, I32, I32]),
     "zk_csr_create": (I32, [ctypes.POINTER(P), I64, I64, I64, P, P, P, U32, P, I64, P]),
     "zk_csr_destroy": (I32, [P]),
+    "zk_csr_update_values": (I32, [P, P, U32, P]),
     "zk_csr_info": (I32, [P, ctypes.POINTER(zk_csr_info_t)]),
     "zk_zcsrmv": (I32, [P, zk_z, P, zk_z, P, P]),
     "zk_zdotc": (I32, [I64, P, P, P, P, P]),
@@ -238,6 +239,17 @@ class Csr:
         _check(lib().zk_csr_info(h, ctypes.byref(info)))
         self.info = {f: getattr(info, f) for f, _ in zk_csr_info_t._fields_}
         self.n_rows, self.n_cols, self.nnz = info.n_rows, info.n_cols, info.nnz
+
+    def update_values(self, values=None, stream=None, validate: bool = True):
+        """zk_csr_update_values: new values for the same pattern (host / CUDA array in the original
+        CSR order), or None after changing a borrowed values array in place."""
+        flags = 0 if validate else ZK_SKIP_VALIDATE
+        ptr, keep = None, None
+        if values is not None:
+            ptr, keep, where = _as_ptr_array(values, np.complex128, "values")
+            flags |= ZK_PTRS_HOST if where == "host" else ZK_PTRS_DEVICE
+        _check(lib().zk_csr_update_values(self.handle, ptr, flags, _stream(stream)))
+        return self
 
     def close(self):
         if self.handle:

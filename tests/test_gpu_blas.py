@@ -29,11 +29,9 @@ def row_scale(m, x):
     return A @ np.abs(x)
 
 
-MAPPINGS = [(0, 2, None), (0, 4, None), (0, 8, None), (0, 16, None), (0, 32, None),
-            (1, 4, None), (1, 8, None), (1, 16, None), (1, 8, (2, 700)), (1, 4, (4, 640)),
-            (2, 4, None), (2, 8, None), (2, 16, None), (3, 32, None)]
-MAP_NAMES = {0: "subwarp", 1: "tma", 2: "blocked4", 3: "sell32"}
-MAP_IDS = [f"{MAP_NAMES[m]}-W{w}" + (f"-S{c[0]}-nnz{c[1]}" if c else "") for m, w, c in MAPPINGS]
+MAPPINGS = [(0, 2, None), (0, 4, None), (0, 8, None), (0, 16, None), (0, 32, None), (3, 32, None)]
+MAP_NAMES = {0: "subwarp", 3: "sell32"}
+MAP_IDS = [f"{MAP_NAMES[m]}-W{w}" for m, w, c in MAPPINGS]
 
 
 def make_csr(m, W=None, mode=None, tma=None, **kw):
@@ -43,8 +41,6 @@ def make_csr(m, W=None, mode=None, tma=None, **kw):
         env["ZK_SPMV_W"] = str(W)
     if mode is not None:
         env["ZK_SPMV_MODE"] = str(mode)
-    if tma is not None:
-        env["ZK_TMA_STAGES"], env["ZK_TMA_NNZ"] = str(tma[0]), str(tma[1])
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
@@ -85,29 +81,6 @@ def test_zcsrmv_integer_exact_bitwise(mapping):
     assert np.array_equal(y.cpu().numpy(), oracle.zcsrmv(m, x))
 
 
-def test_blocked_mapping_alignment_fallback_and_tail(monkeypatch):
-    """The blocked-4 mapping needs 32-B aligned values: a borrowed, misaligned value array falls
-    back to the sub-warp mapping; nnz % 4 != 0 exercises the element-wise final block."""
-    monkeypatch.setenv("ZK_SPMV_MODE", "2")
-    m = gen.random_csr(2001, seed=21, max_len=30)
-    assert m["nnz"] % 4 != 0
-    x = gen.rand_vector(2001, 3)
-    want = oracle.zcsrmv(m, x)
-    rp, ci = cuda(m["row_ptr"]), cuda(m["col_idx"])
-    buf = torch.zeros(m["nnz"] + 1, dtype=torch.complex128, device=DEV)
-    buf[1:] = cuda(m["values"])
-    vals = buf[1:]                                                # 16-B but not 32-B aligned
-    A = zk.csr_create(rp, ci, vals, 2001, borrow=True)
-    assert A.info["spmv_mode"] == 0
-    y = torch.empty(2001, dtype=torch.complex128, device=DEV)
-    zk.zcsrmv(A, 1, cuda(x), 0, y)
-    assert np.all(np.abs(y.cpu().numpy() - want) <= 1e-13 * row_scale(m, x) + 1e-300)
-    B = make_csr(m, 8, 2)
-    assert B.info["spmv_mode"] == 2
-    zk.zcsrmv(B, 1, cuda(x), 0, y)
-    assert np.all(np.abs(y.cpu().numpy() - want) <= 1e-13 * row_scale(m, x) + 1e-300)
-
-
 def test_zcsrmv_beta_zero_ignores_nan_and_empty_rows():
     m = gen.random_csr(777, seed=5)
     x = gen.rand_vector(777, 1)
@@ -118,7 +91,7 @@ def test_zcsrmv_beta_zero_ignores_nan_and_empty_rows():
     assert np.all(got[np.diff(m["row_ptr"]) == 0] == 0)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 3])
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C3T"])
 def test_zcsrmv_paper_shapes(cfg, mode):
     m = gen.make_matrix(cfg)
@@ -370,3 +343,40 @@ def test_plain_cudamalloc_path_subprocess():
     env = dict(os.environ, ZK_POOL="0", PYTHONPATH=root)
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("where", ["host", "device", "borrow"])
+def test_csr_update_values_frequency_sweep(where):
+    """zk_csr_update_values: same pattern, new values — the C2 mesh at another
+    wavelength (a Helmholtz frequency sweep, §2).  The SELL copy is refilled and the
+    Jacobi cache rebuilt: SpMV and Jacobi-BiCGStab match the oracle on the NEW matrix."""
+    m1 = gen.make_matrix("C2")
+    m2 = gen.make_matrix("C2", k=2 * np.pi / 2.5)
+    assert np.array_equal(m1["col_idx"], m2["col_idx"]) and not np.array_equal(m1["values"], m2["values"])
+    b = gen.make_rhs(m1)
+    x = gen.rand_vector(m1["n"], 6)
+    if where == "borrow":
+        vals = cuda(m1["values"])
+        A = zk.csr_create(cuda(m1["row_ptr"]), cuda(m1["col_idx"]), vals, m1["n"], borrow=True)
+    else:
+        A = zk.csr_create(m1["row_ptr"], m1["col_idx"], m1["values"], m1["n"])
+    y = torch.empty(m1["n"], dtype=torch.complex128, device=DEV)
+    r1 = zk.solve(A, cuda(b), method="bicgstab_jacobi")                # builds the Jacobi cache of m1
+    assert r1["status"] == "CONVERGED"
+    if where == "borrow":
+        vals.copy_(cuda(m2["values"]))
+        A.update_values(None)
+    else:
+        A.update_values(m2["values"] if where == "host" else cuda(m2["values"]))
+    zk.zcsrmv(A, 1, cuda(x), 0, y)
+    assert np.all(np.abs(y.cpu().numpy() - oracle.zcsrmv(m2, x)) <= 1e-13 * row_scale(m2, x) + 1e-300)
+    r2 = zk.solve(A, cuda(b), method="bicgstab_jacobi")
+    ref = oracle.bicgstab_jacobi(m2, b)
+    assert r2["status"] == ref["status"] == "CONVERGED"
+    assert np.linalg.norm(r2["x"].cpu().numpy() - ref["x"]) <= 1e-6 * np.linalg.norm(ref["x"])
+    bad = m2["values"].copy()
+    bad[17] = np.nan
+    if where != "borrow":
+        with pytest.raises(zk.ZkError) as e:
+            A.update_values(bad)
+        assert e.value.code == -3 and "value 17" in str(e.value)

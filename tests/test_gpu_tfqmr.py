@@ -45,7 +45,7 @@ def diag(n, c):
                 values=np.full(n, c, np.complex128), n=n)
 
 
-@pytest.mark.parametrize("spmv_mode", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("spmv_mode", ["0", "3"])
 @pytest.mark.parametrize("cfg", ["C1", "C2", "T0"])
 def test_tfqmr_parity(cfg, spmv_mode, monkeypatch):
     monkeypatch.setenv("ZK_SPMV_MODE", spmv_mode)
@@ -140,8 +140,6 @@ def test_tfqmr_loop_modes_bitwise_identical(mode, monkeypatch):
     assert r["loop_mode"] == int(mode)
     assert r["iters"] == base["iters"] and np.array_equal(r["x"], base["x"])
     assert np.array_equal(r["hist"], base["hist"])
-    monkeypatch.setenv("ZK_LOOP_MODE", "4")                                # persistent: BiCGStab/CG only
-    assert gpu_solve(m, b, tol=1e-8)["loop_mode"] == 1
 
 
 def test_tfqmr_deterministic():
