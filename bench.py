@@ -65,10 +65,11 @@ BLAS1_SIZES = (648_849, 2_000_000, 9_000_000, 14_000_000, 1 << 26, 1 << 28)  # P
 def blas1_sweep(zk, torch, dev, stream, peak, read_gbs, reps=10):
     """zdotc, dznrm2, zaxpy, zscal, zassign, zaxmy GB/s (algorithmic bytes, metrics.blas1_bytes) at
     the paper's vector lengths (T2-T7: 648,849 / 2M / 9M / 14M) and at 64M / 256M elements.  Each
-    rep: a 512 MB L2 flush (outside the timed pair), then CUDA events around the one call on its
-    stream; the median rep is reported."""
+    rep: a 512 MB L2 flush by READING a buffer (outside the timed pair: L2 is left full of clean
+    lines, so the timed call pays no write-back of the flush's own data), then CUDA events around
+    the one call on its stream; the median rep is reported."""
     from paper_2112_11880_b200 import metrics as M
-    flush = torch.empty(1 << 29, dtype=torch.uint8, device=dev)
+    flush = torch.ones(1 << 27, dtype=torch.float32, device=dev)
     out = {}
     res_c = torch.empty(1, dtype=torch.complex128, device=dev)
     res_d = torch.empty(1, dtype=torch.float64, device=dev)
@@ -87,7 +88,7 @@ def blas1_sweep(zk, torch, dev, stream, peak, read_gbs, reps=10):
             ts = []
             for _ in range(reps):
                 with torch.cuda.stream(stream):
-                    flush.zero_()
+                    flush.sum()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 f()
@@ -102,7 +103,7 @@ def blas1_sweep(zk, torch, dev, stream, peak, read_gbs, reps=10):
         out[str(n)] = row
         del x, y
     del flush
-    return {"sizes": out, "l2": "512 MB flush before every timed call", "reps": reps, "stat": "median",
+    return {"sizes": out, "l2": "512 MB read (clean-line L2 flush) before every timed call", "reps": reps, "stat": "median",
             "headline_zdotc_gbs_256M": out[str(1 << 28)]["zdotc"]["gbs"]}
 
 
@@ -157,11 +158,15 @@ def hbm_peak():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
+def ncu_traffic(cfg: str):
+    """profiles/ncu_traffic.json[cfg]: DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) and
+    duration per in-loop SpMV launch from the ncu launch list of this bench command (cold-cache,
+    serialised), or None for a config without a capture."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
-        d = json.load(open(p))
-        return d.get("spmv_dram_bytes_per_launch")
+        d = json.load(open(p)).get(cfg)
+        if d:
+            return d
     return None
 
 
@@ -325,9 +330,9 @@ def main():
     spmv_gbs = spmv_alg / (k_ms * 1e-3) / 1e9
     peak, peak_src = hbm_peak()
     roofline = {"bound": "hbm", "achieved": spmv_gbs, "peak": peak, "unit": "GB/s", "frac": spmv_gbs / peak,
-                "traffic": ncu_traffic(), "kernel": ("in-loop ZSpMV (BiCGStab K1/K3, store-only SELL SpMV + its r1/r3 reduction pass, "
-                                                     "both inside the timed class)" if n >= (1 << 18) else
-                                                     "in-loop ZSpMV (BiCGStab K1/K3, fused epilogues)"),
+                "traffic": (ncu_traffic(a.config) or {}).get("spmv_dram_bytes_per_launch"),
+                "kernel": ("in-loop ZSpMV (BiCGStab K1/K3: store-only SELL SpMV, its dot products in the same "
+                           "kernel's tail)" if n >= (1 << 18) else "in-loop ZSpMV (BiCGStab K1/K3, fused epilogues)"),
                 "launch_us": 1e3 * k_ms / max(k_n, 1), "bytes_per_launch": spmv_alg / max(k_n, 1),
                 "peak_source": peak_src,
                 "share_of_step": k_ms / ms}
@@ -359,6 +364,12 @@ def main():
     read_gbs = 16.0 * (1 << 28) * 10 / (q0.elapsed_time(q1) * 1e-3) / 1e9
     del big
     roofline["read_stream_gbs"] = read_gbs
+    nt = ncu_traffic(a.config)
+    if nt and nt.get("duration_us_per_launch"):
+        # ncu-measured DRAM GB/s of the same kernel (cold-cache, serialised launches)
+        roofline["ncu_dram_gbs"] = nt["spmv_dram_bytes_per_launch"] / (nt["duration_us_per_launch"] * 1e-6) / 1e9
+        roofline["ncu_dram_frac"] = roofline["ncu_dram_gbs"] / peak
+        roofline["ncu_source"] = nt.get("source")
     roofline["frac_of_read_stream"] = spmv_gbs / read_gbs
     spmv = {"us": spmv_us, "us_median": per[len(per) // 2], "us_min": per[0], "reps": a.spmv_reps,
             "gbs": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9,

@@ -575,6 +575,17 @@ struct EpiStoreTail {
     __device__ void finish(double (&)[K]) {}  // the tail's Op finishes the stage
 };
 
+// The fused epilogue with per-slice warp reductions (SPLIT = 3, SELL only): E's row() as is, its
+// running sums kept in shared memory by the SELL body (sell_warpacc), its row operand loaded with
+// the slice's last batch of matrix loads (kPrePlace 1), the store-only kernel's ordered loads.
+template <class E>
+struct WarpAcc : E {
+    static constexpr bool kWarpAcc = true;
+    static constexpr int kPrePlace = 1;
+    static constexpr bool kOrdered = ZK_STORE_ORD;
+    using E::E;
+};
+
 struct EpiK1Cg {  // q = A p ; {δ = ⟨p, q⟩}
     static constexpr int K = 2;
     using Pre = double2;
@@ -1011,7 +1022,10 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_bicg(SolveCt
     if (c->done) return;
     stamp_start<S_K1_BICG>(c);
     const double2* p = c->p;
-    if constexpr (SPLIT == 2) {
+    if constexpr (SPLIT == 3) {
+        WarpAcc<EpiK1Bicg> e(c);
+        spmv_any<W, MODE>(A, p, e);
+    } else if constexpr (SPLIT == 2) {
         EpiStoreTail<OpRed1Bicg> e(c->v, c);
         spmv_any<W, MODE>(A, p, e);
     } else if constexpr (SPLIT == 1) {
@@ -1047,7 +1061,10 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k3_bicg(SolveCt
     if (c->done) return;
     stamp_start<S_K3_BICG>(c);
     const double2* s = c->s;
-    if constexpr (SPLIT == 2) {
+    if constexpr (SPLIT == 3) {
+        WarpAcc<EpiK3Bicg> e(c);
+        spmv_any<W, MODE>(A, s, e);
+    } else if constexpr (SPLIT == 2) {
         EpiStoreTail<OpRed3Bicg> e(c->t, c);
         spmv_any<W, MODE>(A, s, e);
     } else if constexpr (SPLIT == 1) {
@@ -1082,7 +1099,10 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cocg(SolveCt
     if (c->done) return;
     stamp_start<S_K1_COCG>(c);
     const double2* p = c->p;
-    if constexpr (SPLIT == 2) {
+    if constexpr (SPLIT == 3) {
+        WarpAcc<EpiK1Cocg> e(c);
+        spmv_any<W, MODE>(A, p, e);
+    } else if constexpr (SPLIT == 2) {
         EpiStoreTail<OpRedPq<false, S_K1_COCG>> e(c->q, c);
         spmv_any<W, MODE>(A, p, e);
     } else if constexpr (SPLIT == 1) {
@@ -1114,7 +1134,10 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cg(SolveCtx*
     if (c->done) return;
     stamp_start<S_K1_CG>(c);
     const double2* p = c->p;
-    if constexpr (SPLIT == 2) {
+    if constexpr (SPLIT == 3) {
+        WarpAcc<EpiK1Cg> e(c);
+        spmv_any<W, MODE>(A, p, e);
+    } else if constexpr (SPLIT == 2) {
         EpiStoreTail<OpRedPq<true, S_K1_CG>> e(c->q, c);
         spmv_any<W, MODE>(A, p, e);
     } else if constexpr (SPLIT == 1) {
@@ -2628,6 +2651,19 @@ static bool split_tail(const zk_csr_s* A) {
     if (const char* e = getenv("ZK_SPLIT_TAIL")) return atoi(e) != 0;
     return true;
 }
+// From 2^20 rows the BiCGStab K1/K3 and CG/COCG K1 SpMVs fuse their dot products again, with
+// per-slice warp reductions into shared memory (WarpAcc: no accumulator register across the slice
+// loop, the row operand loaded with the slice's last matrix batch) instead of the tail pass — no
+// second read of the product vector.  Measured (tools/ab_split.py, µs per iteration, tail →
+// warp-reduced): C4 BiCGStab 1749.7 → 1689.5, CG 939.2 → 896.0; C3 BiCGStab 147.9 → 147.9, CG
+// 73.1 → 75.2 (profiles/r02_split_wacc.txt), so below 2^20 rows the tail pass stays.
+// ZK_SPLIT_TAIL: 0 separate pass, 1 tail, 2 warp-reduced (where the kernel has it), unset = auto.
+constexpr int64_t kWarpAccRows = 1 << 20;
+static int tail_kind(const zk_csr_s* A) {
+    if (!split_tail(A)) return 0;
+    if (const char* e = getenv("ZK_SPLIT_TAIL")) return atoi(e) == 2 ? 3 : 2;
+    return A->n_rows >= kWarpAccRows ? 3 : 2;
+}
 
 bool dist_overlap(const zk_csr_s* A);                                            // dist.cu
 void dist_launch_extra(const zk_csr_s* A, int* per_spmv, int* per_allreduce);    // dist.cu
@@ -2680,6 +2716,7 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
     if (dist) pdl = false;
     const bool split = split_reductions(A);
     const bool tail = split_tail(A);
+    const bool wacc = tail_kind(A) == 3;
     return with_spmv(A, [&](auto wc, auto mc) -> zk_status {
         constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
         // a split-schedule SpMV kernel over the slice set `a` (the whole matrix, or one part)
@@ -2690,7 +2727,9 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             };
         };
         if (method == ZK_BICGSTAB) {
-            if (tail) {
+            if (wacc) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_bicg<W, MODE, 3>)));
+            } else if (tail) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_bicg<W, MODE, 2>)));
             } else if (split) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_bicg<W, MODE, 1>)));
@@ -2703,7 +2742,9 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             if (dist) ZK_TRY((dist_finish<S_K1_BICG>(A, dc, 3, s)));
             ZK_TRY(launch_loop(pdl, k2_bicg, vec_grid(A, (const void*)k2_bicg), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_K2_BICG>(A, dc, 1, s)));
-            if (tail) {
+            if (wacc) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.s, s, part(k3_bicg<W, MODE, 3>)));
+            } else if (tail) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.s, s, part(k3_bicg<W, MODE, 2>)));
             } else if (split) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.s, s, part(k3_bicg<W, MODE, 1>)));
@@ -2786,7 +2827,9 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             }
             if (dist) ZK_TRY((dist_finish<S_T4_TFQMR>(A, dc, 2, s)));
         } else if (method == ZK_COCG) {
-            if (tail) {
+            if (wacc) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cocg<W, MODE, 3>)));
+            } else if (tail) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cocg<W, MODE, 2>)));
             } else if (split) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cocg<W, MODE, 1>)));
@@ -2802,7 +2845,9 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             if (dist) ZK_TRY((dist_finish<S_K2_COCG>(A, dc, 3, s)));
             ZK_TRY(launch_loop(pdl, k3_cocg, vec_grid(A, (const void*)k3_cocg), 0, s, dc));
         } else {
-            if (tail) {
+            if (wacc) {
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cg<W, MODE, 3>)));
+            } else if (tail) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cg<W, MODE, 2>)));
             } else if (split) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cg<W, MODE, 1>)));
@@ -3039,7 +3084,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     GraphCache& gc = A->graph[method];
     // one graph per (method, ℓ, Jacobi): the SpMV kernels take the CSR view (A or A·M⁻¹) as a
     // launch parameter baked into the graph
-    const int gkey = ((method * 16 + ell) * 2 + (jacobi ? 1 : 0)) * 2 + (split_tail(A) ? 1 : 0);
+    const int gkey = ((method * 16 + ell) * 2 + (jacobi ? 1 : 0)) * 4 + tail_kind(A);
     // key: workspace pointer, loop mode, method/ℓ/Jacobi and maxit (ws_layout places the partials,
     // tickets and vectors after hist[maxit+1]; BiCGStab(ℓ) bakes its vector pointers into the graph)
     if (mode <= 2 && (gc.ws != workspace || gc.mode != mode || gc.method != gkey || gc.maxit != maxit || !gc.exec)) {

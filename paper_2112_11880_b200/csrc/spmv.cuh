@@ -164,6 +164,16 @@ struct sell_tail {
 // Per epilogue (Epi::kOrdered): the store-only epilogue of the split solver SpMVs needs it — left
 // to itself the compiler schedules that kernel at 64 registers with 3 matrix loads in flight per
 // gather batch instead of 9 (SASS; in-loop K1 708 µs vs 647 µs standalone at C4, ncu).
+// Per epilogue (Epi::kWarpAcc): the epilogue's running sums are reduced over the warp after every
+// slice and kept in a per-warp shared-memory slot (lane 0 adds), so no accumulator register is live
+// across the slice loop (the fused-epilogue variant of the split schedule: the dot products come
+// out of the SpMV itself, with no second pass over the vectors).
+template <class E>
+struct sell_warpacc {
+    template <class T> static constexpr bool get(decltype(T::kWarpAcc)*) { return T::kWarpAcc; }
+    template <class T> static constexpr bool get(...) { return false; }
+    static constexpr bool value = get<E>(nullptr);
+};
 template <class E>
 struct sell_ordered {
     template <class T> static constexpr bool get(decltype(T::kOrdered)*) { return T::kOrdered; }
@@ -181,11 +191,18 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
     constexpr int PRE = pre_place<Epi>::value;
     constexpr bool ORD = sell_ordered<Epi>::value;
     constexpr bool AHEAD = PRE == 0 && pre_ahead<Epi>::value;
+    constexpr bool WACC = sell_warpacc<Epi>::value;
     const uint64_t pol = make_policy<LP>();
     double acc[KA];
 #pragma unroll
     for (int k = 0; k < KA; k++) acc[k] = 0.0;
     const int lane = threadIdx.x & 31;
+    __shared__ double wacc[WACC ? kWarps : 1][KA];
+    if constexpr (WACC) {
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < KA; k++) wacc[threadIdx.x >> 5][k] = 0.0;
+    }
     const int n = (int)A.n_rows;
     // logical slices t ∈ [0, sl_cnt) → physical slice phys(t) (the whole matrix, or one part of a
     // distributed SpMV split into interior / boundary slices, CsrDev)
@@ -251,10 +268,25 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
         }
         if (PRE == 1 && width == 0 && row < n) pre = epi.pre(row);
         if (PRE == 2 && row < n) pre = epi.pre(row);
-        if (row < n) epi.row(row, sum, pre, acc);
+        if constexpr (WACC) {
+            double part[KA];
+#pragma unroll
+            for (int k = 0; k < KA; k++) part[k] = 0.0;
+            if (row < n) epi.row(row, sum, pre, part);
+            warp_sum<KA>(part);  // the slice is warp-uniform: every lane takes part
+            if (lane == 0)
+#pragma unroll
+                for (int k = 0; k < KA; k++) wacc[threadIdx.x >> 5][k] += part[k];
+        } else {
+            if (row < n) epi.row(row, sum, pre, acc);
+        }
         base = nbase;
         width = nwidth;
         if (AHEAD) pre = npre;
+    }
+    if constexpr (WACC) {
+#pragma unroll
+        for (int k = 0; k < KA; k++) acc[k] = lane == 0 ? wacc[threadIdx.x >> 5][k] : 0.0;
     }
     if constexpr (sell_tail<Epi>::value) {
         constexpr int TU = vec_unroll<typename Epi::TailOp>::value;  // slices in flight per step

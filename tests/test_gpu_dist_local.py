@@ -296,3 +296,47 @@ def test_local_bicgstab_l_unsupported():
         return True
 
     assert all(run_ranks(2, fn))
+
+
+def test_local_c4_zslabs_two_ranks_vs_golden():
+    """The bench's strong-scaling partition at full size: C4 (8M rows) split into 2 z-slabs of
+    100 planes (one halo plane of 40,000 entries per rank, interior = every slice but the
+    boundary plane's), BiCGStab through the LOCAL transport with the exchange overlapped, against
+    the oracle's full C4 solves (tests/golden/c4_oracle.json): count within the L11 envelope of
+    the three orders, 12-iteration history to 1e-10, x sample within 4x the orders' spread."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c4_oracle.json")) as f:
+        G = json.load(f)
+    spec = gen.CONFIGS["C4"]
+    plane = spec.nx * spec.ny
+    off = np.array([0, 100 * plane, 200 * plane], dtype=np.int64)
+    idx = np.array(G["sample_idx"])
+
+    def fn(r, comm, s):
+        m = gen.make_matrix(spec, row_range=(off[r], off[r + 1]))
+        b = gen.make_rhs(m)
+        A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], spec.n, comm=comm, row_begin=off[r], stream=s)
+        del m
+        out = zk.solve(A, cuda(b), tol=1e-8, maxit=1000, method="bicgstab")
+        out["x"] = out["x"].cpu().numpy()
+        out["info"] = A.info
+        A.close()
+        return out
+
+    res = run_ranks(2, fn)
+    for q in res:
+        assert q["info"]["n_halo"] == plane and q["info"]["interior_rows"] >= 99 * plane - 32
+        assert q["iters"] == res[0]["iters"] and np.array_equal(q["hist"], res[0]["hist"])
+    r = res[0]
+    its = [G["results"][f"bicgstab/{o}"]["iters"] for o in ("seq", "rev", "block256")]
+    assert r["status"] == "CONVERGED" and 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    h0 = np.array(G["results"]["bicgstab/seq"]["hist"])
+    assert np.max(np.abs(r["hist"][:13] - h0[:13]) / h0[:13]) <= 1e-10
+    x = np.concatenate([q["x"] for q in res])[idx]
+
+    def xs(g):
+        return np.array(g["x_sample_re"]) + 1j * np.array(g["x_sample_im"])
+    x0 = xs(G["results"]["bicgstab/seq"])
+    spread = max(relerr(xs(G["results"][f"bicgstab/{o}"]), x0) for o in ("rev", "block256"))
+    assert relerr(x, x0) <= 4 * spread

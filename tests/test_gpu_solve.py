@@ -285,6 +285,7 @@ def test_distributed_path_single_rank_comm(monkeypatch):
     b = gen.make_rhs(m)
     monkeypatch.setenv("ZK_LOOP_MODE", "3")
     monkeypatch.setenv("ZK_SPLIT_RED", "1")  # a distributed solve always runs the split schedule
+    monkeypatch.setenv("ZK_SPLIT_TAIL", "0")  # ... with separate reduction passes
     base = gpu_solve(m, b, tol=1e-8)
     monkeypatch.delenv("ZK_LOOP_MODE")
     comm = zk.Comm(zk.Comm.unique_id(), 1, 0, 0)
@@ -579,3 +580,32 @@ def test_cg_cluster_outcomes(monkeypatch):
     bb = np.ones(n, np.complex128)
     q = gpu_solve(d, bb, tol=1e-10, method="cg")
     assert q["loop_mode"] == 5 and q["status"] == oracle.cg(d, bb, tol=1e-10)["status"] == "NOT_HPD"
+
+
+def test_bicgstab_c5_full_size_closed_form():
+    """C5 (BASELINE.json configs[4], unit-cube interior 400^3: 64M rows, 1.72G nonzeros) on ONE
+    B200 — the system the row-partitioned runs split: BiCGStab to 1e-8 through zk_solve, the
+    forward error against the DST-I exact solution within 2κ·tol (L12; κ = 2.4e4 closed form),
+    the true residual, and the first 2 iterations' history against the oracle (one oracle
+    iteration at 64M rows is ~11 s of single-thread SpMV)."""
+    spec = gen.CONFIGS["C5"]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    A = zk.csr_create(cuda(m["row_ptr"]), cuda(m["col_idx"]), cuda(m["values"]), m["n"], borrow=True)
+    assert A.info["spmv_mode"] == 3 and A.info["nnz"] == 1_719_374_392
+    r = zk.solve(A, cuda(b), tol=1e-8, maxit=2000, method="bicgstab")
+    assert r["status"] == "CONVERGED" and r["true_relres"] <= 2e-8
+    x = r["x"].cpu().numpy()
+    hist = r["hist"]
+    del r
+    A.close()
+    torch.cuda.empty_cache()
+    oracle.use_all_cores(True)  # the bit-identical OpenMP build (test_oracle_openmp_build_is_bitwise_identical)
+    try:
+        ref = oracle.bicgstab(m, b, tol=1e-8, maxit=2)
+    finally:
+        oracle.use_all_cores(False)
+    assert np.max(np.abs(hist[:3] - ref["hist"][:3]) / ref["hist"][:3]) <= 1e-10
+    del m
+    xe = cf.box_solve(spec, b, gen.ETA)
+    assert relerr(x, xe) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8

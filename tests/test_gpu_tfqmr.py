@@ -159,6 +159,7 @@ def test_tfqmr_distributed_path_single_rank_comm(monkeypatch):
     b = gen.make_rhs(m)
     monkeypatch.setenv("ZK_LOOP_MODE", "3")
     monkeypatch.setenv("ZK_SPLIT_RED", "1")  # a distributed solve always runs the split schedule
+    monkeypatch.setenv("ZK_SPLIT_TAIL", "0")  # ... with separate reduction passes
     base = gpu_solve(m, b, tol=1e-8)
     monkeypatch.delenv("ZK_LOOP_MODE")
     comm = zk.Comm(zk.Comm.unique_id(), 1, 0, 0)

@@ -39,7 +39,7 @@ for cfg in sys.argv[1:] or ["C3"]:
     del m, mg
     for meth in ("bicgstab", "cg", "tfqmr"):
         row = []
-        for tail in ("0", "1"):
+        for tail in os.environ.get("AB_TAILS", "0,1").split(","):
             os.environ["ZK_SPLIT_TAIL"] = tail
             AA, bb = (Ag, bg) if meth == "cg" else (A, b)
             ms, it, h = timed(AA, bb, meth)
