@@ -1797,16 +1797,24 @@ __device__ __forceinline__ void cl_true(SolveCtx* c, ClusterRed& R, const double
     __syncthreads();
 }
 
+// init: the x0 = 0 start (x = 0, r = r̂ = p = b, ‖b‖, hist[0]) runs here from the context passed
+// by value, instead of the k_set_ctx + k_init_zero launches (Audi3D-1: fixed cost of a solve
+// 79.8 → 71.4 µs, tools/latency_probe.py).
+// (Tried and removed: every CTA holding a shared-memory copy of the WHOLE SpMV input, filled over
+// distributed shared memory before each publishing barrier, so the gathers are shared-memory
+// loads — Audi3D-1 9.9 → 11.5 µs per iteration: the 16-way DSMEM broadcast costs more than the L2
+// round trips it removes.)
 // dynamic shared memory: kCVecs × rpc vectors | [values nnz_max] | columns nnz_max | offsets rpc + 1
 template <int W, bool VS>
-__global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, const CsrDev A, int nnz_max, int do_true) {
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, const SolveCtx hctx, const CsrDev A,
+                                                             int nnz_max, int do_true, int init) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ double2 own[];
     __shared__ SolveCtx cs;
     __shared__ ClusterRed R;
     if (threadIdx.x == 0) {
-        cs = *gctx;
+        cs = init ? hctx : *gctx;
         R.parity = 0;
     }
     const int n = (int)A.n_rows;
@@ -1822,11 +1830,32 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
     __syncthreads();
     SolveCtx* c = &cs;
     double2 *xg = cs.x, *pg = cs.p, *sg = cs.s;
-    for (int l = threadIdx.x; l < nr; l += kCBlock) {  // r0, r̂, p, x0 from the init kernel
-        X[l] = xg[row0 + l];
-        Rv[l] = cs.r[row0 + l];
-        RH[l] = cs.rh[row0 + l];
-        P[l] = pg[row0 + l];
+    if (init) {  // x0 = 0: x = 0 ; r = r̂ = p = b ; {‖b‖², ‖r‖², Re bᵀb, Im bᵀb} (OpInitZero, fin_init_bicg)
+        const double2* bg = cs.b;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int l = threadIdx.x; l < nr; l += kCBlock) {
+            const double2 bl = bg[row0 + l];
+            X[l] = make_double2(0.0, 0.0);
+            Rv[l] = RH[l] = P[l] = bl;
+            pg[row0 + l] = bl;
+            const double bb = cabs2(bl);
+            acc[0] += bb;
+            acc[1] += bb;
+            acc[2] = fma(bl.x, bl.x, fma(-bl.y, bl.y, acc[2]));
+            acc[3] = fma(2.0 * bl.x, bl.y, acc[3]);
+        }
+        if (cl.block_rank() == 0 && threadIdx.x == 0)
+            for (int i = 0; i < kTickets; i++) cs.tickets[i] = 0u;  // as k_set_ctx: recycled workspace
+        cl_sum<4>(acc, R);  // its cluster barrier also publishes p for the K1 gathers
+        if (threadIdx.x == 0) fin_init_bicg(c, R.tot);
+        __syncthreads();
+    } else {
+        for (int l = threadIdx.x; l < nr; l += kCBlock) {  // r0, r̂, p, x0 from the init kernel
+            X[l] = xg[row0 + l];
+            Rv[l] = cs.r[row0 + l];
+            RH[l] = cs.rh[row0 + l];
+            P[l] = pg[row0 + l];
+        }
     }
     const double2* gval = cl_stage<VS>(A, row0, nr, sval, scol, soff);
     __syncthreads();
@@ -2563,9 +2592,11 @@ static bool cluster_fits(zk_csr_s* A, cudaStream_t s, int kind, int ell) {
     return nz >= 0 && cluster_smem(A->n_rows, cs, nz, false, kind, ell) <= (size_t)kCSmemMax;
 }
 
-// launch the cluster solver on one cluster (A or A·M⁻¹ in av); false when unavailable
-static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStream_t s, int* out_cs, int kind,
-                           int ell, bool do_true) {
+// launch the cluster solver on one cluster (A or A·M⁻¹ in av); false when unavailable.
+// BiCGStab (kind 0): with `init` the kernel starts from x0 = 0 itself (context hc by value, no
+// k_set_ctx / k_init_zero launches).
+static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc, const CsrDev& av, cudaStream_t s,
+                           int* out_cs, int kind, int ell, bool do_true, bool init) {
     const int cs = cluster_size_available();
     if (cs == 0) return false;
     const int64_t nz = cluster_nnz_max(A, cs, s);
@@ -2593,8 +2624,15 @@ static bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const CsrDev& av, cudaStre
     cfg.numAttrs = 1;
     int nzi = (int)nz;
     int dt = do_true ? 1 : 0;
-    void* args[] = {(void*)&dc, (void*)&av, (void*)&nzi, (void*)&dt};
-    cudaError_t e = cudaLaunchKernelExC(&cfg, cluster_kernel(w, vs, kind), args);
+    int in = init ? 1 : 0;
+    cudaError_t e;
+    if (kind == 0) {
+        void* args[] = {(void*)&dc, (void*)&hc, (void*)&av, (void*)&nzi, (void*)&dt, (void*)&in};
+        e = cudaLaunchKernelExC(&cfg, cluster_kernel(w, vs, 0), args);
+    } else {
+        void* args[] = {(void*)&dc, (void*)&av, (void*)&nzi, (void*)&dt};
+        e = cudaLaunchKernelExC(&cfg, cluster_kernel(w, vs, kind), args);
+    }
     if (e != cudaSuccess) {
         cudaGetLastError();
         return false;
@@ -3128,8 +3166,13 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     int64_t n_spmv = 0;
 
     // ---- init: context, r0 = b − A x0 (or b), ‖b‖, hist[0]
-    k_set_ctx<<<1, 1, 0, s>>>(dc, hc);
-    ZK_CUDA(cudaGetLastError());
+    // (mode-5 BiCGStab from x0 = 0: the cluster kernel does both itself, one launch per solve)
+    const bool fused_init = mode == 5 && method == ZK_BICGSTAB && !x0 &&
+                            !(getenv("ZK_CLUSTER_INIT") && atoi(getenv("ZK_CLUSTER_INIT")) == 0);
+    if (!fused_init) {
+        k_set_ctx<<<1, 1, 0, s>>>(dc, hc);
+        ZK_CUDA(cudaGetLastError());
+    }
     const int kind = method == ZK_BICGSTAB ? 0 : method == ZK_CG ? 1 : method == ZK_COCG ? 3 : method == ZK_TFQMR ? 4 : 5;
     if (x0) {
         const double2* g0 = (const double2*)x0;
@@ -3169,7 +3212,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
             return ZK_OK;
         }));
         n_spmv++;
-    } else {
+    } else if (!fused_init) {
         k_init_zero<<<vec_grid(A, (const void*)k_init_zero), kBlock, 0, s>>>(dc, kind);
         ZK_CUDA(cudaGetLastError());
     }
@@ -3198,7 +3241,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         ZK_CUDA(cudaGraphLaunch(gc.exec, s));
     } else if (mode == 5) {
         int csz = 0;
-        if (!cluster_launch(A, dc, hc.A, s, &csz, cluster_kind(method), ell, !jacobi))  // the kernel also forms the true residual
+        if (!cluster_launch(A, dc, hc, hc.A, s, &csz, cluster_kind(method), ell, !jacobi, fused_init))  // + true residual
             return fail(ZK_ERR_CUDA, "cluster solver launch failed");
     } else {
         hdone = (SolveCtx*)A->pinned;  // the handle's pinned staging (no per-solve cudaMallocHost)
@@ -3268,7 +3311,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         const int fins = A->dist ? (method == ZK_BICGSTAB ? 4 : method == ZK_TFQMR ? 3 : 2) : 0;  // dist: 1-thread finish kernels
         const int pre = method == ZK_TFQMR ? (A->dist ? 2 : 1) : 0;                               // TFQMR: K0 (+ its finish)
         // mode 5: set_ctx + init (+ TFQMR's K0) + the cluster kernel (+ Jacobi: x = M⁻¹u and k_true)
-        info->gpu_launches = mode == 5 ? 3 + pre + (jacobi ? 2 : 0)
+        info->gpu_launches = mode == 5 ? (fused_init ? 1 : 3) + pre + (jacobi ? 2 : 0)
                                                        : 3 + pre + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);
         if (A->dist) {  // + per SpMV: pack kernel, second (boundary) launch; + per allreduce: LOCAL sum kernel
             int per_spmv = 0, per_red = 0;

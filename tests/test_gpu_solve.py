@@ -477,7 +477,8 @@ def test_cluster_solver_parity(cfg, method, monkeypatch):
     m = gen.make_matrix(cfg)
     b = gen.make_rhs(m)
     r = gpu_solve(m, b, tol=1e-8, method=method)
-    assert r["loop_mode"] == 5 and r["gpu_launches"] == (3 if method == "bicgstab" else 5)
+    # BiCGStab from x0 = 0: ONE launch (the cluster kernel does the init); Jacobi: + x = M⁻¹u, k_true
+    assert r["loop_mode"] == 5 and r["gpu_launches"] == (1 if method == "bicgstab" else 3)
     fn = oracle.bicgstab if method == "bicgstab" else oracle.bicgstab_jacobi
     refs = [fn(m, b, tol=1e-8, order=o) for o in ORDERS]
     its = [q["iters"] for q in refs]
@@ -609,3 +610,20 @@ def test_bicgstab_c5_full_size_closed_form():
     del m
     xe = cf.box_solve(spec, b, gen.ETA)
     assert relerr(x, xe) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
+
+
+@pytest.mark.parametrize("init", ["0", "1"])
+def test_cluster_fused_init(init, monkeypatch):
+    """The fused x0 = 0 start of the BiCGStab cluster kernel (init=1: one launch per solve) and the
+    k_set_ctx + k_init_zero start (init=0: three launches) both match the oracle, deterministically."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "5")
+    monkeypatch.setenv("ZK_CLUSTER_INIT", init)
+    m = gen.make_matrix("C1")
+    b = gen.make_rhs(m)
+    r, r2 = gpu_solve(m, b, tol=1e-8), gpu_solve(m, b, tol=1e-8)
+    assert r["gpu_launches"] == (1 if init == "1" else 3)
+    assert np.array_equal(r["x"], r2["x"]) and np.array_equal(r["hist"], r2["hist"])
+    ref = oracle.bicgstab(m, b, tol=1e-8)
+    assert abs(r["iters"] - ref["iters"]) <= 1
+    assert np.max(np.abs(r["hist"][:13] - ref["hist"][:13]) / ref["hist"][:13]) <= 1e-10
+    assert relerr(r["x"], ref["x"]) <= 1e-6
