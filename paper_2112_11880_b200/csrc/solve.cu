@@ -578,10 +578,10 @@ struct EpiStoreTail {
 // The fused epilogue with per-slice warp reductions (SPLIT = 3, SELL only): E's row() as is, its
 // running sums kept in shared memory by the SELL body (sell_warpacc), its row operand loaded with
 // the slice's last batch of matrix loads (kPrePlace 1), the store-only kernel's ordered loads.
-template <class E>
+template <class E, int PRE = 1>
 struct WarpAcc : E {
     static constexpr bool kWarpAcc = true;
-    static constexpr int kPrePlace = 1;
+    static constexpr int kPrePlace = PRE;
     static constexpr bool kOrdered = ZK_STORE_ORD;
     using E::E;
 };
@@ -2841,7 +2841,7 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
         } else if (method == ZK_TFQMR) {
             ZK_TRY(launch_loop(pdl, t1_tfqmr, vec_grid(A, (const void*)t1_tfqmr), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_T1_TFQMR>(A, dc, 1, s)));
-            if (tail) {
+            if (tail) {  // (a warp-reduced T2/T4 epilogue carries 2-3 operands: it spills at 80 registers)
                 ZK_TRY(loop_spmv(A, hc.A, hc.y2, s, part(t2_tfqmr<W, MODE, 2>)));
             } else if (split) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.y2, s, part(t2_tfqmr<W, MODE, 1>)));
