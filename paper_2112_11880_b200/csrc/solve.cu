@@ -1800,10 +1800,12 @@ __device__ __forceinline__ void cl_true(SolveCtx* c, ClusterRed& R, const double
 // init: the x0 = 0 start (x = 0, r = r̂ = p = b, ‖b‖, hist[0]) runs here from the context passed
 // by value, instead of the k_set_ctx + k_init_zero launches (Audi3D-1: fixed cost of a solve
 // 79.8 → 71.4 µs, tools/latency_probe.py).
-// (Tried and removed: every CTA holding a shared-memory copy of the WHOLE SpMV input, filled over
-// distributed shared memory before each publishing barrier, so the gathers are shared-memory
-// loads — Audi3D-1 9.9 → 11.5 µs per iteration: the 16-way DSMEM broadcast costs more than the L2
-// round trips it removes.)
+// (Tried and removed, profiles/r02_cluster_latency.txt: (a) every CTA holding a shared-memory copy
+// of the WHOLE SpMV input, filled over distributed shared memory before each publishing barrier —
+// Audi3D-1 9.9 → 11.5 µs per iteration, the 16-way DSMEM broadcast costs more than the L2 round
+// trips it removes; (b) 3 cluster barriers per iteration instead of 5, with p = r + β(p − ωv) and
+// s = r − αv formed inside the SpMV gathers from the published r, p, v — 9.7 → 15.5 (C1), 24.2 →
+// 53.3 (C2): the 2-3× L2 gathers cost far more than the two barriers.)
 // dynamic shared memory: kCVecs × rpc vectors | [values nnz_max] | columns nnz_max | offsets rpc + 1
 template <int W, bool VS>
 __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, const SolveCtx hctx, const CsrDev A,
@@ -1814,7 +1816,10 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
     __shared__ SolveCtx cs;
     __shared__ ClusterRed R;
     if (threadIdx.x == 0) {
-        cs = init ? hctx : *gctx;
+        if (init)
+            cs = hctx;
+        else
+            cs = *gctx;
         R.parity = 0;
     }
     const int n = (int)A.n_rows;
