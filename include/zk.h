@@ -67,7 +67,8 @@ enum {
     ZK_BICGSTAB = 0,        /* unpreconditioned BiCGStab (O6) */
     ZK_CG = 1,              /* CG, A Hermitian positive definite (O7) */
     ZK_BICGSTAB_JACOBI = 2, /* Jacobi (M = diag A) right-preconditioned BiCGStab, the paper's P-Bi-CGSTAB
-                               (P:308); one GPU; a zero/missing diagonal fails with ZK_ERR_INVALID_CSR */
+                               (P:308); also row-partitioned (the ranks exchange 1/a_jj of their halo
+                               columns once); a zero/missing diagonal fails with ZK_ERR_INVALID_CSR */
     ZK_COCG = 3,            /* COCG: CG with the unconjugated form rᵀr for complex SYMMETRIC A (Aᵀ = A, the
                                absorbing Helmholtz matrices); 1 SpMV per iteration */
     ZK_TFQMR = 4            /* TFQMR (Freund 1993, two half-steps per iteration), the paper's P-TFQMR
@@ -105,6 +106,10 @@ typedef struct {
                               (the longest run of 32-row slices referencing no halo column; the
                               boundary rows follow the exchange); 0 on one GPU or with
                               ZK_DIST_OVERLAP=0 (blocking exchange, then the whole SpMV) */
+    int32_t csr_values_kept; /* 1 if the library keeps its CSR copy of the values; 0 when the SELL copy
+                              is the only one (copied handles above 16384 rows with spmv_mode 3: the
+                              library's matrix memory drops from 2× to ≈ 1.2× the CSR input;
+                              ZK_KEEP_CSR_VALUES=1 keeps it) */
 } zk_csr_info_t;
 
 typedef struct {

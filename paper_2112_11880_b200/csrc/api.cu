@@ -355,6 +355,17 @@ extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, 
             choose_mapping(A, 0);
         }
     }
+    // The SELL copy carries the values the SpMV reads: the library's own CSR copy of the values
+    // (16 B per nonzero, C4 3.4 GB, C5 27.5 GB) is dropped for systems above the cluster solver's
+    // range (it reads CSR).  Row pointers and columns stay (Jacobi's diagonal comes from the SELL
+    // copy, zk_csr_update_values refills it from a temporary).  ZK_KEEP_CSR_VALUES=1 keeps them.
+    if (A->spmv_mode == 3 && A->owned && A->n_rows > kCsrValuesKeepRows &&
+        !(getenv("ZK_KEEP_CSR_VALUES") && atoi(getenv("ZK_KEEP_CSR_VALUES")) != 0)) {
+        cudaError_t e = cudaStreamSynchronize(s);  // the SELL fill read them
+        if (e != cudaSuccess) return cleanup(cuda_fail(e, "zk_csr_create", __FILE__, __LINE__));
+        dev_free(A->val, true);
+        A->val = nullptr;
+    }
     // the arrays may have come from the stream-ordered pool: usable from any stream after this
     {
         cudaError_t e = cudaStreamSynchronize(s);
@@ -401,18 +412,20 @@ extern "C" zk_status zk_csr_destroy(zk_csr A) {
 }
 
 namespace zk {
-zk_status sell_refill(zk_csr_s* A, cudaStream_t s);  // sell.cu
+zk_status sell_refill(zk_csr_s* A, const double2* val, cudaStream_t s);  // sell.cu
 }
 
 extern "C" zk_status zk_csr_update_values(zk_csr A, const zk_z* values, uint32_t flags, zk_stream stream) {
     if (!A) return fail(ZK_ERR_INVALID_VALUE, "NULL handle");
     cudaStream_t s = (cudaStream_t)stream;
     const uint32_t where = flags & 3u;
+    double2* tmp = nullptr;  // the new values when the handle dropped its CSR value copy
     if (A->owned) {
         if (!values && A->nnz > 0) return fail(ZK_ERR_INVALID_VALUE, "NULL values");
         if (where != ZK_PTRS_HOST && where != ZK_PTRS_DEVICE) return fail(ZK_ERR_INVALID_VALUE, "bad flags");
+        if (!A->val && A->nnz > 0) ZK_CUDA(dev_alloc(&tmp, sizeof(double2) * A->nnz, s));
         if (A->nnz > 0)
-            ZK_CUDA(cudaMemcpyAsync(A->val, values, sizeof(double2) * A->nnz,
+            ZK_CUDA(cudaMemcpyAsync(tmp ? tmp : A->val, values, sizeof(double2) * A->nnz,
                                     where == ZK_PTRS_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
     } else if (values && (const void*)values != (const void*)A->val) {
         return fail(ZK_ERR_INVALID_VALUE, "borrowed handle: update the borrowed array in place, pass it or NULL");
@@ -422,7 +435,7 @@ extern "C" zk_status zk_csr_update_values(zk_csr A, const zk_z* values, uint32_t
         ZK_CUDA(cudaMalloc(&d, sizeof h));
         cudaError_t e = cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess) {
-            nonfinite_kernel<<<grid_for(A->nnz, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(A->val, A->nnz, d);
+            nonfinite_kernel<<<grid_for(A->nnz, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(tmp ? tmp : A->val, A->nnz, d);
             e = cudaGetLastError();
         }
         if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s);
@@ -430,12 +443,20 @@ extern "C" zk_status zk_csr_update_values(zk_csr A, const zk_z* values, uint32_t
         cudaFree(d);
         if (e != cudaSuccess) return cuda_fail(e, "zk_csr_update_values", __FILE__, __LINE__);
         if (h != ~0ull) {
+            if (tmp) dev_free(tmp);
             char buf[128];
             snprintf(buf, sizeof buf, "value %llu (CSR order) is not finite", h);
             return fail(ZK_ERR_NONFINITE, buf);
         }
     }
-    if (A->spmv_mode == 3) ZK_TRY(sell_refill(A, s));
+    if (A->spmv_mode == 3) {
+        const zk_status st = sell_refill(A, tmp ? tmp : A->val, s);
+        if (tmp) {
+            cudaStreamSynchronize(s);
+            dev_free(tmp, true);
+        }
+        ZK_TRY(st);
+    }
     ZK_CUDA(cudaStreamSynchronize(s));
     for (auto& g : A->graph) {  // graphs bake the Jacobi values' address: rebuilt on the next solve
         if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -462,6 +483,7 @@ extern "C" zk_status zk_csr_info(zk_csr A, zk_csr_info_t* info) {
     info->spmv_mode = A->spmv_mode;
     info->sell_entries = A->spmv_mode == 3 ? A->sl_nnz : 0;
     info->interior_rows = A->dist ? dist_interior_rows(A) : 0;
+    info->csr_values_kept = A->val ? 1 : 0;
     return ZK_OK;
 }
 

@@ -27,6 +27,28 @@ __global__ void jacobi_diag_kernel(const int64_t* __restrict__ row_ptr, const in
     }
 }
 
+// the same from the SELL copy (handles that dropped their CSR value copy): row r = slice r/32, lane
+// r%32, entry k at sl_ptr[r/32] + 32k + r%32
+__global__ void jacobi_diag_sell_kernel(const int64_t* __restrict__ sl_ptr, const int* __restrict__ sl_col,
+                                        const double2* __restrict__ sl_val, int64_t n, double2* __restrict__ diag,
+                                        double2* __restrict__ dinv, unsigned long long* first_bad) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int64_t base = sl_ptr[i >> 5], width = (sl_ptr[(i >> 5) + 1] - base) >> 5;
+        double2 d = make_double2(0.0, 0.0);
+        for (int64_t k = 0; k < width; k++) {
+            const int64_t q = base + 32 * k + (i & 31);
+            if (sl_col[q] == i) d = sl_val[q];
+        }
+        if (d.x == 0.0 && d.y == 0.0) {
+            atomicMin(first_bad, (unsigned long long)i);
+            d = make_double2(1.0, 0.0);
+        }
+        diag[i] = d;
+        dinv[i] = cdiv(make_double2(1.0, 0.0), d);
+    }
+}
+
 // a'_ij = a_ij · dinv_j
 __global__ void jacobi_scale_kernel(const int* __restrict__ col, const double2* __restrict__ val,
                                     const double2* __restrict__ dinv, int64_t nnz, double2* __restrict__ out) {
@@ -43,59 +65,92 @@ __global__ void cscale_kernel(const double2* __restrict__ d, const double2* in, 
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = cmul(d[i], in[i]);
 }
 
+int64_t dist_gather_len(const zk_csr_s* A);                                         // dist.cu
+zk_status dist_halo(const zk_csr_s* A, double2* xg, cudaStream_t s);                // dist.cu
+zk_status dist_agree_failed(zk_comm_s* c, bool failed, cudaStream_t s, int* any_failed);  // dist.cu
+
+// Build A·M⁻¹ (CSR values and the SELL copy) once per handle.  On a row-partitioned matrix the
+// column scaling needs 1/a_jj of the halo columns too: the ranks exchange their dinv entries once
+// through the SpMV's halo plan (dinv is laid out like a gathered vector: [local rows | halo slots]),
+// after agreeing on whether any rank lacks a diagonal (so no rank is left in the exchange).
 zk_status jacobi_prepare(zk_csr_s* A, cudaStream_t s) {
     if (A->jac_val) return ZK_OK;
-    if (A->dist) return fail(ZK_ERR_UNSUPPORTED, "Jacobi-preconditioned solves on a distributed matrix");
     const int64_t n = A->n_rows, nnz = A->nnz;
+    const int64_t glen = A->dist ? dist_gather_len(A) : n;
     double2 *val = nullptr, *diag = nullptr, *dinv = nullptr;
     unsigned long long* bad = nullptr;
-    cudaError_t e = dev_alloc(&val, sizeof(double2) * (nnz > 0 ? nnz : 1), s);
-    if (e == cudaSuccess) e = dev_alloc(&diag, sizeof(double2) * (n > 0 ? n : 1), s);
-    if (e == cudaSuccess) e = dev_alloc(&dinv, sizeof(double2) * (n > 0 ? n : 1), s);
-    if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s);
-    if (e == cudaSuccess && n > 0) {
-        jacobi_diag_kernel<<<grid_for(n, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(A->row_ptr, A->col, A->val, n,
-                                                                                     diag, dinv, bad);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess && nnz > 0) {
-        jacobi_scale_kernel<<<grid_for(nnz, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(A->col, A->val, dinv, nnz,
-                                                                                        val);
-        e = cudaGetLastError();
-    }
-    unsigned long long hbad = 0;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(bad);
-    if (e != cudaSuccess || hbad != ~0ull) {
+    auto release = [&] {
         dev_free(val);
         dev_free(diag);
         dev_free(dinv);
+        dev_free(A->jac_sl_val);
+        A->jac_sl_val = nullptr;
+    };
+    const bool csr_vals = A->val != nullptr;  // false: the SELL copy is the only value array
+    cudaError_t e = csr_vals ? dev_alloc(&val, sizeof(double2) * (nnz > 0 ? nnz : 1), s) : cudaSuccess;
+    if (e == cudaSuccess) e = dev_alloc(&diag, sizeof(double2) * (n > 0 ? n : 1), s);
+    if (e == cudaSuccess) e = dev_alloc(&dinv, sizeof(double2) * (glen > 0 ? glen : 1), s);
+    if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s);
+    if (e == cudaSuccess && n > 0) {
+        if (csr_vals)
+            jacobi_diag_kernel<<<grid_for(n, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(A->row_ptr, A->col, A->val, n,
+                                                                                         diag, dinv, bad);
+        else
+            jacobi_diag_sell_kernel<<<grid_for(n, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(
+                A->sl_ptr, A->sl_col, A->sl_val, n, diag, dinv, bad);
+        e = cudaGetLastError();
+    }
+    unsigned long long hbad = ~0ull;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(bad);
+    bool failed = e != cudaSuccess || hbad != ~0ull;
+    if (A->dist) {
+        int any = 0;
+        const zk_status st = dist_agree_failed(A->comm, failed, s, &any);
+        if (st != ZK_OK) {
+            release();
+            return st;
+        }
+        if (any && !failed) {
+            release();
+            return fail(ZK_ERR_INVALID_CSR, "another rank has a row without a stored diagonal (Jacobi preconditioner)");
+        }
+    }
+    if (failed) {
+        release();
         if (e != cudaSuccess) return cuda_fail(e, "jacobi_prepare", __FILE__, __LINE__);
         char buf[160];
         snprintf(buf, sizeof buf, "row %lld has no nonzero stored diagonal (Jacobi preconditioner)",
                  (long long)hbad + (long long)A->row_begin);
         return fail(ZK_ERR_INVALID_CSR, buf);
     }
-    if (A->sl_val) {  // the same scaling of the sliced-ELL copy (SpMV mode 3)
+    if (A->dist) {
+        const zk_status st = dist_halo(A, dinv, s);  // 1/a_jj of the halo columns
+        if (st != ZK_OK) {
+            release();
+            return st;
+        }
+    }
+    if (nnz > 0 && csr_vals) {
+        jacobi_scale_kernel<<<grid_for(nnz, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(A->col, A->val, dinv, nnz,
+                                                                                        val);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && A->sl_val) {  // the same scaling of the sliced-ELL copy (SpMV mode 3)
         e = dev_alloc(&A->jac_sl_val, sizeof(double2) * (size_t)(A->sl_nnz > 0 ? A->sl_nnz : 1), s);
         if (e == cudaSuccess && A->sl_nnz > 0) {
             jacobi_scale_kernel<<<grid_for(A->sl_nnz, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(
                 A->sl_col, A->sl_val, dinv, A->sl_nnz, A->jac_sl_val);
             e = cudaGetLastError();
         }
-        if (e != cudaSuccess) {
-            dev_free(val);
-            dev_free(diag);
-            dev_free(dinv);
-            dev_free(A->jac_sl_val);
-            A->jac_sl_val = nullptr;
-            return cuda_fail(e, "jacobi_prepare (sliced ELL)", __FILE__, __LINE__);
-        }
     }
-    e = cudaStreamSynchronize(s);  // pool memory: usable from any stream afterwards
-    if (e != cudaSuccess) return cuda_fail(e, "jacobi_prepare", __FILE__, __LINE__);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // pool memory: usable from any stream afterwards
+    if (e != cudaSuccess) {
+        release();
+        return cuda_fail(e, "jacobi_prepare", __FILE__, __LINE__);
+    }
     A->jac_val = val;
     A->jac_diag = diag;
     A->jac_dinv = dinv;

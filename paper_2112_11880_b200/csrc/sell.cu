@@ -108,11 +108,11 @@ zk_status sell_build(zk_csr_s* A, cudaStream_t s) {
 
 // Re-fill the SELL values (and columns) from the CSR arrays after zk_csr_update_values: same
 // pattern, so the slice layout (sl_ptr) is unchanged.
-zk_status sell_refill(zk_csr_s* A, cudaStream_t s) {
+zk_status sell_refill(zk_csr_s* A, const double2* val, cudaStream_t s) {
     const int64_t n_sl = A->n_slices;
     if (n_sl > 0) {
         sell_fill_kernel<<<grid_for(n_sl * 32, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(
-            A->row_ptr, A->col, A->val, A->n_rows, n_sl, A->sl_ptr, A->sl_col, A->sl_val);
+            A->row_ptr, A->col, val, A->n_rows, n_sl, A->sl_ptr, A->sl_col, A->sl_val);
         ZK_CUDA(cudaGetLastError());
     }
     return ZK_OK;

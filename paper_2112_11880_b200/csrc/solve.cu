@@ -2590,7 +2590,7 @@ static int64_t cluster_nnz_max(zk_csr_s* A, int cs, cudaStream_t s) {
 // can the cluster solver hold this system (own rows + the block's columns in shared memory)?
 static bool cluster_fits(zk_csr_s* A, cudaStream_t s, int kind, int ell) {
     const int cs = cluster_size_available();
-    if (kind < 0 || cs == 0 || A->n_rows == 0 ||
+    if (kind < 0 || cs == 0 || A->n_rows == 0 || !A->val ||  // the cluster kernels stage the CSR values
         A->n_rows > (int64_t)cs * (kCSmemMax / (cluster_nvec(kind, ell) * 16 + 8)))
         return false;
     const int64_t nz = cluster_nnz_max(A, cs, s);

@@ -136,6 +136,7 @@ inline void dev_free(void* p, bool synced = false) {
     cudaFreeAsync(p, 0);
 }
 void sell_destroy(zk_csr_s* A, bool synced = false);    // sell.cu  (synced: the device is already idle)
+constexpr int64_t kCsrValuesKeepRows = 16384;           // ≤ this: the CSR value copy stays (cluster solver)
 void jacobi_destroy(zk_csr_s* A, bool synced = false);  // jacobi.cu
 
 // Call f(std::integral_constant<int, W>, std::integral_constant<int, MODE>) for the matrix's SpMV

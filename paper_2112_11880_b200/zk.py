@@ -53,7 +53,7 @@ class zk_csr_info_t(ctypes.Structure):
                 ("mean_row_len", ctypes.c_double), ("n_halo", ctypes.c_int64),
                 ("borrowed", ctypes.c_int32), ("nranks", ctypes.c_int32), ("spmv_mode", ctypes.c_int32),
                 ("sell_entries", ctypes.c_int64),
-                ("interior_rows", ctypes.c_int64)]
+                ("interior_rows", ctypes.c_int64), ("csr_values_kept", ctypes.c_int32)]
 
 
 class zk_solve_info(ctypes.Structure):

@@ -627,3 +627,44 @@ def test_cluster_fused_init(init, monkeypatch):
     assert abs(r["iters"] - ref["iters"]) <= 1
     assert np.max(np.abs(r["hist"][:13] - ref["hist"][:13]) / ref["hist"][:13]) <= 1e-10
     assert relerr(r["x"], ref["x"]) <= 1e-6
+
+
+@pytest.mark.parametrize("keep", ["0", "1"])
+def test_dropped_csr_values_jacobi_and_update(keep, monkeypatch):
+    """Copied handles above 16384 rows keep only the SELL copy of the values (the library's CSR value
+    copy is dropped; ZK_KEEP_CSR_VALUES=1 keeps it): Jacobi-BiCGStab then takes its diagonal from
+    the SELL copy and zk_csr_update_values refills the SELL copy from a temporary.  Both ways give
+    the oracle's results, and bitwise the same solves."""
+    monkeypatch.setenv("ZK_KEEP_CSR_VALUES", keep)
+    m = gen.make_matrix("A3")                      # Audi3D-3 shape, 85,001 rows
+    b = gen.make_rhs(m)
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+    assert A.info["spmv_mode"] == 3 and A.info["csr_values_kept"] == int(keep)
+    r = zk.solve(A, cuda(b), tol=1e-8, method="bicgstab_jacobi")
+    refs = [oracle.bicgstab_jacobi(m, b, tol=1e-8, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    assert r["status"] == "CONVERGED" and 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    assert relerr(r["x"].cpu().numpy(), refs[0]["x"]) <= 1e-6
+    m2 = gen.make_matrix("A3", k=2 * np.pi / 2.5)
+    A.update_values(m2["values"])
+    x = gen.rand_vector(m["n"], 3)
+    y = torch.empty(m["n"], dtype=torch.complex128, device=DEV)
+    zk.zcsrmv(A, 1, cuda(x), 0, y)
+    want = oracle.zcsrmv(m2, x)
+    scale = np.add.reduceat(np.abs(m2["values"]) * np.abs(x[m2["col_idx"]]), m2["row_ptr"][:-1])
+    assert np.all(np.abs(y.cpu().numpy() - want) <= 1e-13 * scale)
+    r2 = zk.solve(A, cuda(b), tol=1e-8, method="bicgstab_jacobi")
+    ref2 = oracle.bicgstab_jacobi(m2, b, tol=1e-8)
+    assert r2["status"] == "CONVERGED" and relerr(r2["x"].cpu().numpy(), ref2["x"]) <= 1e-6
+    return r["x"].cpu().numpy()
+
+
+def test_dropped_csr_values_bitwise(monkeypatch):
+    m = gen.make_matrix("A3")
+    b = gen.make_rhs(m)
+    out = []
+    for keep in ("0", "1"):
+        monkeypatch.setenv("ZK_KEEP_CSR_VALUES", keep)
+        A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+        out.append(zk.solve(A, cuda(b), tol=1e-8, method="bicgstab_jacobi"))
+    assert out[0]["iters"] == out[1]["iters"] and torch.equal(out[0]["x"], out[1]["x"])
