@@ -377,7 +377,7 @@ def main():
             "gflops": M.spmv_flops(nnz) / (spmv_us * 1e-6) / 1e9,
             "frac_of_peak": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9 / peak,
             "lanes_per_row": A.info["lanes_per_row"],
-            "mapping": {0: "CSR sub-warp", 1: "CSR TMA-staged", 2: "CSR blocked-4",
+            "mapping": {0: "CSR sub-warp",
                         3: "sliced ELL (SELL-32 device copy)"}[A.info["spmv_mode"]],
             "stored_entries": A.info["sell_entries"] or nnz}
 

@@ -656,7 +656,6 @@ def test_dropped_csr_values_jacobi_and_update(keep, monkeypatch):
     r2 = zk.solve(A, cuda(b), tol=1e-8, method="bicgstab_jacobi")
     ref2 = oracle.bicgstab_jacobi(m2, b, tol=1e-8)
     assert r2["status"] == "CONVERGED" and relerr(r2["x"].cpu().numpy(), ref2["x"]) <= 1e-6
-    return r["x"].cpu().numpy()
 
 
 def test_dropped_csr_values_bitwise(monkeypatch):

@@ -47,16 +47,9 @@ def spmv(a):
     n, nnz = m["n"], m["nnz"]
     x = torch.from_numpy(gen.rand_vector(n, 1)).cuda()
     y = torch.empty_like(x)
-    for spec in a.maps.split(","):                      # mode:W[:stages:stage_nnz[:span]]
+    for spec in a.maps.split(","):                      # mode:W  (mode 0 CSR sub-warp, 3 SELL-32)
         f = spec.split(":")
-        env = {"ZK_SPMV_MODE": f[0], "ZK_SPMV_W": f[1]}
-        if len(f) > 3 and f[2]:
-            env.update(ZK_TMA_STAGES=f[2], ZK_TMA_NNZ=f[3])
-        if len(f) > 4:
-            env["ZK_SPMV_SPAN"] = f[4]
-        for k in ("ZK_TMA_STAGES", "ZK_TMA_NNZ", "ZK_SPMV_SPAN"):
-            os.environ.pop(k, None)
-        os.environ.update(env)
+        os.environ.update({"ZK_SPMV_MODE": f[0], "ZK_SPMV_W": f[1]})
         A = zk.csr_create(rp, ci, va, n, borrow=True)
         us = timeit(lambda: zk.zcsrmv(A, 1.0, x, a.beta, y), a.reps)
         gbs = M.spmv_bytes(n, nnz, a.beta != 0) / (us * 1e-6) / 1e9
@@ -109,7 +102,7 @@ if __name__ == "__main__":
     p = argparse.ArgumentParser()
     p.add_argument("what", choices=["spmv", "blas1", "ncu-spmv", "solve"])
     p.add_argument("--config", default="C4")
-    p.add_argument("--maps", default="0:8,1:4,1:8,1:16,1:8:2:1792,1:8:4:1792,1:8:2:896,1:8:4:896,1:8:3:896,1:4:3:3584,1:8:2:3584")
+    p.add_argument("--maps", default="0:4,0:8,3:32")
     p.add_argument("--reps", type=int, default=50)
     p.add_argument("--beta", type=float, default=0.0)
     p.add_argument("--n", type=int, default=1 << 28)
