@@ -331,8 +331,13 @@ def main():
     peak, peak_src = hbm_peak()
     roofline = {"bound": "hbm", "achieved": spmv_gbs, "peak": peak, "unit": "GB/s", "frac": spmv_gbs / peak,
                 "traffic": (ncu_traffic(a.config) or {}).get("spmv_dram_bytes_per_launch"),
-                "kernel": ("in-loop ZSpMV (BiCGStab K1/K3: store-only SELL SpMV, its dot products in the same "
-                           "kernel's tail)" if n >= (1 << 18) else "in-loop ZSpMV (BiCGStab K1/K3, fused epilogues)"),
+                "kernel": ("in-loop ZSpMV (BiCGStab K1/K3: SELL-32 SpMV with its dot products fused by per-slice "
+                           "warp reductions)" if n >= (1 << 20) and comm is None else
+                           "in-loop ZSpMV (BiCGStab K1/K3: SELL-32 SpMV, its dot products in the same kernel's tail)"
+                           if n >= (1 << 18) and comm is None else
+                           "in-loop ZSpMV (BiCGStab K1/K3: interior + boundary SELL launches around the halo "
+                           "exchange, then the reduction pass)" if comm is not None else
+                           "in-loop ZSpMV (BiCGStab K1/K3, fused epilogues)"),
                 "launch_us": 1e3 * k_ms / max(k_n, 1), "bytes_per_launch": spmv_alg / max(k_n, 1),
                 "peak_source": peak_src,
                 "share_of_step": k_ms / ms}
