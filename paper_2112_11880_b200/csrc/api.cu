@@ -80,7 +80,7 @@ int blocks_per_sm(const void* kernel, int smem) {
 
 extern "C" const char* zk_last_error(void) { return zk::g_err.c_str(); }
 
-extern "C" int32_t zk_version(void) { return 100; }
+extern "C" int32_t zk_version(void) { return 200; }  // 2.0: zk_csr_info_t without the TMA fields, + interior_rows, csr_values_kept
 
 extern "C" const char* zk_status_string(zk_status s) {
     switch (s) {

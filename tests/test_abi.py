@@ -48,7 +48,7 @@ def test_sm100a_only(lib):
 
 
 def test_host_only_calls(lib):
-    assert lib.zk_version() == 100
+    assert lib.zk_version() == 200
     assert lib.zk_status_string(-2) == b"ZK_ERR_INVALID_CSR"
     assert lib.zk_status_string(0) == b"ZK_OK"
 
@@ -64,3 +64,17 @@ def test_no_oracle_in_product_path():
                 assert "zk_oracle" not in txt and "liboracle" not in txt, f
     out = subprocess.check_output(["nm", "-D", zk.SO_PATH]).decode()
     assert "oracle_" not in out
+
+
+def test_local_group_host_api(lib):
+    """The LOCAL transport's group object is host-only: create / destroy need no GPU, bad sizes
+    are rejected (zk.h: 1..16 ranks)."""
+    import ctypes
+    from paper_2112_11880_b200 import zk
+    g = zk.LocalGroup(4)
+    assert g.nranks == 4 and g.handle
+    g.close()
+    h = ctypes.c_void_p()
+    assert lib.zk_local_group_create(ctypes.byref(h), 0) == -1
+    assert lib.zk_local_group_create(ctypes.byref(h), 17) == -1
+    assert lib.zk_local_group_destroy(None) == 0

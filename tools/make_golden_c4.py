@@ -9,6 +9,9 @@ Calls only oracle/ (the plain C oracle) and gen/ (seeded inputs).  Runs the solv
   CG (O7) on the gauge-twisted HPD C4 (eta = 0, L9), orders seq / rev / block-256
   TFQMR and COCG on C4 (seq order; NEXT-2 / NEXT-4)
 
+With --bl: tests/golden/c4_oracle_bicgstab_l.json, BiCGStab(2) and BiCGStab(8) (NEXT-3) under the three
+orders (cycles, history, x sample).
+
 With --tight: tests/golden/c4_oracle_tol1e-10.json, BiCGStab at tol 1e-10 (orders seq / rev), the
 L12 optional mode "run both sides at tol 1e-10 and require 1e-6 agreement there" (at tol 1e-8 the
 oracle's own orders disagree by 1e-5 on x at C4, κ = 6.1e3).
@@ -47,7 +50,7 @@ def summarise(r: dict, idx: np.ndarray, t: float) -> dict:
                 seconds=round(t, 1))
 
 
-def main(tight=False, extra=False):
+def main(tight=False, extra=False, bl=False):
     m = gen.make_matrix("C4")
     b = gen.make_rhs(m)
     mg = gen.make_matrix("C4", eta=0.0, twist_seed=gen.SEED_TWIST)
@@ -61,7 +64,10 @@ def main(tight=False, extra=False):
     for name, o in ([] if tight else ORDERS.items()):
         jobs.append((f"bicgstab/{name}", lambda o=o: oracle.bicgstab(m, b, tol=1e-8, maxit=1000, order=o)))
         jobs.append((f"cg_twisted_hpd/{name}", lambda o=o: oracle.cg(mg, bg, tol=1e-8, maxit=3000, order=o)))
-    if extra:  # the other two orders of TFQMR and COCG, merged into the existing file
+    if bl:
+        jobs = [(f"bicgstab_l{ell}/{name}", lambda o=o, ell=ell: oracle.bicgstab_l(m, b, tol=1e-8, maxit=300, ell=ell, order=o))
+                for ell in (2, 8) for name, o in ORDERS.items()]
+    elif extra:  # the other two orders of TFQMR and COCG, merged into the existing file
         jobs = []
         for name in ("rev", "block256"):
             jobs.append((f"tfqmr/{name}", lambda o=ORDERS[name]: oracle.tfqmr(m, b, tol=1e-8, maxit=1000, order=o)))
@@ -85,7 +91,7 @@ def main(tight=False, extra=False):
     out = dict(config="C4", n=int(m["n"]), nnz=int(m["nnz"]), tol=1e-10 if tight else 1e-8, sample_idx=idx.tolist(),
                generator="gen.make_matrix('C4') / make_rhs seed 42; CG: eta=0, twist seed 43, b = e^{i phase} b",
                written_by="tools/make_golden_c4.py (oracle/ only)", results=res)
-    path = OUT.replace(".json", "_tol1e-10.json") if tight else OUT
+    path = OUT.replace(".json", "_tol1e-10.json") if tight else OUT.replace(".json", "_bicgstab_l.json") if bl else OUT
     if extra:
         with open(OUT) as f:
             old = json.load(f)
@@ -97,4 +103,4 @@ def main(tight=False, extra=False):
 
 
 if __name__ == "__main__":
-    main(tight="--tight" in sys.argv, extra="--extra" in sys.argv)
+    main(tight="--tight" in sys.argv, extra="--extra" in sys.argv, bl="--bl" in sys.argv)
