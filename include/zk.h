@@ -78,7 +78,8 @@ enum {
 /* BiCGStab(l) (Sleijpen & Fokkema 1993), the paper's "P-BiCGSTAB parametered (l)" / P-BiCGSTAB(8)
  * without preconditioner (T9/T10): method code ZK_BICGSTAB_L(l), 1 <= l <= 8.  One iteration
  * (iters, hist[j]) is one outer cycle of l BiCG steps + the l-dimensional minimal-residual step,
- * 2l SpMVs; the BiCG part also tests ||r||/||b|| after every step.  One GPU (no comm handle). */
+ * 2l SpMVs; the BiCG part also tests ||r||/||b|| after every step.  Row-partitioned too: the Gram
+ * totals ((l+1)² doubles) are allreduced and every rank solves the same l×l system. */
 #define ZK_BICGSTAB_L(l) (16 + (l))
 enum {
     ZK_CONVERGED = 0, ZK_MAXIT = 1, ZK_BREAKDOWN_RHO = 2, ZK_BREAKDOWN_SIGMA = 3,
@@ -241,7 +242,7 @@ zk_status zk_zaxmy(int64_t n, const zk_z* x, zk_z* y, zk_stream s);
  *            ρ = ⟨r̃,w⟩ ≈ 0 → BREAKDOWN_RHO; hist[j] is the quasi-residual bound τ_m·sqrt(m+1)/||b||
  *            after the second half step m = 2j, or after the first m = 2j−1 when that converges)
  *            or ZK_BICGSTAB_L(l) (γ = ⟨r̃,Aû⟩ ≈ 0 → BREAKDOWN_SIGMA, ρ ≈ 0 → BREAKDOWN_RHO, a singular
- *            l×l minimal-residual system or ω ≈ 0 → BREAKDOWN_OMEGA; ZK_ERR_UNSUPPORTED with a comm).
+ *            l×l minimal-residual system or ω ≈ 0 → BREAKDOWN_OMEGA).
  * b          device zk_z[n_rows]; must not alias x.
  * x0         device zk_z[n_rows] initial guess, or NULL for zero; may alias x.
  * tol        stop when the recurrence residual ||r_j||/||b|| <= tol (BiCGStab also tests the

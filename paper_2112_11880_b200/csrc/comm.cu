@@ -28,7 +28,7 @@
 
 namespace zk {
 constexpr int kLocalMaxRanks = 16;
-constexpr int kLocalMaxRed = 64;  // doubles per local allreduce
+constexpr int kLocalMaxRed = 128;  // doubles per local allreduce (BiCGStab(8)'s Gram totals: 81)
 
 struct LocalOp {
     bool send;
@@ -155,7 +155,7 @@ zk_status comm_allreduce_sum(zk_comm_s* c, double* buf, int count, cudaStream_t 
         pp.p[q] = (const double*)g->ptr[q];
         if (q != c->rank) ZK_CUDA(cudaStreamWaitEvent(s, g->ev_ready[q], 0));
     }
-    local_sum_kernel<<<1, 64, 0, s>>>(pp, g->n, count, c->tmp);
+    local_sum_kernel<<<1, kLocalMaxRed, 0, s>>>(pp, g->n, count, c->tmp);
     ZK_CUDA(cudaGetLastError());
     ZK_TRY(local_retire(c, s));
     ZK_CUDA(cudaMemcpyAsync(buf, c->tmp, sizeof(double) * count, cudaMemcpyDeviceToDevice, s));

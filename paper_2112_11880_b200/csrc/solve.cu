@@ -71,6 +71,7 @@ struct SolveCtx {
     int use_cond;
     int dist;                 // multi-GPU: last blocks publish red[] for an NCCL allreduce
     double red[kMaxRed];
+    double redg[96];          // multi-GPU BiCGStab(ℓ): the Gram totals (≤ 81 doubles) for the allreduce
     int bodies;               // loop bodies executed (counts launches for zk_solve_info)
     // in-loop kernel timers (device global timer): per class, min block start of the running
     // launch, summed durations and launch counts (zk_solve_info.kernel_ms)
@@ -1557,8 +1558,17 @@ __global__ void __launch_bounds__(kBlock, 1) bl_gram(SolveCtx* c, VecSet P) {
         const unsigned long long st = atomicExch(&c->t0[timer_of(S_G_BL)], ~0ull);
         c->tsum[timer_of(S_G_BL)] += gtimer() - st;
         c->tcnt[timer_of(S_G_BL)] += 1;
-        fin_gram_bl<L>(c, tot);
+        if (c->dist) {  // multi-GPU: the rank's totals go to redg for the allreduce + fin_gram_kernel
+            for (int k = 0; k < ND; k++) c->redg[k] = tot[k];
+        } else {
+            fin_gram_bl<L>(c, tot);
+        }
     }
+}
+template <int L>
+__global__ void fin_gram_kernel(SolveCtx* c) {
+    if (c->done) return;
+    fin_gram_bl<L>(c, c->redg);
 }
 
 template <int L>
@@ -1614,6 +1624,19 @@ static BlKernel bl_gram_of(int L) {
         case 6: return bl_gram<6>;
         case 7: return bl_gram<7>;
         default: return bl_gram<8>;
+    }
+}
+using FinKernel = void (*)(SolveCtx*);
+static FinKernel fin_gram_of(int L) {
+    switch (L) {
+        case 1: return fin_gram_kernel<1>;
+        case 2: return fin_gram_kernel<2>;
+        case 3: return fin_gram_kernel<3>;
+        case 4: return fin_gram_kernel<4>;
+        case 5: return fin_gram_kernel<5>;
+        case 6: return fin_gram_kernel<6>;
+        case 7: return fin_gram_kernel<7>;
+        default: return fin_gram_kernel<8>;
     }
 }
 static BlKernel bl_u_of(int L) {
@@ -2810,10 +2833,12 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             for (int q = hc.ell + 1; q <= kMaxEll; q++) P.r[q] = P.u[q] = nullptr;
             for (int j = 0; j < hc.ell; j++) {
                 ZK_TRY(launch_loop(pdl, bl_b1, vec_grid(A, (const void*)bl_b1), 0, s, dc, P, j));
-                if (split) {
+                if (split) {  // (distributed: always — interior / boundary launches around û_j's halo)
                     auto kf = bl_s1<W, MODE, false>;
-                    const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
-                    ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A, P, j));
+                    ZK_TRY(loop_spmv(A, hc.A, P.u[j], s, [&](const CsrDev& a, bool is_part) -> zk_status {
+                        const LaunchCfg L = is_part ? spmv_cfg_part(A, (const void*)kf, a) : spmv_cfg(A, (const void*)kf, W, MODE);
+                        return launch_loop(pdl, kf, L.grid, L.smem, s, dc, a, P, j);
+                    }));
                     auto kr = bl_r<S_S1_BL>;
                     ZK_TRY(launch_loop(pdl, kr, vec_grid(A, (const void*)kr), 0, s, dc, (const double2*)P.u[j + 1]));
                 } else {
@@ -2821,18 +2846,24 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
                     const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
                     ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A, P, j));
                 }
+                if (dist) ZK_TRY((dist_finish<S_S1_BL>(A, dc, 3, s)));
                 ZK_TRY(launch_loop(pdl, bl_b2, vec_grid(A, (const void*)bl_b2), 0, s, dc, P, j));
+                if (dist) ZK_TRY((dist_finish<S_B2_BL>(A, dc, 1, s)));
                 if (j < hc.ell - 1 && !split) {
                     auto kf = bl_s2<W, MODE, true>;
                     const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
                     ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A, P, j, 1));
                 } else {
                     auto kf = bl_s2<W, MODE, false>;
-                    const LaunchCfg L = spmv_cfg(A, (const void*)kf, W, MODE);
-                    ZK_TRY(launch_loop(pdl, kf, L.grid, L.smem, s, dc, hc.A, P, j, j < hc.ell - 1 ? 1 : 0));
+                    const int stamp = j < hc.ell - 1 ? 1 : 0;
+                    ZK_TRY(loop_spmv(A, hc.A, P.r[j], s, [&](const CsrDev& a, bool is_part) -> zk_status {
+                        const LaunchCfg L = is_part ? spmv_cfg_part(A, (const void*)kf, a) : spmv_cfg(A, (const void*)kf, W, MODE);
+                        return launch_loop(pdl, kf, L.grid, L.smem, s, dc, a, P, j, stamp);
+                    }));
                     if (j < hc.ell - 1) {
                         auto kr = bl_r<S_S2_BL>;
                         ZK_TRY(launch_loop(pdl, kr, vec_grid(A, (const void*)kr), 0, s, dc, (const double2*)P.r[j + 1]));
+                        if (dist) ZK_TRY((dist_finish<S_S2_BL>(A, dc, 3, s)));
                     }
                 }
             }
@@ -2841,8 +2872,14 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             const int gcap = kMaxRed * kMaxGrid / bl_nd(hc.ell);  // partials [ND][grid]
             if (gg > gcap) gg = gcap;
             ZK_TRY(launch_loop(pdl, kg, gg, 0, s, dc, P));
+            if (dist) {  // the Gram totals over the ranks, then the (replicated) Cholesky
+                ZK_TRY(dist_allreduce_ctx(A, dc->redg, bl_nd(hc.ell), s));
+                fin_gram_of(hc.ell)<<<1, 1, 0, s>>>(dc);
+                ZK_CUDA(cudaGetLastError());
+            }
             const BlKernel ku = bl_u_of(hc.ell);
             ZK_TRY(launch_loop(pdl, ku, vec_grid(A, (const void*)ku), 0, s, dc, P));
+            if (dist) ZK_TRY((dist_finish<S_U_BL>(A, dc, 3, s)));
         } else if (method == ZK_TFQMR) {
             ZK_TRY(launch_loop(pdl, t1_tfqmr, vec_grid(A, (const void*)t1_tfqmr), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_T1_TFQMR>(A, dc, 1, s)));
@@ -3050,8 +3087,6 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     if (!A || !b || !x || !iters || !resid_hist || !workspace) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
     int method, ell;
     if (!decode_method(code, &method, &ell)) return fail(ZK_ERR_INVALID_VALUE, "unknown method");
-    if (method == kBiCGStabL && A->dist)
-        return fail(ZK_ERR_UNSUPPORTED, "BiCGStab(l) runs on one GPU (no comm handle)");
     const bool jacobi = method == ZK_BICGSTAB_JACOBI;
     if (jacobi) {
         ZK_TRY(jacobi_prepare(A, (cudaStream_t)stream));  // A·M⁻¹ built once, cached in the handle
@@ -3225,7 +3260,8 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         ZK_TRY(kind == 0   ? dist_finish<S_INIT_BICG>(A, dc, 4, s)
                : kind == 1 ? dist_finish<S_INIT_CG>(A, dc, 4, s)
                : kind == 3 ? dist_finish<S_INIT_COCG>(A, dc, 4, s)
-                           : dist_finish<S_INIT_TFQMR>(A, dc, 4, s));
+               : kind == 4 ? dist_finish<S_INIT_TFQMR>(A, dc, 4, s)
+                           : dist_finish<S_INIT_BL>(A, dc, 4, s));
     if (method == ZK_TFQMR) {  // u1 = v = A y1 and σ = ⟨r̃, v⟩ → α for iteration 1
         if (A->dist) ZK_TRY(dist_halo(A, hc.y1, s));
         ZK_TRY(with_spmv(A, [&](auto wc, auto mc) -> zk_status {
@@ -3313,7 +3349,8 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         if (split_reductions(A) && !split_tail(A))  // the separate reduction / update passes
             per_body += method == ZK_BICGSTAB ? 2 : (method == ZK_CG || method == ZK_COCG) ? 1
                         : method == ZK_TFQMR ? 2 : method == kBiCGStabL ? 2 * ell - 1 : 0;
-        const int fins = A->dist ? (method == ZK_BICGSTAB ? 4 : method == ZK_TFQMR ? 3 : 2) : 0;  // dist: 1-thread finish kernels
+        const int fins = !A->dist ? 0 : method == ZK_BICGSTAB ? 4 : method == ZK_TFQMR ? 3
+                       : method == kBiCGStabL ? 3 * ell + 1 : 2;  // dist: 1-thread finish kernels
         const int pre = method == ZK_TFQMR ? (A->dist ? 2 : 1) : 0;                               // TFQMR: K0 (+ its finish)
         // mode 5: set_ctx + init (+ TFQMR's K0) + the cluster kernel (+ Jacobi: x = M⁻¹u and k_true)
         info->gpu_launches = mode == 5 ? (fused_init ? 1 : 3) + pre + (jacobi ? 2 : 0)
@@ -3321,7 +3358,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         if (A->dist) {  // + per SpMV: pack kernel, second (boundary) launch; + per allreduce: LOCAL sum kernel
             int per_spmv = 0, per_red = 0;
             dist_launch_extra(A, &per_spmv, &per_red);
-            const int spmv_it = (method == ZK_BICGSTAB || method == ZK_TFQMR) ? 2 : 1;
+            const int spmv_it = (method == ZK_BICGSTAB || method == ZK_TFQMR) ? 2 : method == kBiCGStabL ? 2 * ell : 1;
             const int red_it = fins;
             const int init_spmv = (x0 ? 1 : 0) + (method == ZK_TFQMR ? 1 : 0) + 1;  // + final true residual
             const int init_red = 2 + (method == ZK_TFQMR ? 1 : 0);

@@ -10,7 +10,8 @@ Bars (iterations are outer cycles of 2ℓ SpMVs):
     rounding (the orders already differ by 9e-5 at ℓ = 8);
   * solutions to 1e-6 relative (C1/C2/T0); true residual ≤ 10·tol (S:388);
   * C4 (bench shape, ℓ = 8): DST-I closed form within 2κ·tol, first cycle's residual vs the oracle;
-  * outcomes match the oracle's; loop modes bitwise identical; a comm handle → ZK_ERR_UNSUPPORTED."""
+  * outcomes match the oracle's; loop modes bitwise identical; the row-partitioned path on a 1-rank
+    communicator is bitwise the local split schedule (multi-rank parity: test_gpu_dist_local.py)."""
 import numpy as np
 import pytest
 import torch
@@ -147,15 +148,52 @@ def test_bicgstab_l_deterministic_and_ell_switch():
     assert r8["iters"] == oracle.bicgstab_l(m, b, ell=8)["iters"]
 
 
-def test_bicgstab_l_rejects_comm():
-    m = gen.make_matrix("C1")
+def test_bicgstab_l_single_rank_comm(monkeypatch):
+    """The row-partitioned BiCGStab(ℓ) path (halo before every S1/S2 SpMV, allreduce of each
+    reduction point and of the Gram totals, replicated Cholesky) on a 1-rank NCCL communicator
+    is bitwise the local split-schedule solve (same kernels, identity allreduces)."""
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
+    monkeypatch.setenv("ZK_LOOP_MODE", "3")
+    monkeypatch.setenv("ZK_SPLIT_RED", "1")
+    base = gpu_solve(m, b, 4, tol=1e-8)
+    monkeypatch.delenv("ZK_LOOP_MODE")
     comm = zk.Comm(zk.Comm.unique_id(), 1, 0, 0)
     A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"], comm=comm, row_begin=0)
-    with pytest.raises(zk.ZkError) as e:
-        zk.solve(A, cuda(gen.make_rhs(m)), method="bicgstab_l", ell=2)
-    assert e.value.code == -10
+    r = zk.solve(A, cuda(b), method="bicgstab_l", ell=4)
+    assert r["loop_mode"] == 3 and r["iters"] == base["iters"]
+    assert np.array_equal(r["x"].cpu().numpy(), base["x"]) and np.array_equal(r["hist"], base["hist"])
     A.close()
     comm.close()
+
+
+@pytest.mark.parametrize("ell", [2, 8])
+def test_bicgstab_l_c4_vs_golden(ell):
+    """C4 (8M rows) against the oracle's full BiCGStab(ℓ) solves (tests/golden/
+    c4_oracle_bicgstab_l.json, tools/make_golden_c4.py --bl; seq / rev / block-256 orders): cycle
+    count within [0.95·min, 1.05·max] of the orders, the first 3 cycles' history to HTOL[ℓ], and
+    the seeded x sample within 4× the orders' own spread (and within 2κ·tol)."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c4_oracle_bicgstab_l.json")) as f:
+        G = json.load(f)
+    spec = gen.CONFIGS["C4"]
+    m = gen.make_matrix(spec)
+    b = gen.make_rhs(m)
+    A = zk.csr_create(cuda(m["row_ptr"]), cuda(m["col_idx"]), cuda(m["values"]), m["n"], borrow=True)
+    r = zk.solve(A, cuda(b), tol=1e-8, maxit=300, method="bicgstab_l", ell=ell)
+    refs = {o: G["results"][f"bicgstab_l{ell}/{o}"] for o in ("seq", "rev", "block256")}
+    its = [q["iters"] for q in refs.values()]
+    assert r["status"] == "CONVERGED" and 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    h0 = np.array(refs["seq"]["hist"])
+    assert np.max(np.abs(r["hist"][:4] - h0[:4]) / h0[:4]) <= htol(ell)
+
+    def xs(g):
+        return np.array(g["x_sample_re"]) + 1j * np.array(g["x_sample_im"])
+    x0 = xs(refs["seq"])
+    spread = max(relerr(xs(refs[o]), x0) for o in ("rev", "block256"))
+    got = r["x"].cpu().numpy()[np.array(G["sample_idx"])]
+    assert relerr(got, x0) <= max(4 * spread, 1e-9) and relerr(got, x0) <= 2 * cf.box_kappa(spec, gen.ETA) * 1e-8
 
 
 def test_bicgstab_l8_c4_full_size():

@@ -285,17 +285,34 @@ def test_local_validation_agreement():
     assert "out of range" in res[1], res
 
 
-def test_local_bicgstab_l_unsupported():
-    m = gen.make_matrix("C1")
-    off = offsets(m, 2)
+@pytest.mark.parametrize("ell", [1, 2, 4])
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_local_bicgstab_l(nranks, ell):
+    """BiCGStab(ℓ) row-partitioned: halo before every S1/S2 SpMV, each reduction point and the
+    (ℓ+1)² Gram totals allreduced, the Cholesky replicated on every rank; against the oracle's
+    envelope, the history to HTOL[ℓ] and x to 1e-6."""
+    from tests.test_gpu_bicgstab_l import HTOL
+    m = gen.make_matrix("C2")
+    b = gen.make_rhs(m)
 
     def fn(r, comm, s):
+        off = offsets(m, nranks)
         A = dist_csr(m, off, r, comm, s)
-        with pytest.raises(zk.ZkError):
-            zk.solve(A, cuda(gen.make_rhs(m)[off[r]:off[r + 1]]), method="bicgstab_l", ell=2)
-        return True
+        lo, hi = int(off[r]), int(off[r + 1])
+        out = zk.solve(A, cuda(b[lo:hi]), tol=1e-8, method="bicgstab_l", ell=ell)
+        out["x"] = out["x"].cpu().numpy()
+        out["n_halo"] = A.info["n_halo"]
+        return out
 
-    assert all(run_ranks(2, fn))
+    res = run_ranks(nranks, fn)
+    x = _check_ranks(res, nranks)
+    refs = [oracle.bicgstab_l(m, b, tol=1e-8, ell=ell, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    r = res[0]
+    assert r["status"] == "CONVERGED" and 0.95 * min(its) <= r["iters"] <= 1.05 * max(its), (r["iters"], its)
+    k = min(6, r["iters"], refs[0]["iters"]) + 1
+    assert np.max(np.abs(r["hist"][:k] - refs[0]["hist"][:k]) / refs[0]["hist"][:k]) <= HTOL[ell]
+    assert relerr(x, refs[0]["x"]) <= 1e-6 and r["true_relres"] <= 1e-7
 
 
 def test_local_c4_zslabs_two_ranks_vs_golden():
