@@ -52,6 +52,9 @@ def args_():
     p.add_argument("--no-methods", action="store_true",
                    help="skip the per-method C4 solves (CG, Jacobi-BiCGStab, COCG, TFQMR, BiCGStab(2), BiCGStab(8))")
     p.add_argument("--no-blas1", action="store_true", help="skip the BLAS-1 GB/s sweep")
+    p.add_argument("--local-ranks", type=int, default=0,
+                   help="run the row-partitioned path on ONE GPU with N in-process ranks (LOCAL transport, "
+                        "threads): the C5 z-slab split of the strong-scaling run, timed as max over ranks")
     p.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                    help="N > 1: strong = the fixed C5 system (400^3, 64M rows; BASELINE.json configs[4]) "
                         "split into z-slabs; weak = a 200x200x(200N) box, 8M rows per GPU")
@@ -212,10 +215,88 @@ def run_reference(a):
 
 
 # ---------------------------------------------------------------- the zk arm
+def run_local_ranks(a):
+    """The strong-scaling partition (C5 split into N z-slabs) on ONE GPU through the LOCAL transport:
+    N host threads, one stream and one rank each, halo exchange overlapped with the interior rows,
+    rank-order allreduces.  Not a scaling number (the ranks share one GPU's HBM): it measures the
+    row-partitioned loop at full size against the same system on one rank."""
+    import threading
+
+    import torch
+
+    import gen
+    from paper_2112_11880_b200 import metrics as M
+    from paper_2112_11880_b200 import zk
+    N = a.local_ranks
+    cfg = "C5" if a.config == "C4" else a.config
+    spec = gen.CONFIGS[cfg]
+    plane = spec.nx * spec.ny
+    group = zk.LocalGroup(N)
+    out, errs = [None] * N, [None] * N
+    ready = threading.Barrier(N)
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                comm = zk.Comm.local(group, r, 0)
+                z0, z1 = r * spec.nz // N, (r + 1) * spec.nz // N
+                mat = gen.make_matrix(spec, row_range=(z0 * plane, z1 * plane))
+                b = torch.from_numpy(gen.make_rhs(mat)).cuda()
+                A = zk.csr_create(mat["row_ptr"], mat["col_idx"], mat["values"], spec.n, comm=comm,
+                                  row_begin=mat["row_begin"], stream=st)
+                n, nnz = len(mat["row_ptr"]) - 1, mat["nnz"]
+                del mat
+                ws = zk.alloc_workspace(A, "bicgstab", a.maxit)
+                x = torch.empty_like(b)
+                for _ in range(max(a.warmup, 1)):
+                    zk.solve(A, b, None, a.tol, a.maxit, "bicgstab", x=x, workspace=ws, stream=st)
+                st.synchronize()
+                ready.wait()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                res = [zk.solve(A, b, None, a.tol, a.maxit, "bicgstab", x=x, workspace=ws, stream=st)
+                       for _ in range(a.steps)]
+                e1.record(st)
+                st.synchronize()
+                out[r] = dict(ms=e0.elapsed_time(e1), iters=res[-1]["iters"], n=n, nnz=nnz,
+                              n_halo=A.info["n_halo"], interior=A.info["interior_rows"],
+                              status=res[-1]["status"], true_relres=res[-1]["true_relres"])
+                A.close()
+            comm.close()
+        except BaseException as e:  # noqa: BLE001
+            errs[r] = e
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(N)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    group.close()
+    for e in errs:
+        if e is not None:
+            raise e
+    ms = max(q["ms"] for q in out)
+    iters = out[0]["iters"]
+    byts = sum(step_bytes(q["n"], q["nnz"], q["iters"]) for q in out) * a.steps
+    line = {"metric": METRIC, "value": byts / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": 1, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "none (one GPU)",
+            "dtype": "complex128 (f64)", "data": "synthetic",
+            "config": {"workload": f"{cfg}: {spec.nx}x{spec.ny}x{spec.nz} (n={spec.n:,}) split into {N} z-slabs",
+                       "parallelism": f"LOCAL transport: {N} in-process ranks (threads) on one GPU, halo overlapped"},
+            "bicgstab": {"iters": iters, "status": out[0]["status"], "ms_per_iteration": ms / a.steps / iters,
+                         "true_relres": out[0]["true_relres"]},
+            "ranks": [{k: q[k] for k in ("n", "nnz", "n_halo", "interior", "ms", "iters")} for q in out]}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     a = args_()
     if a.impl == "reference":
         return run_reference(a)
+    if a.local_ranks > 1:
+        return run_local_ranks(a)
 
     import torch
     import torch.distributed as dist
