@@ -3346,9 +3346,12 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         info->solve_ms = ms;
         info->loop_mode = mode;
         int per_body = method == ZK_BICGSTAB ? 5 : method == ZK_TFQMR ? 4 : method == kBiCGStabL ? 4 * ell + 2 : 3;
-        if (split_reductions(A) && !split_tail(A))  // the separate reduction / update passes
-            per_body += method == ZK_BICGSTAB ? 2 : (method == ZK_CG || method == ZK_COCG) ? 1
-                        : method == ZK_TFQMR ? 2 : method == kBiCGStabL ? 2 * ell - 1 : 0;
+        if (split_reductions(A)) {  // the separate reduction / update passes
+            if (method == kBiCGStabL)  // (no tail variant: a warp-reduced S1/S2 measured slower at C4,
+                per_body += 2 * ell - 1;  // BiCGStab(8) 16.86 → 17.20 ms per cycle)
+            else if (!split_tail(A))
+                per_body += method == ZK_BICGSTAB ? 2 : (method == ZK_CG || method == ZK_COCG) ? 1 : 2;
+        }
         const int fins = !A->dist ? 0 : method == ZK_BICGSTAB ? 4 : method == ZK_TFQMR ? 3
                        : method == kBiCGStabL ? 3 * ell + 1 : 2;  // dist: 1-thread finish kernels
         const int pre = method == ZK_TFQMR ? (A->dist ? 2 : 1) : 0;                               // TFQMR: K0 (+ its finish)

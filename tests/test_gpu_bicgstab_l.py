@@ -214,8 +214,9 @@ def test_bicgstab_l8_c4_full_size():
 @pytest.mark.parametrize("split", ["0", "1"])
 @pytest.mark.parametrize("ell", [1, 3])
 def test_bicgstab_l_split_schedule(split, ell, monkeypatch):
-    """Both BiCGStab(ℓ) schedules (fused SpMV reductions; split: SpMV stores, a vector pass
-    reduces — the default from 2^20 rows) against the oracle on C2."""
+    """Both BiCGStab(ℓ) schedules (fused SpMV reductions; split: SpMV stores, a vector pass reduces —
+    the default from 2^18 rows) against the oracle on C2 in the WHILE-graph loop."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "1")  # the WHILE-graph kernels (C2 would take the cluster solver)
     monkeypatch.setenv("ZK_SPLIT_RED", split)
     m = gen.make_matrix("C2")
     b = gen.make_rhs(m)
