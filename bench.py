@@ -450,11 +450,13 @@ def main():
     read_gbs = 16.0 * (1 << 28) * 10 / (q0.elapsed_time(q1) * 1e-3) / 1e9
     del big
     roofline["read_stream_gbs"] = read_gbs
+    roofline["frac_of_8tbs_spec"] = spmv_gbs / 8000.0  # also against the 8.0 TB/s spec
     nt = ncu_traffic(a.config)
     if nt and nt.get("duration_us_per_launch"):
         # ncu-measured DRAM GB/s of the same kernel (cold-cache, serialised launches)
         roofline["ncu_dram_gbs"] = nt["spmv_dram_bytes_per_launch"] / (nt["duration_us_per_launch"] * 1e-6) / 1e9
         roofline["ncu_dram_frac"] = roofline["ncu_dram_gbs"] / peak
+        roofline["ncu_dram_frac_of_8tbs_spec"] = roofline["ncu_dram_gbs"] / 8000.0
         roofline["ncu_source"] = nt.get("source")
     roofline["frac_of_read_stream"] = spmv_gbs / read_gbs
     spmv = {"us": spmv_us, "us_median": per[len(per) // 2], "us_min": per[0], "reps": a.spmv_reps,
@@ -462,6 +464,7 @@ def main():
             "frac_of_read_stream": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9 / read_gbs,
             "gflops": M.spmv_flops(nnz) / (spmv_us * 1e-6) / 1e9,
             "frac_of_peak": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9 / peak,
+            "frac_of_8tbs_spec": M.spmv_bytes(n, nnz) / (spmv_us * 1e-6) / 1e9 / 8000.0,
             "lanes_per_row": A.info["lanes_per_row"],
             "mapping": {0: "CSR sub-warp",
                         3: "sliced ELL (SELL-32 device copy)"}[A.info["spmv_mode"]],
