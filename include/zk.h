@@ -18,7 +18,9 @@
  *    breakdowns, ...) are not errors: they come back in zk_solve_info.
  *  - A zk_csr handle owns reduction scratch: do not use one handle on two
  *    streams concurrently.  The standalone reductions (zk_zdotc, zk_dznrm2)
- *    share one per-device scratch: do not run them concurrently on two streams.
+ *    use a scratch per (device, stream), allocated on the first call on that
+ *    stream (128 KB, kept for the process lifetime): calls on different streams
+ *    (or host threads) may run concurrently; calls on one stream are serialised.
  *  - No CPU fallback: every call runs in libzk's sm_100a kernels; without a
  *    usable device the calls fail with ZK_ERR_CUDA.
  */
