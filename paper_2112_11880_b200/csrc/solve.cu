@@ -94,6 +94,17 @@ __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Opposite sweeps: a streaming kernel of a solver loop that walks its rows last to
+// first starts on the rows its predecessor (a first-to-last sweep) touched last — the lines still
+// in L2 (126 MB against 128 MB per vector at C4; a same-direction sweep finds the oldest lines of
+// the previous sweep evicted first).  Fixed per kernel: BiCGStab K2 and K4, CG/COCG K2 and
+// TFQMR T2/T4 run backwards, the rest forwards (an odd kernel count per iteration leaves one
+// same-direction boundary: BiCGStab K5 → K1, CG K3 → K1).  -DZK_SWEEP=0 makes every sweep forward.
+#ifndef ZK_SWEEP
+#define ZK_SWEEP 1
+#endif
+constexpr bool kSweep = ZK_SWEEP != 0;
+
 __device__ __forceinline__ void set_cond(SolveCtx* c) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         c->bodies += 1;
@@ -1023,7 +1034,7 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_bicg(SolveCt
     if (c->done) return;
     stamp_start<S_K1_BICG>(c);
     const double2* p = c->p;
-    if constexpr (SPLIT == 3) {
+        if constexpr (SPLIT == 3) {
         WarpAcc<EpiK1Bicg> e(c);
         spmv_any<W, MODE>(A, p, e);
     } else if constexpr (SPLIT == 2) {
@@ -1054,7 +1065,7 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_bicg(SolveCtx* c) {
     if (c->done) return;
     stamp_start<S_K2_BICG>(c);
     OpK2Bicg op(c);
-    vec_body(c->A.n_rows, op);
+    vec_body<kSweep>(c->A.n_rows, op);  // ←
 }
 template <int W, int MODE, int SPLIT>
 __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k3_bicg(SolveCtx* c, const CsrDev A) {
@@ -1062,7 +1073,7 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k3_bicg(SolveCt
     if (c->done) return;
     stamp_start<S_K3_BICG>(c);
     const double2* s = c->s;
-    if constexpr (SPLIT == 3) {
+        if constexpr (SPLIT == 3) {
         WarpAcc<EpiK3Bicg> e(c);
         spmv_any<W, MODE>(A, s, e);
     } else if constexpr (SPLIT == 2) {
@@ -1082,7 +1093,7 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k4_bicg(SolveCtx* c) {
     if (c->done && !half) return;
     if (!half) stamp_start<S_K4_BICG>(c);
     OpK4Bicg op(c, half);
-    vec_body(c->A.n_rows, op);
+    vec_body<kSweep>(c->A.n_rows, op);  // ←
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k5_bicg(SolveCtx* c) {
     pdl_enter();
@@ -1100,7 +1111,7 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cocg(SolveCt
     if (c->done) return;
     stamp_start<S_K1_COCG>(c);
     const double2* p = c->p;
-    if constexpr (SPLIT == 3) {
+        if constexpr (SPLIT == 3) {
         WarpAcc<EpiK1Cocg> e(c);
         spmv_any<W, MODE>(A, p, e);
     } else if constexpr (SPLIT == 2) {
@@ -1119,7 +1130,7 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_cocg(SolveCtx* c) {
     if (c->done) return;
     stamp_start<S_K2_COCG>(c);
     OpK2Cocg op(c);
-    vec_body(c->A.n_rows, op);
+    vec_body<kSweep>(c->A.n_rows, op);  // ←
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k3_cocg(SolveCtx* c) {
     pdl_enter();
@@ -1135,7 +1146,7 @@ __global__ void __launch_bounds__(kBlock, spmv_min_blocks(MODE)) k1_cg(SolveCtx*
     if (c->done) return;
     stamp_start<S_K1_CG>(c);
     const double2* p = c->p;
-    if constexpr (SPLIT == 3) {
+        if constexpr (SPLIT == 3) {
         WarpAcc<EpiK1Cg> e(c);
         spmv_any<W, MODE>(A, p, e);
     } else if constexpr (SPLIT == 2) {
@@ -1161,7 +1172,7 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k2_cg(SolveCtx* c) {
     if (c->done) return;
     stamp_start<S_K2_CG>(c);
     OpK2Cg op(c);
-    vec_body(c->A.n_rows, op);
+    vec_body<kSweep>(c->A.n_rows, op);  // ←
 }
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) k3_cg(SolveCtx* c) {
     pdl_enter();
@@ -1184,7 +1195,7 @@ __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) t1_tfqmr(SolveCtx* c) {
     if (c->done) return;
     stamp_start<S_T1_TFQMR>(c);
     OpT1Tfqmr op(c);
-    vec_body(c->A.n_rows, op);
+    vec_body(c->A.n_rows, op);  // TFQMR: an even kernel count, fixed directions T1 →, T2 ←, T3 →, T4 ←
 }
 template <int W, int MODE, int SPLIT>
 __global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t2_tfqmr(SolveCtx* c, const CsrDev A) {
@@ -1210,7 +1221,7 @@ __global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t2_tfqmr(SolveCtx* c, cons
     const double2* y2 = c->y2;
     if constexpr (SPLIT == 2) {
         EpiStoreTail<OpT2bTfqmr> e(c->u2, c);
-        spmv_any<W, MODE>(A, y2, e);
+        spmv_any<W, MODE, kSweep>(A, y2, e);  // ←
     } else if constexpr (SPLIT == 1) {
         EpiStore e(c->u2);
         spmv_any<W, MODE>(A, y2, e);
@@ -1253,7 +1264,7 @@ __global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t4_tfqmr(SolveCtx* c, cons
         const double2* y1 = c->y1;
         if constexpr (SPLIT == 2) {
             EpiStoreTail<OpT4bTfqmr> e(c->u1, c);
-            spmv_any<W, MODE>(A, y1, e);
+            spmv_any<W, MODE, kSweep>(A, y1, e);  // ←
         } else if constexpr (SPLIT == 1) {
             EpiStore e(c->u1);
             spmv_any<W, MODE>(A, y1, e);

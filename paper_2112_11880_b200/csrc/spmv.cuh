@@ -180,7 +180,9 @@ struct sell_ordered {
     template <class T> static constexpr bool get(...) { return false; }
     static constexpr bool value = get<E>(nullptr);
 };
-template <class Epi, int LP = ZK_SELL_LP>
+// REV: walk the slices last to first (opposite sweeps: the kernel starts on the rows
+// its predecessor in the solver loop touched last, still in L2)
+template <class Epi, int LP = ZK_SELL_LP, bool REV = false>
 __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
     constexpr int U = ZK_SELL_U;
     constexpr int KA = Epi::K > 0 ? Epi::K : 1;
@@ -207,7 +209,10 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
     // logical slices t ∈ [0, sl_cnt) → physical slice phys(t) (the whole matrix, or one part of a
     // distributed SpMV split into interior / boundary slices, CsrDev)
     const int n_sl = A.sl_cnt;
-    auto phys = [&](int t) { return A.sl_lo + t + (t >= A.sl_gap_at ? A.sl_gap : 0); };
+    auto phys = [&](int t) {
+        const int u = REV ? n_sl - 1 - t : t;
+        return A.sl_lo + u + (u >= A.sl_gap_at ? A.sl_gap : 0);
+    };
     const int nw = gridDim.x * kWarps;
     int t = blockIdx.x * kWarps + (threadIdx.x >> 5);
     int64_t base = 0;
@@ -313,13 +318,14 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
 
 // The SpMV body of a mapping: MODE 3 sliced ELL (the default), MODE 0 CSR sub-warp rows
 // (matrices whose SELL padding would exceed 10 %).
-template <int W, int MODE, class Epi>
+// (REV: SELL only; the CSR sub-warp body keeps its order)
+template <int W, int MODE, bool REV = false, class Epi>
 __device__ __forceinline__ void spmv_any(const CsrDev& A, const double2* __restrict__ x, Epi& epi) {
     static_assert(MODE == 0 || MODE == 3, "SpMV mappings: 0 (CSR sub-warp) and 3 (SELL-32)");
     if constexpr (sell_tail<Epi>::value && MODE != 3) {
         __trap();  // tail epilogues exist only in the SELL body (the host never launches this)
     } else if constexpr (MODE == 3) {
-        spmv_body_sell(A, x, epi);
+        spmv_body_sell<Epi, ZK_SELL_LP, REV>(A, x, epi);
     } else {
         spmv_body<W>(A, x, epi);
     }
@@ -331,7 +337,8 @@ __host__ __device__ constexpr int spmv_min_blocks(int mode) { return mode == 3 ?
 // Grid-stride elementwise body with U elements in flight per thread.
 //   Op::K, Op::In, In load(int64_t i), void apply(int64_t i, const In&, double (&acc)[K]), finish(acc)
 
-template <class Op>
+// REV: element i is processed as n − 1 − i (a last-to-first sweep; warps stay coalesced)
+template <bool REV = false, class Op>
 __device__ __forceinline__ void vec_body(int64_t n, Op& op) {
     constexpr int U = vec_unroll<Op>::value;  // elements in flight per thread (Op::U, default 4)
     constexpr int KA = Op::K > 0 ? Op::K : 1;
@@ -344,12 +351,12 @@ __device__ __forceinline__ void vec_body(int64_t n, Op& op) {
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int64_t i = base + u * kBlock;
-            if (i < n) in[u] = op.load(i);
+            if (i < n) in[u] = op.load(REV ? n - 1 - i : i);
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int64_t i = base + u * kBlock;
-            if (i < n) op.apply(i, in[u], acc);
+            if (i < n) op.apply(REV ? n - 1 - i : i, in[u], acc);
         }
     }
     op.finish(acc);

@@ -41,7 +41,7 @@ for cfg in sys.argv[1:] or ["C3"]:
                        torch.from_numpy(mg["values"]).cuda(), mg["n"])
     bg = torch.from_numpy(np.exp(1j * mg["phase"]) * gen.make_rhs(mg)).cuda()
     del m, mg
-    for meth in ("bicgstab", "cg", "tfqmr"):
+    for meth in os.environ.get("AB_METHODS", "bicgstab,cg,tfqmr").split(","):
         AA, bb = (Ag, bg) if meth == "cg" else (A, b)
         ws = zk.alloc_workspace(AA, meth, 2000)
         zk.solve(AA, bb, tol=1e-8, maxit=2000, method=meth, workspace=ws)
