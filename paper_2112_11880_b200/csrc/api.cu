@@ -6,6 +6,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "spmv.cuh"
 #include "zk_host.h"
@@ -54,6 +55,41 @@ cudaMemPool_t dev_pool(int device) {
     }
     g_pools[device] = pool;
     return pool;
+}
+
+static std::mutex g_pin_mu;
+static std::vector<std::pair<void*, size_t>> g_pin_free;  // (buffer, bytes), reused across handles
+constexpr size_t kPinMin = 64 * 1024, kPinKeep = 64;
+
+cudaError_t pinned_get(void** p, size_t bytes, size_t* got) {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        size_t best = g_pin_free.size();
+        for (size_t i = 0; i < g_pin_free.size(); i++)
+            if (g_pin_free[i].second >= bytes && (best == g_pin_free.size() || g_pin_free[i].second < g_pin_free[best].second))
+                best = i;
+        if (best < g_pin_free.size()) {
+            *p = g_pin_free[best].first;
+            *got = g_pin_free[best].second;
+            g_pin_free.erase(g_pin_free.begin() + (std::ptrdiff_t)best);
+            return cudaSuccess;
+        }
+    }
+    const size_t b = bytes > kPinMin ? bytes : kPinMin;
+    cudaError_t e = cudaMallocHost(p, b);
+    *got = e == cudaSuccess ? b : 0;
+    return e;
+}
+void pinned_put(void* p, size_t bytes) {
+    if (!p) return;
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        if (g_pin_free.size() < kPinKeep) {
+            g_pin_free.emplace_back(p, bytes);
+            return;
+        }
+    }
+    cudaFreeHost(p);
 }
 
 void handle_count(int delta) {
@@ -280,10 +316,14 @@ static zk_status csr_create_local(zk_csr_s** outA, int64_t n_rows, int64_t n_col
         if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMemcpyAsync(csr)", __FILE__, __LINE__));
     }
 
+    const bool trace = getenv("ZK_TRACE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = now();
     // ---- validation + row statistics on the device (one pass over the arrays)
     {
         ValidateOut h{~0ull, 0u}, *d = nullptr;
-        cudaError_t e = cudaMalloc(&d, sizeof(ValidateOut));
+        cudaError_t e = scratch_alloc(&d, sizeof(ValidateOut), s);
         if (e == cudaSuccess) e = cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cleanup(cuda_fail(e, "validate setup", __FILE__, __LINE__));
         if (n_rows > 0) {
@@ -295,7 +335,8 @@ static zk_status csr_create_local(zk_csr_s** outA, int64_t n_rows, int64_t n_col
         }
         if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        cudaFree(d);
+        scratch_free(d, s);
+        if (trace) fprintf(stderr, "  create: copies+validate %.2f ms\n", ms(t0, now()));
         if (e != cudaSuccess) return cleanup(cuda_fail(e, "validate", __FILE__, __LINE__));
         if (!(flags & ZK_SKIP_VALIDATE) && h.first_bad != ~0ull) {
             const long long row = (long long)(h.first_bad >> 3);
@@ -328,7 +369,12 @@ extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, 
         zk_csr_destroy(A);
         return st;
     };
+    const bool trace = getenv("ZK_TRACE") != nullptr;  // host-side phase times on stderr
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = now();
     zk_status st = csr_create_local(&A, n_rows, n_cols, nnz, row_ptr, col_idx, values, flags, comm, row_begin, s);
+    const auto t1 = now();
     if (comm) {
         // every rank learns whether any rank failed before the setup collectives (a rank that
         // returned early would leave its peers blocked in the halo-plan allgather)
@@ -346,6 +392,7 @@ extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, 
     } else if (st != ZK_OK) {
         return cleanup(st);
     }
+    const auto t2 = now();
     if (A->spmv_mode == 3) {  // after the halo renumbering: the copy holds the final column ids
         st = sell_build(A, s);
         if (st != ZK_OK) return cleanup(st);
@@ -364,13 +411,18 @@ extern "C" zk_status zk_csr_create(zk_csr* out, int64_t n_rows, int64_t n_cols, 
         cudaError_t e = cudaStreamSynchronize(s);  // the SELL fill read them
         if (e != cudaSuccess) return cleanup(cuda_fail(e, "zk_csr_create", __FILE__, __LINE__));
         dev_free(A->val, true);
+        dev_free_done();
         A->val = nullptr;
     }
+    const auto t3 = now();
     // the arrays may have come from the stream-ordered pool: usable from any stream after this
     {
         cudaError_t e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) return cleanup(cuda_fail(e, "zk_csr_create", __FILE__, __LINE__));
     }
+    if (trace)
+        fprintf(stderr, "zk_csr_create: local (alloc, copy, validate) %.2f ms, dist %.2f ms, sell %.2f ms, sync %.2f ms\n",
+                ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, now()));
     handle_count(+1);
     A->counted = true;
     *out = A;
@@ -398,16 +450,19 @@ extern "C" zk_status zk_csr_destroy(zk_csr A) {
         dev_free(A->col, true);
         dev_free(A->val, true);
     }
+    dev_free_done();
     const auto t3 = now();
     if (A->cap_stream) cudaStreamDestroy(A->cap_stream);
-    if (A->pinned) cudaFreeHost(A->pinned);
+    const auto t4 = now();
+    pinned_put(A->pinned, A->pinned_bytes);
+    const auto t5 = now();
     for (auto& e : A->ev)
         if (e) cudaEventDestroy(e);
     if (A->counted) handle_count(-1);
     delete A;
     if (trace)
-        fprintf(stderr, "zk_csr_destroy: sync %.2f ms, graphs %.2f ms, frees %.2f ms, rest %.2f ms\n", ms(t0, t1),
-                ms(t1, t2), ms(t2, t3), ms(t3, now()));
+        fprintf(stderr, "zk_csr_destroy: sync %.2f ms, graphs %.2f ms, frees %.2f ms, stream %.2f ms, pinned %.2f ms, rest %.2f ms\n",
+                ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5), ms(t5, now()));
     return ZK_OK;
 }
 
@@ -432,7 +487,7 @@ extern "C" zk_status zk_csr_update_values(zk_csr A, const zk_z* values, uint32_t
     }
     if (!(flags & ZK_SKIP_VALIDATE) && A->nnz > 0) {  // finite values (the pattern is unchanged)
         unsigned long long h = ~0ull, *d = nullptr;
-        ZK_CUDA(cudaMalloc(&d, sizeof h));
+        ZK_CUDA(scratch_alloc(&d, sizeof h, s));
         cudaError_t e = cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess) {
             nonfinite_kernel<<<grid_for(A->nnz, kBlock, A->dev.num_sms * 8), kBlock, 0, s>>>(tmp ? tmp : A->val, A->nnz, d);
@@ -440,7 +495,7 @@ extern "C" zk_status zk_csr_update_values(zk_csr A, const zk_z* values, uint32_t
         }
         if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        cudaFree(d);
+        scratch_free(d, s);
         if (e != cudaSuccess) return cuda_fail(e, "zk_csr_update_values", __FILE__, __LINE__);
         if (h != ~0ull) {
             if (tmp) dev_free(tmp);
@@ -454,6 +509,7 @@ extern "C" zk_status zk_csr_update_values(zk_csr A, const zk_z* values, uint32_t
         if (tmp) {
             cudaStreamSynchronize(s);
             dev_free(tmp, true);
+            dev_free_done();
         }
         ZK_TRY(st);
     }

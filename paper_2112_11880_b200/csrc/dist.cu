@@ -55,9 +55,9 @@ __global__ void pack_kernel(const double2* __restrict__ x, const int* __restrict
 void dist_destroy(zk_csr_s* A) {
     DistPlan* P = plan(A);
     if (!P) return;
-    cudaFree(P->d_send_idx);
-    cudaFree(P->d_sendbuf);
-    cudaFree(P->d_xg);
+    dev_free(P->d_send_idx, true);  // (zk_csr_destroy synchronised the device)
+    dev_free(P->d_sendbuf, true);
+    dev_free(P->d_xg, true);
     if (P->cs) cudaStreamDestroy(P->cs);
     if (P->ev_pack) cudaEventDestroy(P->ev_pack);
     if (P->ev_halo) cudaEventDestroy(P->ev_halo);
@@ -69,7 +69,7 @@ void dist_destroy(zk_csr_s* A) {
 zk_status dist_agree_failed(zk_comm_s* c, bool failed, cudaStream_t s, int* any_failed) {
     double* d = nullptr;
     double h = failed ? 1.0 : 0.0;
-    ZK_CUDA(cudaMalloc(&d, sizeof(double)));
+    ZK_CUDA(scratch_alloc(&d, sizeof(double), s));
     cudaError_t e = cudaMemcpyAsync(d, &h, sizeof h, cudaMemcpyHostToDevice, s);
     zk_status st = e == cudaSuccess ? comm_allreduce_sum(c, d, 1, s) : cuda_fail(e, "agree", __FILE__, __LINE__);
     if (st == ZK_OK) {
@@ -77,7 +77,7 @@ zk_status dist_agree_failed(zk_comm_s* c, bool failed, cudaStream_t s, int* any_
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) st = cuda_fail(e, "agree", __FILE__, __LINE__);
     }
-    cudaFree(d);
+    scratch_free(d, s);
     *any_failed = h > 0.0 ? 1 : 0;
     return st;
 }
@@ -93,7 +93,7 @@ zk_status dist_setup(zk_csr_s* A, const int64_t*, const int*, cudaStream_t s) {
     P->rank = me;
     // ---- 1. row ranges of all ranks
     int64_t* d_rng = nullptr;
-    ZK_CUDA(cudaMalloc(&d_rng, sizeof(int64_t) * 2 * (np + np * (size_t)np + 1)));
+    ZK_CUDA(scratch_alloc(&d_rng, sizeof(int64_t) * 2 * (np + np * (size_t)np + 1), s));
     int64_t mine[2] = {A->row_begin, A->n_rows};
     ZK_CUDA(cudaMemcpyAsync(d_rng, mine, sizeof mine, cudaMemcpyHostToDevice, s));
     ZK_TRY(comm_allgather(c, d_rng, d_rng + 2, sizeof mine, s));
@@ -103,7 +103,7 @@ zk_status dist_setup(zk_csr_s* A, const int64_t*, const int*, cudaStream_t s) {
     P->offsets.assign(np + 1, 0);
     for (int r = 0; r < np; r++) {
         if (rng[2 * r] != P->offsets[r]) {
-            cudaFree(d_rng);
+            scratch_free(d_rng, s);
             return fail(ZK_ERR_INVALID_VALUE, "rank row blocks must be contiguous and in rank order");
         }
         P->offsets[r + 1] = rng[2 * r] + rng[2 * r + 1];
@@ -116,7 +116,7 @@ zk_status dist_setup(zk_csr_s* A, const int64_t*, const int*, cudaStream_t s) {
     int64_t n_ext = 0;
     std::vector<int64_t> cnt(np, 0);
     zk_status st = zk_halo_plan(A->nnz, col.data(), np, me, P->offsets.data(), &n_ext, nullptr, nullptr);
-    if (st != ZK_OK) { cudaFree(d_rng); return st; }
+    if (st != ZK_OK) { scratch_free(d_rng, s); return st; }
     std::vector<int> ext(n_ext > 0 ? n_ext : 1);
     ZK_TRY(zk_halo_plan(A->nnz, col.data(), np, me, P->offsets.data(), &n_ext, ext.data(), cnt.data()));
     P->n_ext = n_ext;
@@ -130,7 +130,7 @@ zk_status dist_setup(zk_csr_s* A, const int64_t*, const int*, cudaStream_t s) {
     std::vector<int64_t> all(np * (size_t)np);
     ZK_CUDA(cudaMemcpyAsync(all.data(), d_cnt + np, sizeof(int64_t) * np * np, cudaMemcpyDeviceToHost, s));
     ZK_CUDA(cudaStreamSynchronize(s));
-    cudaFree(d_rng);
+    scratch_free(d_rng, s);
     P->send_cnt.assign(np, 0);
     P->send_off.assign(np + 1, 0);
     for (int q = 0; q < np; q++) P->send_cnt[q] = all[(size_t)q * np + me];
@@ -138,8 +138,8 @@ zk_status dist_setup(zk_csr_s* A, const int64_t*, const int*, cudaStream_t s) {
     P->n_send = P->send_off[np];
     // ---- 4. exchange the requested global ids (grouped p2p), turn them into local rows
     int *d_req_out = nullptr, *d_req_in = nullptr;
-    ZK_CUDA(cudaMalloc(&d_req_out, sizeof(int) * (n_ext > 0 ? n_ext : 1)));
-    ZK_CUDA(cudaMalloc(&d_req_in, sizeof(int) * (P->n_send > 0 ? P->n_send : 1)));
+    ZK_CUDA(scratch_alloc(&d_req_out, sizeof(int) * (n_ext > 0 ? n_ext : 1), s));
+    ZK_CUDA(dev_alloc(&d_req_in, sizeof(int) * (P->n_send > 0 ? P->n_send : 1), s));
     if (n_ext) ZK_CUDA(cudaMemcpyAsync(d_req_out, ext.data(), sizeof(int) * n_ext, cudaMemcpyHostToDevice, s));
     ZK_TRY(comm_group_start(c));
     for (int q = 0; q < np; q++) {
@@ -151,19 +151,19 @@ zk_status dist_setup(zk_csr_s* A, const int64_t*, const int*, cudaStream_t s) {
     std::vector<int> req(P->n_send > 0 ? P->n_send : 1);
     if (P->n_send) ZK_CUDA(cudaMemcpyAsync(req.data(), d_req_in, sizeof(int) * P->n_send, cudaMemcpyDeviceToHost, s));
     ZK_CUDA(cudaStreamSynchronize(s));
-    cudaFree(d_req_out);
+    scratch_free(d_req_out, s);
     for (int64_t k = 0; k < P->n_send; k++) {
         const int64_t loc = (int64_t)req[k] - A->row_begin;
         if (loc < 0 || loc >= A->n_rows) {
-            cudaFree(d_req_in);
+            scratch_free(d_req_in, s);
             return fail(ZK_ERR_INVALID_VALUE, "halo request outside this rank's rows");
         }
         req[k] = (int)loc;
     }
     if (P->n_send) ZK_CUDA(cudaMemcpyAsync(d_req_in, req.data(), sizeof(int) * P->n_send, cudaMemcpyHostToDevice, s));
     P->d_send_idx = d_req_in;
-    ZK_CUDA(cudaMalloc(&P->d_sendbuf, sizeof(double2) * (P->n_send > 0 ? P->n_send : 1)));
-    ZK_CUDA(cudaMalloc(&P->d_xg, sizeof(double2) * (A->n_rows + n_ext > 0 ? A->n_rows + n_ext : 1)));
+    ZK_CUDA(dev_alloc(&P->d_sendbuf, sizeof(double2) * (P->n_send > 0 ? P->n_send : 1), s));
+    ZK_CUDA(dev_alloc(&P->d_xg, sizeof(double2) * (A->n_rows + n_ext > 0 ? A->n_rows + n_ext : 1), s));
     // ---- 5. renumber columns to [local | halo] in the library's own copy
     ZK_TRY(zk_halo_renumber(A->nnz, col.data(), A->row_begin, A->n_rows, n_ext, ext.data(), col.data()));
     if (A->nnz) ZK_CUDA(cudaMemcpyAsync(A->col, col.data(), sizeof(int) * A->nnz, cudaMemcpyHostToDevice, s));

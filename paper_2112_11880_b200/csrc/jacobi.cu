@@ -90,7 +90,7 @@ zk_status jacobi_prepare(zk_csr_s* A, cudaStream_t s) {
     cudaError_t e = csr_vals ? dev_alloc(&val, sizeof(double2) * (nnz > 0 ? nnz : 1), s) : cudaSuccess;
     if (e == cudaSuccess) e = dev_alloc(&diag, sizeof(double2) * (n > 0 ? n : 1), s);
     if (e == cudaSuccess) e = dev_alloc(&dinv, sizeof(double2) * (glen > 0 ? glen : 1), s);
-    if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = scratch_alloc(&bad, sizeof(unsigned long long), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s);
     if (e == cudaSuccess && n > 0) {
         if (csr_vals)
@@ -104,7 +104,7 @@ zk_status jacobi_prepare(zk_csr_s* A, cudaStream_t s) {
     unsigned long long hbad = ~0ull;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(bad);
+    scratch_free(bad, s);
     bool failed = e != cudaSuccess || hbad != ~0ull;
     if (A->dist) {
         int any = 0;

@@ -70,9 +70,9 @@ zk_status sell_build(zk_csr_s* A, cudaStream_t s) {
     A->n_slices = n_sl;
     int* w = nullptr;
     cudaError_t e = dev_alloc(&A->sl_ptr, sizeof(int64_t) * (size_t)(n_sl + 1), s);
-    if (e == cudaSuccess) e = cudaMalloc(&w, sizeof(int) * (size_t)(n_sl > 0 ? n_sl : 1));
+    if (e == cudaSuccess) e = scratch_alloc(&w, sizeof(int) * (size_t)(n_sl > 0 ? n_sl : 1), s);
     if (e != cudaSuccess) {
-        cudaFree(w);
+        scratch_free(w, s);
         sell_destroy(A);
         return cuda_fail(e, "sell_build alloc", __FILE__, __LINE__);
     }
@@ -82,7 +82,7 @@ zk_status sell_build(zk_csr_s* A, cudaStream_t s) {
     std::vector<int64_t> hp((size_t)n_sl + 1);
     if (n_sl > 0) e = cudaMemcpyAsync(hw.data(), w, sizeof(int) * (size_t)n_sl, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(w);
+    scratch_free(w, s);
     if (e != cudaSuccess) {
         sell_destroy(A);
         return cuda_fail(e, "sell_build widths", __FILE__, __LINE__);

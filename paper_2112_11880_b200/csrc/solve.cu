@@ -3207,11 +3207,10 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     cudaEvent_t ev0 = A->ev[0], ev1 = A->ev[1];
     const size_t rb_bytes = sizeof(SolveCtx) + sizeof(double) * ((size_t)maxit + 1);
     if (A->pinned_bytes < rb_bytes) {  // pinned readback staging, grown on demand
-        if (A->pinned) cudaFreeHost(A->pinned);
+        pinned_put(A->pinned, A->pinned_bytes);  // (process-wide free list, api.cu)
         A->pinned = nullptr;
         A->pinned_bytes = 0;
-        ZK_CUDA(cudaMallocHost(&A->pinned, rb_bytes));
-        A->pinned_bytes = rb_bytes;
+        ZK_CUDA(pinned_get(&A->pinned, rb_bytes, &A->pinned_bytes));
     }
     ZK_CUDA(cudaEventRecord(ev0, s));
     int64_t n_spmv = 0;

@@ -135,6 +135,35 @@ inline void dev_free(void* p, bool synced = false) {
     if (!synced) cudaDeviceSynchronize();
     cudaFreeAsync(p, 0);
 }
+// After a batch of dev_free calls: wait until stream 0 has executed the frees, so the pool's
+// opportunistic reuse hands the blocks to the next allocation on ANY stream.  Without it, a create
+// on another (non-blocking) stream right after a destroy could not reuse them and the pool mapped
+// fresh memory (measured C4: zk_csr_create 85 ms → 660-1420 ms on a torch side stream).
+inline void dev_free_done() {
+    if (pool_enabled()) cudaStreamSynchronize(0);
+}
+// Small per-call device scratch (validation flags, SELL widths, ...): a stream-ordered pool
+// allocation on s, returned on s.  No cudaMalloc / cudaFree on the create / solve / destroy path:
+// with GBs of pinned host memory in the process (torch pin_memory), cudaFree of a 16-byte buffer
+// measured 2-580 ms and cudaFreeHost of the readback staging up to 474 ms (tools/e2e_probe.py
+// with ZK_TRACE=1, profiles/r02_e2e_probe.txt) — the driver's free path, not the GPU.
+template <class T>
+inline cudaError_t scratch_alloc(T** p, size_t bytes, cudaStream_t s) {
+    return dev_alloc(reinterpret_cast<void**>(p), bytes, s);
+}
+inline void scratch_free(void* p, cudaStream_t s) {
+    if (!p) return;
+    if (!pool_enabled()) {
+        cudaFree(p);
+        return;
+    }
+    cudaFreeAsync(p, s);
+}
+// Pinned host staging (zk_solve's context + history readback) from a process-wide free list:
+// handles take a buffer at their first solve and give it back at destroy (no cudaMallocHost /
+// cudaFreeHost per handle).  api.cu.
+cudaError_t pinned_get(void** p, size_t bytes, size_t* got);
+void pinned_put(void* p, size_t bytes);
 void sell_destroy(zk_csr_s* A, bool synced = false);    // sell.cu  (synced: the device is already idle)
 constexpr int64_t kCsrValuesKeepRows = 16384;           // ≤ this: the CSR value copy stays (cluster solver)
 void jacobi_destroy(zk_csr_s* A, bool synced = false);  // jacobi.cu
