@@ -180,6 +180,37 @@ struct sell_ordered {
     template <class T> static constexpr bool get(...) { return false; }
     static constexpr bool value = get<E>(nullptr);
 };
+// The rows of this warp's slices under the SELL body's static schedule (logical slices t0 + k·nw,
+// physical slice as in spmv_body_sell with the same REV) — the rows the warp's SpMV wrote — with
+// Op::U slices in flight: op.apply(row, op.load(row), acc) on each.  BACK walks the warp's slices
+// in the reverse time order (its most recently written rows first).  The SpMV tail reductions and
+// the phases of the phase-fused solver kernels run on it.
+template <bool REV, bool BACK, class Op, int KA>
+__device__ __forceinline__ void sell_walk_own(const CsrDev& A, const Op& op, double (&acc)[KA]) {
+    constexpr int TU = vec_unroll<Op>::value;
+    const int n = (int)A.n_rows;
+    const int n_sl = A.sl_cnt;
+    const int nw = gridDim.x * kWarps;
+    const int lane = threadIdx.x & 31;
+    const int t0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const int cnt = t0 < n_sl ? (n_sl - 1 - t0) / nw + 1 : 0;
+    for (int kb = 0; kb < cnt; kb += TU) {
+        typename Op::In in[TU] = {};
+        int rows[TU];
+#pragma unroll
+        for (int u = 0; u < TU; u++) {
+            const int k = kb + u;
+            const int t = t0 + (BACK ? cnt - 1 - k : k) * nw;
+            const int q = REV ? n_sl - 1 - t : t;
+            rows[u] = k < cnt ? (A.sl_lo + q + (q >= A.sl_gap_at ? A.sl_gap : 0)) * 32 + lane : n;
+            if (rows[u] < n) in[u] = op.load(rows[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < TU; u++)
+            if (rows[u] < n) op.apply(rows[u], in[u], acc);
+    }
+}
+
 // REV: walk the slices last to first (opposite sweeps: the kernel starts on the rows
 // its predecessor in the solver loop touched last, still in L2)
 template <class Epi, int LP = ZK_SELL_LP, bool REV = false>
@@ -294,22 +325,8 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
         for (int k = 0; k < KA; k++) acc[k] = lane == 0 ? wacc[threadIdx.x >> 5][k] : 0.0;
     }
     if constexpr (sell_tail<Epi>::value) {
-        constexpr int TU = vec_unroll<typename Epi::TailOp>::value;  // slices in flight per step
         const auto op = epi.tail_op();
-        const int t0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
-        for (int tb = t0; tb < n_sl; tb += TU * nw) {
-            typename Epi::TailOp::In in[TU] = {};
-            int rows[TU];
-#pragma unroll
-            for (int u = 0; u < TU; u++) {
-                const int tt = tb + u * nw;
-                rows[u] = tt < n_sl ? phys(tt) * 32 + lane : n;
-                if (rows[u] < n) in[u] = op.load(rows[u]);
-            }
-#pragma unroll
-            for (int u = 0; u < TU; u++)
-                if (rows[u] < n) op.apply(rows[u], in[u], acc);
-        }
+        sell_walk_own<REV, false>(A, op, acc);
         op.finish(acc);
     } else {
         epi.finish(acc);
