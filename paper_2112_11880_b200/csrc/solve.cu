@@ -22,6 +22,7 @@
 // operand they need (y1 before it is overwritten, y2, d): d and x are read and written once per
 // iteration, and the SpMV epilogue of T2 carries 2 row operands.  2·Mat + 25 vector passes.
 //   T4  u1 = A y1 ; v = u1 + β(u2 + βv) ; σ = ⟨r̃,v⟩        → α = ρ/σ, c1 (writes the WHILE condition)
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1688,6 +1689,7 @@ static int bl_nd(int L) { return (L + 1) + (L + 1) * L; }
 #endif
 constexpr int kCBlock = ZK_CBLOCK;
 constexpr int kCWarps = kCBlock / 32;
+constexpr int kCMaxCta = 16;  // cluster size: 16 (non-portable), else 8
 constexpr int kCVecs = 7;                        // BiCGStab: x r r̂ p v s t own rows in shared memory
 constexpr int kCVecsTfqmr = 9;                   // TFQMR: x w y1 y2 u1 u2 v d r̃
 constexpr int kCVecsCg = 4;                      // CG / COCG: x r p q
@@ -1697,14 +1699,28 @@ constexpr int kCSmemMax = 216 * 1024;            // dynamic shared memory: own r
 #endif
 constexpr int64_t kClusterDefaultRows = ZK_CLUSTER_DEFAULT_ROWS;  // default up to this size
 
+// The solve context into / out of a cluster CTA's shared copy, 8-byte words over all threads (a
+// struct assignment by one thread went through local memory: ~1.2 KB of STL/LDL in the prologue).
+__device__ __forceinline__ void ctx_copy(SolveCtx* dst, const SolveCtx* src) {
+    static_assert(sizeof(SolveCtx) % 8 == 0, "SolveCtx in 8-byte words");
+    const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(dst);
+    for (int i = threadIdx.x; i < (int)(sizeof(SolveCtx) / 8); i += blockDim.x) d[i] = s[i];
+}
+
 struct ClusterRed {
-    double slot[2][kMaxRed];      // this CTA's partial sums, double-buffered across reductions
+    double slot[2][kCMaxCta][kMaxRed];  // every CTA's partial sums, pushed here by their owners (double-buffered)
     double warp_part[kMaxRed][kCWarps];
     double tot[kMaxRed];
     int parity;
 };
 
-// cluster-wide sum of K doubles; result in R.tot (valid after the caller's __syncthreads)
+// cluster-wide sum of K doubles; result in R.tot (valid after the caller's __syncthreads).  Warps
+// → the CTA's partial (warp 0, lane 0's value), which lanes r < ncta PUSH into CTA r's slot array
+// (st.shared::cluster) before the cluster barrier; after it every CTA adds the ncta slots of its
+// own shared memory in rank order — identical totals in every CTA, and no remote load on the
+// critical path (a DSMEM load is ≈ 215 cycles, B300_MICROARCH.md; the pull version read the ncta
+// slots over DSMEM after the barrier).
 template <int K>
 __device__ __forceinline__ void cl_sum(double (&v)[K], ClusterRed& R) {
     namespace cg = cooperative_groups;
@@ -1717,34 +1733,29 @@ __device__ __forceinline__ void cl_sum(double (&v)[K], ClusterRed& R) {
     }
     __syncthreads();
     const int par = R.parity;
+    const unsigned ncta = cl.num_blocks();
     if (warp == 0) {
         double w[K];
 #pragma unroll
         for (int k = 0; k < K; k++) w[k] = lane < kCWarps ? R.warp_part[k][lane] : 0.0;
         warp_sum<K>(w);
-        if (lane == 0) {
 #pragma unroll
-            for (int k = 0; k < K; k++) R.slot[par][k] = w[k];
+        for (int k = 0; k < K; k++) w[k] = __shfl_sync(0xffffffffu, w[k], 0);  // lane 0's value, everywhere
+        if ((unsigned)lane < ncta) {
+            double* dst = cl.map_shared_rank(&R.slot[par][cl.block_rank()][0], lane);
+#pragma unroll
+            for (int k = 0; k < K; k++) dst[k] = w[k];
         }
     }
-    cl.sync();  // release/acquire at cluster scope: slots (and this phase's global writes) visible
+    cl.sync();  // release/acquire at cluster scope: the pushed slots (and this phase's global writes) visible
     if (warp == 0) {
-        const unsigned ncta = cl.num_blocks();
-        double t[K];
-        if ((unsigned)lane < ncta) {
-            const double* rs = cl.map_shared_rank(&R.slot[par][0], lane);
-#pragma unroll
-            for (int k = 0; k < K; k++) t[k] = rs[k];
-        } else {
-#pragma unroll
-            for (int k = 0; k < K; k++) t[k] = 0.0;
+        if (lane < K) {
+            double t = 0.0;
+            for (unsigned r = 0; r < ncta; r++) t += R.slot[par][r][lane];
+            R.tot[lane] = t;
         }
-        warp_sum<K>(t);  // fixed xor tree: every CTA forms lane 0's total in the same order
-        if (lane == 0) {
-#pragma unroll
-            for (int k = 0; k < K; k++) R.tot[k] = t[k];
-            R.parity = par ^ 1;
-        }
+        __syncwarp();  // R.tot for thread 0 (the caller's scalar step)
+        if (lane == 0) R.parity = par ^ 1;
     }
 }
 
@@ -1758,13 +1769,19 @@ __device__ __forceinline__ double2 ld_l1(const double2* p) {
     return v;
 }
 
+// Values in global memory (!VS) are loaded with L1::no_allocate: they are re-read from L2 every
+// SpMV anyway (a CTA's block does not fit the L1 left beside the shared-memory carve-out), and
+// allocating them evicted the gathered x window from L1.
+#ifndef ZK_CL_VAL_NA
+#define ZK_CL_VAL_NA 1
+#endif
 // own row l of A·x on W lanes (sub = lane within the row's group): columns (and values when VS)
 // from the CTA's shared-memory copy, x gathered through L2.  valid == false: the lanes take part
 // in the shuffles only.
 template <int W, bool VS>
 __device__ __forceinline__ double2 cl_row(const double2* __restrict__ gval, const double2* sval, const int* scol,
                                           const int* soff, const double2* x, int l, bool valid, int sub) {
-    constexpr int U = 4;  // 8 spills at the 128-register cap of 512-thread CTAs
+    constexpr int U = 4;  // 8 spills at the 128-register cap of 512-thread CTAs (U = 8 at W = 2: 2.4 KB, 2x slower)
     double2 sum = make_double2(0.0, 0.0);
     if (valid) {
         const int rs = soff[l], re = soff[l + 1];
@@ -1776,7 +1793,7 @@ __device__ __forceinline__ double2 cl_row(const double2* __restrict__ gval, cons
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 if (c[u] >= 0) {
-                    v[u] = VS ? sval[p0 + u * W] : __ldg(gval + p0 + u * W);
+                    v[u] = VS ? sval[p0 + u * W] : (ZK_CL_VAL_NA ? ld_stream(gval + p0 + u * W) : __ldg(gval + p0 + u * W));
                     xv[u] = ld_l1(x + c[u]);
                 }
             }
@@ -1841,21 +1858,28 @@ __device__ __forceinline__ void cl_true(SolveCtx* c, ClusterRed& R, const double
 // s = r − αv formed inside the SpMV gathers from the published r, p, v — 9.7 → 15.5 (C1), 24.2 →
 // 53.3 (C2): the 2-3× L2 gathers cost far more than the two barriers.)
 // dynamic shared memory: kCVecs × rpc vectors | [values nnz_max] | columns nnz_max | offsets rpc + 1
+// ZK_CLUSTER_PROF (tools build only): per-phase SM-cycle totals of CTA 0's thread 0, printed at exit
+#ifndef ZK_CLUSTER_PROF
+#define ZK_CLUSTER_PROF 0
+#endif
+#define CPROF(k)                                                            \
+    do {                                                                    \
+        if (ZK_CLUSTER_PROF && threadIdx.x == 0 && cl.block_rank() == 0) {  \
+            const long long t_ = clock64();                                 \
+            prof_[k] += t_ - prof_t_;                                       \
+            prof_t_ = t_;                                                   \
+        }                                                                   \
+    } while (0)
 template <int W, bool VS>
-__global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, const SolveCtx hctx, const CsrDev A,
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, const __grid_constant__ SolveCtx hctx, const CsrDev A,
                                                              int nnz_max, int do_true, int init) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ double2 own[];
     __shared__ SolveCtx cs;
     __shared__ ClusterRed R;
-    if (threadIdx.x == 0) {
-        if (init)
-            cs = hctx;
-        else
-            cs = *gctx;
-        R.parity = 0;
-    }
+    ctx_copy(&cs, init ? &hctx : gctx);
+    if (threadIdx.x == 0) R.parity = 0;
     const int n = (int)A.n_rows;
     const int ncta = (int)cl.num_blocks();
     const int rpc = (n + ncta - 1) / ncta;
@@ -1902,6 +1926,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
     const int sub = threadIdx.x & (W - 1);
     const int grp = threadIdx.x / W;
     int bodies = 0;
+    long long prof_[13] = {}, prof_t_ = clock64();
     while (!c->done) {
         {   // K1: v = A p ; σ = ⟨r̂, v⟩, ‖v‖²
             double acc[3] = {0.0, 0.0, 0.0};
@@ -1916,9 +1941,12 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
                     acc[2] += cabs2(y);
                 }
             }
+            CPROF(0);
             cl_sum<3>(acc, R);
+            CPROF(1);
             if (threadIdx.x == 0) fin_k1_bicg(c, R.tot);
             __syncthreads();
+            CPROF(2);
             if (c->done) break;
         }
         {   // K2: s = r − α v ; ‖s‖²
@@ -1933,9 +1961,12 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
                 sg[row0 + l] = o;
                 acc[0] += cabs2(o);
             }
+            CPROF(3);
             cl_sum<1>(acc, R);  // its cluster barrier also publishes s for the K3 gathers
+            CPROF(4);
             if (threadIdx.x == 0) fin_k2_bicg(c, R.tot);
             __syncthreads();
+            CPROF(5);
             if (c->done) {  // half-step exit: x += α p
                 if (c->half) {
                     for (int l = threadIdx.x; l < nr; l += kCBlock) cfma(X[l], al, P[l]);
@@ -1958,9 +1989,12 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
                     acc[2] += cabs2(y);
                 }
             }
+            CPROF(6);
             cl_sum<3>(acc, R);
+            CPROF(7);
             if (threadIdx.x == 0) fin_k3_bicg(c, R.tot);
             __syncthreads();
+            CPROF(8);
             if (c->done) break;
         }
         {   // K4: x += α p + ω s ; r = s − ω t ; ‖r‖², ⟨r̂, r⟩
@@ -1981,9 +2015,12 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
                 acc[1] = fma(q.x, rn.x, fma(q.y, rn.y, acc[1]));
                 acc[2] = fma(q.x, rn.y, fma(-q.y, rn.x, acc[2]));
             }
+            CPROF(9);
             cl_sum<3>(acc, R);
+            CPROF(10);
             if (threadIdx.x == 0) fin_k4_bicg(c, R.tot);
             __syncthreads();
+            CPROF(11);
             if (c->done) break;
         }
         {   // K5: p = r + β (p − ω v), then a cluster barrier (p is gathered by K1)
@@ -1999,15 +2036,19 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
                 pg[row0 + l] = o;
             }
             cl.sync();
+            CPROF(12);
         }
         bodies++;
     }
+    if (ZK_CLUSTER_PROF && threadIdx.x == 0 && cl.block_rank() == 0)
+        printf("cluster_prof bodies %d cycles: k1 %lld red %lld fin %lld | k2 %lld red %lld fin %lld | k3 %lld red %lld fin %lld | k4 %lld red %lld fin %lld | k5+sync %lld\n",
+               bodies, prof_[0], prof_[1], prof_[2], prof_[3], prof_[4], prof_[5], prof_[6], prof_[7], prof_[8],
+               prof_[9], prof_[10], prof_[11], prof_[12]);
     for (int l = threadIdx.x; l < nr; l += kCBlock) xg[row0 + l] = X[l];  // the solution leaves shared memory
     if (do_true) cl_true<W, VS>(c, R, gval, sval, scol, soff, xg, row0, nr);
-    if (cl.block_rank() == 0 && threadIdx.x == 0) {
-        cs.bodies = bodies;
-        *gctx = cs;
-    }
+    if (threadIdx.x == 0) cs.bodies = bodies;
+    __syncthreads();
+    if (cl.block_rank() == 0) ctx_copy(gctx, &cs);
     cl.sync();  // no CTA leaves while another may still read its reduction slots
 }
 
@@ -2022,10 +2063,8 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, co
     extern __shared__ double2 own[];
     __shared__ SolveCtx cs;
     __shared__ ClusterRed R;
-    if (threadIdx.x == 0) {
-        cs = *gctx;
-        R.parity = 0;
-    }
+    ctx_copy(&cs, gctx);
+    if (threadIdx.x == 0) R.parity = 0;
     const int n = (int)A.n_rows;
     const int ncta = (int)cl.num_blocks();
     const int rpc = (n + ncta - 1) / ncta;
@@ -2163,11 +2202,12 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, co
     __syncthreads();
     for (int l = threadIdx.x; l < nr; l += kCBlock) xg[row0 + l] = X[l];
     if (do_true) cl_true<W, VS>(c, R, gval, sval, scol, soff, xg, row0, nr);
-    if (cl.block_rank() == 0 && threadIdx.x == 0) {
+    if (threadIdx.x == 0) {
         cs.half = 0;
         cs.bodies = bodies;
-        *gctx = cs;
     }
+    __syncthreads();
+    if (cl.block_rank() == 0) ctx_copy(gctx, &cs);
     cl.sync();
 }
 
@@ -2181,10 +2221,8 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const
     extern __shared__ double2 own[];
     __shared__ SolveCtx cs;
     __shared__ ClusterRed R;
-    if (threadIdx.x == 0) {
-        cs = *gctx;
-        R.parity = 0;
-    }
+    ctx_copy(&cs, gctx);
+    if (threadIdx.x == 0) R.parity = 0;
     const int n = (int)A.n_rows;
     const int ncta = (int)cl.num_blocks();
     const int rpc = (n + ncta - 1) / ncta;
@@ -2291,10 +2329,9 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const
     __syncthreads();
     for (int l = threadIdx.x; l < nr; l += kCBlock) xg[row0 + l] = X[l];
     if (do_true) cl_true<W, VS>(c, R, gval, sval, scol, soff, xg, row0, nr);
-    if (cl.block_rank() == 0 && threadIdx.x == 0) {
-        cs.bodies = bodies;
-        *gctx = cs;
-    }
+    if (threadIdx.x == 0) cs.bodies = bodies;
+    __syncthreads();
+    if (cl.block_rank() == 0) ctx_copy(gctx, &cs);
     cl.sync();
 }
 
@@ -2329,10 +2366,8 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
     __shared__ double gpart[kGramMax][kGramSub];
     __shared__ double gslot[2][kGramMax];
     __shared__ double gtot[kGramMax];
-    if (threadIdx.x == 0) {
-        cs = *gctx;
-        R.parity = 0;
-    }
+    ctx_copy(&cs, gctx);
+    if (threadIdx.x == 0) R.parity = 0;
     __syncthreads();
     const int n = (int)A.n_rows;
     const int ncta = (int)cl.num_blocks();
@@ -2528,10 +2563,9 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
     __syncthreads();
     for (int l = threadIdx.x; l < nr; l += kCBlock) xg[row0 + l] = X[l];  // the solution leaves shared memory
     if (do_true) cl_true<W, VS>(c, R, gval, sval, scol, soff, xg, row0, nr);
-    if (cl.block_rank() == 0 && threadIdx.x == 0) {
-        cs.bodies = bodies;
-        *gctx = cs;
-    }
+    if (threadIdx.x == 0) cs.bodies = bodies;
+    __syncthreads();
+    if (cl.block_rank() == 0) ctx_copy(gctx, &cs);
     cl.sync();
 }
 
@@ -3095,6 +3129,8 @@ extern "C" size_t zk_solve_workspace_size(zk_csr A, int32_t code, int32_t maxit)
 extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double tol, int32_t maxit, int32_t code,
                               zk_z* x, int32_t* iters, double* resid_hist, zk_solve_info* info, void* workspace,
                               size_t ws_bytes, zk_stream stream) {
+    static const bool trace = getenv("ZK_TRACE") != nullptr;  // host-side phase times on stderr
+    const auto tr0 = std::chrono::steady_clock::now();
     if (!A || !b || !x || !iters || !resid_hist || !workspace) return fail(ZK_ERR_INVALID_VALUE, "NULL argument");
     int method, ell;
     if (!decode_method(code, &method, &ell)) return fail(ZK_ERR_INVALID_VALUE, "unknown method");
@@ -3213,6 +3249,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         ZK_CUDA(pinned_get(&A->pinned, rb_bytes, &A->pinned_bytes));
     }
     ZK_CUDA(cudaEventRecord(ev0, s));
+    const auto tr1 = std::chrono::steady_clock::now();
     int64_t n_spmv = 0;
 
     // ---- init: context, r0 = b − A x0 (or b), ‖b‖, hist[0]
@@ -3337,8 +3374,10 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     SolveCtx out;
     double* hist_pinned = (double*)((char*)A->pinned + sizeof(SolveCtx));
     static_assert(sizeof(SolveCtx) % sizeof(double) == 0, "hist follows the ctx");
+    const auto tr2 = std::chrono::steady_clock::now();
     ZK_CUDA(cudaMemcpyAsync(A->pinned, dc, rb_bytes, cudaMemcpyDeviceToHost, s));  // ctx + hist
     cudaError_t e = cudaStreamSynchronize(s);
+    const auto tr3 = std::chrono::steady_clock::now();
     if (e != cudaSuccess) return cuda_fail(e, "zk_solve", __FILE__, __LINE__);
     memcpy(&out, A->pinned, sizeof(SolveCtx));
     memcpy(resid_hist, hist_pinned, sizeof(double) * ((size_t)maxit + 1));
@@ -3382,6 +3421,11 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
             info->kernel_ms[i] = out.tsum[i] * 1e-6;
             info->kernel_launches[i] = out.tcnt[i];
         }
+    }
+    if (trace) {
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        fprintf(stderr, "zk_solve: setup %.1f us, enqueue %.1f us, readback+sync %.1f us, rest %.1f us (device %.1f us, mode %d)\n",
+                us(tr0, tr1), us(tr1, tr2), us(tr2, tr3), us(tr3, std::chrono::steady_clock::now()), 1e3 * ms, mode);
     }
     if (out.status == ST_ZERO_RHS) return fail(ZK_ERR_ZERO_RHS, "||b|| = 0 (S:361)");
     return ZK_OK;

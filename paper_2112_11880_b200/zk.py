@@ -123,20 +123,25 @@ def _z(a) -> zk_z:
     return zk_z(a.real, a.imag)
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream(stream) -> int:
-    if stream is None:
+    if stream is None:  # torch's current stream (the raw handle: no Stream object per call)
+        if _raw_stream is not None:
+            return _raw_stream(torch.cuda.current_device())
         return torch.cuda.current_stream().cuda_stream
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
 def _dev_c128(t: torch.Tensor, name: str) -> int:
+    if isinstance(t, torch.Tensor) and t.is_cuda and t.dtype is torch.complex128 and t.is_contiguous():
+        return t.data_ptr()  # (the common case: one combined test)
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor")
     if t.dtype != torch.complex128:
         raise TypeError(f"{name} must be complex128")
-    if not t.is_contiguous():
-        raise ValueError(f"{name} must be contiguous")
-    return t.data_ptr()
+    raise ValueError(f"{name} must be contiguous")
 
 
 class Comm:
@@ -349,7 +354,7 @@ def solve(A: Csr, b: torch.Tensor, x0: torch.Tensor | None = None, tol: float = 
     if workspace is None:
         workspace = alloc_workspace(A, method, maxit, b.device, ell)
     iters = I32(0)
-    hist = np.full(maxit + 1, np.nan)
+    hist = np.empty(maxit + 1)  # (entries past iters are unspecified, zk.h; only hist[:iters+1] is returned)
     info = zk_solve_info()
     _check(lib().zk_solve(A.handle, pb, px0, float(tol), int(maxit), m, px, ctypes.byref(iters),
                           hist.ctypes.data, ctypes.byref(info), workspace.data_ptr(), workspace.numel(),
