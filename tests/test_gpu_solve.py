@@ -667,3 +667,36 @@ def test_dropped_csr_values_bitwise(monkeypatch):
         A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
         out.append(zk.solve(A, cuda(b), tol=1e-8, method="bicgstab_jacobi"))
     assert out[0]["iters"] == out[1]["iters"] and torch.equal(out[0]["x"], out[1]["x"])
+
+
+@pytest.mark.parametrize("cfg", ["C1", "T1"])
+def test_create_solve_destroy_loop_on_side_stream(cfg):
+    """The e2e pattern (bench.py e2e_step) on a torch side stream: pinned host CSR → create →
+    solve → x back → destroy, many times with no other handle alive and with one alive.  The
+    library's small scratch comes from its stream-ordered pool and its pinned readback staging
+    from a process-wide free list (no cudaMalloc / cudaFree / cudaFreeHost on this path): every
+    round must give the same iterations and the same x bits as the first."""
+    m = gen.make_matrix(cfg)
+    rp, ci, va = (torch.from_numpy(a).pin_memory() for a in (m["row_ptr"], m["col_idx"], m["values"]))
+    b_pin = torch.from_numpy(gen.make_rhs(m)).pin_memory()
+    x_h = torch.empty(m["n"], dtype=torch.complex128).pin_memory()
+    side = torch.cuda.Stream()
+    ref = None
+    keep = None
+    for rnd in range(12):
+        if rnd == 6:  # second half: another handle stays alive (the pool is not trimmed between rounds)
+            keep = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+        with torch.cuda.stream(side):
+            A = zk.csr_create(rp, ci, va, m["n"], stream=side)
+            bd = b_pin.to(DEV, non_blocking=True)
+            # maxit varies: the readback staging grows, old buffers go back to the free list
+            r = zk.solve(A, bd, tol=1e-8, maxit=500 + 100 * rnd, method="bicgstab", stream=side)
+            x_h.copy_(r["x"], non_blocking=True)
+            A.close()
+        side.synchronize()
+        got = (r["iters"], r["status"], x_h.numpy().copy())
+        if ref is None:
+            ref = got
+        assert got[0] == ref[0] and got[1] == ref[1] == "CONVERGED"
+        assert np.array_equal(got[2], ref[2]), f"round {rnd}: x differs"
+    keep.close()
