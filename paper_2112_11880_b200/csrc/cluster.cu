@@ -1,6 +1,10 @@
-// cluster.cu — loop mode 5: the whole Krylov loop of a small system (the paper's Audi3D / Twingo3D
-// shapes) in ONE thread-block cluster, every reduction over distributed shared memory, the scalar
-// steps replicated per CTA (solve_ctx.cuh).  DESIGN.md §7 "Solver loop".
+// cluster.cu — loop mode 5: the whole Krylov loop of a small system in ONE thread-block cluster,
+// every reduction over distributed shared memory, the scalar steps replicated per CTA
+// (solve_ctx.cuh).  The paper's own matrices (PAPER.md T1 P:52-70: Audi3D-1..4, Twingo3D-0..2; the
+// solvers of §4, T9 P:313-341) are 1.7k-650k rows: latency-bound on a B200, where a
+// kernel boundary costs more than an iteration's arithmetic.  Same per-row arithmetic and scalar
+// steps as the grid kernels of solve.cu (NEXT-1..4), parity-
+// tested against the oracle in every instantiation.  DESIGN.md §7 "Solver loop".
 #include <algorithm>
 #include <cstdio>
 #include <cstring>

@@ -1,7 +1,8 @@
 // solve_ctx.cuh — what the solver loops (solve.cu) and the single-cluster solvers (cluster.cu)
 // share: the device-resident solve context, the per-method scalar steps (oracle O6/O7 and the NEXT
-// rows' steps, line by line, run by one thread), the BiCGStab(ℓ) Gram/Cholesky step, and the
-// cluster solver's host entry points.  See solve.cu's header for the schedules.
+// rows' steps, line by line, run by one thread: PAPER.md §4, SPEC S:361-392 for the
+// tests and breakdowns, DESIGN.md §4 R5-R18 for the readings), the BiCGStab(ℓ) Gram/Cholesky step
+// (R18), and the cluster solver's host entry points.  See solve.cu's header for the schedules.
 #pragma once
 #include <cuda_runtime.h>
 
