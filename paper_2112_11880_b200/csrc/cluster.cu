@@ -54,6 +54,22 @@ __device__ __forceinline__ void ctx_copy(SolveCtx* dst, const SolveCtx* src) {
     for (int i = threadIdx.x; i < (int)(sizeof(SolveCtx) / 8); i += blockDim.x) d[i] = s[i];
 }
 
+// The x0 = 0 start inside a cluster kernel (init = 1: k_set_ctx and k_init_zero are not launched):
+// OpInitZero's per-row sums {‖b‖², ‖r0‖², Re r0ᵀr0, Im r0ᵀr0} of one own row (r0 = b), and the
+// workspace tickets cleared as k_set_ctx does (recycled workspace memory; CTA 0 only).
+__device__ __forceinline__ void cl_init_row(const double2 bl, double (&acc)[4]) {
+    const double bb = cabs2(bl);
+    acc[0] += bb;
+    acc[1] += bb;
+    acc[2] = fma(bl.x, bl.x, fma(-bl.y, bl.y, acc[2]));
+    acc[3] = fma(2.0 * bl.x, bl.y, acc[3]);
+}
+__device__ __forceinline__ void cl_init_tickets(const SolveCtx& cs) {
+    namespace cg = cooperative_groups;
+    if (cg::this_cluster().block_rank() == 0 && threadIdx.x == 0)
+        for (int i = 0; i < kTickets; i++) cs.tickets[i] = 0u;
+}
+
 struct ClusterRed {
     double slot[2][kCMaxCta][kMaxRed];  // every CTA's partial sums, pushed here by their owners (double-buffered)
     double warp_part[kMaxRed][kCWarps];
@@ -403,13 +419,14 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
 // only x += η1·d1 remains; half = 2: T3's d and x updates without y1).  y1 and y2 are gathered by
 // the SpMVs, so they are also written to global memory.
 template <int W, bool VS>
-__global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, const CsrDev A, int nnz_max, int do_true) {
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, const __grid_constant__ SolveCtx hctx,
+                                                              const CsrDev A, int nnz_max, int do_true, int init) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ double2 own[];
     __shared__ SolveCtx cs;
     __shared__ ClusterRed R;
-    ctx_copy(&cs, gctx);
+    ctx_copy(&cs, init ? &hctx : gctx);
     if (threadIdx.x == 0) R.parity = 0;
     const int n = (int)A.n_rows;
     const int ncta = (int)cl.num_blocks();
@@ -424,23 +441,60 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, co
     __syncthreads();
     SolveCtx* c = &cs;
     double2 *xg = cs.x, *y1g = cs.y1, *y2g = cs.y2;
-    for (int l = threadIdx.x; l < nr; l += kCBlock) {  // state after the init kernel and K0
-        const int i = row0 + l;
-        X[l] = xg[i];
-        Wv[l] = cs.w[i];
-        Y1[l] = y1g[i];
-        U1[l] = cs.u1[i];
-        V[l] = cs.v[i];
-        D[l] = cs.d[i];
-        RT[l] = cs.rt[i];
-        U2[l] = make_double2(0.0, 0.0);
-        Y2[l] = make_double2(0.0, 0.0);
+    double iacc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (init) {  // x0 = 0: x = 0 ; w = y1 = r̃ = b ; d = 0 (OpInitZero kind 4); y1 published for K0
+        const double2* bg = cs.b;
+        for (int l = threadIdx.x; l < nr; l += kCBlock) {
+            const double2 bl = bg[row0 + l];
+            X[l] = make_double2(0.0, 0.0);
+            Wv[l] = Y1[l] = RT[l] = bl;
+            y1g[row0 + l] = bl;
+            D[l] = U1[l] = V[l] = make_double2(0.0, 0.0);
+            U2[l] = Y2[l] = make_double2(0.0, 0.0);
+            cl_init_row(bl, iacc);
+        }
+        cl_init_tickets(cs);
+    } else {
+        for (int l = threadIdx.x; l < nr; l += kCBlock) {  // state after the init kernel and K0
+            const int i = row0 + l;
+            X[l] = xg[i];
+            Wv[l] = cs.w[i];
+            Y1[l] = y1g[i];
+            U1[l] = cs.u1[i];
+            V[l] = cs.v[i];
+            D[l] = cs.d[i];
+            RT[l] = cs.rt[i];
+            U2[l] = make_double2(0.0, 0.0);
+            Y2[l] = make_double2(0.0, 0.0);
+        }
     }
     const double2* gval = cl_stage<VS>(A, row0, nr, sval, scol, soff);
     __syncthreads();
     constexpr int RPP = kCBlock / W;
     const int sub = threadIdx.x & (W - 1);
     const int grp = threadIdx.x / W;
+    if (init) {
+        cl_sum<4>(iacc, R);  // its cluster barrier also publishes y1 for K0's gathers
+        if (threadIdx.x == 0) fin_init_tfqmr(c, R.tot);
+        __syncthreads();
+        if (!c->done) {  // K0: u1 = v = A y1 ; σ = ⟨r̃, v⟩ (EpiT4Tfqmr<S_K0_TFQMR>, fin_sigma_tfqmr)
+            double acc[2] = {0.0, 0.0};
+            for (int b = 0; b < nr; b += RPP) {
+                const int l = b + grp;
+                const double2 y = cl_row<W, VS>(gval, sval, scol, soff, y1g, l, l < nr, sub);
+                if (sub == 0 && l < nr) {
+                    U1[l] = y;
+                    V[l] = y;
+                    const double2 q = RT[l];
+                    acc[0] = fma(q.x, y.x, fma(q.y, y.y, acc[0]));
+                    acc[1] = fma(q.x, y.y, fma(-q.y, y.x, acc[1]));
+                }
+            }
+            cl_sum<2>(acc, R);
+            if (threadIdx.x == 0) fin_sigma_tfqmr(c, R.tot);
+            __syncthreads();
+        }
+    }
     int bodies = 0;
     while (!c->done) {
         {   // T1: y2 = y1 − α v ; w −= α u1 ; ‖w‖²
@@ -561,13 +615,14 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, co
 // the per-row arithmetic of EpiK1Cg/OpK2Cg/OpK3Cg and EpiK1Cocg/OpK2Cocg/OpK3Cocg, the same
 // scalar steps.  p is gathered by the SpMV, so it is also written to global memory.
 template <int W, bool VS, bool COCG>
-__global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const CsrDev A, int nnz_max, int do_true) {
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const __grid_constant__ SolveCtx hctx,
+                                                           const CsrDev A, int nnz_max, int do_true, int init) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ double2 own[];
     __shared__ SolveCtx cs;
     __shared__ ClusterRed R;
-    ctx_copy(&cs, gctx);
+    ctx_copy(&cs, init ? &hctx : gctx);
     if (threadIdx.x == 0) R.parity = 0;
     const int n = (int)A.n_rows;
     const int ncta = (int)cl.num_blocks();
@@ -581,10 +636,29 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const
     __syncthreads();
     SolveCtx* c = &cs;
     double2 *xg = cs.x, *pg = cs.p;
-    for (int l = threadIdx.x; l < nr; l += kCBlock) {
-        X[l] = xg[row0 + l];
-        Rv[l] = cs.r[row0 + l];
-        P[l] = pg[row0 + l];
+    if (init) {  // x0 = 0: x = 0 ; r = p = b (OpInitZero kinds 1, 3) ; fin_init_cg / fin_init_cocg
+        const double2* bg = cs.b;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int l = threadIdx.x; l < nr; l += kCBlock) {
+            const double2 bl = bg[row0 + l];
+            X[l] = make_double2(0.0, 0.0);
+            Rv[l] = P[l] = bl;
+            pg[row0 + l] = bl;
+            cl_init_row(bl, acc);
+        }
+        cl_init_tickets(cs);
+        cl_sum<4>(acc, R);  // its cluster barrier also publishes p for the K1 gathers
+        if (threadIdx.x == 0) {
+            if (COCG) fin_init_cocg(c, R.tot);
+            else fin_init_cg(c, R.tot);
+        }
+        __syncthreads();
+    } else {
+        for (int l = threadIdx.x; l < nr; l += kCBlock) {
+            X[l] = xg[row0 + l];
+            Rv[l] = cs.r[row0 + l];
+            P[l] = pg[row0 + l];
+        }
     }
     const double2* gval = cl_stage<VS>(A, row0, nr, sval, scol, soff);
     __syncthreads();
@@ -703,7 +777,8 @@ __device__ __noinline__ void fin_gram_any(SolveCtx* c, const double* g, int ell)
     }
 }
 template <int W, bool VS>
-__global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const CsrDev A, int nnz_max, int do_true) {
+__global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const __grid_constant__ SolveCtx hctx,
+                                                           const CsrDev A, int nnz_max, int do_true, int init) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ double2 own[];  // (2ℓ+4) × rpc: r̂_0..ℓ, û_0..ℓ, x, r̃ | [values] | columns | offsets
@@ -712,7 +787,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
     __shared__ double gpart[kGramMax][kGramSub];
     __shared__ double gslot[2][kGramMax];
     __shared__ double gtot[kGramMax];
-    ctx_copy(&cs, gctx);
+    ctx_copy(&cs, init ? &hctx : gctx);
     if (threadIdx.x == 0) R.parity = 0;
     __syncthreads();
     const int n = (int)A.n_rows;
@@ -733,14 +808,32 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
     double2* const* rl = cs.rl;  // global copies: only the SpMV inputs r̂_j / û_j are written through
     double2* const* ul = cs.ul;
     double2* xg = cs.x;
-    for (int l = threadIdx.x; l < nr; l += kCBlock) {
-        const int i = row0 + l;
-        for (int q = 0; q <= ell; q++) {
-            Rs[q * rpc + l] = rl[q][i];
-            Us[q * rpc + l] = ul[q][i];
+    if (init) {  // x0 = 0: r̂_0 = r̃ = b, û_0 = 0, x = 0 (OpInitZero kind 5) ; fin_init_bl
+        const double2* bg = cs.b;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int l = threadIdx.x; l < nr; l += kCBlock) {
+            const double2 bl = bg[row0 + l];
+            for (int q = 0; q <= ell; q++) Rs[q * rpc + l] = Us[q * rpc + l] = make_double2(0.0, 0.0);
+            Rs[l] = bl;
+            Us[rpc + l] = bl;  // (the shared init's p = û_1 = r0; overwritten before use)
+            X[l] = make_double2(0.0, 0.0);
+            RT[l] = bl;
+            cl_init_row(bl, acc);
         }
-        X[l] = xg[i];
-        RT[l] = cs.rh[i];
+        cl_init_tickets(cs);
+        cl_sum<4>(acc, R);
+        if (threadIdx.x == 0) fin_init_bl(c, R.tot);
+        __syncthreads();
+    } else {
+        for (int l = threadIdx.x; l < nr; l += kCBlock) {
+            const int i = row0 + l;
+            for (int q = 0; q <= ell; q++) {
+                Rs[q * rpc + l] = rl[q][i];
+                Us[q * rpc + l] = ul[q][i];
+            }
+            X[l] = xg[i];
+            RT[l] = cs.rh[i];
+        }
     }
     const double2* gval = cl_stage<VS>(A, row0, nr, sval, scol, soff);
     __syncthreads();
@@ -1045,11 +1138,8 @@ bool cluster_launch(zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc, const CsrDev&
     int dt = do_true ? 1 : 0;
     int in = init ? 1 : 0;
     cudaError_t e;
-    if (kind == 0) {
+    {
         void* args[] = {(void*)&dc, (void*)&hc, (void*)&av, (void*)&nzi, (void*)&dt, (void*)&in};
-        e = cudaLaunchKernelExC(&cfg, cluster_kernel(w, vs, 0), args);
-    } else {
-        void* args[] = {(void*)&dc, (void*)&av, (void*)&nzi, (void*)&dt};
         e = cudaLaunchKernelExC(&cfg, cluster_kernel(w, vs, kind), args);
     }
     if (e != cudaSuccess) {

@@ -1841,9 +1841,9 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     int64_t n_spmv = 0;
 
     // ---- init: context, r0 = b − A x0 (or b), ‖b‖, hist[0]
-    // (mode-5 BiCGStab from x0 = 0: the cluster kernel does both itself, one launch per solve)
-    const bool fused_init = mode == 5 && method == ZK_BICGSTAB && !x0 &&
-                            !(getenv("ZK_CLUSTER_INIT") && atoi(getenv("ZK_CLUSTER_INIT")) == 0);
+    // (mode 5 from x0 = 0: the cluster kernel does both itself — and TFQMR's K0 — one launch per
+    // solve; ZK_CLUSTER_INIT=0 launches k_set_ctx + k_init_zero (+ k0_tfqmr) first)
+    const bool fused_init = mode == 5 && !x0 && !(getenv("ZK_CLUSTER_INIT") && atoi(getenv("ZK_CLUSTER_INIT")) == 0);
     if (!fused_init) {
         k_set_ctx<<<1, 1, 0, s>>>(dc, hc);
         ZK_CUDA(cudaGetLastError());
@@ -1897,7 +1897,8 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
                : kind == 3 ? dist_finish<S_INIT_COCG>(A, dc, 4, s)
                : kind == 4 ? dist_finish<S_INIT_TFQMR>(A, dc, 4, s)
                            : dist_finish<S_INIT_BL>(A, dc, 4, s));
-    if (method == ZK_TFQMR) {  // u1 = v = A y1 and σ = ⟨r̃, v⟩ → α for iteration 1
+    if (method == ZK_TFQMR && fused_init) n_spmv++;  // K0 inside the cluster kernel
+    if (method == ZK_TFQMR && !fused_init) {  // u1 = v = A y1 and σ = ⟨r̃, v⟩ → α for iteration 1
         if (A->dist) ZK_TRY(dist_halo(A, hc.y1, s));
         ZK_TRY(with_spmv(A, [&](auto wc, auto mc) -> zk_status {
             constexpr int W = decltype(wc)::value, MODE = decltype(mc)::value;
@@ -1991,7 +1992,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         }
         const int fins = !A->dist ? 0 : method == ZK_BICGSTAB ? 4 : method == ZK_TFQMR ? 3
                        : method == kBiCGStabL ? 3 * ell + 1 : 2;  // dist: 1-thread finish kernels
-        const int pre = method == ZK_TFQMR ? (A->dist ? 2 : 1) : 0;                               // TFQMR: K0 (+ its finish)
+        const int pre = method == ZK_TFQMR && !fused_init ? (A->dist ? 2 : 1) : 0;               // TFQMR: K0 (+ its finish)
         // mode 5: set_ctx + init (+ TFQMR's K0) + the cluster kernel (+ Jacobi: x = M⁻¹u and k_true)
         info->gpu_launches = mode == 5 ? (fused_init ? 1 : 3) + pre + (jacobi ? 2 : 0)
                                                        : 3 + pre + out.bodies * (per_body + fins) + (A->dist ? 2 : 0);

@@ -555,7 +555,7 @@ def test_cg_cocg_cluster_parity(method, cfg, variant, monkeypatch):
         b = gen.make_rhs(m)
         ref = oracle.cocg(m, b, tol=1e-8)
     r = gpu_solve(m, b, tol=1e-8, method=method)
-    assert r["loop_mode"] == 5 and r["gpu_launches"] == 3  # set_ctx, init, the cluster kernel
+    assert r["loop_mode"] == 5 and r["gpu_launches"] == 1  # the cluster kernel starts from x0 = 0 itself
     assert r["status"] == ref["status"] == "CONVERGED"
     assert abs(r["iters"] - ref["iters"]) <= 0.05 * ref["iters"], (r["iters"], ref["iters"])
     k = min(12, r["iters"]) + 1
@@ -700,3 +700,44 @@ def test_create_solve_destroy_loop_on_side_stream(cfg):
         assert got[0] == ref[0] and got[1] == ref[1] == "CONVERGED"
         assert np.array_equal(got[2], ref[2]), f"round {rnd}: x differs"
     keep.close()
+
+
+
+@pytest.mark.parametrize("method", ["cg", "cocg", "tfqmr", "bicgstab_l2", "bicgstab_l8"])
+@pytest.mark.parametrize("cfg", ["C1", "T0"])
+def test_cluster_fused_init_all_solvers(cfg, method, monkeypatch):
+    """Every cluster solver starts from x0 = 0 inside its kernel (OpInitZero's rows and sums, the
+    method's fin_init step; TFQMR also its K0 SpMV and σ): one launch per solve instead of
+    k_set_ctx + k_init_zero (+ k0_tfqmr) + the cluster kernel.  Both starts against the oracle (the
+    per-method bars of the cluster parity tests) and against each other (same count ±1, histories
+    to 1e-9 — 1e-3 for BiCGStab(8), R20 — only the init reductions' order differs)."""
+    monkeypatch.setenv("ZK_LOOP_MODE", "5")
+    ell = int(method[-1]) if method.startswith("bicgstab_l") else 8
+    meth = "bicgstab_l" if method.startswith("bicgstab_l") else method
+    if method == "cg":
+        m = gen.make_matrix(cfg, eta=0.0, twist_seed=gen.SEED_TWIST)
+        b = np.exp(1j * m["phase"]) * gen.make_rhs(m)
+        refs = [oracle.cg(m, b, tol=1e-8, order=o) for o in ORDERS]
+    else:
+        m = gen.make_matrix(cfg)
+        b = gen.make_rhs(m)
+        fn = {"cocg": oracle.cocg, "tfqmr": oracle.tfqmr,
+              "bicgstab_l": lambda mm, bb, **kw: oracle.bicgstab_l(mm, bb, ell=ell, **kw)}[meth]
+        refs = [fn(m, b, tol=1e-8, order=o) for o in ORDERS]
+    its = [q["iters"] for q in refs]
+    out = {}
+    for init in ("0", "1"):
+        monkeypatch.setenv("ZK_CLUSTER_INIT", init)
+        r = gpu_solve(m, b, tol=1e-8, maxit=1000, method=meth, ell=ell)
+        extra = 1 if (meth == "tfqmr" and init == "0") else 0
+        assert r["loop_mode"] == 5 and r["gpu_launches"] == (1 if init == "1" else 3 + extra)
+        assert r["status"] == "CONVERGED" and 0.95 * min(its) - 1 <= r["iters"] <= 1.05 * max(its) + 1, (r["iters"], its)
+        assert r["true_relres"] <= 10 * 1e-8
+        out[init] = r
+    a, f = out["0"], out["1"]
+    assert abs(a["iters"] - f["iters"]) <= 1
+    k = min(a["iters"], f["iters"], 8) + 1
+    # BiCGStab(8)'s normal-equations step amplifies rounding-order differences (DESIGN.md R20: the
+    # oracle's own summation orders spread by 9.2e-5 at ℓ = 8, bar 1e-3); 1e-9 elsewhere
+    bar = 1e-3 if method == "bicgstab_l8" else 1e-9
+    assert np.max(np.abs(a["hist"][:k] - f["hist"][:k]) / a["hist"][:k]) <= bar
