@@ -224,6 +224,10 @@ __device__ __forceinline__ void cl_true(SolveCtx* c, ClusterRed& R, const double
 #ifndef ZK_CLUSTER_PROF
 #define ZK_CLUSTER_PROF 0
 #endif
+#define CPT(k)                                                                        \
+    do {                                                                              \
+        if (ZK_CLUSTER_PROF && threadIdx.x == 0 && cl.block_rank() == 0) pts_[k] = gtimer(); \
+    } while (0)
 #define CPROF(k)                                                            \
     do {                                                                    \
         if (ZK_CLUSTER_PROF && threadIdx.x == 0 && cl.block_rank() == 0) {  \
@@ -240,6 +244,8 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
     extern __shared__ double2 own[];
     __shared__ SolveCtx cs;
     __shared__ ClusterRed R;
+    unsigned long long pts_[8] = {};  // ZK_CLUSTER_PROF: global-timer marks of the prologue / epilogue
+    CPT(0);
     ctx_copy(&cs, init ? &hctx : gctx);
     if (threadIdx.x == 0) R.parity = 0;
     const int n = (int)A.n_rows;
@@ -263,17 +269,14 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
             X[l] = make_double2(0.0, 0.0);
             Rv[l] = RH[l] = P[l] = bl;
             pg[row0 + l] = bl;
-            const double bb = cabs2(bl);
-            acc[0] += bb;
-            acc[1] += bb;
-            acc[2] = fma(bl.x, bl.x, fma(-bl.y, bl.y, acc[2]));
-            acc[3] = fma(2.0 * bl.x, bl.y, acc[3]);
+            cl_init_row(bl, acc);
         }
-        if (cl.block_rank() == 0 && threadIdx.x == 0)
-            for (int i = 0; i < kTickets; i++) cs.tickets[i] = 0u;  // as k_set_ctx: recycled workspace
+        cl_init_tickets(cs);
+        CPT(1);
         cl_sum<4>(acc, R);  // its cluster barrier also publishes p for the K1 gathers
         if (threadIdx.x == 0) fin_init_bicg(c, R.tot);
         __syncthreads();
+        CPT(2);
     } else {
         for (int l = threadIdx.x; l < nr; l += kCBlock) {  // r0, r̂, p, x0 from the init kernel
             X[l] = xg[row0 + l];
@@ -284,6 +287,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
     }
     const double2* gval = cl_stage<VS>(A, row0, nr, sval, scol, soff);
     __syncthreads();
+    CPT(3);
     constexpr int RPP = kCBlock / W;  // rows per SpMV pass
     const int sub = threadIdx.x & (W - 1);
     const int grp = threadIdx.x / W;
@@ -402,16 +406,23 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
         }
         bodies++;
     }
-    if (ZK_CLUSTER_PROF && threadIdx.x == 0 && cl.block_rank() == 0)
-        printf("cluster_prof bodies %d cycles: k1 %lld red %lld fin %lld | k2 %lld red %lld fin %lld | k3 %lld red %lld fin %lld | k4 %lld red %lld fin %lld | k5+sync %lld\n",
-               bodies, prof_[0], prof_[1], prof_[2], prof_[3], prof_[4], prof_[5], prof_[6], prof_[7], prof_[8],
-               prof_[9], prof_[10], prof_[11], prof_[12]);
+    CPT(4);
     for (int l = threadIdx.x; l < nr; l += kCBlock) xg[row0 + l] = X[l];  // the solution leaves shared memory
     if (do_true) cl_true<W, VS>(c, R, gval, sval, scol, soff, xg, row0, nr);
+    CPT(5);
     if (threadIdx.x == 0) cs.bodies = bodies;
     __syncthreads();
     if (cl.block_rank() == 0) ctx_copy(gctx, &cs);
     cl.sync();  // no CTA leaves while another may still read its reduction slots
+    CPT(6);
+    if (ZK_CLUSTER_PROF && threadIdx.x == 0 && cl.block_rank() == 0) {
+        printf("cluster_prof bodies %d cycles: k1 %lld red %lld fin %lld | k2 %lld red %lld fin %lld | k3 %lld red %lld fin %lld | k4 %lld red %lld fin %lld | k5+sync %lld\n",
+               bodies, prof_[0], prof_[1], prof_[2], prof_[3], prof_[4], prof_[5], prof_[6], prof_[7], prof_[8],
+               prof_[9], prof_[10], prof_[11], prof_[12]);
+        printf("cluster_prof ns: ctx+init rows %llu | init reduce %llu | stage %llu | loop %llu | x out + true %llu | ctx out %llu\n",
+               pts_[1] - pts_[0], pts_[2] - pts_[1], pts_[3] - pts_[2], pts_[4] - pts_[3], pts_[5] - pts_[4],
+               pts_[6] - pts_[5]);
+    }
 }
 
 // TFQMR (NEXT-2) in one cluster: the per-row arithmetic of OpT1/EpiT2/OpT3/EpiT4 and the same

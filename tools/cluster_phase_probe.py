@@ -17,6 +17,6 @@ for cfg in sys.argv[1:] or ["C1", "T0", "C2"]:
     b = torch.from_numpy(gen.make_rhs(m)).cuda()
     ws = zk.alloc_workspace(A, "bicgstab", 64)
     for _ in range(3):
-        r = zk.solve(A, b, tol=1e-300, maxit=20, method="bicgstab", workspace=ws)
+        r = zk.solve(A, b, tol=1e-300, maxit=int(os.environ.get("MAXIT", "20")), method="bicgstab", workspace=ws)
     torch.cuda.synchronize()
     print(cfg, "n", m["n"], "W", A.info.get("lanes_per_row"), "loop_mode", r["loop_mode"], "solve_ms", r["solve_ms"], flush=True)
