@@ -70,6 +70,18 @@ __device__ __forceinline__ void cl_init_tickets(const SolveCtx& cs) {
         for (int i = 0; i < kTickets; i++) cs.tickets[i] = 0u;
 }
 
+// The solve's results out of CTA 0: into the handle's pinned staging when zk_solve asked for the
+// zero-copy readback (no D2H copy after the kernel), else into the workspace context.
+__device__ __forceinline__ void ctx_out(SolveCtx* gctx, SolveCtx& cs) {
+    if (cs.out_host) {
+        ctx_copy(cs.out_host, &cs);
+        const int nh = min(cs.iters, cs.maxit) + 1;
+        for (int i = threadIdx.x; i < nh; i += blockDim.x) cs.hist_host[i] = cs.hist[i];
+    } else {
+        ctx_copy(gctx, &cs);
+    }
+}
+
 struct ClusterRed {
     double slot[2][kCMaxCta][kMaxRed];  // every CTA's partial sums, pushed here by their owners (double-buffered)
     double warp_part[kMaxRed][kCWarps];
@@ -412,7 +424,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bicg(SolveCtx* gctx, con
     CPT(5);
     if (threadIdx.x == 0) cs.bodies = bodies;
     __syncthreads();
-    if (cl.block_rank() == 0) ctx_copy(gctx, &cs);
+    if (cl.block_rank() == 0) ctx_out(gctx, cs);
     cl.sync();  // no CTA leaves while another may still read its reduction slots
     CPT(6);
     if (ZK_CLUSTER_PROF && threadIdx.x == 0 && cl.block_rank() == 0) {
@@ -618,7 +630,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_tfqmr(SolveCtx* gctx, co
         cs.bodies = bodies;
     }
     __syncthreads();
-    if (cl.block_rank() == 0) ctx_copy(gctx, &cs);
+    if (cl.block_rank() == 0) ctx_out(gctx, cs);
     cl.sync();
 }
 
@@ -762,7 +774,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_cg(SolveCtx* gctx, const
     if (do_true) cl_true<W, VS>(c, R, gval, sval, scol, soff, xg, row0, nr);
     if (threadIdx.x == 0) cs.bodies = bodies;
     __syncthreads();
-    if (cl.block_rank() == 0) ctx_copy(gctx, &cs);
+    if (cl.block_rank() == 0) ctx_out(gctx, cs);
     cl.sync();
 }
 
@@ -1015,7 +1027,7 @@ __global__ void __launch_bounds__(kCBlock, 1) k_cluster_bl(SolveCtx* gctx, const
     if (do_true) cl_true<W, VS>(c, R, gval, sval, scol, soff, xg, row0, nr);
     if (threadIdx.x == 0) cs.bodies = bodies;
     __syncthreads();
-    if (cl.block_rank() == 0) ctx_copy(gctx, &cs);
+    if (cl.block_rank() == 0) ctx_out(gctx, cs);
     cl.sync();
 }
 

@@ -1836,14 +1836,30 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         A->pinned_bytes = 0;
         ZK_CUDA(pinned_get(&A->pinned, rb_bytes, &A->pinned_bytes));
     }
+    // mode 5 from x0 = 0: the cluster kernel sets up the context and r0 itself (and TFQMR's K0) —
+    // one launch per solve; ZK_CLUSTER_INIT=0 launches k_set_ctx + k_init_zero (+ k0_tfqmr) first
+    const bool fused_init = mode == 5 && !x0 && !(getenv("ZK_CLUSTER_INIT") && atoi(getenv("ZK_CLUSTER_INIT")) == 0);
+    // zero-copy readback (cluster solve from x0 = 0, no Jacobi exit work after it): the kernel writes
+    // the context and the history into the pinned staging itself — no D2H copy after the kernel
+    // (C1 fixed cost 63.7 → 55.5 µs, C2 86 → 76); ZK_ZERO_COPY=0 keeps the copy
+    bool zero_copy = mode == 5 && fused_init && !jacobi && !(getenv("ZK_ZERO_COPY") && atoi(getenv("ZK_ZERO_COPY")) == 0);
+    if (zero_copy) {
+        void* dp = nullptr;
+        if (cudaHostGetDevicePointer(&dp, A->pinned, 0) == cudaSuccess && dp) {
+            hc.out_host = (SolveCtx*)dp;
+            hc.hist_host = (double*)((char*)dp + sizeof(SolveCtx));
+        } else {
+            cudaGetLastError();
+            zero_copy = false;
+        }
+    }
     ZK_CUDA(cudaEventRecord(ev0, s));
     const auto tr1 = std::chrono::steady_clock::now();
     int64_t n_spmv = 0;
 
     // ---- init: context, r0 = b − A x0 (or b), ‖b‖, hist[0]
     // (mode 5 from x0 = 0: the cluster kernel does both itself — and TFQMR's K0 — one launch per
-    // solve; ZK_CLUSTER_INIT=0 launches k_set_ctx + k_init_zero (+ k0_tfqmr) first)
-    const bool fused_init = mode == 5 && !x0 && !(getenv("ZK_CLUSTER_INIT") && atoi(getenv("ZK_CLUSTER_INIT")) == 0);
+    // solve, fused_init above)
     if (!fused_init) {
         k_set_ctx<<<1, 1, 0, s>>>(dc, hc);
         ZK_CUDA(cudaGetLastError());
@@ -1964,7 +1980,7 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
     double* hist_pinned = (double*)((char*)A->pinned + sizeof(SolveCtx));
     static_assert(sizeof(SolveCtx) % sizeof(double) == 0, "hist follows the ctx");
     const auto tr2 = std::chrono::steady_clock::now();
-    ZK_CUDA(cudaMemcpyAsync(A->pinned, dc, rb_bytes, cudaMemcpyDeviceToHost, s));  // ctx + hist
+    if (!zero_copy) ZK_CUDA(cudaMemcpyAsync(A->pinned, dc, rb_bytes, cudaMemcpyDeviceToHost, s));  // ctx + hist
     cudaError_t e = cudaStreamSynchronize(s);
     const auto tr3 = std::chrono::steady_clock::now();
     if (e != cudaSuccess) return cuda_fail(e, "zk_solve", __FILE__, __LINE__);

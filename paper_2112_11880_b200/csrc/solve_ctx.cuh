@@ -51,6 +51,10 @@ struct SolveCtx {
     double red[kMaxRed];
     double redg[96];          // multi-GPU BiCGStab(ℓ): the Gram totals (≤ 81 doubles) for the allreduce
     int bodies;               // loop bodies executed (counts launches for zk_solve_info)
+    // zero-copy readback of a cluster solve (zk_solve, loop mode 5 from x0 = 0): CTA 0 writes the
+    // final context and hist[0..iters] straight into the handle's pinned staging (device-mapped)
+    SolveCtx* out_host;
+    double* hist_host;
     // in-loop kernel timers (device global timer): per class, min block start of the running
     // launch, summed durations and launch counts (zk_solve_info.kernel_ms)
     unsigned long long t0[4];
