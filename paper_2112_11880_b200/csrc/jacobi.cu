@@ -74,7 +74,10 @@ zk_status dist_agree_failed(zk_comm_s* c, bool failed, cudaStream_t s, int* any_
 // through the SpMV's halo plan (dinv is laid out like a gathered vector: [local rows | halo slots]),
 // after agreeing on whether any rank lacks a diagonal (so no rank is left in the exchange).
 zk_status jacobi_prepare(zk_csr_s* A, cudaStream_t s) {
-    if (A->jac_val) return ZK_OK;
+    // built already?  (jac_diag, not jac_val: a handle whose CSR value copy was dropped keeps A·M⁻¹
+    // only in the SELL copy, jac_val stays NULL — keying on it rebuilt, and leaked, A·M⁻¹ on every
+    // Jacobi solve above 16384 rows)
+    if (A->jac_diag) return ZK_OK;
     const int64_t n = A->n_rows, nnz = A->nnz;
     const int64_t glen = A->dist ? dist_gather_len(A) : n;
     double2 *val = nullptr, *diag = nullptr, *dinv = nullptr;
@@ -168,7 +171,8 @@ void jacobi_destroy(zk_csr_s* A, bool synced) {
     dev_free(A->jac_val, synced);
     dev_free(A->jac_diag, synced);
     dev_free(A->jac_dinv, synced);
-    A->jac_val = A->jac_diag = A->jac_dinv = nullptr;
+    dev_free(A->jac_sl_val, synced);  // (the SELL copy's A·M⁻¹ values: stale after zk_csr_update_values)
+    A->jac_val = A->jac_diag = A->jac_dinv = A->jac_sl_val = nullptr;
 }
 
 }  // namespace zk

@@ -741,3 +741,35 @@ def test_cluster_fused_init_all_solvers(cfg, method, monkeypatch):
     # oracle's own summation orders spread by 9.2e-5 at ℓ = 8, bar 1e-3); 1e-9 elsewhere
     bar = 1e-3 if method == "bicgstab_l8" else 1e-9
     assert np.max(np.abs(a["hist"][:k] - f["hist"][:k]) / a["hist"][:k]) <= bar
+
+
+def test_jacobi_cache_without_csr_values():
+    """Above 16384 rows a copied handle keeps A·M⁻¹ only in its SELL copy (csr_values_kept = 0):
+    Jacobi-BiCGStab builds it once per handle — repeated solves allocate no device memory and give
+    the same bits — and zk_csr_update_values invalidates it (regression: the cache was keyed on the
+    CSR copy and A·M⁻¹ was rebuilt and leaked on every solve)."""
+    m = gen.make_matrix("T1")
+    assert m["n"] > 16384
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+    assert A.info["csr_values_kept"] == 0 and A.info["spmv_mode"] == 3
+    b = cuda(gen.make_rhs(m))
+    x = torch.empty_like(b)
+    ws = zk.alloc_workspace(A, "bicgstab_jacobi", 1000)
+    r0 = zk.solve(A, b, tol=1e-8, method="bicgstab_jacobi", workspace=ws, x=x)
+    x0 = x.cpu()  # (host-side comparisons: no torch kernel is loaded lazily inside the measured loop)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(6):
+        r = zk.solve(A, b, tol=1e-8, method="bicgstab_jacobi", workspace=ws, x=x)
+        assert r["iters"] == r0["iters"] and torch.equal(x.cpu(), x0)
+    torch.cuda.synchronize()
+    assert free0 - torch.cuda.mem_get_info()[0] < (4 << 20)   # one A·M⁻¹ SELL copy is ≈ 27 MB
+    its = [oracle.bicgstab_jacobi(m, gen.make_rhs(m), tol=1e-8, order=o)["iters"] for o in ORDERS]
+    assert r0["status"] == "CONVERGED" and 0.95 * min(its) <= r0["iters"] <= 1.05 * max(its), (r0["iters"], its)
+    # new values on the same pattern: A·M⁻¹ rebuilt from them.  For 2·A every step of the scaling
+    # is exact (powers of two), so A·M⁻¹ and the iterates are bitwise the same and x is exactly x0 / 2
+    A.update_values(2.0 * m["values"])
+    r2 = zk.solve(A, b, tol=1e-8, method="bicgstab_jacobi", workspace=ws, x=x)
+    assert r2["status"] == "CONVERGED" and r2["iters"] == r0["iters"]
+    assert torch.equal(2.0 * x.cpu(), x0)
+    A.close()
