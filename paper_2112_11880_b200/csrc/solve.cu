@@ -1794,9 +1794,10 @@ extern "C" zk_status zk_solve(zk_csr A, const zk_z* b, const zk_z* x0, double to
         mode = A->dist ? 3 : 1;
     if (A->dist && (mode == 1 || mode == 5)) mode = 3;  // collectives inside WHILE bodies / clusters are not used
     static_assert(kBiCGStabL < (int)(sizeof(((zk_csr_s*)nullptr)->graph) / sizeof(GraphCache)), "graph slot per method");
-    GraphCache& gc = A->graph[method];
-    // one graph per (method, ℓ, Jacobi): the SpMV kernels take the CSR view (A or A·M⁻¹) as a
-    // launch parameter baked into the graph
+    // one graph per (method, ℓ, Jacobi) — Jacobi-BiCGStab in its own slot (the ABI's method code), so
+    // alternating plain and Jacobi solves on one handle do not rebuild each other's graph; the SpMV
+    // kernels take the CSR view (A or A·M⁻¹) as a launch parameter baked into the graph
+    GraphCache& gc = A->graph[jacobi ? (int)ZK_BICGSTAB_JACOBI : method];
     const int gkey = ((method * 16 + ell) * 2 + (jacobi ? 1 : 0)) * 4 + tail_kind(A);
     // key: workspace pointer, loop mode, method/ℓ/Jacobi and maxit (ws_layout places the partials,
     // tickets and vectors after hist[maxit+1]; BiCGStab(ℓ) bakes its vector pointers into the graph)
