@@ -773,3 +773,44 @@ def test_jacobi_cache_without_csr_values():
     assert r2["status"] == "CONVERGED" and r2["iters"] == r0["iters"]
     assert torch.equal(2.0 * x.cpu(), x0)
     A.close()
+
+
+def test_concurrent_solves_on_two_streams():
+    """Two host threads, each with its own handle and torch stream, solving at the same time (a
+    cluster solve on C1 and a WHILE-graph solve on T1, plus zdotc / dznrm2 on each stream): every
+    result equals the one computed alone (per-handle staging, per-stream reduction scratch, the
+    process-wide pinned free list and memory pool are shared safely)."""
+    import threading
+    cases = []
+    for cfg in ("C1", "T1"):
+        m = gen.make_matrix(cfg)
+        A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+        b = cuda(gen.make_rhs(m))
+        alone = zk.solve(A, b, tol=1e-8, maxit=1000)
+        cases.append((A, b, alone["x"].cpu(), alone["iters"], float(zk.dznrm2(b).cpu()[0])))
+    errors = []
+
+    def work(A, b, x_ref, it_ref, nb_ref):
+        st = torch.cuda.Stream()
+        try:
+            with torch.cuda.stream(st):
+                for _ in range(15):
+                    r = zk.solve(A, b, tol=1e-8, maxit=1000, stream=st)
+                    nb = zk.dznrm2(b, stream=st)
+                    d = zk.zdotc(b, b, stream=st)
+                    st.synchronize()
+                    if r["iters"] != it_ref or not torch.equal(r["x"].cpu(), x_ref):
+                        errors.append("solve differs")
+                    if float(nb.cpu()[0]) != nb_ref or abs(float(d.cpu()[0].real) - nb_ref ** 2) > 1e-12 * nb_ref ** 2:
+                        errors.append("reduction differs")
+        except Exception as e:  # noqa: BLE001 — reported below
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=work, args=c) for c in cases]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors[:3]
+    for c in cases:
+        c[0].close()
