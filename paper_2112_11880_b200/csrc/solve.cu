@@ -1587,6 +1587,12 @@ static void drop_graph(GraphCache& g) {
 }
 
 // WHILE-node graph: body = one iteration; condition written by the last kernel of the body.
+// Iterations per WHILE-graph body: the conditional node's per-body cost is paid once per
+// kWhileUnroll iterations; an exit inside a body leaves at most kWhileUnroll − 1 iterations of
+// early-returning kernels.  Measured (tools/ab_unroll.sh, µs per iteration, 1 → 4): Audi3D-4 (C3)
+// BiCGStab 148.9 → 147.5, CG 74.2 → 72.2, TFQMR 154.0 → 152.3; Twingo3D-2 116.4 → 114.3, 58.1 →
+// 56.2 (profiles/r02_while_unroll_ab.txt).  ZK_WHILE_UNROLL overrides.
+constexpr int kWhileUnroll = 4;
 static zk_status build_while_graph(zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc, int method, GraphCache& g,
                                    bool pdl) {
     cudaGraph_t graph = nullptr;
@@ -1616,7 +1622,9 @@ static zk_status build_while_graph(zk_csr_s* A, SolveCtx* dc, const SolveCtx& hc
         cudaGraphDestroy(graph);
         return cuda_fail(e, "cudaStreamBeginCaptureToGraph", __FILE__, __LINE__);
     }
-    zk_status st = enqueue_iteration(A, dc, hc, method, A->cap_stream, pdl);
+    static const int unroll = getenv("ZK_WHILE_UNROLL") ? std::max(1, atoi(getenv("ZK_WHILE_UNROLL"))) : kWhileUnroll;
+    zk_status st = ZK_OK;
+    for (int u = 0; u < unroll && st == ZK_OK; u++) st = enqueue_iteration(A, dc, hc, method, A->cap_stream, pdl);
     cudaGraph_t captured = nullptr;
     e = cudaStreamEndCapture(A->cap_stream, &captured);
     if (st != ZK_OK || e != cudaSuccess) {
