@@ -16,8 +16,10 @@
  *  - Return value: ZK_OK (0) or a negative zk_status error; the thread-local
  *    message is available from zk_last_error().  Solver *outcomes* (MAXIT,
  *    breakdowns, ...) are not errors: they come back in zk_solve_info.
- *  - A zk_csr handle owns reduction scratch: do not use one handle on two
- *    streams concurrently.  The standalone reductions (zk_zdotc, zk_dznrm2)
+ *  - A zk_csr handle owns reduction scratch, its solve graphs and its pinned
+ *    readback staging (which small cluster solves write directly from the
+ *    device): do not use one handle on two streams, or from two host threads,
+ *    concurrently.  Different handles may solve concurrently.  The standalone reductions (zk_zdotc, zk_dznrm2)
  *    use a scratch per (device, stream), allocated on the first call on that
  *    stream (128 KB, kept for the process lifetime): calls on different streams
  *    (or host threads) may run concurrently; calls on one stream are serialised.
