@@ -814,3 +814,33 @@ def test_concurrent_solves_on_two_streams():
     assert not errors, errors[:3]
     for c in cases:
         c[0].close()
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "cg", "tfqmr", "bicgstab_l2"])
+def test_while_body_exits_at_every_position(method, monkeypatch):
+    """The WHILE graph runs four iterations per body (solve.cu kWhileUnroll): a solve that stops
+    after k iterations (MAXIT, k = 1..6, and the converged count) must give the bits of the direct-
+    launch loop (one iteration per host step), whatever the exit's position inside a body."""
+    ell = 2 if method == "bicgstab_l2" else 8
+    meth = "bicgstab_l" if method == "bicgstab_l2" else method
+    if method == "cg":
+        m = gen.make_matrix("T1", eta=0.0, twist_seed=gen.SEED_TWIST)
+        b = np.exp(1j * m["phase"]) * gen.make_rhs(m)
+    else:
+        m = gen.make_matrix("T1")
+        b = gen.make_rhs(m)
+    A = zk.csr_create(m["row_ptr"], m["col_idx"], m["values"], m["n"])
+    bd = cuda(b)
+    for maxit in (1, 2, 3, 4, 5, 6, 1000):
+        out = {}
+        for mode in ("1", "3"):
+            monkeypatch.setenv("ZK_LOOP_MODE", mode)
+            r = zk.solve(A, bd, tol=1e-8, maxit=maxit, method=meth, ell=ell)
+            assert r["loop_mode"] == int(mode)
+            out[mode] = r
+        a, d = out["1"], out["3"]
+        assert a["status"] == d["status"] and a["iters"] == d["iters"], (maxit, a["status"], a["iters"], d["iters"])
+        assert (a["status"] == "MAXIT") == (maxit < 1000) and a["iters"] <= maxit
+        assert torch.equal(a["x"], d["x"]) and np.array_equal(a["hist"], d["hist"])
+        assert a["true_relres"] == d["true_relres"]
+    A.close()
