@@ -55,6 +55,8 @@ def args_():
     p.add_argument("--local-ranks", type=int, default=0,
                    help="run the row-partitioned path on ONE GPU with N in-process ranks (LOCAL transport, "
                         "threads): the C5 z-slab split of the strong-scaling run, timed as max over ranks")
+    p.add_argument("--local-config", default=None,
+                   help="--local-ranks: the system to split (default C5, the strong-scaling system)")
     p.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                    help="N > 1: strong = the fixed C5 system (400^3, 64M rows; BASELINE.json configs[4]) "
                         "split into z-slabs; weak = a 200x200x(200N) box, 8M rows per GPU")
@@ -233,7 +235,7 @@ def run_local_ranks(a):
     from paper_2112_11880_b200 import metrics as M
     from paper_2112_11880_b200 import zk
     N = a.local_ranks
-    cfg = "C5" if a.config == "C4" else a.config
+    cfg = a.local_config or ("C5" if a.config == "C4" else a.config)
     spec = gen.CONFIGS[cfg]
     plane = spec.nx * spec.ny
     group = zk.LocalGroup(N)
