@@ -200,7 +200,7 @@ struct EpiAxpby {
         if (!beta_zero) r = cadd(r, cmul(beta, yo));
         y[i] = r;
     }
-    __device__ void finish(double (&)[1]) {}
+    __device__ void finish(double (&)[1], int = 0, int = 0) {}
 };
 
 template <int W, int MODE>

@@ -83,9 +83,9 @@ __device__ __forceinline__ void finish_stage(SolveCtx* c, const double* tot) {
 // grid reduction of K values, then (single GPU) the stage's scalar step in the last block, or
 // (multi-GPU) publish the local sums in c->red for the allreduce + fin_kernel.
 template <int S, int K>
-__device__ __forceinline__ void reduce_finish(SolveCtx* c, double (&acc)[K]) {
+__device__ __forceinline__ void reduce_finish(SolveCtx* c, double (&acc)[K], int off = 0, int total = 0) {
     double tot[K];
-    if (grid_sum<K>(acc, c->partials, c->tickets + S, tot) && threadIdx.x == 0) {
+    if (grid_sum<K>(acc, c->partials, c->tickets + S, tot, off, total) && threadIdx.x == 0) {
         constexpr int T = timer_of(S);
         const unsigned long long st = atomicExch(&c->t0[T], ~0ull);
         c->tsum[T] += gtimer() - st;
@@ -136,7 +136,7 @@ struct EpiInit {  // r = b − A x0 ; x = x0 ; r̂ = p = r ; {‖b‖², ‖r‖
         acc[2] = fma(rr.x, rr.x, fma(-rr.y, rr.y, acc[2]));  // rᵀr (COCG's ρ0)
         acc[3] = fma(2.0 * rr.x, rr.y, acc[3]);
     }
-    __device__ void finish(double (&acc)[4]) { reduce_finish<S, 4>(c, acc); }
+    __device__ void finish(double (&acc)[4], int off = 0, int tot = 0) { reduce_finish<S, 4>(c, acc, off, tot); }
 };
 
 struct EpiTrue {  // {‖b − A x‖²}
@@ -147,7 +147,7 @@ struct EpiTrue {  // {‖b − A x‖²}
     __device__ explicit EpiTrue(SolveCtx* c_) : c(c_), b(c_->b) {}
     __device__ Pre pre(int64_t i) const { return ld_vec(b + i); }
     __device__ void row(int64_t, double2 y, const Pre& bi, double (&acc)[1]) { acc[0] += cabs2(csub(bi, y)); }
-    __device__ void finish(double (&acc)[1]) { reduce_finish<S_TRUE, 1>(c, acc); }
+    __device__ void finish(double (&acc)[1], int off = 0, int tot = 0) { reduce_finish<S_TRUE, 1>(c, acc, off, tot); }
 };
 
 struct EpiK1Bicg {  // v = A p ; {σ = ⟨r̂, v⟩, ‖v‖²}
@@ -164,7 +164,7 @@ struct EpiK1Bicg {  // v = A p ; {σ = ⟨r̂, v⟩, ‖v‖²}
         acc[1] = fma(r.x, y.y, fma(-r.y, y.x, acc[1]));
         acc[2] += cabs2(y);
     }
-    __device__ void finish(double (&acc)[3]) { reduce_finish<S_K1_BICG, 3>(c, acc); }
+    __device__ void finish(double (&acc)[3], int off = 0, int tot = 0) { reduce_finish<S_K1_BICG, 3>(c, acc, off, tot); }
 };
 
 struct EpiK3Bicg {  // t = A s ; {⟨t, s⟩, ⟨t, t⟩}
@@ -181,7 +181,7 @@ struct EpiK3Bicg {  // t = A s ; {⟨t, s⟩, ⟨t, t⟩}
         acc[1] = fma(y.x, si.y, fma(-y.y, si.x, acc[1]));
         acc[2] += cabs2(y);
     }
-    __device__ void finish(double (&acc)[3]) { reduce_finish<S_K3_BICG, 3>(c, acc); }
+    __device__ void finish(double (&acc)[3], int off = 0, int tot = 0) { reduce_finish<S_K3_BICG, 3>(c, acc, off, tot); }
 };
 
 // Split reductions (large systems): the SpMV of BiCGStab K1/K3 and CG/COCG K1 only stores its
@@ -204,7 +204,7 @@ struct EpiStore {  // out = A x
     __device__ explicit EpiStore(double2* o) : out(o) {}
     __device__ Pre pre(int64_t) const { return make_double2(0.0, 0.0); }
     __device__ void row(int64_t i, double2 y, const Pre&, double (&)[1]) { st_vec(out + i, y); }
-    __device__ void finish(double (&)[1]) {}
+    __device__ void finish(double (&)[1], int = 0, int = 0) {}
 };
 struct OpRed1Bicg {  // {⟨r̂, v⟩, ‖v‖²}
     static constexpr int K = 3;
@@ -218,7 +218,7 @@ struct OpRed1Bicg {  // {⟨r̂, v⟩, ‖v‖²}
         acc[1] = fma(in.r.x, in.v.y, fma(-in.r.y, in.v.x, acc[1]));
         acc[2] += cabs2(in.v);
     }
-    __device__ void finish(double (&acc)[3]) const { reduce_finish<S_K1_BICG, 3>(c, acc); }
+    __device__ void finish(double (&acc)[3], int off = 0, int tot = 0) const { reduce_finish<S_K1_BICG, 3>(c, acc, off, tot); }
 };
 template <bool CONJ, int S>
 struct OpRedPq {  // {⟨p, q⟩} (CG, CONJ) or {pᵀq} (COCG)
@@ -237,7 +237,7 @@ struct OpRedPq {  // {⟨p, q⟩} (CG, CONJ) or {pᵀq} (COCG)
             acc[1] = fma(in.p.x, in.q.y, fma(in.p.y, in.q.x, acc[1]));
         }
     }
-    __device__ void finish(double (&acc)[2]) const { reduce_finish<S, 2>(c, acc); }
+    __device__ void finish(double (&acc)[2], int off = 0, int tot = 0) const { reduce_finish<S, 2>(c, acc, off, tot); }
 };
 struct OpRed3Bicg {  // {⟨t, s⟩, ‖t‖²}
     static constexpr int K = 3;
@@ -251,7 +251,7 @@ struct OpRed3Bicg {  // {⟨t, s⟩, ‖t‖²}
         acc[1] = fma(in.t.x, in.s.y, fma(-in.t.y, in.s.x, acc[1]));
         acc[2] += cabs2(in.t);
     }
-    __device__ void finish(double (&acc)[3]) const { reduce_finish<S_K3_BICG, 3>(c, acc); }
+    __device__ void finish(double (&acc)[3], int off = 0, int tot = 0) const { reduce_finish<S_K3_BICG, 3>(c, acc, off, tot); }
 };
 
 // Split schedule with a TAIL reduction (SPLIT = 2, SELL mapping on one GPU): the SpMV stores
@@ -271,7 +271,7 @@ struct EpiStoreTail {
     __device__ Pre pre(int64_t) const { return make_double2(0.0, 0.0); }
     __device__ void row(int64_t i, double2 y, const Pre&, double (&)[K]) { st_vec(out + i, y); }
     __device__ Op tail_op() const { return Op(c); }
-    __device__ void finish(double (&)[K]) {}  // the tail's Op finishes the stage
+    __device__ void finish(double (&)[K], int = 0, int = 0) {}  // the tail's Op finishes the stage
 };
 
 // The fused epilogue with per-slice warp reductions (SPLIT = 3, SELL only): E's row() as is, its
@@ -298,7 +298,7 @@ struct EpiK1Cg {  // q = A p ; {δ = ⟨p, q⟩}
         acc[0] = fma(pi.x, y.x, fma(pi.y, y.y, acc[0]));
         acc[1] = fma(pi.x, y.y, fma(-pi.y, y.x, acc[1]));
     }
-    __device__ void finish(double (&acc)[2]) { reduce_finish<S_K1_CG, 2>(c, acc); }
+    __device__ void finish(double (&acc)[2], int off = 0, int tot = 0) { reduce_finish<S_K1_CG, 2>(c, acc, off, tot); }
 };
 
 // Vector ops: every pointer and scalar is copied out of the SolveCtx once per thread at kernel
@@ -326,12 +326,12 @@ struct OpInitZero {  // x0 = 0: x = 0 ; r = r̂ = p = b ; {‖b‖², ‖r‖²,
         acc[2] = fma(v.b.x, v.b.x, fma(-v.b.y, v.b.y, acc[2]));
         acc[3] = fma(2.0 * v.b.x, v.b.y, acc[3]);
     }
-    __device__ void finish(double (&acc)[4]) const {
-        if (kind == 0) reduce_finish<S_INIT_BICG, 4>(c, acc);
-        else if (kind == 1) reduce_finish<S_INIT_CG, 4>(c, acc);
-        else if (kind == 3) reduce_finish<S_INIT_COCG, 4>(c, acc);
-        else if (kind == 4) reduce_finish<S_INIT_TFQMR, 4>(c, acc);
-        else reduce_finish<S_INIT_BL, 4>(c, acc);
+    __device__ void finish(double (&acc)[4], int off = 0, int tot = 0) const {
+        if (kind == 0) reduce_finish<S_INIT_BICG, 4>(c, acc, off, tot);
+        else if (kind == 1) reduce_finish<S_INIT_CG, 4>(c, acc, off, tot);
+        else if (kind == 3) reduce_finish<S_INIT_COCG, 4>(c, acc, off, tot);
+        else if (kind == 4) reduce_finish<S_INIT_TFQMR, 4>(c, acc, off, tot);
+        else reduce_finish<S_INIT_BL, 4>(c, acc, off, tot);
     }
 };
 
@@ -351,7 +351,7 @@ struct OpK2Bicg {  // s = r − α v ; {‖s‖²}
         st_vec(s + i, o);
         acc[0] += cabs2(o);
     }
-    __device__ void finish(double (&acc)[1]) const { reduce_finish<S_K2_BICG, 1>(c, acc); }
+    __device__ void finish(double (&acc)[1], int off = 0, int tot = 0) const { reduce_finish<S_K2_BICG, 1>(c, acc, off, tot); }
 };
 
 struct OpK4Bicg {  // x += αp + ωs ; r = s − ωt ; {‖r‖², ⟨r̂, r⟩}   (half: x += αp only)
@@ -394,9 +394,9 @@ struct OpK4Bicg {  // x += αp + ωs ; r = s − ωt ; {‖r‖², ⟨r̂, r⟩}
         acc[1] = fma(in.rh.x, rn.x, fma(in.rh.y, rn.y, acc[1]));
         acc[2] = fma(in.rh.x, rn.y, fma(-in.rh.y, rn.x, acc[2]));
     }
-    __device__ void finish(double (&acc)[3]) const {
+    __device__ void finish(double (&acc)[3], int off = 0, int tot = 0) const {
         if (half) return;  // no reduction on the half-step exit; K5 clears the flag
-        reduce_finish<S_K4_BICG, 3>(c, acc);
+        reduce_finish<S_K4_BICG, 3>(c, acc, off, tot);
     }
 };
 
@@ -417,7 +417,7 @@ struct OpK5Bicg {  // p = r + β(p − ω v)
         cfma(o, beta, d);
         st_vec(p + i, o);
     }
-    __device__ void finish(double (&)[1]) const {}
+    __device__ void finish(double (&)[1], int = 0, int = 0) const {}
 };
 
 struct OpK2Cg {  // x += α p ; r −= α q ; {‖r‖²}
@@ -438,7 +438,7 @@ struct OpK2Cg {  // x += α p ; r −= α q ; {‖r‖²}
         st_vec(r + i, rn);
         acc[0] += cabs2(rn);
     }
-    __device__ void finish(double (&acc)[1]) const { reduce_finish<S_K2_CG, 1>(c, acc); }
+    __device__ void finish(double (&acc)[1], int off = 0, int tot = 0) const { reduce_finish<S_K2_CG, 1>(c, acc, off, tot); }
 };
 
 struct OpK3Cg {  // p = r + β p
@@ -452,7 +452,7 @@ struct OpK3Cg {  // p = r + β p
     __device__ void apply(int64_t i, const In& in, double (&)[1]) const {
         st_vec(p + i, make_double2(fma(beta, in.p.x, in.r.x), fma(beta, in.p.y, in.r.y)));
     }
-    __device__ void finish(double (&)[1]) const {}
+    __device__ void finish(double (&)[1], int = 0, int = 0) const {}
 };
 
 struct EpiK1Cocg {  // q = A p ; {μ = pᵀ q} (unconjugated)
@@ -468,7 +468,7 @@ struct EpiK1Cocg {  // q = A p ; {μ = pᵀ q} (unconjugated)
         acc[0] = fma(pi.x, y.x, fma(-pi.y, y.y, acc[0]));
         acc[1] = fma(pi.x, y.y, fma(pi.y, y.x, acc[1]));
     }
-    __device__ void finish(double (&acc)[2]) { reduce_finish<S_K1_COCG, 2>(c, acc); }
+    __device__ void finish(double (&acc)[2], int off = 0, int tot = 0) { reduce_finish<S_K1_COCG, 2>(c, acc, off, tot); }
 };
 
 struct OpK2Cocg {  // x += α p ; r −= α q ; {‖r‖², rᵀr}
@@ -493,7 +493,7 @@ struct OpK2Cocg {  // x += α p ; r −= α q ; {‖r‖², rᵀr}
         acc[1] = fma(rn.x, rn.x, fma(-rn.y, rn.y, acc[1]));
         acc[2] = fma(2.0 * rn.x, rn.y, acc[2]);
     }
-    __device__ void finish(double (&acc)[3]) const { reduce_finish<S_K2_COCG, 3>(c, acc); }
+    __device__ void finish(double (&acc)[3], int off = 0, int tot = 0) const { reduce_finish<S_K2_COCG, 3>(c, acc, off, tot); }
 };
 
 struct OpK3Cocg {  // p = r + β p (complex β)
@@ -509,7 +509,7 @@ struct OpK3Cocg {  // p = r + β p (complex β)
         cfma(o, beta, in.p);
         st_vec(p + i, o);
     }
-    __device__ void finish(double (&)[1]) const {}
+    __device__ void finish(double (&)[1], int = 0, int = 0) const {}
 };
 
 // TFQMR epilogues and vector ops (the loops of oracle_tfqmr, fused per kernel T1..T4)
@@ -546,7 +546,7 @@ struct OpT1Tfqmr {  // y2 = y1 − α v ; w −= α u1 ; {‖w‖²}
         st_vec(w + i, wn);
         acc[0] += cabs2(wn);
     }
-    __device__ void finish(double (&acc)[1]) const { reduce_finish<S_T1_TFQMR, 1>(c, acc); }
+    __device__ void finish(double (&acc)[1], int off = 0, int tot = 0) const { reduce_finish<S_T1_TFQMR, 1>(c, acc, off, tot); }
 };
 
 struct EpiT2Tfqmr {  // u2 = A y2 ; w −= α u2 ; {‖w‖², ⟨r̃, w⟩}
@@ -570,7 +570,7 @@ struct EpiT2Tfqmr {  // u2 = A y2 ; w −= α u2 ; {‖w‖², ⟨r̃, w⟩}
         acc[1] = fma(q.rt.x, wn.x, fma(q.rt.y, wn.y, acc[1]));
         acc[2] = fma(q.rt.x, wn.y, fma(-q.rt.y, wn.x, acc[2]));
     }
-    __device__ void finish(double (&acc)[3]) { reduce_finish<S_T2_TFQMR, 3>(c, acc); }
+    __device__ void finish(double (&acc)[3], int off = 0, int tot = 0) { reduce_finish<S_T2_TFQMR, 3>(c, acc, off, tot); }
 };
 
 // d1 = y1 + c1·d ; d = y2 + c2·d1 ; x += η1·d1 + η2·d ; y1 = w + β y2   (exit: no y1)
@@ -609,7 +609,7 @@ struct OpT3Tfqmr {
         cfma(o, beta, in.y2);
         st_vec(y1 + i, o);
     }
-    __device__ void finish(double (&)[1]) const {}
+    __device__ void finish(double (&)[1], int = 0, int = 0) const {}
 };
 
 // split schedule (large systems): T2/T4 store A·y only, these passes do the rest
@@ -632,7 +632,7 @@ struct OpT2bTfqmr {  // w −= α u2 ; {‖w‖², ⟨r̃, w⟩}
         acc[1] = fma(in.rt.x, wn.x, fma(in.rt.y, wn.y, acc[1]));
         acc[2] = fma(in.rt.x, wn.y, fma(-in.rt.y, wn.x, acc[2]));
     }
-    __device__ void finish(double (&acc)[3]) const { reduce_finish<S_T2_TFQMR, 3>(c, acc); }
+    __device__ void finish(double (&acc)[3], int off = 0, int tot = 0) const { reduce_finish<S_T2_TFQMR, 3>(c, acc, off, tot); }
 };
 struct OpT4bTfqmr {  // v = u1 + β(u2 + β v) ; {σ = ⟨r̃, v⟩}
     static constexpr int K = 2;
@@ -653,7 +653,7 @@ struct OpT4bTfqmr {  // v = u1 + β(u2 + β v) ; {σ = ⟨r̃, v⟩}
         acc[0] = fma(in.rt.x, vn.x, fma(in.rt.y, vn.y, acc[0]));
         acc[1] = fma(in.rt.x, vn.y, fma(-in.rt.y, vn.x, acc[1]));
     }
-    __device__ void finish(double (&acc)[2]) const { reduce_finish<S_T4_TFQMR, 2>(c, acc); }
+    __device__ void finish(double (&acc)[2], int off = 0, int tot = 0) const { reduce_finish<S_T4_TFQMR, 2>(c, acc, off, tot); }
 };
 
 template <int S>
@@ -684,7 +684,7 @@ struct EpiT4Tfqmr {  // u1 = A y1 ; v = u1 + β(u2 + β v) (first: v = u1) ; {σ
         acc[0] = fma(q.rt.x, vn.x, fma(q.rt.y, vn.y, acc[0]));
         acc[1] = fma(q.rt.x, vn.y, fma(-q.rt.y, vn.x, acc[1]));
     }
-    __device__ void finish(double (&acc)[2]) { reduce_finish<S, 2>(c, acc); }
+    __device__ void finish(double (&acc)[2], int off = 0, int tot = 0) { reduce_finish<S, 2>(c, acc, off, tot); }
 };
 
 // ------------------------------------------------------------------ kernels
@@ -960,7 +960,9 @@ __global__ void __launch_bounds__(kBlock, ZK_TF_MINB) t4_tfqmr(SolveCtx* c, cons
             spmv_any<W, MODE>(A, y1, e);
         }
     }
-    if (SPLIT != 1) set_cond(c);  // split: t4b_tfqmr is the body's last kernel
+    // split: t4b_tfqmr is the body's last kernel; a distributed SpMV is two launches: count the
+    // body once (main_part: the interior launch)
+    if (SPLIT != 1 && A.main_part) set_cond(c);
 }
 // ------------------------------------------------------------------ BiCGStab(ℓ) kernels (NEXT-3)
 // One outer cycle (oracle_bicgstab_l): for j = 0..ℓ−1 the BiCG step runs as
@@ -1099,8 +1101,8 @@ struct EpiBl {  // out = A v ; {⟨r̃, out⟩, ‖out‖²} when RED
             acc[2] += cabs2(y);
         }
     }
-    __device__ void finish(double (&acc)[KA]) {
-        if constexpr (RED) reduce_finish<S, 3>(c, acc);
+    __device__ void finish(double (&acc)[KA], int off = 0, int tot = 0) {
+        if constexpr (RED) reduce_finish<S, 3>(c, acc, off, tot);
     }
 };
 
@@ -1135,7 +1137,7 @@ struct OpRedBl {  // {⟨r̃, y⟩, ‖y‖²} of the vector y just produced by 
         acc[1] = fma(in.r.x, in.y.y, fma(-in.r.y, in.y.x, acc[1]));
         acc[2] += cabs2(in.y);
     }
-    __device__ void finish(double (&acc)[3]) const { reduce_finish<S, 3>(c, acc); }
+    __device__ void finish(double (&acc)[3], int off = 0, int tot = 0) const { reduce_finish<S, 3>(c, acc, off, tot); }
 };
 template <int S>
 __global__ void __launch_bounds__(kBlock, ZK_VEC_MINB) bl_r(SolveCtx* c, const double2* y) {
@@ -1330,9 +1332,10 @@ static zk_status dist_finish(const zk_csr_s* A, SolveCtx* c, int count, cudaStre
     return ZK_OK;
 }
 
-// Split schedule (store-only SpMVs + a reduction pass): from kSplitRows rows, and always on a
-// distributed matrix, whose SpMVs are split into interior / boundary launches around the halo
-// exchange (a fused epilogue reduction cannot span two launches)
+// Split schedule (the SpMV stores its product; its reductions run as the kernel's tail, as a
+// warp-reduced epilogue, or — ZK_SPLIT_TAIL=0 / CSR sub-warp mapping — as a separate pass): from
+// kSplitRows rows, and always on a distributed matrix, whose SpMVs are split into interior /
+// boundary launches around the halo exchange (their fused reductions span both, loop_spmv)
 static bool split_reductions(const zk_csr_s* A) {
     if (A->dist) return true;
     if (const char* e = getenv("ZK_SPLIT_RED")) return atoi(e) != 0;
@@ -1346,7 +1349,11 @@ static bool split_reductions(const zk_csr_s* A) {
 // 133.3 → 128.0, 69.0 → 64.8, 138.0 → 129.7; C4 1707 → 1694, 901 → 908, 1808 → 1797
 // (profiles/r02_split_tail.txt).
 static bool split_tail(const zk_csr_s* A) {
-    if (A->dist || A->spmv_mode != 3 || !split_reductions(A)) return false;
+    if (A->spmv_mode != 3 || !split_reductions(A)) return false;
+    // a distributed SpMV is two launches (interior slices, then the boundary after the halo): the
+    // fused reductions span them (grid_sum off / total, loop_spmv); ZK_DIST_FUSED=0 keeps the
+    // store-only SpMVs and separate reduction passes
+    if (A->dist && getenv("ZK_DIST_FUSED") && atoi(getenv("ZK_DIST_FUSED")) == 0) return false;
     if (const char* e = getenv("ZK_SPLIT_TAIL")) return atoi(e) != 0;
     return true;
 }
@@ -1375,8 +1382,12 @@ zk_status dist_halo_end(const zk_csr_s* A, cudaStream_t s);                     
 // exchange of xg runs on the plan's stream while the interior slices (no halo column) compute,
 // then the boundary slices (SURVEY.md §8(e) "Halo": pack → send/recv ‖ interior SpMV → boundary
 // SpMV); without an interior run (or with ZK_DIST_OVERLAP=0) a blocking exchange first.
+// fused: the SpMV kernel's reduction is fused (tail or warp-reduced epilogue): with the overlap its
+// two launches share one grid reduction — the interior launch's blocks are partials [0, G1), the
+// boundary launch's [G1, G1 + G2), and the boundary launch's last block finishes (grid_sum).
 template <class L>
-static zk_status loop_spmv(const zk_csr_s* A, const CsrDev& av, double2* xg, cudaStream_t s, L&& launch) {
+static zk_status loop_spmv(const zk_csr_s* A, const CsrDev& av, double2* xg, cudaStream_t s, L&& launch,
+                           const void* fused = nullptr) {
     if (!A->dist) return launch(av, false);
     if (!dist_overlap(A)) {
         ZK_TRY(dist_halo(A, xg, s));
@@ -1384,6 +1395,14 @@ static zk_status loop_spmv(const zk_csr_s* A, const CsrDev& av, double2* xg, cud
     }
     CsrDev in, bd;
     dist_split(A, av, &in, &bd);
+    if (fused) {
+        const int g1 = spmv_cfg_part(A, fused, in).grid;
+        const int g2 = bd.sl_cnt > 0 ? spmv_cfg_part(A, fused, bd).grid : 0;
+        in.red_off = 0;
+        in.red_total = g1 + g2;
+        bd.red_off = g1;
+        bd.red_total = g1 + g2;
+    }
     ZK_TRY(dist_halo_begin(A, xg, s));
     ZK_TRY(launch(in, true));
     ZK_TRY(dist_halo_end(A, s));
@@ -1427,9 +1446,9 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
         };
         if (method == ZK_BICGSTAB) {
             if (wacc) {
-                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_bicg<W, MODE, 3>)));
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_bicg<W, MODE, 3>), (const void*)k1_bicg<W, MODE, 3>));
             } else if (tail) {
-                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_bicg<W, MODE, 2>)));
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_bicg<W, MODE, 2>), (const void*)k1_bicg<W, MODE, 2>));
             } else if (split) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_bicg<W, MODE, 1>)));
                 ZK_TRY(launch_loop(pdl, r1_bicg, vec_grid(A, (const void*)r1_bicg), 0, s, dc));
@@ -1442,9 +1461,9 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             ZK_TRY(launch_loop(pdl, k2_bicg, vec_grid(A, (const void*)k2_bicg), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_K2_BICG>(A, dc, 1, s)));
             if (wacc) {
-                ZK_TRY(loop_spmv(A, hc.A, hc.s, s, part(k3_bicg<W, MODE, 3>)));
+                ZK_TRY(loop_spmv(A, hc.A, hc.s, s, part(k3_bicg<W, MODE, 3>), (const void*)k3_bicg<W, MODE, 3>));
             } else if (tail) {
-                ZK_TRY(loop_spmv(A, hc.A, hc.s, s, part(k3_bicg<W, MODE, 2>)));
+                ZK_TRY(loop_spmv(A, hc.A, hc.s, s, part(k3_bicg<W, MODE, 2>), (const void*)k3_bicg<W, MODE, 2>));
             } else if (split) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.s, s, part(k3_bicg<W, MODE, 1>)));
                 ZK_TRY(launch_loop(pdl, r3_bicg, vec_grid(A, (const void*)r3_bicg), 0, s, dc));
@@ -1517,7 +1536,7 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             ZK_TRY(launch_loop(pdl, t1_tfqmr, vec_grid(A, (const void*)t1_tfqmr), 0, s, dc));
             if (dist) ZK_TRY((dist_finish<S_T1_TFQMR>(A, dc, 1, s)));
             if (tail) {  // (a warp-reduced T2/T4 epilogue carries 2-3 operands: it spills at 80 registers)
-                ZK_TRY(loop_spmv(A, hc.A, hc.y2, s, part(t2_tfqmr<W, MODE, 2>)));
+                ZK_TRY(loop_spmv(A, hc.A, hc.y2, s, part(t2_tfqmr<W, MODE, 2>), (const void*)t2_tfqmr<W, MODE, 2>));
             } else if (split) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.y2, s, part(t2_tfqmr<W, MODE, 1>)));
                 ZK_TRY(launch_loop(pdl, t2b_tfqmr, vec_grid(A, (const void*)t2b_tfqmr), 0, s, dc));
@@ -1529,7 +1548,7 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             if (dist) ZK_TRY((dist_finish<S_T2_TFQMR>(A, dc, 3, s)));
             ZK_TRY(launch_loop(pdl, t3_tfqmr, vec_grid(A, (const void*)t3_tfqmr), 0, s, dc));
             if (tail) {
-                ZK_TRY(loop_spmv(A, hc.A, hc.y1, s, part(t4_tfqmr<W, MODE, 2>)));
+                ZK_TRY(loop_spmv(A, hc.A, hc.y1, s, part(t4_tfqmr<W, MODE, 2>), (const void*)t4_tfqmr<W, MODE, 2>));
             } else if (split) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.y1, s, part(t4_tfqmr<W, MODE, 1>)));
                 ZK_TRY(launch_loop(pdl, t4b_tfqmr, vec_grid(A, (const void*)t4b_tfqmr), 0, s, dc));
@@ -1541,9 +1560,9 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             if (dist) ZK_TRY((dist_finish<S_T4_TFQMR>(A, dc, 2, s)));
         } else if (method == ZK_COCG) {
             if (wacc) {
-                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cocg<W, MODE, 3>)));
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cocg<W, MODE, 3>), (const void*)k1_cocg<W, MODE, 3>));
             } else if (tail) {
-                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cocg<W, MODE, 2>)));
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cocg<W, MODE, 2>), (const void*)k1_cocg<W, MODE, 2>));
             } else if (split) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cocg<W, MODE, 1>)));
                 auto kr = rq_kernel<false, S_K1_COCG>;
@@ -1559,9 +1578,9 @@ static zk_status enqueue_iteration(const zk_csr_s* A, SolveCtx* dc, const SolveC
             ZK_TRY(launch_loop(pdl, k3_cocg, vec_grid(A, (const void*)k3_cocg), 0, s, dc));
         } else {
             if (wacc) {
-                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cg<W, MODE, 3>)));
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cg<W, MODE, 3>), (const void*)k1_cg<W, MODE, 3>));
             } else if (tail) {
-                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cg<W, MODE, 2>)));
+                ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cg<W, MODE, 2>), (const void*)k1_cg<W, MODE, 2>));
             } else if (split) {
                 ZK_TRY(loop_spmv(A, hc.A, hc.p, s, part(k1_cg<W, MODE, 1>)));
                 auto kr = rq_kernel<true, S_K1_CG>;

@@ -327,9 +327,9 @@ __device__ __forceinline__ void spmv_body_sell(const CsrDev& A, const double2* _
     if constexpr (sell_tail<Epi>::value) {
         const auto op = epi.tail_op();
         sell_walk_own<REV, false>(A, op, acc);
-        op.finish(acc);
+        op.finish(acc, A.red_off, A.red_total);
     } else {
-        epi.finish(acc);
+        epi.finish(acc, A.red_off, A.red_total);
     }
 }
 

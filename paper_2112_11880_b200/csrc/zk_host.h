@@ -185,7 +185,7 @@ zk_status with_spmv(const zk_csr_s* A, F&& f) {
 
 inline CsrDev csr_dev(const zk_csr_s* A) {
     const int ns = (int)A->n_slices;
-    return CsrDev{A->row_ptr, A->col, A->val, A->n_rows, A->nnz, A->sl_ptr, A->sl_col, A->sl_val, 0, ns, ns, 0, 1};
+    return CsrDev{A->row_ptr, A->col, A->val, A->n_rows, A->nnz, A->sl_ptr, A->sl_col, A->sl_val, 0, ns, ns, 0, 1, 0, 0};
 }
 
 struct LaunchCfg {

@@ -201,16 +201,20 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* sm) {
 // last ticket sums the partials in index order (fixed tree) and returns true, with the totals
 // in `out` (valid in thread 0).  The ticket is reset by the last block, so the scratch is
 // self-cleaning.  partials: [K][gridDim.x] doubles.
+// off / total: a reduction spread over two launches of one SpMV (the interior and boundary slices
+// of a distributed matrix, dist.cu): this launch's blocks are partials [off, off + gridDim.x) of
+// `total`, one shared ticket, and only the block that takes the last of the `total` tickets — in the
+// second launch — finishes.  total = 0: one launch.
 template <int K>
 __device__ __forceinline__ bool grid_sum(double (&v)[K], double* partials, unsigned int* ticket,
-                                         double (&out)[K]) {
+                                         double (&out)[K], int off = 0, int total = 0) {
     __shared__ double sm[kWarps * kMaxRed];
     __shared__ bool last;
     block_sum<K>(v, sm);
-    const int G = gridDim.x;
+    const int G = total > 0 ? total : (int)gridDim.x;
     if (threadIdx.x == 0) {
 #pragma unroll
-        for (int k = 0; k < K; k++) partials[k * G + blockIdx.x] = v[k];
+        for (int k = 0; k < K; k++) partials[k * G + off + blockIdx.x] = v[k];
         __threadfence();
         unsigned int t = atomicAdd(ticket, 1u);
         last = (t == (unsigned)G - 1);
@@ -253,6 +257,8 @@ struct CsrDev {
     // launch of one SpMV (work that must happen once per SpMV is skipped there).
     int sl_lo, sl_cnt, sl_gap_at, sl_gap;
     int main_part;
+    // the SpMV's fused reduction spans two launches (grid_sum off / total; 0 = one launch)
+    int red_off, red_total;
 };
 
 }  // namespace zk
